@@ -1,0 +1,58 @@
+/* orc.h -- CPU ORACLE for arXiv 2406.07048's ADMM hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant with the product (paper_2406_07048_b200/, include/).
+ *
+ * Citation key: P:n = /root/reference/PAPER.md line n (the LaTeX source);
+ * "reading #k" = DESIGN.md "Readings of the paper" item k.
+ *
+ * Pair index p = ((b*N + (t-1))*n_parts + i)*n_obs + j, t = 1..N (reading #5).
+ * y is stored padded: y[p*ny + k], k < n_p = n_r(i) + n_o(b,j) + 1,
+ * rows ordered (lambda_1..lambda_nr, mu_1..mu_no, gamma) as in P:368-371.
+ */
+#ifndef ORC_H
+#define ORC_H
+
+enum { ORC_POSE_TRANSLATION = 0, ORC_POSE_SE2 = 1, ORC_POSE_TRANS_YAW = 2 };
+enum { ORC_OK = 0, ORC_RAY = 1, ORC_ITER_LIMIT = 2, ORC_NEG_YE = 3 };
+
+typedef struct {
+  int dim, n_scenes, horizon, n_state, n_ctrl;
+  int pose_model;
+  int pose_idx[4];
+  int n_parts;
+  const int* part_off;
+  const double* part_A;
+  const double* part_b;
+  int n_obs;
+  const int* obs_off;
+  const double* obs_C;
+  const double* obs_d;
+  int dyn_per_scene, dyn_per_time;
+  const double* dyn_A;
+  const double* dyn_B;
+  const double* dyn_c;
+  const double* Qs;
+  const double* Qu;
+  const double* s0;
+  const double* s_ref;
+  double sigma;
+  double pivot_tol;
+  double tie_tol;
+  int max_pivot_factor;
+  int ny;
+  double prox_eps; /* 0 = paper-exact Eq. 19 (reading #2) */
+} orc_problem;
+
+typedef struct {
+  double* s;    /* [B][N+1][ns] */
+  double* u;    /* [B][N][nu]   */
+  double* y;    /* [P][ny]      */
+  double* zeta; /* [P]          */
+  double* xi;   /* [P][d]       */
+  int* pivots;  /* [P] pivots of the last dual sweep */
+  int* status;  /* [P] ORC_* of the last dual sweep */
+} orc_iterate;
+
+#endif
