@@ -1,0 +1,187 @@
+/* ca.h -- C ABI of the B200 (sm_100a) FP64 implementation of the ADMM hot path of
+ * arXiv 2406.07048 (scale-based collision avoidance; ADMM over per-pair dual QPs).
+ *
+ * Citation key: P:n = line n of the paper's LaTeX source; DESIGN.md
+ * "reading #k" = how this library resolves a point the paper leaves open.
+ *
+ * Conventions for every entry point
+ *  - All pointers passed IN are HOST pointers unless stated; the library copies
+ *    what it needs before returning (the caller keeps ownership).  Outputs are
+ *    written to caller-allocated HOST buffers.  Device state is owned by the handle.
+ *  - Row-major FP64 arrays; int32 offsets.  Scene b, timestep t = 1..N, robot
+ *    part i, obstacle j form pair p = ((b*N + (t-1))*n_parts + i)*n_obs + j
+ *    (reading #5: collision pairs exist for t = 1..N only).
+ *  - All device work is ordered on the CUDA stream given at create.  A handle is
+ *    not thread-safe; distinct handles are independent.
+ *  - Return value: CA_OK (0), an error (< 0; details in ca_last_error()) or a
+ *    warning (> 0).  Validation errors create no handle.  A CUDA error is sticky:
+ *    the handle must be destroyed.  Per-pair Lemke failures are not fatal: the
+ *    pair keeps its previous certificate, the failure is counted and
+ *    CA_W_PAIR_FAILURES is returned.  No exception crosses the ABI.
+ *  - No CPU fallback: without a usable sm_100 device every call that needs the
+ *    GPU returns CA_E_CUDA.
+ */
+#ifndef CA_H
+#define CA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ca_status;
+enum {
+  CA_OK = 0,
+  CA_E_INVALID = -1,     /* null pointer, non-positive size, bad parameter */
+  CA_E_DIM = -2,         /* d not in {2,3}; n = n_r + n_o + 1 > 32; pose index out of range */
+  CA_E_GEOMETRY = -3,    /* robot part with b_i not > 0 (reading #22) or < d+1 rows */
+  CA_E_UNSUPPORTED = -4, /* unknown pose model, n_state > 8, n_ctrl > 4 */
+  CA_E_CUDA = -5,        /* CUDA error / no sm_100 device */
+  CA_E_NCCL = -6,
+  CA_E_OOM = -7,
+  CA_W_NOT_CONVERGED = 1, /* ca_admm_solve hit max_iters */
+  CA_W_PAIR_FAILURES = 2  /* >= 1 pair hit RAY / ITER_LIMIT / y_e < -1e-6 */
+};
+
+/* pose models R(s), rho(s) (reading #9) */
+enum {
+  CA_POSE_TRANSLATION = 0, /* rho = s[idx[0..d-1]], R = I */
+  CA_POSE_SE2 = 1,         /* d = 2: rho = (s[idx0], s[idx1]), R = Rot(s[idx2]) */
+  CA_POSE_TRANS_YAW = 2    /* d = 3: rho = s[idx0..2], R = Rot_z(s[idx3]) */
+};
+
+/* per-pair Lemke status (reading #4) */
+enum { CA_PAIR_OK = 0, CA_PAIR_RAY = 1, CA_PAIR_ITER_LIMIT = 2, CA_PAIR_NEG_YE = 3 };
+
+typedef struct ca_problem ca_problem;
+
+/* Problem description.  All arrays are HOST arrays, copied at create/load.
+ *  robot parts: part_off[n_parts+1]; part_A[rows*d] body-frame face
+ *                normals a_k; part_b[rows] > 0.  A_i x <= b_i.
+ *  obstacles: obs_off[n_scenes*n_obs+1]; obs_C[rows*d]; obs_d[rows];
+ *                C_j y <= d_j in world coordinates; obstacle (b, j) = b*n_obs + j.
+ *  dynamics      (P:176-182 linearised): s_{t+1} = A_t s_t + B_t u_t + c_t;
+ *                dyn_A[nd*ns*ns], dyn_B[nd*ns*nu], dyn_c[nd*ns] with
+ *                nd = (dyn_per_scene ? n_scenes : 1) * (dyn_per_time ? horizon : 1).
+ *  cost: sum_t ||s_t - s_ref_t||^2_Qs + ||u_t||^2_Qu (no 1/2);
+ *                Qs[ns*ns], Qu[nu*nu] SPD.  s0[B*ns], s_ref[B*(N+1)*ns];
+ *                s_init nullable (default: s_ref, reading #11).
+ *  ADMM: sigma > 0 (paper: 300); eps_pri/eps_dual per scene
+ *                (<= 0: default 1e-3 * pairs per scene); max_iters for ca_admm_solve.
+ *  Lemke         (reading #4): pivot_tol (1e-11), tie_tol (1e-9), max pivots
+ *                = lemke_max_pivot_factor * n (50).  <= 0 selects the default.
+ *  prox_eps      (reading #2): 0 = paper-exact Eq. 19; > 0 adds eps/2 ||y - y^k||^2.
+ */
+typedef struct {
+  int32_t dim, n_scenes, horizon, n_state, n_ctrl;
+  int32_t pose_model;
+  int32_t pose_idx[4];
+  int32_t n_parts;
+  const int32_t* part_off;
+  const double* part_A;
+  const double* part_b;
+  int32_t n_obs;
+  const int32_t* obs_off;
+  const double* obs_C;
+  const double* obs_d;
+  int32_t dyn_per_scene, dyn_per_time;
+  const double* dyn_A;
+  const double* dyn_B;
+  const double* dyn_c;
+  const double* Qs;
+  const double* Qu;
+  const double* s0;
+  const double* s_ref;
+  const double* s_init;
+  double sigma, eps_pri, eps_dual;
+  int32_t max_iters;
+  double lemke_pivot_tol, lemke_tie_tol;
+  int32_t lemke_max_pivot_factor;
+  double prox_eps;
+} ca_problem_desc;
+
+/* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;
+ * r_dual excludes gamma, reading #19).  pivots = total Lemke pivots of the sweep. */
+typedef struct {
+  double r_pri, r_dual;
+  int64_t n_pairs, n_fail, pivots;
+} ca_residuals;
+
+typedef struct {
+  int32_t iterations, converged;
+  ca_residuals last;
+} ca_solve_report;
+
+/* Validate, allocate device state (~(2n_max + 2d + 8) * 8 bytes per pair), upload the
+ * problem and initialise the iterate (reading #11).  device: CUDA ordinal; stream:
+ * cudaStream_t (NULL = legacy default stream).  On error *out is NULL. */
+ca_status ca_problem_create(const ca_problem_desc* desc, int device, void* stream, ca_problem** out);
+void ca_problem_destroy(ca_problem* h);
+
+/* Re-upload every per-batch input of a problem with the SAME shapes (n_scenes,
+ * horizon, parts, per-obstacle row counts) and reset the iterate.  The end-to-end
+ * path: load -> ca_admm_iterate -> ca_get_trajectory. */
+ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* desc);
+
+/* n_pairs, ny (= n_max, the per-pair y stride of ca_get_pair_state), device bytes. */
+ca_status ca_problem_info(const ca_problem* h, int64_t* n_pairs, int32_t* ny, int64_t* device_bytes);
+
+/* Eq. 3: alpha*_p for every pair at the states `states` (HOST
+ * [B*(N+1)*ns], NULL = current iterate).  alpha: HOST [n_pairs] or NULL;
+ * min_alpha: HOST [n_scenes] (per-scene minimum) or NULL. */
+ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, double* min_alpha);
+
+/* `iters` fixed ADMM iterations (Eqs. 15-17, reading #1 Gauss-Seidel), no
+ * early stop.  hist: HOST [iters] per-iteration residuals or NULL. */
+ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist);
+
+/* Iterate until every scene meets Eq. 18 (r_pri <= eps_pri and r_dual <= eps_dual,
+ * '<=' per P:325-326) or max_iters; CA_W_NOT_CONVERGED if the cap was hit. */
+ca_status ca_admm_solve(ca_problem* h, ca_solve_report* out);
+
+/* The three ADMM steps one at a time (frozen-input parity): step 1 (Eq. 15),
+ * step 2 (Eq. 16), step 3 (Eq. 17).  out may be NULL. */
+ca_status ca_dual_sweep(ca_problem* h, ca_residuals* out);
+ca_status ca_primal_step(ca_problem* h);
+ca_status ca_multiplier_update(ca_problem* h, ca_residuals* out);
+
+/* Per-scene residuals of the last completed step: HOST [n_scenes] each (nullable). */
+ca_status ca_get_scene_residuals(ca_problem* h, double* r_pri, double* r_dual);
+
+/* HOST s[B*(N+1)*ns], u[B*N*nu] (either may be NULL). */
+ca_status ca_get_trajectory(ca_problem* h, double* s, double* u);
+
+/* Pair state for pairs [p0, p0+count): y[count*ny] (padded with 0 beyond n_p),
+ * zeta[count], xi[count*d], pivots[count], status[count] (CA_PAIR_*), zmask[count]
+ * (bit j = z_j basic in the final Lemke basis, bit 31 = z0).  Any may be NULL. */
+ca_status ca_get_pair_state(ca_problem* h, int64_t p0, int64_t count, double* y, double* zeta,
+                            double* xi, int32_t* pivots, int32_t* status, uint32_t* zmask);
+
+/* Overwrite the iterate (any pointer may be NULL = keep).  Layouts as the getters. */
+ca_status ca_set_iterate(ca_problem* h, const double* s, const double* u, const double* y,
+                         const double* zeta, const double* xi);
+
+/* Device milliseconds accumulated per kernel family since the last reset (CUDA
+ * events on the handle's stream): ms[0] pair sweep, [1] primal, [2] multiplier,
+ * [3] scale detect; launches[0..3] the matching launch counts.  reset != 0 zeroes. */
+ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t reset);
+
+/* Enable (1) / disable (0) per-launch event timing (default off). */
+ca_status ca_set_timing(ca_problem* h, int32_t enable);
+
+/* Enable (1) / disable (0) recording of each pair's final Lemke basis (zmask of
+ * ca_get_pair_state; costs 4 bytes per pair per sweep of extra HBM writes). */
+ca_status ca_set_record_basis(ca_problem* h, int32_t enable);
+
+/* Measured FP64 FMA throughput of the device: a register-resident DFMA loop on all
+ * SMs for ~`ms` milliseconds; *tflops = 2 * FMAs / s / 1e12. */
+ca_status ca_fp64_peak(int device, double ms, double* tflops);
+
+const char* ca_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,77 @@
+"""Build the in-tree C-ABI shared library libca.so for sm_100a (B200).
+
+nvcc cross-compiles here without a GPU.  FP policy: --fmad=false so the compiler
+never contracts a*b+c on its own; every fused multiply-add in the kernels is an
+explicit __fma_rn (reading #18).  IEEE division / sqrt (no fast-math).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libca.so")
+import glob
+SOURCES = [os.path.join(CSRC, "ca_api.cu")] + sorted(glob.glob(os.path.join(CSRC, "ca_sweep_*.cu")))
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("ca_kernels.cuh", "ca_lemke.cuh")] + [
+    os.path.join(ROOT, "include", "ca.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *FLAGS, "-c", "-o", obj, src]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, res
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    log = os.path.join(HERE, "build.log")
+    bad = []
+    with open(log, "w") as f:
+        for src, obj, cmd, res in results:
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            if res.returncode != 0:
+                bad.append((src, res.stderr))
+    if bad:
+        for src, err in bad:
+            sys.stderr.write(f"--- {src}\n{err[-6000:]}")
+        raise RuntimeError(f"nvcc failed (see {log})")
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
+            *[r[1] for r in results], "-cudart", "static"]
+    res = subprocess.run(link, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr)
+        raise RuntimeError("link failed")
+    os.replace(LIB + ".tmp", LIB)
+    if verbose:
+        print(open(log).read()[-3000:])
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

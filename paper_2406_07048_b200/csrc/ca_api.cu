@@ -1,0 +1,806 @@
+// ca_api.cu -- C ABI (include/ca.h) and host orchestration of the sm_100a kernels.
+// Every step of the method runs in the kernels of ca_kernels.cuh; this file only
+// validates input, lays data out in HBM, launches, and copies results back.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ca.h"
+#define CA_COMMON_KERNELS 1
+#include "ca_kernels.cuh"
+
+// the pair-sweep instantiations live in ca_sweep_d2.cu / ca_sweep_d3.cu
+#define CA_EXTERN_SWEEP(D, NM, F) extern template cudaError_t ca::sweep_launch<D, NM, F>(const ca::Dev&, unsigned, cudaStream_t);
+CA_SWEEP_NMAX_LIST(CA_EXTERN_SWEEP, 2, false)
+CA_SWEEP_NMAX_LIST(CA_EXTERN_SWEEP, 2, true)
+CA_SWEEP_NMAX_LIST(CA_EXTERN_SWEEP, 3, false)
+CA_SWEEP_NMAX_LIST(CA_EXTERN_SWEEP, 3, true)
+
+namespace {
+
+thread_local std::string g_err;
+
+ca_status fail(ca_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      return fail(CA_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+    }                                                                                         \
+  } while (0)
+
+constexpr int NMAX_SET[] = {9, 11, 13, 15, 20, 32};
+
+}  // namespace
+
+struct ca_problem {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ca::Dev dev{};
+  int d = 0, B = 0, N = 0, ns = 0, nu = 0, np = 0, M = 0, nmax = 0, nmax_t = 0, rows_max = 0;
+  long long P = 0;
+  std::vector<int> obs_counts;  // per obstacle row counts (shape check on load)
+  std::vector<int> part_off;
+  std::vector<void*> allocs;
+  double* alpha = nullptr;
+  double* slots = nullptr;
+  int slots_cap = 0;
+  double* scene_res = nullptr;  // [B*4] (rdual, rpri, piv, fail) of the last step
+  double* hist_dev = nullptr;
+  int hist_cap = 0;
+  double eps_pri = 0, eps_dual = 0;
+  int max_iters = 100;
+  bool timing = false;
+  double ms[4] = {0, 0, 0, 0};
+  long long launches[4] = {0, 0, 0, 0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> event_pool;
+  bool sticky = false;
+  long long bytes = 0;
+
+  ~ca_problem() {
+    for (void* p : allocs) cudaFree(p);
+    for (auto& e : event_pool) cudaEventDestroy(e);
+    for (auto& pe : pending) {
+      cudaEventDestroy(pe.second.first);
+      cudaEventDestroy(pe.second.second);
+    }
+  }
+  template <class T>
+  ca_status alloc(T** p, size_t count) {
+    void* q = nullptr;
+    size_t nb = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&q, nb);
+    if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? CA_E_OOM : CA_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    allocs.push_back(q);
+    bytes += (long long)nb;
+    *p = static_cast<T*>(q);
+    return CA_OK;
+  }
+  cudaEvent_t ev() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+
+// ------------------------------ validation --------------------------------
+bool spd(const double* Q, int n) {
+  std::vector<double> L(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double s = Q[j * n + j];
+    for (int k = 0; k < j; ++k) s -= L[j * n + k] * L[j * n + k];
+    if (!(s > 0.0)) return false;
+    L[j * n + j] = std::sqrt(s);
+    for (int i = j + 1; i < n; ++i) {
+      double a = Q[i * n + j];
+      for (int k = 0; k < j; ++k) a -= L[i * n + k] * L[j * n + k];
+      L[i * n + j] = a / L[j * n + j];
+    }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      if (std::fabs(Q[i * n + j] - Q[j * n + i]) > 1e-12 * (1 + std::fabs(Q[i * n + j]))) return false;
+  return true;
+}
+
+bool riccati_supported(int ns, int nu) {
+  return (ns == 4 && nu == 2) || (ns == 7 && nu == 4) || (ns == 2 && nu == 1) || (ns == 4 && nu == 1) ||
+         (ns == 6 && nu == 3) || (ns == 3 && nu == 2) || (ns == 4 && nu == 3) || (ns == 6 && nu == 2);
+}
+
+ca_status validate(const ca_problem_desc* D) {
+  if (!D) return fail(CA_E_INVALID, "desc is NULL");
+  if (D->dim != 2 && D->dim != 3) return fail(CA_E_DIM, "dim must be 2 or 3");
+  if (D->n_scenes <= 0 || D->horizon <= 0 || D->n_state <= 0 || D->n_ctrl <= 0 || D->n_parts <= 0 ||
+      D->n_obs < 0)
+    return fail(CA_E_INVALID, "non-positive size");
+  if (!D->part_off || !D->part_A || !D->part_b || !D->dyn_A || !D->dyn_B || !D->dyn_c || !D->Qs || !D->Qu ||
+      !D->s0 || !D->s_ref)
+    return fail(CA_E_INVALID, "NULL input array");
+  if (D->n_obs > 0 && (!D->obs_off || !D->obs_C || !D->obs_d)) return fail(CA_E_INVALID, "NULL obstacle array");
+  if (!(D->sigma > 0.0)) return fail(CA_E_INVALID, "sigma must be > 0");
+  if (D->prox_eps != 0.0) return fail(CA_E_UNSUPPORTED, "prox_eps > 0 (reading #2) is oracle-only in this build");
+  const int d = D->dim;
+  const int pm = D->pose_model;
+  if (pm < 0 || pm > 2) return fail(CA_E_UNSUPPORTED, "unknown pose model");
+  if ((pm == CA_POSE_SE2 && d != 2) || (pm == CA_POSE_TRANS_YAW && d != 3))
+    return fail(CA_E_DIM, "pose model does not match dim");
+  const int npc = (pm == CA_POSE_TRANSLATION) ? d : d + 1;
+  for (int a = 0; a < npc; ++a)
+    if (D->pose_idx[a] < 0 || D->pose_idx[a] >= D->n_state) return fail(CA_E_DIM, "pose index out of range");
+  if (!riccati_supported(D->n_state, D->n_ctrl))
+    return fail(CA_E_UNSUPPORTED, "(n_state, n_ctrl) combination not instantiated");
+  int nrmax = 0;
+  for (int i = 0; i < D->n_parts; ++i) {
+    const int r0 = D->part_off[i], nr = D->part_off[i + 1] - r0;
+    if (nr < d + 1) return fail(CA_E_GEOMETRY, "robot part with fewer than d+1 faces");
+    for (int k = 0; k < nr; ++k)
+      if (!(D->part_b[r0 + k] > 0.0)) return fail(CA_E_GEOMETRY, "robot part b_i must be > 0 (body origin inside)");
+    nrmax = std::max(nrmax, nr);
+  }
+  int nomax = 0;
+  for (long long o = 0; o < (long long)D->n_scenes * D->n_obs; ++o) {
+    const int no = D->obs_off[o + 1] - D->obs_off[o];
+    if (no < d + 1) return fail(CA_E_GEOMETRY, "obstacle with fewer than d+1 faces");
+    nomax = std::max(nomax, no);
+  }
+  if (nrmax + nomax + 1 > 32) return fail(CA_E_DIM, "n = n_r + n_o + 1 > 32");
+  if (!spd(D->Qs, D->n_state) || !spd(D->Qu, D->n_ctrl)) return fail(CA_E_INVALID, "Qs/Qu must be SPD");
+  return CA_OK;
+}
+
+template <class T>
+ca_status h2d(ca_problem* h, T* dst, const T* src, size_t count) {
+  if (count == 0) return CA_OK;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  return CA_OK;
+}
+
+// upload all per-batch inputs and reset the iterate (reading #11)
+ca_status upload(ca_problem* h, const ca_problem_desc* D) {
+  const int d = h->d, B = h->B, N = h->N, ns = h->ns, nu = h->nu;
+  ca::Dev& v = h->dev;
+  // robot rows (a_0, a_1, a_2|0, b)
+  const int prow = D->part_off[h->np];
+  std::vector<double> pr(4 * (size_t)prow, 0.0);
+  for (int r = 0; r < prow; ++r) {
+    for (int a = 0; a < d; ++a) pr[4 * r + a] = D->part_A[r * d + a];
+    pr[4 * r + 3] = D->part_b[r];
+  }
+  const long long orow = (h->M > 0) ? D->obs_off[(long long)B * h->M] : 0;
+  std::vector<double> orr(4 * (size_t)std::max<long long>(orow, 1), 0.0);
+  for (long long r = 0; r < orow; ++r) {
+    for (int a = 0; a < d; ++a) orr[4 * r + a] = D->obs_C[r * d + a];
+    orr[4 * r + 3] = D->obs_d[r];
+  }
+  ca_status st;
+  if ((st = h2d(h, const_cast<double*>(v.part_rows), pr.data(), pr.size()))) return st;
+  if ((st = h2d(h, const_cast<int*>(v.part_off), D->part_off, (size_t)h->np + 1))) return st;
+  if (h->M > 0) {
+    if ((st = h2d(h, const_cast<double*>(v.obs_rows), orr.data(), 4 * (size_t)orow))) return st;
+    if ((st = h2d(h, const_cast<int*>(v.obs_off), D->obs_off, (size_t)B * h->M + 1))) return st;
+  }
+  const long long nd = (long long)(D->dyn_per_scene ? B : 1) * (D->dyn_per_time ? N : 1);
+  if ((st = h2d(h, const_cast<double*>(v.dynA), D->dyn_A, (size_t)nd * ns * ns))) return st;
+  if ((st = h2d(h, const_cast<double*>(v.dynB), D->dyn_B, (size_t)nd * ns * nu))) return st;
+  if ((st = h2d(h, const_cast<double*>(v.dync), D->dyn_c, (size_t)nd * ns))) return st;
+  if ((st = h2d(h, const_cast<double*>(v.Qs), D->Qs, (size_t)ns * ns))) return st;
+  if ((st = h2d(h, const_cast<double*>(v.Qu), D->Qu, (size_t)nu * nu))) return st;
+  if ((st = h2d(h, const_cast<double*>(v.s0), D->s0, (size_t)B * ns))) return st;
+  if ((st = h2d(h, const_cast<double*>(v.sref), D->s_ref, (size_t)B * (N + 1) * ns))) return st;
+  // iterate: s = s_init (default s_ref) with s_0 = s0; u = 0; lambda = 1/sum(b) 1; rest 0
+  std::vector<double> s0v((size_t)B * (N + 1) * ns);
+  const double* si = D->s_init ? D->s_init : D->s_ref;
+  for (int b = 0; b < B; ++b)
+    for (int t = 0; t <= N; ++t)
+      for (int a = 0; a < ns; ++a)
+        s0v[((size_t)b * (N + 1) + t) * ns + a] = (t == 0) ? D->s0[b * ns + a] : si[((size_t)b * (N + 1) + t) * ns + a];
+  if ((st = h2d(h, v.s, s0v.data(), s0v.size()))) return st;
+  CUDA_TRY(cudaMemsetAsync(v.u, 0, sizeof(double) * (size_t)B * N * nu, h->stream));
+  if (h->P > 0) {
+    CUDA_TRY(cudaMemsetAsync(v.y, 0, sizeof(double) * (size_t)h->nmax * h->P, h->stream));
+    CUDA_TRY(cudaMemsetAsync(v.zeta, 0, sizeof(double) * (size_t)h->P, h->stream));
+    CUDA_TRY(cudaMemsetAsync(v.xi, 0, sizeof(double) * (size_t)d * h->P, h->stream));
+    CUDA_TRY(cudaMemsetAsync(v.pst, 0, sizeof(uint32_t) * (size_t)h->P, h->stream));
+    // lambda^0 = 1/sum(b_i) 1 (satisfies b_i^T lambda = 1), mu = gamma = 0
+    const unsigned grid = (unsigned)((h->P + 255) / 256);
+    ca::k_init_y<<<grid, 256, 0, h->stream>>>(h->dev);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+// ------------------------------ launches -----------------------------------
+void t_begin(ca_problem* h, cudaEvent_t* e) {
+  if (h->timing) {
+    *e = h->ev();
+    cudaEventRecord(*e, h->stream);
+  }
+}
+void t_end(ca_problem* h, int fam, cudaEvent_t e0) {
+  h->launches[fam]++;
+  if (h->timing) {
+    cudaEvent_t e1 = h->ev();
+    cudaEventRecord(e1, h->stream);
+    h->pending.push_back({fam, {e0, e1}});
+  }
+}
+ca_status flush_timing(ca_problem* h) {
+  for (auto& pe : h->pending) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventSynchronize(pe.second.second));
+    CUDA_TRY(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
+    h->ms[pe.first] += ms;
+    h->event_pool.push_back(pe.second.first);
+    h->event_pool.push_back(pe.second.second);
+  }
+  h->pending.clear();
+  return CA_OK;
+}
+
+int nmax_template(int nmax) {
+  for (int v : NMAX_SET)
+    if (nmax <= v) return v;
+  return 32;
+}
+
+template <int D, int NM, bool F>
+ca_status launch_sweep_t(ca_problem* h) {
+  const long long grid = (long long)h->B * h->N * h->dev.nchunk;
+  CUDA_TRY((ca::sweep_launch<D, NM, F>(h->dev, (unsigned)grid, h->stream)));
+  return CA_OK;
+}
+
+template <int D, bool F>
+ca_status launch_sweep_d(ca_problem* h) {
+  switch (h->nmax_t) {
+    case 9: return launch_sweep_t<D, 9, F>(h);
+    case 11: return launch_sweep_t<D, 11, F>(h);
+    case 13: return launch_sweep_t<D, 13, F>(h);
+    case 15: return launch_sweep_t<D, 15, F>(h);
+    case 20: return launch_sweep_t<D, 20, F>(h);
+    default: return launch_sweep_t<D, 32, F>(h);
+  }
+}
+
+ca_status launch_sweep(ca_problem* h, bool fused) {
+  if (h->P == 0) return CA_OK;
+  cudaEvent_t e0 = nullptr;
+  t_begin(h, &e0);
+  ca_status st;
+  if (h->d == 2) st = fused ? launch_sweep_d<2, true>(h) : launch_sweep_d<2, false>(h);
+  else st = fused ? launch_sweep_d<3, true>(h) : launch_sweep_d<3, false>(h);
+  t_end(h, 0, e0);
+  return st;
+}
+
+template <int NS, int NU>
+ca_status launch_riccati_t(ca_problem* h, double* cur, double* prev) {
+  const int thr = 64;
+  ca::k_riccati<NS, NU><<<(h->B + thr - 1) / thr, thr, 0, h->stream>>>(h->dev, cur, prev);
+  CUDA_TRY(cudaGetLastError());
+  return CA_OK;
+}
+
+ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
+  cudaEvent_t e0 = nullptr;
+  t_begin(h, &e0);
+  ca_status st;
+  const int ns = h->ns, nu = h->nu;
+  if (ns == 4 && nu == 2) st = launch_riccati_t<4, 2>(h, cur, prev);
+  else if (ns == 7 && nu == 4) st = launch_riccati_t<7, 4>(h, cur, prev);
+  else if (ns == 2 && nu == 1) st = launch_riccati_t<2, 1>(h, cur, prev);
+  else if (ns == 4 && nu == 1) st = launch_riccati_t<4, 1>(h, cur, prev);
+  else if (ns == 6 && nu == 3) st = launch_riccati_t<6, 3>(h, cur, prev);
+  else if (ns == 3 && nu == 2) st = launch_riccati_t<3, 2>(h, cur, prev);
+  else if (ns == 4 && nu == 3) st = launch_riccati_t<4, 3>(h, cur, prev);
+  else st = launch_riccati_t<6, 2>(h, cur, prev);
+  t_end(h, 1, e0);
+  return st;
+}
+
+ca_status launch_mult(ca_problem* h) {
+  if (h->P == 0) return CA_OK;
+  cudaEvent_t e0 = nullptr;
+  t_begin(h, &e0);
+  const long long grid = (long long)h->B * h->N * h->dev.nchunk;
+  if (h->d == 2) ca::k_mult<2><<<(unsigned)grid, ca::CTA, 0, h->stream>>>(h->dev);
+  else ca::k_mult<3><<<(unsigned)grid, ca::CTA, 0, h->stream>>>(h->dev);
+  CUDA_TRY(cudaGetLastError());
+  t_end(h, 2, e0);
+  return CA_OK;
+}
+
+ca_status launch_collect(ca_problem* h, double* dst, int mask) {
+  if (h->P == 0) {
+    CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * 4 * h->B, h->stream));
+    return CA_OK;
+  }
+  ca::k_collect<<<(h->B + 127) / 128, 128, 0, h->stream>>>(h->dev, dst, mask);
+  CUDA_TRY(cudaGetLastError());
+  return CA_OK;
+}
+
+ca_status ensure_slots(ca_problem* h, int n) {
+  if (n <= h->slots_cap) return CA_OK;
+  ca_status st;
+  if ((st = h->alloc(&h->slots, (size_t)n * h->B * 4))) return st;
+  if ((st = h->alloc(&h->hist_dev, (size_t)n * 4))) return st;
+  h->slots_cap = n;
+  return CA_OK;
+}
+
+ca_status sums(ca_problem* h, const double* dst_dev, ca_residuals* out) {
+  std::vector<double> v((size_t)h->B * 4);
+  CUDA_TRY(cudaMemcpyAsync(v.data(), dst_dev, sizeof(double) * v.size(), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ca_residuals r{};
+  for (int b = 0; b < h->B; ++b) {
+    r.r_dual += v[b * 4 + 0];
+    r.r_pri += v[b * 4 + 1];
+    r.pivots += (int64_t)v[b * 4 + 2];
+    r.n_fail += (int64_t)v[b * 4 + 3];
+  }
+  r.n_pairs = h->P;
+  if (out) *out = r;
+  return CA_OK;
+}
+
+ca_status check_handle(ca_problem* h) {
+  if (!h) return fail(CA_E_INVALID, "NULL handle");
+  if (h->sticky) return fail(CA_E_CUDA, "handle unusable after an earlier CUDA error");
+  if (cudaSetDevice(h->device) != cudaSuccess) return fail(CA_E_CUDA, "cudaSetDevice failed");
+  return CA_OK;
+}
+
+ca_status mark(ca_problem* h, ca_status st) {
+  if (st == CA_E_CUDA) h->sticky = true;
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ca_last_error(void) { return g_err.c_str(); }
+
+ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, ca_problem** out) {
+  if (!out) return fail(CA_E_INVALID, "out is NULL");
+  *out = nullptr;
+  ca_status st = validate(D);
+  if (st) return st;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
+    return fail(CA_E_CUDA, "no CUDA device (this library has no CPU fallback)");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(CA_E_CUDA, "built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
+  CUDA_TRY(cudaSetDevice(device));
+  ca_problem* h = new ca_problem();
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(stream);
+  h->d = D->dim;
+  h->B = D->n_scenes;
+  h->N = D->horizon;
+  h->ns = D->n_state;
+  h->nu = D->n_ctrl;
+  h->np = D->n_parts;
+  h->M = D->n_obs;
+  h->part_off.assign(D->part_off, D->part_off + h->np + 1);
+  int nrmax = 0, nomax = 0;
+  for (int i = 0; i < h->np; ++i) nrmax = std::max(nrmax, D->part_off[i + 1] - D->part_off[i]);
+  h->obs_counts.resize((size_t)h->B * h->M);
+  for (long long o = 0; o < (long long)h->B * h->M; ++o) {
+    h->obs_counts[o] = D->obs_off[o + 1] - D->obs_off[o];
+    nomax = std::max(nomax, h->obs_counts[o]);
+  }
+  h->nmax = (h->M > 0) ? nrmax + nomax + 1 : 1;
+  h->nmax_t = nmax_template(h->nmax);
+  h->rows_max = nrmax + nomax;
+  h->P = (long long)h->B * h->N * h->np * h->M;
+  ca::Dev& v = h->dev;
+  v.d = h->d; v.B = h->B; v.N = h->N; v.ns = h->ns; v.nu = h->nu; v.np = h->np; v.M = h->M;
+  v.pose_model = D->pose_model;
+  v.npc = (D->pose_model == CA_POSE_TRANSLATION) ? h->d : h->d + 1;
+  for (int a = 0; a < 4; ++a) v.pidx[a] = D->pose_idx[a];
+  v.dyn_ps = D->dyn_per_scene ? 1 : 0;
+  v.dyn_pt = D->dyn_per_time ? 1 : 0;
+  v.sigma = D->sigma;
+  v.lp.pivot_tol = D->lemke_pivot_tol > 0 ? D->lemke_pivot_tol : 1e-11;
+  v.lp.tie_tol = D->lemke_tie_tol > 0 ? D->lemke_tie_tol : 1e-9;
+  v.lp.max_pivot_factor = D->lemke_max_pivot_factor > 0 ? D->lemke_max_pivot_factor : 50;
+  v.ny = h->nmax;
+  v.P = h->P;
+  v.G = h->np * h->M;
+  v.nchunk = std::max(1, (v.G + ca::CTA - 1) / ca::CTA);
+  v.CH = std::max(1, (v.G + v.nchunk - 1) / v.nchunk);
+  h->eps_pri = D->eps_pri;
+  h->eps_dual = D->eps_dual;
+  h->max_iters = D->max_iters > 0 ? D->max_iters : 100;
+  const int d = h->d, B = h->B, N = h->N, ns = h->ns, nu = h->nu;
+  const long long nd = (long long)(D->dyn_per_scene ? B : 1) * (D->dyn_per_time ? N : 1);
+  const long long orow = (h->M > 0) ? D->obs_off[(long long)B * h->M] : 0;
+#define AL(ptr, T, cnt)                                  \
+  do {                                                   \
+    T* tmp_ = nullptr;                                   \
+    if ((st = h->alloc(&tmp_, (size_t)(cnt)))) {         \
+      delete h;                                          \
+      return st;                                         \
+    }                                                    \
+    ptr = tmp_;                                          \
+  } while (0)
+  AL(v.part_rows, double, 4 * (size_t)D->part_off[h->np]);
+  AL(v.part_off, int, h->np + 1);
+  AL(v.obs_rows, double, 4 * (size_t)std::max<long long>(orow, 1));
+  AL(v.obs_off, int, (size_t)B * h->M + 1);
+  AL(v.dynA, double, nd * ns * ns);
+  AL(v.dynB, double, nd * ns * nu);
+  AL(v.dync, double, nd * ns);
+  AL(v.Qs, double, ns * ns);
+  AL(v.Qu, double, nu * nu);
+  AL(v.s0, double, (size_t)B * ns);
+  AL(v.sref, double, (size_t)B * (N + 1) * ns);
+  AL(v.s, double, (size_t)B * (N + 1) * ns);
+  AL(v.u, double, (size_t)B * N * nu);
+  AL(v.y, double, (size_t)h->nmax * std::max<long long>(h->P, 1));
+  AL(v.zeta, double, std::max<long long>(h->P, 1));
+  AL(v.xi, double, (size_t)d * std::max<long long>(h->P, 1));
+  AL(v.pst, uint32_t, std::max<long long>(h->P, 1));
+  AL(v.agg, double, (size_t)B * N * v.nchunk * ca::REC);
+  AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
+  AL(h->scene_res, double, (size_t)B * 4);
+#undef AL
+  v.zmask = nullptr;
+  if ((st = upload(h, D))) {
+    delete h;
+    return st;
+  }
+  *out = h;
+  return CA_OK;
+}
+
+void ca_problem_destroy(ca_problem* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  delete h;
+}
+
+ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* D) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if ((st = validate(D))) return st;
+  if (D->dim != h->d || D->n_scenes != h->B || D->horizon != h->N || D->n_state != h->ns ||
+      D->n_ctrl != h->nu || D->n_parts != h->np || D->n_obs != h->M)
+    return fail(CA_E_INVALID, "ca_problem_load: shapes differ from the handle");
+  for (int i = 0; i <= h->np; ++i)
+    if (D->part_off[i] != h->part_off[i]) return fail(CA_E_INVALID, "ca_problem_load: robot part rows differ");
+  for (long long o = 0; o < (long long)h->B * h->M; ++o)
+    if (D->obs_off[o + 1] - D->obs_off[o] != h->obs_counts[o])
+      return fail(CA_E_INVALID, "ca_problem_load: obstacle row counts differ");
+  return mark(h, upload(h, D));
+}
+
+ca_status ca_problem_info(const ca_problem* h, int64_t* n_pairs, int32_t* ny, int64_t* device_bytes) {
+  if (!h) return fail(CA_E_INVALID, "NULL handle");
+  if (n_pairs) *n_pairs = h->P;
+  if (ny) *ny = h->nmax;
+  if (device_bytes) *device_bytes = h->bytes;
+  return CA_OK;
+}
+
+ca_status ca_set_timing(ca_problem* h, int32_t enable) {
+  if (!h) return fail(CA_E_INVALID, "NULL handle");
+  h->timing = enable != 0;
+  return CA_OK;
+}
+
+ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t reset) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if ((st = flush_timing(h))) return mark(h, st);
+  for (int f = 0; f < 4; ++f) {
+    if (ms) ms[f] = h->ms[f];
+    if (launches) launches[f] = h->launches[f];
+    if (reset) {
+      h->ms[f] = 0;
+      h->launches[f] = 0;
+    }
+  }
+  return CA_OK;
+}
+
+ca_status ca_set_record_basis(ca_problem* h, int32_t enable) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (enable && !h->dev.zmask) {
+    uint32_t* z = nullptr;
+    if ((st = h->alloc(&z, std::max<long long>(h->P, 1)))) return st;
+    CUDA_TRY(cudaMemsetAsync(z, 0, sizeof(uint32_t) * std::max<long long>(h->P, 1), h->stream));
+    h->dev.zmask = z;
+  } else if (!enable) {
+    h->dev.zmask = nullptr;
+  }
+  return CA_OK;
+}
+
+ca_status ca_dual_sweep(ca_problem* h, ca_residuals* out) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if ((st = launch_sweep(h, false))) return mark(h, st);
+  if ((st = launch_collect(h, h->scene_res, 1 | 4 | 8))) return mark(h, st);
+  ca_residuals r{};
+  if ((st = sums(h, h->scene_res, &r))) return mark(h, st);
+  r.r_pri = 0.0;
+  if (out) *out = r;
+  return r.n_fail ? CA_W_PAIR_FAILURES : CA_OK;
+}
+
+ca_status ca_primal_step(ca_problem* h) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if ((st = launch_riccati(h, nullptr, nullptr))) return mark(h, st);
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+ca_status ca_multiplier_update(ca_problem* h, ca_residuals* out) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if ((st = launch_mult(h))) return mark(h, st);
+  if ((st = launch_collect(h, h->scene_res, 2))) return mark(h, st);
+  ca_residuals r{};
+  if ((st = sums(h, h->scene_res, &r))) return mark(h, st);
+  if (out) {
+    out->r_pri = r.r_pri;
+    out->n_pairs = h->P;
+  }
+  return CA_OK;
+}
+
+ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (iters <= 0) return fail(CA_E_INVALID, "iters must be > 0");
+  if ((st = ensure_slots(h, iters))) return mark(h, st);
+  CUDA_TRY(cudaMemsetAsync(h->slots, 0, sizeof(double) * (size_t)iters * h->B * 4, h->stream));
+  for (int it = 0; it < iters; ++it) {
+    if ((st = launch_sweep(h, it > 0))) return mark(h, st);
+    double* cur = h->slots + (size_t)it * h->B * 4;
+    double* prev = it > 0 ? h->slots + (size_t)(it - 1) * h->B * 4 : nullptr;
+    if ((st = launch_riccati(h, cur, prev))) return mark(h, st);
+  }
+  if ((st = launch_mult(h))) return mark(h, st);
+  double* last = h->slots + (size_t)(iters - 1) * h->B * 4;
+  if ((st = launch_collect(h, last, 2))) return mark(h, st);
+  CUDA_TRY(cudaMemcpyAsync(h->scene_res, last, sizeof(double) * h->B * 4, cudaMemcpyDeviceToDevice, h->stream));
+  int64_t fails = 0;
+  if (hist) {
+    ca::k_hist<<<iters, 256, 0, h->stream>>>(h->slots, h->B, iters, h->hist_dev);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<double> hv((size_t)iters * 4);
+    CUDA_TRY(cudaMemcpyAsync(hv.data(), h->hist_dev, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (int k = 0; k < iters; ++k) {
+      hist[k].r_dual = hv[k * 4 + 0];
+      hist[k].r_pri = hv[k * 4 + 1];
+      hist[k].pivots = (int64_t)hv[k * 4 + 2];
+      hist[k].n_fail = (int64_t)hv[k * 4 + 3];
+      hist[k].n_pairs = h->P;
+      fails += hist[k].n_fail;
+    }
+  } else {
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  return fails ? CA_W_PAIR_FAILURES : CA_OK;
+}
+
+ca_status ca_admm_solve(ca_problem* h, ca_solve_report* out) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  const double pairs_per_scene = (double)h->N * h->np * h->M;
+  const double ep = h->eps_pri > 0 ? h->eps_pri : 1e-3 * std::max(1.0, pairs_per_scene);
+  const double ed = h->eps_dual > 0 ? h->eps_dual : 1e-3 * std::max(1.0, pairs_per_scene);
+  ca_solve_report rep{};
+  std::vector<double> v((size_t)h->B * 4);
+  for (int k = 0; k < h->max_iters; ++k) {
+    ca_residuals r{};
+    st = ca_admm_iterate(h, 1, &r);
+    if (st < 0) return st;
+    rep.iterations = k + 1;
+    rep.last = r;
+    CUDA_TRY(cudaMemcpy(v.data(), h->scene_res, sizeof(double) * v.size(), cudaMemcpyDeviceToHost));
+    bool all = true;
+    for (int b = 0; b < h->B && all; ++b) all = (v[b * 4 + 1] <= ep) && (v[b * 4 + 0] <= ed);  // Eq. 18 '<='
+    if (all) {
+      rep.converged = 1;
+      break;
+    }
+  }
+  if (out) *out = rep;
+  return rep.converged ? CA_OK : CA_W_NOT_CONVERGED;
+}
+
+ca_status ca_get_scene_residuals(ca_problem* h, double* r_pri, double* r_dual) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  std::vector<double> v((size_t)h->B * 4);
+  CUDA_TRY(cudaMemcpyAsync(v.data(), h->scene_res, sizeof(double) * v.size(), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (int b = 0; b < h->B; ++b) {
+    if (r_pri) r_pri[b] = v[b * 4 + 1];
+    if (r_dual) r_dual[b] = v[b * 4 + 0];
+  }
+  return CA_OK;
+}
+
+ca_status ca_get_trajectory(ca_problem* h, double* s, double* u) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (s) CUDA_TRY(cudaMemcpyAsync(s, h->dev.s, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns, cudaMemcpyDeviceToHost, h->stream));
+  if (u) CUDA_TRY(cudaMemcpyAsync(u, h->dev.u, sizeof(double) * (size_t)h->B * h->N * h->nu, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+ca_status ca_get_pair_state(ca_problem* h, int64_t p0, int64_t count, double* y, double* zeta, double* xi,
+                            int32_t* pivots, int32_t* status, uint32_t* zmask) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (p0 < 0 || count < 0 || p0 + count > h->P) return fail(CA_E_INVALID, "pair range out of bounds");
+  if (count == 0) return CA_OK;
+  const int ny = h->nmax, d = h->d;
+  std::vector<double> tmp((size_t)count);
+  if (y) {
+    for (int k = 0; k < ny; ++k) {
+      CUDA_TRY(cudaMemcpyAsync(tmp.data(), h->dev.y + (size_t)k * h->P + p0, sizeof(double) * count, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+      for (int64_t q = 0; q < count; ++q) y[q * ny + k] = tmp[q];
+    }
+  }
+  if (zeta) CUDA_TRY(cudaMemcpyAsync(zeta, h->dev.zeta + p0, sizeof(double) * count, cudaMemcpyDeviceToHost, h->stream));
+  if (xi) {
+    for (int a = 0; a < d; ++a) {
+      CUDA_TRY(cudaMemcpyAsync(tmp.data(), h->dev.xi + (size_t)a * h->P + p0, sizeof(double) * count, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+      for (int64_t q = 0; q < count; ++q) xi[q * d + a] = tmp[q];
+    }
+  }
+  if (pivots || status) {
+    std::vector<uint32_t> ps((size_t)count);
+    CUDA_TRY(cudaMemcpyAsync(ps.data(), h->dev.pst + p0, sizeof(uint32_t) * count, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (int64_t q = 0; q < count; ++q) {
+      if (pivots) pivots[q] = (int32_t)(ps[q] & 0xffffu);
+      if (status) status[q] = (int32_t)(ps[q] >> 16);
+    }
+  }
+  if (zmask) {
+    if (!h->dev.zmask) return fail(CA_E_INVALID, "basis recording is off (ca_set_record_basis)");
+    CUDA_TRY(cudaMemcpyAsync(zmask, h->dev.zmask + p0, sizeof(uint32_t) * count, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+ca_status ca_set_iterate(ca_problem* h, const double* s, const double* u, const double* y, const double* zeta,
+                         const double* xi) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  const int ny = h->nmax, d = h->d;
+  if (s) CUDA_TRY(cudaMemcpyAsync(h->dev.s, s, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns, cudaMemcpyHostToDevice, h->stream));
+  if (u) CUDA_TRY(cudaMemcpyAsync(h->dev.u, u, sizeof(double) * (size_t)h->B * h->N * h->nu, cudaMemcpyHostToDevice, h->stream));
+  if (zeta && h->P) CUDA_TRY(cudaMemcpyAsync(h->dev.zeta, zeta, sizeof(double) * h->P, cudaMemcpyHostToDevice, h->stream));
+  std::vector<double> tmp;
+  if (y && h->P) {
+    tmp.resize((size_t)h->P);
+    for (int k = 0; k < ny; ++k) {
+      for (long long q = 0; q < h->P; ++q) tmp[q] = y[q * ny + k];
+      CUDA_TRY(cudaMemcpyAsync(h->dev.y + (size_t)k * h->P, tmp.data(), sizeof(double) * h->P, cudaMemcpyHostToDevice, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+  }
+  if (xi && h->P) {
+    tmp.resize((size_t)h->P);
+    for (int a = 0; a < d; ++a) {
+      for (long long q = 0; q < h->P; ++q) tmp[q] = xi[q * d + a];
+      CUDA_TRY(cudaMemcpyAsync(h->dev.xi + (size_t)a * h->P, tmp.data(), sizeof(double) * h->P, cudaMemcpyHostToDevice, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, double* min_alpha) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (h->P == 0) {
+    if (min_alpha)
+      for (int b = 0; b < h->B; ++b) min_alpha[b] = INFINITY;
+    return CA_OK;
+  }
+  if (!h->alpha) {
+    if ((st = h->alloc(&h->alpha, (size_t)h->P + h->B))) return st;
+  }
+  const double* sd = h->dev.s;
+  double* tmp_states = nullptr;
+  if (states) {
+    if ((st = h->alloc(&tmp_states, (size_t)h->B * (h->N + 1) * h->ns))) return st;
+    CUDA_TRY(cudaMemcpyAsync(tmp_states, states, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns, cudaMemcpyHostToDevice, h->stream));
+    sd = tmp_states;
+  }
+  cudaEvent_t e0 = nullptr;
+  t_begin(h, &e0);
+  const size_t sm = sizeof(double) * (size_t)ca::CTA * h->rows_max * (h->d + 2);
+  const long long grid = (long long)h->B * h->N * h->dev.nchunk;
+  if (h->d == 2) {
+    CUDA_TRY(cudaFuncSetAttribute(ca::k_scale<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ca::k_scale<2><<<(unsigned)grid, ca::CTA, sm, h->stream>>>(h->dev, sd, h->alpha);
+  } else {
+    CUDA_TRY(cudaFuncSetAttribute(ca::k_scale<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ca::k_scale<3><<<(unsigned)grid, ca::CTA, sm, h->stream>>>(h->dev, sd, h->alpha);
+  }
+  CUDA_TRY(cudaGetLastError());
+  ca::k_scene_min<<<h->B, 256, 0, h->stream>>>(h->alpha, h->P / h->B, h->alpha + h->P);
+  CUDA_TRY(cudaGetLastError());
+  t_end(h, 3, e0);
+  if (alpha) CUDA_TRY(cudaMemcpyAsync(alpha, h->alpha, sizeof(double) * h->P, cudaMemcpyDeviceToHost, h->stream));
+  if (min_alpha) CUDA_TRY(cudaMemcpyAsync(min_alpha, h->alpha + h->P, sizeof(double) * h->B, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (tmp_states) {
+    cudaFree(tmp_states);
+    h->allocs.erase(std::remove(h->allocs.begin(), h->allocs.end(), (void*)tmp_states), h->allocs.end());
+  }
+  return CA_OK;
+}
+
+ca_status ca_fp64_peak(int device, double ms_target, double* tflops) {
+  if (!tflops) return fail(CA_E_INVALID, "tflops is NULL");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  double* out = nullptr;
+  CUDA_TRY(cudaMalloc(&out, sizeof(double)));
+  const int blocks = prop.multiProcessorCount * 8, threads = 256;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  long long iters = 1000;
+  float ms = 0.f;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(a);
+    ca::k_dfma<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(b);
+    CUDA_TRY(cudaEventSynchronize(b));
+    CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+    if (ms >= 0.5 * ms_target) break;
+    iters = (long long)(iters * std::min(50.0, std::max(2.0, ms_target / std::max(ms, 1e-3f))));
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  const double fmas = (double)blocks * threads * iters * 32.0;
+  *tflops = 2.0 * fmas / (ms * 1e-3) / 1e12;
+  return CA_OK;
+}
+
+}  // extern "C"

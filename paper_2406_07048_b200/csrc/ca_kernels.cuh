@@ -1,0 +1,870 @@
+// ca_kernels.cuh -- sm_100a FP64 kernels of the ADMM hot path (arXiv 2406.07048).
+//
+//   k_sweep<D,NMAX,FUSED>  ADMM step 1 (Eq. 15) for one pair per thread:
+//                          [FUSED: step 3 of the previous iteration, Eq. 17, first]
+//                          Eq. 19 build -> Eqs. 20-21 elimination -> Eq. 24 LCP ->
+//                          revised Lemke (ca_lemke.cuh) -> y recovery,
+//                          dual-residual partial (Eq. 18b) and the Gauss-Newton
+//                          aggregates of step 2, reduced per (scene, t, chunk).
+//   k_riccati<NS,NU>       ADMM step 2 (Eq. 16, one SQP QP)
+//                          as a Riccati recursion per scene.
+//   k_mult<D>              ADMM step 3 (Eq. 17) standalone + r_pri.
+//   k_scale<D>             Eq. 3 scale LP per pair (vertex enumeration).
+//   k_collect / k_scene_min / k_hist  small deterministic reductions.
+//   k_dfma                 FP64 FMA peak microbenchmark.
+// No floating-point atomics anywhere: every reduction has a fixed order, so results
+// are bitwise reproducible run to run.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ca_lemke.cuh"
+
+namespace ca {
+
+constexpr int REC = 20;  // per (scene, t, chunk) record
+constexpr int R_RDUAL = 16, R_RPRI = 17, R_PIV = 18, R_FAIL = 19;
+constexpr int CTA = 128;  // threads per pair-sweep CTA
+
+struct Dev {
+  int d, B, N, ns, nu, np, M, pose_model, npc;
+  int pidx[4];
+  const int* part_off;
+  const double* part_rows;  // [rows][4] = (a_0, a_1, a_2, b)
+  const int* obs_off;
+  const double* obs_rows;  // [rows][4] = (c_0, c_1, c_2, d)
+  int dyn_ps, dyn_pt;
+  const double *dynA, *dynB, *dync, *Qs, *Qu, *s0, *sref;
+  double sigma;
+  LemkeParams lp;
+  int ny;
+  long long P;
+  int G, CH, nchunk;
+  double *s, *u, *y, *zeta, *xi;
+  uint32_t* pst;
+  uint32_t* zmask;
+  double* agg;
+  double* ric;
+};
+
+__device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* R, double* rho) {
+  const int d = P.d;
+  for (int a = 0; a < d; ++a)
+    for (int c = 0; c < d; ++c) R[a * d + c] = (a == c) ? 1.0 : 0.0;
+  for (int a = 0; a < d; ++a) rho[a] = st[P.pidx[a]];
+  if (P.pose_model == 1) {
+    double sn, cs;
+    sincos(st[P.pidx[2]], &sn, &cs);
+    R[0] = cs; R[1] = -sn; R[2] = sn; R[3] = cs;
+  } else if (P.pose_model == 2) {
+    double sn, cs;
+    sincos(st[P.pidx[3]], &sn, &cs);
+    R[0] = cs; R[1] = -sn; R[3] = sn; R[4] = cs;
+  }
+}
+
+__device__ __forceinline__ int sym_idx(int a, int c, int npc) { return a * npc - a * (a - 1) / 2 + (c - a); }
+
+// deterministic CTA sum of `nf` fields starting at rec[f0]; thread 0 gets totals
+template <int NF>
+__device__ __forceinline__ void cta_sum(double* rec, double* red /* smem [NF][CTA/32] */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    double v = rec[f];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[f * 32 + w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      double acc = 0.0;
+      for (int k = 0; k < nw; ++k) acc += red[f * 32 + k];
+      rec[f] = acc;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// ADMM step 1 (+ fused step 3 of the previous iteration)
+// ----------------------------------------------------------------------------
+template <int D, int NMAX, bool FUSED>
+__global__ void __launch_bounds__(CTA) k_sweep(Dev P) {
+  extern __shared__ double smem[];
+  __shared__ double sR[9], srho[3], red[REC * 32];
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x % P.nchunk;
+  const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
+  const int b = bt / P.N, t = bt % P.N + 1;
+  if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
+  __syncthreads();
+  constexpr int MMAX = D + 4;
+  Rows<D> W{smem + tid, CTA};
+  double* Gs = smem + NMAX * (D + 2) * CTA + tid;
+  double rec[REC];
+#pragma unroll
+  for (int f = 0; f < REC; ++f) rec[f] = 0.0;
+  const int g = chunk * P.CH + tid;
+  if (tid < P.CH && g < P.G) {
+    const long long p = (long long)bt * P.G + g;
+    const long long PP = P.P;
+    const int i = g / P.M, j = g % P.M;
+    const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
+    const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
+    const int n = nr + no + 1;
+    const double* prow = P.part_rows + 4 * r0;
+    const double* orow = P.obs_rows + 4 * (long long)l0;
+    // e = argmax_k b_k, lowest k on ties (reading #3)
+    int e = 0;
+    double be = __ldg(prow + 3);
+    for (int k = 1; k < nr; ++k) {
+      const double bk = __ldg(prow + 4 * k + 3);
+      if (bk > be) { be = bk; e = k; }
+    }
+    double ae[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) ae[a] = __ldg(prow + 4 * e + a);
+    // y^k (SoA planes), zeta, xi
+    double yk[NMAX];
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k) yk[k] = (k < n) ? P.y[(long long)k * PP + p] : 0.0;
+    double zeta = P.zeta[p], xi[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
+    // K rows of the obstacle at pose(s^k) (Eq. 19b): (d_l - c_l.rho, R^T c_l); LCP index nr-1+l
+    for (int lo = 0; lo < no; ++lo) {
+      const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);
+      const double c[3] = {cr.x, cr.y, cr.z};
+      const double dl = cr.w;
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc = __fma_rn(c[a], srho[a], acc);
+      const int u = nr - 1 + lo;
+      W.setF(u, 0, dl - acc);
+#pragma unroll
+      for (int mm = 0; mm < D; ++mm) {
+        double r = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) r = __fma_rn(c[a], sR[a * D + mm], r);
+        W.setF(u, 1 + mm, r);
+      }
+      W.setk(u, 0.0);
+    }
+    if (FUSED) {
+      // Eq. 17 for the previous iteration at s^k with y^k (Eqs. 10-11):
+      //   T = 1 + sum mu_l (d_l - c_l.rho) + gamma,  R = A^T lambda + (C R)^T mu
+      double Tv = 1.0, Rv[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) Rv[a] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k) {
+        if (k < nr) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yk[k], __ldg(prow + 4 * k + a), Rv[a]);
+        } else if (k < nr + no) {
+          const int u = k - 1;
+          Tv = __fma_rn(yk[k], W.F(u, 0), Tv);
+#pragma unroll
+          for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yk[k], W.F(u, 1 + a), Rv[a]);
+        } else if (k == nr + no) {
+          Tv += yk[k];
+        }
+      }
+      zeta += Tv;
+      double r2 = Tv * Tv;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        xi[a] += Rv[a];
+        r2 = __fma_rn(Rv[a], Rv[a], r2);
+      }
+      rec[R_RPRI] = r2;
+      P.zeta[p] = zeta;
+#pragma unroll
+      for (int a = 0; a < D; ++a) P.xi[(long long)a * PP + p] = xi[a];
+    }
+    // Eqs. 20-21: lambda rows k != e, ratio = b_k / b_e
+    for (int k = 0; k < nr; ++k) {
+      if (k == e) continue;
+      const int u = k - (k > e);
+      const double ratio = __ldg(prow + 4 * k + 3) / be;
+      W.setF(u, 0, __fma_rn(-ratio, 0.0, 0.0));
+#pragma unroll
+      for (int a = 0; a < D; ++a) W.setF(u, 1 + a, __fma_rn(-ratio, ae[a], __ldg(prow + 4 * k + a)));
+      W.setk(u, ratio);
+    }
+    {  // gamma row (1, 0): ratio 0; phi row: zeros
+      const int u = n - 2;
+      W.setF(u, 0, 1.0);
+#pragma unroll
+      for (int a = 0; a < D; ++a) W.setF(u, 1 + a, 0.0);
+      W.setk(u, 0.0);
+#pragma unroll
+      for (int c = 0; c <= D; ++c) W.setF(n - 1, c, 0.0);
+      W.setk(n - 1, 0.0);
+    }
+    // btil = bvec + K_e / b_e, etatil = 1 / b_e;  q = [Ktil btil; etatil] (Eq. 25)
+    double bt_[D + 1];
+    bt_[0] = (1.0 + zeta) + 0.0 / be;
+#pragma unroll
+    for (int a = 0; a < D; ++a) bt_[1 + a] = xi[a] + ae[a] / be;
+    double q[NMAX];
+#pragma unroll
+    for (int u = 0; u < NMAX; ++u) {
+      q[u] = 0.0;
+      if (u < n - 1) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c <= D; ++c) acc = __fma_rn(W.F(u, c), bt_[c], acc);
+        q[u] = acc;
+      } else if (u == n - 1) {
+        q[u] = 1.0 / be;
+      }
+    }
+    Lemke<D, NMAX> L;
+    L.solve(W, Gs, CTA, q, n, P.lp);
+    double zU[NMAX];
+    L.solution(zU);
+    // recovery: y_U = z[0..n-2], y_e = (1 - sum_{k != e} b_k lambda_k) / b_e
+    double ynew[NMAX];
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k) {
+      double v = 0.0;
+      if (k < n) {
+        if (k < e) v = zU[k];
+        else if (k > e) v = zU[k - 1];
+      }
+      ynew[k] = v;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k)
+      if (k < nr && k != e) acc = __fma_rn(__ldg(prow + 4 * k + 3), ynew[k], acc);
+    const double ye = (1.0 - acc) / be;
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k)
+      if (k == e) ynew[k] = ye;
+    int st = L.status;
+    if (st == ST_OK && ye < -1e-6) st = ST_NEGYE;
+    const bool solved = (st == ST_OK);
+    if (st == ST_OK) {
+      double rd = 0.0;
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k) {
+        if (k < nr + no) {
+          const double df = ynew[k] - yk[k];
+          rd = __fma_rn(df, df, rd);
+        }
+        if (k < n) P.y[(long long)k * PP + p] = ynew[k];
+      }
+      rec[R_RDUAL] = rd;
+
+    } else {
+      rec[R_FAIL] = 1.0;
+    }
+    rec[R_PIV] = (double)L.pivots;
+    P.pst[p] = (uint32_t)min(L.pivots, 65535) | ((uint32_t)st << 16);
+    if (P.zmask) P.zmask[p] = L.zmask();
+    // Gauss-Newton aggregates at pose(s^k) (step 2 data):
+    //   u* = K^T y + bvec = (eT, eR);  v = C_j^T mu;  gth = J^T R^T v
+    double eT = (1.0 + zeta), eR[D], v[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) { eR[a] = xi[a]; v[a] = 0.0; }
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k) {
+      const double yv = solved ? ynew[k] : yk[k];
+      if (k < nr) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, __ldg(prow + 4 * k + a), eR[a]);
+      } else if (k < nr + no) {
+        const int u = k - 1;
+        eT = __fma_rn(yv, W.F(u, 0), eT);
+#pragma unroll
+        for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, W.F(u, 1 + a), eR[a]);
+        const double* cr = orow + 4 * (k - nr);
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = __fma_rn(yv, __ldg(cr + a), v[a]);
+      } else if (k == nr + no) {
+        eT += yv;
+      }
+    }
+    // record layout always reserves D+1 pose coordinates (compile-time offsets)
+    constexpr int L1 = D + 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int c = a; c < D; ++c) rec[sym_idx(a, c, L1)] = v[a] * v[c];
+      rec[L1 * (L1 + 1) / 2 + a] = -eT * v[a];
+    }
+    if (P.pose_model != 0) {
+      // w = R^T v; gth = J^T w = (w_1, -w_0, 0)
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        w0 = __fma_rn(sR[c * D + 0], v[c], w0);
+        w1 = __fma_rn(sR[c * D + 1], v[c], w1);
+      }
+      const double g0 = w1, g1 = -w0;
+      rec[sym_idx(D, D, L1)] = g0 * g0 + g1 * g1;
+      rec[L1 * (L1 + 1) / 2 + D] = g0 * eR[0] + g1 * eR[1];
+    }
+  }
+  cta_sum<REC>(rec, red);
+  if (tid == 0) {
+    double* out = P.agg + (long long)blockIdx.x * REC;
+#pragma unroll
+    for (int f = 0; f < REC; ++f) out[f] = rec[f];
+  }
+}
+
+inline size_t sweep_smem_bytes(int d, int nmaxt) {
+  const int mmax = d + 4;
+  return sizeof(double) * (size_t)CTA * ((size_t)nmaxt * (d + 2) + (size_t)mmax * (mmax + 1));
+}
+
+// host-side launcher; explicitly instantiated in ca_sweep_d{2,3}.cu (parallel build)
+template <int D, int NM, bool F>
+cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
+  static bool configured = false;
+  const size_t sm = sweep_smem_bytes(D, NM);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_sweep<D, NM, F><<<grid, CTA, sm, stream>>>(P);
+  return cudaGetLastError();
+}
+
+#define CA_SWEEP_NMAX_LIST(X, D, F) X(D, 9, F) X(D, 11, F) X(D, 13, F) X(D, 15, F) X(D, 20, F) X(D, 32, F)
+
+// ----------------------------------------------------------------------------
+// ADMM step 3 standalone (Eq. 17 with Eqs. 10-11 at s^{k+1}, y^{k+1})
+// ----------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(CTA) k_mult(Dev P) {
+  __shared__ double sR[9], srho[3], red[32];
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x % P.nchunk;
+  const int bt = blockIdx.x / P.nchunk;
+  const int b = bt / P.N, t = bt % P.N + 1;
+  if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
+  __syncthreads();
+  double rec[1] = {0.0};
+  const int g = chunk * P.CH + tid;
+  if (tid < P.CH && g < P.G) {
+    const long long p = (long long)bt * P.G + g, PP = P.P;
+    const int i = g / P.M, j = g % P.M;
+    const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
+    const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
+    const double* prow = P.part_rows + 4 * r0;
+    const double* orow = P.obs_rows + 4 * (long long)l0;
+    double Tv = 1.0, Rv[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) Rv[a] = 0.0;
+    for (int k = 0; k < nr; ++k) {
+      const double yv = P.y[(long long)k * PP + p];
+#pragma unroll
+      for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yv, __ldg(prow + 4 * k + a), Rv[a]);
+    }
+    for (int lo = 0; lo < no; ++lo) {
+      const double yv = P.y[(long long)(nr + lo) * PP + p];
+      const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);
+      const double c[3] = {cr.x, cr.y, cr.z};
+      const double dl = cr.w;
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc = __fma_rn(c[a], srho[a], acc);
+      Tv = __fma_rn(yv, dl - acc, Tv);
+#pragma unroll
+      for (int mm = 0; mm < D; ++mm) {
+        double r = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) r = __fma_rn(c[a], sR[a * D + mm], r);
+        Rv[mm] = __fma_rn(yv, r, Rv[mm]);
+      }
+    }
+    Tv += P.y[(long long)(nr + no) * PP + p];
+    P.zeta[p] += Tv;
+    double r2 = Tv * Tv;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      P.xi[(long long)a * PP + p] += Rv[a];
+      r2 = __fma_rn(Rv[a], Rv[a], r2);
+    }
+    rec[0] = r2;
+  }
+  cta_sum<1>(rec, red);
+  if (tid == 0) P.agg[(long long)blockIdx.x * REC + R_RPRI] = rec[0];
+}
+
+#ifdef CA_COMMON_KERNELS
+// per-scene sums of the record statistics -> dst[b*4 + {rdual, rpri, piv, fail}]
+// (fields with mask bit f clear are left untouched)
+__global__ void k_collect(Dev P, double* dst, int mask) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  double acc[4] = {0, 0, 0, 0};
+  const long long base = (long long)b * P.N * P.nchunk;
+  for (long long r = 0; r < (long long)P.N * P.nchunk; ++r) {
+    const double* rec = P.agg + (base + r) * REC;
+    acc[0] += rec[R_RDUAL];
+    acc[1] += rec[R_RPRI];
+    acc[2] += rec[R_PIV];
+    acc[3] += rec[R_FAIL];
+  }
+  for (int f = 0; f < 4; ++f)
+    if ((mask >> f) & 1) dst[b * 4 + f] = acc[f];
+}
+#endif
+
+// ----------------------------------------------------------------------------
+// ADMM step 2: Riccati recursion per scene (one thread per scene)
+//   stage t = 1..N:  1/2 s^T H_t s + h_t^T s,  H_t = 2Qs + sigma P^T S_t P,
+//                    h_t = -2 Qs sref_t + sigma P^T (g_t - S_t P s^k_t)
+//   control:         1/2 u^T (2 Qu) u;   s_{t+1} = A_t s_t + B_t u_t + c_t
+// Also collects per-scene statistics (rdual of this sweep -> dst_cur,
+// rpri of the fused multiplier update -> dst_prev) in fixed order.
+// ----------------------------------------------------------------------------
+template <int NS, int NU>
+__global__ void k_riccati(Dev P, double* dst_cur, double* dst_prev) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  const int N = P.N, npc = P.npc, L1 = P.d + 1;
+  const double sig = P.sigma;
+  double Pm[NS][NS], pv[NS];
+  double st[4] = {0, 0, 0, 0};
+  // stage cost assembly for time t (1..N)
+  auto stage = [&](int t, double H[NS][NS], double h[NS]) {
+    double S[16], gv[4];
+    for (int f = 0; f < 16; ++f) S[f] = 0.0;
+    for (int f = 0; f < 4; ++f) gv[f] = 0.0;
+    const long long base = ((long long)b * N + (t - 1)) * P.nchunk;
+    for (int c = 0; c < P.nchunk; ++c) {
+      const double* rec = P.agg + (base + c) * REC;
+      for (int f = 0; f < L1 * (L1 + 1) / 2; ++f) S[f] += rec[f];
+      for (int f = 0; f < L1; ++f) gv[f] += rec[L1 * (L1 + 1) / 2 + f];
+      st[0] += rec[R_RDUAL];
+      st[1] += rec[R_RPRI];
+      st[2] += rec[R_PIV];
+      st[3] += rec[R_FAIL];
+    }
+    const double* sref = P.sref + ((long long)b * (N + 1) + t) * NS;
+    const double* sk = P.s + ((long long)b * (N + 1) + t) * NS;
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        H[a][c] = 2.0 * P.Qs[a * NS + c];
+        acc += P.Qs[a * NS + c] * sref[c];
+      }
+      h[a] = -2.0 * acc;
+    }
+    for (int a = 0; a < npc; ++a) {
+      double spv = gv[a];
+      for (int c = 0; c < npc; ++c) {
+        const double Sac = (a <= c) ? S[sym_idx(a, c, L1)] : S[sym_idx(c, a, L1)];
+        spv -= Sac * sk[P.pidx[c]];
+      }
+      for (int c = 0; c < npc; ++c) {
+        const double Sac = (a <= c) ? S[sym_idx(a, c, L1)] : S[sym_idx(c, a, L1)];
+        // pose index writes (runtime indices into register arrays -> unrolled select)
+#pragma unroll
+        for (int aa = 0; aa < NS; ++aa)
+#pragma unroll
+          for (int cc = 0; cc < NS; ++cc)
+            if (aa == P.pidx[a] && cc == P.pidx[c]) H[aa][cc] += sig * Sac;
+      }
+#pragma unroll
+      for (int aa = 0; aa < NS; ++aa)
+        if (aa == P.pidx[a]) h[aa] += sig * spv;
+    }
+  };
+  auto dynp = [&](const double* base, int t, int blk) {
+    const long long nt = P.dyn_pt ? N : 1;
+    const long long idx = (P.dyn_ps ? (long long)b * nt : 0) + (P.dyn_pt ? t : 0);
+    return base + idx * blk;
+  };
+  {
+    double H[NS][NS], h[NS];
+    stage(N, H, h);
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      pv[a] = h[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) Pm[a][c] = H[a][c];
+    }
+  }
+  double* ric = P.ric + (long long)b * N * NU * (NS + 1);
+  for (int t = N - 1; t >= 0; --t) {
+    const double* A = dynp(P.dynA, t, NS * NS);
+    const double* Bm = dynp(P.dynB, t, NS * NU);
+    const double* cv = dynp(P.dync, t, NS);
+    double H[NS][NS], h[NS];
+    if (t >= 1) {
+      stage(t, H, h);
+    } else {
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        h[a] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NS; ++c) H[a][c] = 0.0;
+      }
+    }
+    // PA = P A, PB = P B, w = P c + p
+    double PA[NS][NS], PB[NS][NU], w[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double acc = pv[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) acc = __fma_rn(Pm[a][c], cv[c], acc);
+      w[a] = acc;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Pm[a][k], A[k * NS + c], s);
+        PA[a][c] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < NU; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Pm[a][k], Bm[k * NU + c], s);
+        PB[a][c] = s;
+      }
+    }
+    double Quu[NU][NU], Qux[NU][NS], qu[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+#pragma unroll
+      for (int c = 0; c < NU; ++c) {
+        double s = 2.0 * P.Qu[a * NU + c];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PB[k][c], s);
+        Quu[a][c] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PA[k][c], s);
+        Qux[a][c] = s;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
+      qu[a] = s;
+    }
+    // Cholesky Quu = L L^T
+    double Lc[NU][NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a)
+#pragma unroll
+      for (int c = 0; c < NU; ++c) Lc[a][c] = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < NU; ++jj) {
+      double s = Quu[jj][jj];
+#pragma unroll
+      for (int k = 0; k < jj; ++k) s -= Lc[jj][k] * Lc[jj][k];
+      const double ljj = sqrt(s);
+      Lc[jj][jj] = ljj;
+#pragma unroll
+      for (int ii = jj + 1; ii < NU; ++ii) {
+        double a = Quu[ii][jj];
+#pragma unroll
+        for (int k = 0; k < jj; ++k) a -= Lc[ii][k] * Lc[jj][k];
+        Lc[ii][jj] = a / ljj;
+      }
+    }
+    // K = -Quu^{-1} Qux, k = -Quu^{-1} qu (columns solved with the factor)
+    double Kg[NU][NS + 1];
+#pragma unroll
+    for (int c = 0; c <= NS; ++c) {
+      double rhs[NU];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) rhs[a] = (c < NS) ? Qux[a][c] : qu[a];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) {
+        double s = rhs[a];
+#pragma unroll
+        for (int k = 0; k < a; ++k) s -= Lc[a][k] * rhs[k];
+        rhs[a] = s / Lc[a][a];
+      }
+#pragma unroll
+      for (int a = NU - 1; a >= 0; --a) {
+        double s = rhs[a];
+#pragma unroll
+        for (int k = a + 1; k < NU; ++k) s -= Lc[k][a] * rhs[k];
+        rhs[a] = s / Lc[a][a];
+      }
+#pragma unroll
+      for (int a = 0; a < NU; ++a) Kg[a][c] = -rhs[a];
+    }
+#pragma unroll
+    for (int a = 0; a < NU; ++a)
+#pragma unroll
+      for (int c = 0; c <= NS; ++c) ric[((long long)t * NU + a) * (NS + 1) + c] = Kg[a][c];
+    // P <- H + A^T P A + Qux^T K ;  p <- h + A^T w + Qux^T k
+    double Pn[NS][NS], pn[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double s = h[a];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s = __fma_rn(A[k * NS + a], w[k], s);
+#pragma unroll
+      for (int k = 0; k < NU; ++k) s = __fma_rn(Qux[k][a], Kg[k][NS], s);
+      pn[a] = s;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double v = H[a][c];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) v = __fma_rn(A[k * NS + a], PA[k][c], v);
+#pragma unroll
+        for (int k = 0; k < NU; ++k) v = __fma_rn(Qux[k][a], Kg[k][c], v);
+        Pn[a][c] = v;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      pv[a] = pn[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) Pm[a][c] = 0.5 * (Pn[a][c] + Pn[c][a]);
+    }
+  }
+  // forward rollout from s_0 (Eq. 13b holds exactly)
+  double x[NS];
+  double* sb = P.s + (long long)b * (N + 1) * NS;
+#pragma unroll
+  for (int a = 0; a < NS; ++a) {
+    x[a] = P.s0[b * NS + a];
+    sb[a] = x[a];
+  }
+  for (int t = 0; t < N; ++t) {
+    const double* A = dynp(P.dynA, t, NS * NS);
+    const double* Bm = dynp(P.dynB, t, NS * NU);
+    const double* cv = dynp(P.dync, t, NS);
+    double uu[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], x[c], s);
+      uu[a] = s;
+      P.u[((long long)b * N + t) * NU + a] = s;
+    }
+    double xn[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double s = cv[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(A[a * NS + c], x[c], s);
+#pragma unroll
+      for (int c = 0; c < NU; ++c) s = __fma_rn(Bm[a * NU + c], uu[c], s);
+      xn[a] = s;
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      x[a] = xn[a];
+      sb[(t + 1) * NS + a] = xn[a];
+    }
+  }
+  if (dst_cur) {
+    dst_cur[b * 4 + 0] = st[0];
+    dst_cur[b * 4 + 2] = st[2];
+    dst_cur[b * 4 + 3] = st[3];
+  }
+  if (dst_prev) dst_prev[b * 4 + 1] = st[1];
+}
+
+// ----------------------------------------------------------------------------
+// Eq. 3 scale LP per pair, vertex enumeration over (d+1)-subsets of the rows of
+//   (R a_k)^T y - b_k alpha <= (R a_k)^T rho ,   c_l^T y <= d_l
+// ----------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ bool solve_sq(double A[D + 1][D + 2], double x[D + 1]) {
+  constexpr int m = D + 1;
+  double scale = 0.0;
+#pragma unroll
+  for (int i = 0; i < m; ++i)
+#pragma unroll
+    for (int c = 0; c < m; ++c) scale = fmax(scale, fabs(A[i][c]));
+  if (scale == 0.0) return false;
+#pragma unroll
+  for (int k = 0; k < m; ++k) {
+    int piv = k;
+#pragma unroll
+    for (int i = k + 1; i < m; ++i)
+      if (fabs(A[i][k]) > fabs(A[piv][k])) piv = i;
+#pragma unroll
+    for (int i = k + 1; i < m; ++i) {
+      if (i == piv) {
+#pragma unroll
+        for (int c = 0; c <= m; ++c) { double t = A[k][c]; A[k][c] = A[i][c]; A[i][c] = t; }
+      }
+    }
+    if (fabs(A[k][k]) < 1e-12 * scale) return false;
+#pragma unroll
+    for (int i = k + 1; i < m; ++i) {
+      const double f = A[i][k] / A[k][k];
+#pragma unroll
+      for (int c = k; c <= m; ++c) A[i][c] -= f * A[k][c];
+    }
+  }
+#pragma unroll
+  for (int i = m - 1; i >= 0; --i) {
+    double acc = A[i][m];
+#pragma unroll
+    for (int c = i + 1; c < m; ++c) acc -= A[i][c] * x[c];
+    x[i] = acc / A[i][i];
+  }
+  return true;
+}
+
+template <int D>
+__global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, double* alpha) {
+  extern __shared__ double smem[];
+  __shared__ double sR[9], srho[3];
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x % P.nchunk;
+  const int bt = blockIdx.x / P.nchunk;
+  const int b = bt / P.N, t = bt % P.N + 1;
+  if (tid == 0) pose_of(P, states + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
+  __syncthreads();
+  const int g = chunk * P.CH + tid;
+  if (!(tid < P.CH && g < P.G)) return;
+  const long long p = (long long)bt * P.G + g;
+  const int i = g / P.M, j = g % P.M;
+  const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
+  const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
+  const int m = nr + no;
+  double* Gr = smem + tid;  // rows [m][D+2] (g_0..g_D, h), stride CTA
+#define GR(r_, c_) Gr[((r_) * (D + 2) + (c_)) * CTA]
+  for (int k = 0; k < nr; ++k) {
+    const double* a = P.part_rows + 4 * (r0 + k);
+    double h = 0.0;
+#pragma unroll
+    for (int aa = 0; aa < D; ++aa) {
+      double ra = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) ra += sR[aa * D + c] * __ldg(a + c);
+      GR(k, aa) = ra;
+      h += ra * srho[aa];
+    }
+    GR(k, D) = -__ldg(a + 3);
+    GR(k, D + 1) = h;
+  }
+  for (int lo = 0; lo < no; ++lo) {
+    const double* c = P.obs_rows + 4 * ((long long)l0 + lo);
+#pragma unroll
+    for (int aa = 0; aa < D; ++aa) GR(nr + lo, aa) = __ldg(c + aa);
+    GR(nr + lo, D) = 0.0;
+    GR(nr + lo, D + 1) = __ldg(c + 3);
+  }
+  double best = 1e308;
+  int sub[D + 1];
+#pragma unroll
+  for (int k = 0; k <= D; ++k) sub[k] = k;
+  for (;;) {
+    double A[D + 1][D + 2], z[D + 1];
+#pragma unroll
+    for (int r = 0; r <= D; ++r) {
+#pragma unroll
+      for (int c = 0; c <= D; ++c) A[r][c] = GR(sub[r], c);
+      A[r][D + 1] = GR(sub[r], D + 1);
+    }
+    if (solve_sq<D>(A, z) && z[D] < best) {
+      bool feas = true;
+      for (int r = 0; r < m && feas; ++r) {
+        double lhs = 0.0, h = GR(r, D + 1), mag = fabs(h);
+#pragma unroll
+        for (int c = 0; c <= D; ++c) {
+          const double tc = GR(r, c) * z[c];
+          lhs += tc;
+          mag += fabs(tc);
+        }
+        if (lhs - h > 1e-9 * (1.0 + mag)) feas = false;
+      }
+      if (feas) best = z[D];
+    }
+    int k = D;
+    while (k >= 0 && sub[k] == m - (D + 1) + k) --k;
+    if (k < 0) break;
+    ++sub[k];
+    for (int q = k + 1; q <= D; ++q) sub[q] = sub[q - 1] + 1;
+  }
+#undef GR
+  alpha[p] = (best < 1e307) ? best : nan("");
+}
+
+#ifdef CA_COMMON_KERNELS
+__global__ void k_scene_min(const double* alpha, long long per_scene, double* out) {
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  double v = 1e308;
+  for (long long k = threadIdx.x; k < per_scene; k += blockDim.x) v = fmin(v, alpha[(long long)b * per_scene + k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 1e308;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r = fmin(r, red[k]);
+    out[b] = r;
+  }
+}
+
+// sum per-scene stats of `nslot` iteration slots: hist[k*4 + f] = sum_b slots[(k*B + b)*4 + f]
+__global__ void k_hist(const double* slots, int B, int nslot, double* hist) {
+  const int k = blockIdx.x;
+  if (k >= nslot) return;
+  __shared__ double red[4][32];
+  double acc[4] = {0, 0, 0, 0};
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    for (int f = 0; f < 4; ++f) acc[f] += slots[((long long)k * B + b) * 4 + f];
+  for (int f = 0; f < 4; ++f) {
+    double v = acc[f];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int f = 0; f < 4; ++f) {
+      double r = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red[f][w];
+      hist[k * 4 + f] = r;
+    }
+}
+
+// O1 initial dual iterate (reading #11): lambda = 1/sum(b_i) 1, mu = gamma = 0
+__global__ void k_init_y(Dev P) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P.P) return;
+  const int i = (int)((p / P.M) % P.np);
+  const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
+  double sb = 0.0;
+  for (int k = 0; k < nr; ++k) sb += P.part_rows[4 * (r0 + k) + 3];
+  for (int k = 0; k < P.ny; ++k) P.y[(long long)k * P.P + p] = (k < nr) ? 1.0 / sb : 0.0;
+}
+
+__global__ void k_dfma(double* out, long long iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double mlt = 0.999999999, add = 1e-7;
+  for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      a0 = __fma_rn(a0, mlt, add); a1 = __fma_rn(a1, mlt, add); a2 = __fma_rn(a2, mlt, add);
+      a3 = __fma_rn(a3, mlt, add); a4 = __fma_rn(a4, mlt, add); a5 = __fma_rn(a5, mlt, add);
+      a6 = __fma_rn(a6, mlt, add); a7 = __fma_rn(a7, mlt, add);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[0] = s;  // keep the loop alive
+}
+#endif  // CA_COMMON_KERNELS
+
+}  // namespace ca

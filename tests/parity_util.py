@@ -1,0 +1,58 @@
+"""Helpers for GPU-vs-oracle parity (test infrastructure)."""
+import numpy as np
+
+import oracle
+
+
+def pair_geometry(sc, p):
+    N, npt, M = sc.horizon, sc.n_parts, sc.n_obs
+    j = p % M
+    r = p // M
+    i = r % npt
+    r //= npt
+    t = r % N + 1
+    b = r // N
+    A = sc.part_A[sc.part_off[i]:sc.part_off[i + 1]]
+    bb = sc.part_b[sc.part_off[i]:sc.part_off[i + 1]]
+    o = b * M + j
+    Cm = sc.obs_C[sc.obs_off[o]:sc.obs_off[o + 1]]
+    dv = sc.obs_d[sc.obs_off[o]:sc.obs_off[o + 1]]
+    return b, t, A, bb, Cm, dv
+
+
+def validate_pair_choice(sc, s, zeta, xi, p, y_gpu, y_orc, tol=1e-9):
+    """Where Lemke's choice among non-unique minimisers differs (reading #2), check
+    what is unique -- u* = K^T y + b and the optimal value -- and that the GPU's y
+    is a KKT point of Eq. 19 (hence a global minimiser)."""
+    b, t, A, bb, Cm, dv = pair_geometry(sc, p)
+    R, rho = oracle.pose(sc.pose_model, sc.pose_idx, sc.dim, s[b, t])
+    K, bvec, e, M, q = oracle.pair_lcp(A, bb, Cm, dv, R, rho, zeta[p], xi[p])
+    n = K.shape[0]
+    yg, yo = y_gpu[:n], y_orc[:n]
+    ug, uo = K.T @ yg + bvec, K.T @ yo + bvec
+    scale = 1.0 + np.abs(uo).max()
+    assert np.abs(ug - uo).max() <= 1e-7 * scale, (p, ug, uo)
+    kappa = np.r_[bb, np.zeros(n - len(bb))]
+    g = K @ ug
+    lam = kappa > 0
+    nu = np.min(g[lam] / kappa[lam])
+    r = g - nu * kappa
+    sc_g = 1 + np.abs(g).max()
+    assert yg.min() >= -1e-9, (p, yg)
+    assert abs(kappa @ yg - 1) <= 1e-9
+    assert r.min() >= -1e-7 * sc_g, (p, r)
+    assert np.all(np.abs(r[yg > 1e-7]) <= 1e-6 * sc_g), (p, r, yg)
+
+
+def compare_dual_sweep(sc, s, zeta, xi, y_gpu, y_orc, piv_gpu, piv_orc, st_gpu, st_orc, rtol=1e-9,
+                       max_flip_frac=1e-3):
+    """T1 contract: per pair ||y_gpu - y_orc||_inf <= rtol max(1, ||y_orc||_inf) and equal
+    pivot counts/status, except rare near-tie Lemke path flips, each validated."""
+    assert np.array_equal(st_gpu, st_orc), np.nonzero(st_gpu != st_orc)[0][:10]
+    sc_y = np.maximum(1.0, np.abs(y_orc).max(1))
+    dy = np.abs(y_gpu - y_orc).max(1)
+    bad = np.nonzero((dy > rtol * sc_y) | (piv_gpu != piv_orc))[0]
+    assert len(bad) <= max(1, max_flip_frac * len(dy)), (len(bad), bad[:10], dy[bad[:10]])
+    for p in bad:
+        validate_pair_choice(sc, s, zeta, xi, p, y_gpu[p], y_orc[p])
+    return len(bad)

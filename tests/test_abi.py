@@ -1,0 +1,72 @@
+"""CPU-side checks of the C-ABI boundary: the library loads, exports every symbol
+include/ca.h declares, validates inputs before touching the GPU, and fails loudly
+(CA_E_CUDA) where there is no B200 -- no CPU fallback."""
+import dataclasses
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import scenes
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ca.h")
+
+
+@pytest.fixture(scope="module")
+def ca():
+    from paper_2406_07048_b200 import build
+
+    build.build()
+    import paper_2406_07048_b200 as ca
+
+    return ca
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(ca_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_exports_every_header_symbol(ca):
+    syms = header_symbols()
+    assert len(syms) >= 18
+    out = subprocess.run(["nm", "-D", "--defined-only", ca.library_path()], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ca_[a-z0-9_]+)$", out, re.M))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    L = ca.lib()
+    for s in syms:
+        assert hasattr(L, s)
+
+
+def test_no_dynamic_cudart_dependency(ca):
+    out = subprocess.run(["ldd", ca.library_path()], capture_output=True, text=True).stdout
+    assert "libcudart" not in out
+
+
+def _create(ca, sc, **kw):
+    try:
+        ca.Problem(sc, **kw)
+    except ca.CAError as e:
+        return e.code, str(e)
+    return 0, ""
+
+
+def test_validation_errors_precede_device(ca):
+    sc = scenes.make_config(2)
+    bad = dataclasses.replace(sc, part_b=-sc.part_b)
+    assert _create(ca, bad)[0] == -3  # CA_E_GEOMETRY: b_i must be > 0 (reading #22)
+    bad = dataclasses.replace(sc, dim=4)
+    assert _create(ca, bad)[0] == -2  # CA_E_DIM
+    assert _create(ca, sc, prox_eps=1e-3)[0] == -4  # CA_E_UNSUPPORTED
+    bad = dataclasses.replace(sc, Qs=-sc.Qs)
+    assert _create(ca, bad)[0] == -1  # CA_E_INVALID (not SPD)
+
+
+@pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="GPU present")
+def test_fails_loudly_without_gpu(ca):
+    code, msg = _create(ca, scenes.make_config(1))
+    assert code == -5 and "no CPU fallback" in msg

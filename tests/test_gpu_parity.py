@@ -1,0 +1,249 @@
+"""GPU (C-ABI, libca.so on a B200) vs the CPU oracle, on the same seeded inputs.
+
+T1 frozen inputs: one ADMM step from an identical iterate -- per-pair y within
+1e-9 (relative), identical pivot counts / status except rare near-tie Lemke
+flips which are validated (unique u* and optimum, KKT certificate); primal and
+multiplier steps within 1e-9.  T2: K full iterations on C1-C4 within 1e-6.
+C5 at full size in the bench launch configuration: every iteration of sampled
+scenes checked step by step against the oracle.  Plus scale detection, edge
+cases (no obstacles, n > 16, d = 3), bitwise run-to-run and fused == stepwise.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import scenes
+from conftest import poly_from_vertices
+from parity_util import compare_dual_sweep
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ca():
+    from paper_2406_07048_b200 import build
+
+    build.build()
+    import paper_2406_07048_b200 as ca
+
+    return ca
+
+
+def scene(cfg):
+    if cfg == 5:
+        return scenes.make_c5(scene_ids=[0, 1777, 4095])
+    return scenes.make_config(cfg)
+
+
+def warm(sc, k0):
+    o = oracle.Oracle(sc)
+    if k0:
+        o.admm_iterate(k0)
+    return o
+
+
+def close(a, b, rtol, what):
+    a, b = np.asarray(a), np.asarray(b)
+    err = np.abs(a - b) / np.maximum(1.0, np.abs(b))
+    assert err.max() <= rtol, f"{what}: max rel err {err.max():.3e} at {np.unravel_index(err.argmax(), err.shape)}"
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("k0", [0, 3])
+def test_t1_dual_sweep(ca, cfg, k0):
+    sc = scene(cfg)
+    o = warm(sc, k0)
+    g = ca.Problem(sc)
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    s, zeta, xi = o.s.copy(), o.zeta.copy(), o.xi.copy()
+    rc, r = g.dual_sweep()
+    rd, fails = o.dual_sweep()
+    st = g.pair_state()
+    flips = compare_dual_sweep(sc, s, zeta, xi, st["y"], o.y, st["pivots"], o.pivots, st["status"], o.status)
+    assert r.n_fail == fails
+    assert r.pivots == o.pivots.sum() or flips
+    if not flips:
+        close(r.r_dual, rd.sum(), 1e-9, "r_dual")
+    # zeta, xi untouched by step 1
+    assert np.array_equal(st["zeta"], zeta) and np.array_equal(st["xi"], xi)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_t1_primal_and_multiplier(ca, cfg):
+    sc = scene(cfg)
+    o = warm(sc, 3)
+    g = ca.Problem(sc)
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    g.dual_sweep()
+    o.dual_sweep()
+    g.primal_step()
+    o.primal_step()
+    s, u = g.trajectory()
+    close(s, o.s, 1e-9, "s after primal step")
+    close(u, o.u, 1e-9, "u after primal step")
+    r = g.multiplier_update()
+    rp = o.multiplier_update()
+    st = g.pair_state()
+    scale = 1.0 + np.abs(o.zeta).max()
+    assert np.abs(st["zeta"] - o.zeta).max() <= 1e-9 * scale
+    assert np.abs(st["xi"] - o.xi).max() <= 1e-9 * scale
+    close(r.r_pri, rp.sum(), 1e-8, "r_pri")
+    # dynamics hold exactly (Eq. 13b)
+    sc0 = sc
+    for t in range(sc0.horizon):
+        nt = sc0.horizon if sc0.dyn_per_time else 1
+        k = t if sc0.dyn_per_time else 0
+        A, B, c = sc0.dyn_A[k], sc0.dyn_B[k], sc0.dyn_c[k]
+        assert np.abs(s[0, t + 1] - (A @ s[0, t] + B @ u[0, t] + c)).max() <= 1e-12 * (1 + np.abs(s).max())
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_t2_full_iterations(ca, cfg):
+    sc = scene(cfg)
+    K = sc.iters
+    g = ca.Problem(sc)
+    rc, hist = g.admm_iterate(K)
+    o = oracle.Oracle(sc)
+    hp, hd, fails = o.admm_iterate(K)
+    s, u = g.trajectory()
+    close(s, o.s, 1e-6, "s")
+    close(u, o.u, 1e-6, "u")
+    assert np.abs(hist["r_pri"] - hp.sum(1)).max() <= 1e-6 * max(1, hp.max())
+    assert np.abs(hist["r_dual"] - hd.sum(1)).max() <= 1e-6 * max(1, hd.max())
+    assert hist["n_fail"].sum() == fails == 0
+    st = g.pair_state()
+    scale = 1.0 + np.abs(o.zeta).max()
+    assert np.abs(st["zeta"] - o.zeta[: g.n_pairs]).max() <= 1e-6 * scale
+
+
+def test_fused_pipeline_equals_stepwise_bitwise(ca):
+    sc = scene(2)
+    a = ca.Problem(sc)
+    a.admm_iterate(12)
+    b = ca.Problem(sc)
+    for _ in range(12):
+        b.admm_iterate(1)
+    sa, ua = a.trajectory()
+    sb, ub = b.trajectory()
+    pa, pb = a.pair_state(), b.pair_state()
+    assert np.array_equal(sa, sb) and np.array_equal(ua, ub)
+    for k in ("y", "zeta", "xi", "pivots"):
+        assert np.array_equal(pa[k], pb[k]), k
+
+
+def test_run_to_run_bitwise(ca):
+    sc = scenes.make_c5(n_scenes=8)
+    outs = []
+    for _ in range(2):
+        g = ca.Problem(sc)
+        rc, h = g.admm_iterate(10)
+        outs.append((g.trajectory(), g.pair_state(), h))
+    (s1, u1), p1, h1 = outs[0]
+    (s2, u2), p2, h2 = outs[1]
+    assert np.array_equal(s1, s2) and np.array_equal(u1, u2)
+    assert np.array_equal(p1["y"], p2["y"]) and np.array_equal(h1["r_pri"], h2["r_pri"])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_scale_detect(ca, cfg):
+    sc = scene(cfg)
+    o = warm(sc, 5)
+    g = ca.Problem(sc)
+    for states in (sc.s_ref, o.s):
+        a_g, amin = g.scale_detect(states)
+        a_o = o.scale_detect(states)
+        close(a_g, a_o, 1e-9, "alpha*")
+        per = a_o.reshape(sc.n_scenes, -1).min(1)
+        close(amin, per, 1e-9, "min alpha")
+
+
+def test_zero_obstacles(ca):
+    sc = scenes.make_config(2)
+    sc = dataclasses.replace(sc, n_obs=0, obs_off=np.zeros(1, np.int32), obs_C=np.zeros((0, 2)),
+                             obs_d=np.zeros(0))
+    g = ca.Problem(sc)
+    g.admm_iterate(2)
+    o = oracle.Oracle(sc)
+    o.admm_iterate(2)
+    s, u = g.trajectory()
+    close(s, o.s, 1e-9, "s")
+    close(u, o.u, 1e-9, "u")
+
+
+def many_faced_scene(nv_lo=14, nv_hi=22, n_obs=6, seed=99):
+    """C1-like car scene whose obstacles have 14-22 faces: n up to 27 (NMAX=32 path)."""
+    rng = np.random.default_rng(seed)
+    base = scenes.make_config(2)
+    polys = []
+    for k in range(n_obs):
+        nv = int(rng.integers(nv_lo, nv_hi + 1))
+        ang = 2 * np.pi * np.arange(nv) / nv + rng.uniform(-0.1, 0.1, nv) + rng.uniform(0, 6.28)
+        r = rng.uniform(0.8, 2.0)
+        c = np.array([4.0 + 2.2 * k, rng.uniform(-1.5, 1.5)])
+        V = c + r * np.stack([np.cos(ang), np.sin(ang)], 1)
+        polys.append(poly_from_vertices(V))
+    off = np.concatenate([[0], np.cumsum([len(p[1]) for p in polys])]).astype(np.int32)
+    return dataclasses.replace(base, n_obs=n_obs, obs_off=off, obs_C=np.concatenate([p[0] for p in polys]),
+                               obs_d=np.concatenate([p[1] for p in polys]), iters=40)
+
+
+def test_large_n_path(ca):
+    sc = many_faced_scene()
+    assert sc.n_max > 20
+    o = warm(sc, 3)
+    g = ca.Problem(sc)
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    s, zeta, xi = o.s.copy(), o.zeta.copy(), o.xi.copy()
+    g.dual_sweep()
+    o.dual_sweep()
+    st = g.pair_state()
+    compare_dual_sweep(sc, s, zeta, xi, st["y"], o.y, st["pivots"], o.pivots, st["status"], o.status)
+    g2 = ca.Problem(sc)
+    g2.admm_iterate(sc.iters)
+    o2 = oracle.Oracle(sc)
+    o2.admm_iterate(sc.iters)
+    s2, u2 = g2.trajectory()
+    close(s2, o2.s, 1e-6, "s (large n)")
+
+
+def test_c5_full_size_stepwise(ca):
+    """C5 at BASELINE size (4096 scenes x 200 obstacles x N=50) in the bench's launch
+    configuration; sampled scenes are followed iteration by iteration: each GPU
+    iteration equals the oracle's iteration applied to the GPU's previous iterate
+    (non-unique Lemke choices validated, then adopted, reading #2)."""
+    sc = scenes.make_c5()
+    g = ca.Problem(sc)
+    K = 12
+    samples = [0, 2049, 4095]
+    per = sc.horizon * sc.n_parts * sc.n_obs
+    subs = {b: sc.subset([b]) for b in samples}
+
+    def grab(b):
+        s, u = g.trajectory()
+        st = g.pair_state(b * per, per)
+        return s[b:b + 1], u[b:b + 1], st
+
+    prev = {b: grab(b) for b in samples}
+    total_flips = 0
+    for k in range(K):
+        g.admm_iterate(1)
+        for b in samples:
+            s0, u0, st0 = prev[b]
+            o = oracle.Oracle(subs[b])
+            o.set_iterate(s=s0, u=u0, y=st0["y"], zeta=st0["zeta"], xi=st0["xi"])
+            o.dual_sweep()
+            s1, u1, st1 = grab(b)
+            total_flips += compare_dual_sweep(subs[b], s0, st0["zeta"], st0["xi"], st1["y"], o.y, st1["pivots"],
+                                              o.pivots, st1["status"], o.status)
+            o.y[...] = st1["y"]  # adopt the GPU's (validated) minimisers
+            o.primal_step()
+            close(s1, o.s, 1e-9, f"s scene {b} iter {k}")
+            close(u1, o.u, 1e-9, f"u scene {b} iter {k}")
+            o.multiplier_update()
+            sc_z = 1 + np.abs(o.zeta).max()
+            assert np.abs(st1["zeta"] - o.zeta).max() <= 1e-9 * sc_z
+            assert np.abs(st1["xi"] - o.xi).max() <= 1e-9 * sc_z
+            prev[b] = (s1, u1, st1)
+    print("C5 validated Lemke flips:", total_flips)
