@@ -125,6 +125,11 @@ void ca_problem_destroy(ca_problem* h);
  * path: load -> ca_admm_iterate -> ca_get_trajectory. */
 ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* desc);
 
+/* Reset the iterate to the initial point (reading #11) from the device-resident
+ * inputs: s = s_ref (s_0 = s0), u = 0, lambda = 1/sum(b_i), mu = gamma = zeta = xi = 0.
+ * Device-only (no host transfer): starts a new solve on the same inputs. */
+ca_status ca_reset_iterate(ca_problem* h);
+
 /* n_pairs, ny (= n_max, the per-pair y stride of ca_get_pair_state), device bytes. */
 ca_status ca_problem_info(const ca_problem* h, int64_t* n_pairs, int32_t* ny, int64_t* device_bytes);
 
@@ -164,8 +169,11 @@ ca_status ca_set_iterate(ca_problem* h, const double* s, const double* u, const 
                          const double* zeta, const double* xi);
 
 /* Device milliseconds accumulated per kernel family since the last reset (CUDA
- * events on the handle's stream): ms[0] pair sweep, [1] primal, [2] multiplier,
- * [3] scale detect; launches[0..3] the matching launch counts.  reset != 0 zeroes. */
+ * events on the handle's stream, only while ca_set_timing(h, 1)): ms[0] pair
+ * sweep, [1] primal, [2] multiplier, [3] scale detect (+ per-scene min), [4] other
+ * small kernels (init, collect, history; not timed, ms[4] = 0); launches[0..4] the
+ * matching kernel-launch counts (always counted).  Arrays have 5 entries; reset != 0
+ * zeroes. */
 ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t reset);
 
 /* Enable (1) / disable (0) per-launch event timing (default off). */

@@ -84,11 +84,12 @@ def lib():
         L.ca_set_timing.argtypes = [vp, C.c_int32]
         L.ca_set_record_basis.argtypes = [vp, C.c_int32]
         L.ca_fp64_peak.argtypes = [C.c_int, C.c_double, dp]
+        L.ca_reset_iterate.argtypes = [vp]
         for name in ("ca_problem_create", "ca_problem_load", "ca_problem_info", "ca_scale_detect",
                      "ca_admm_iterate", "ca_admm_solve", "ca_dual_sweep", "ca_primal_step",
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
-                     "ca_set_record_basis", "ca_fp64_peak"):
+                     "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib
@@ -181,6 +182,9 @@ class Problem:
         _check(lib().ca_problem_load(self.h, C.byref(desc)), ok=(CA_OK,))
         self.sc = sc
 
+    def reset_iterate(self):
+        _check(lib().ca_reset_iterate(self.h))
+
     # -- the method -------------------------------------------------------------
     def admm_iterate(self, iters: int, hist: bool = True):
         H = (Residuals * iters)() if hist else None
@@ -257,10 +261,10 @@ class Problem:
         _check(lib().ca_set_record_basis(self.h, int(on)))
 
     def kernel_times(self, reset: bool = False):
-        ms = (C.c_double * 4)()
-        ln = (C.c_int64 * 4)()
+        ms = (C.c_double * 5)()
+        ln = (C.c_int64 * 5)()
         _check(lib().ca_kernel_times(self.h, ms, ln, int(reset)))
-        names = ("sweep", "primal", "multiplier", "scale")
+        names = ("sweep", "primal", "multiplier", "scale", "other")
         return {n: (ms[i], ln[i]) for i, n in enumerate(names)}
 
 

@@ -16,8 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libca.so")
 import glob
 SOURCES = [os.path.join(CSRC, "ca_api.cu")] + sorted(glob.glob(os.path.join(CSRC, "ca_sweep_*.cu")))
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("ca_kernels.cuh", "ca_lemke.cuh")] + [
-    os.path.join(ROOT, "include", "ca.h")]
+DEPS = SOURCES + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "ca.h"),
+                                                                    os.path.abspath(__file__)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

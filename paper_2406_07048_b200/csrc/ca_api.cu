@@ -13,6 +13,7 @@
 #include "../../include/ca.h"
 #define CA_COMMON_KERNELS 1
 #include "ca_kernels.cuh"
+#include "ca_sweep.cuh"
 
 // the pair-sweep instantiations live in ca_sweep_d2.cu / ca_sweep_d3.cu
 #define CA_EXTERN_SWEEP(D, NM, F) extern template cudaError_t ca::sweep_launch<D, NM, F>(const ca::Dev&, unsigned, cudaStream_t);
@@ -60,8 +61,9 @@ struct ca_problem {
   double eps_pri = 0, eps_dual = 0;
   int max_iters = 100;
   bool timing = false;
-  double ms[4] = {0, 0, 0, 0};
-  long long launches[4] = {0, 0, 0, 0};
+  double ms[5] = {0, 0, 0, 0, 0};
+  long long launches[5] = {0, 0, 0, 0, 0};
+  double* s_start = nullptr;  // initial state trajectory (reset point)
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::vector<cudaEvent_t> event_pool;
   bool sticky = false;
@@ -147,8 +149,11 @@ ca_status validate(const ca_problem_desc* D) {
     if (D->pose_idx[a] < 0 || D->pose_idx[a] >= D->n_state) return fail(CA_E_DIM, "pose index out of range");
   if (!riccati_supported(D->n_state, D->n_ctrl))
     return fail(CA_E_UNSUPPORTED, "(n_state, n_ctrl) combination not instantiated");
+  if (D->n_parts > ca::NPMAX) return fail(CA_E_UNSUPPORTED, "more than 8 robot parts");
   int nrmax = 0;
   for (int i = 0; i < D->n_parts; ++i) {
+    if (D->part_off[i + 1] - D->part_off[i] > ca::NRMAX)
+      return fail(CA_E_UNSUPPORTED, "robot part with more than 16 faces");
     const int r0 = D->part_off[i], nr = D->part_off[i + 1] - r0;
     if (nr < d + 1) return fail(CA_E_GEOMETRY, "robot part with fewer than d+1 faces");
     for (int k = 0; k < nr; ++k)
@@ -170,6 +175,25 @@ template <class T>
 ca_status h2d(ca_problem* h, T* dst, const T* src, size_t count) {
   if (count == 0) return CA_OK;
   CUDA_TRY(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  return CA_OK;
+}
+
+// O1 initial iterate on the device (reading #11): s = s_start, u = 0,
+// lambda = 1/sum(b_i) 1, mu = gamma = zeta = xi = 0
+ca_status reset_iterate(ca_problem* h) {
+  ca::Dev& v = h->dev;
+  CUDA_TRY(cudaMemcpyAsync(v.s, h->s_start, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns,
+                           cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(cudaMemsetAsync(v.u, 0, sizeof(double) * (size_t)h->B * h->N * h->nu, h->stream));
+  if (h->P > 0) {
+    CUDA_TRY(cudaMemsetAsync(v.zeta, 0, sizeof(double) * (size_t)h->P, h->stream));
+    CUDA_TRY(cudaMemsetAsync(v.xi, 0, sizeof(double) * (size_t)h->d * h->P, h->stream));
+    CUDA_TRY(cudaMemsetAsync(v.pst, 0, sizeof(uint32_t) * (size_t)h->P, h->stream));
+    const unsigned grid = (unsigned)((h->P + 255) / 256);
+    ca::k_init_y<<<grid, 256, 0, h->stream>>>(h->dev);
+    CUDA_TRY(cudaGetLastError());
+    h->launches[4]++;
+  }
   return CA_OK;
 }
 
@@ -212,18 +236,26 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
     for (int t = 0; t <= N; ++t)
       for (int a = 0; a < ns; ++a)
         s0v[((size_t)b * (N + 1) + t) * ns + a] = (t == 0) ? D->s0[b * ns + a] : si[((size_t)b * (N + 1) + t) * ns + a];
-  if ((st = h2d(h, v.s, s0v.data(), s0v.size()))) return st;
-  CUDA_TRY(cudaMemsetAsync(v.u, 0, sizeof(double) * (size_t)B * N * nu, h->stream));
+  // execution order of each (b, t) group: pairs stably sorted by LCP size n so that a
+  // warp's 32 threads mostly run the same-size Lemke (pure scheduling; results are
+  // stored at the pair's own index p)
   if (h->P > 0) {
-    CUDA_TRY(cudaMemsetAsync(v.y, 0, sizeof(double) * (size_t)h->nmax * h->P, h->stream));
-    CUDA_TRY(cudaMemsetAsync(v.zeta, 0, sizeof(double) * (size_t)h->P, h->stream));
-    CUDA_TRY(cudaMemsetAsync(v.xi, 0, sizeof(double) * (size_t)d * h->P, h->stream));
-    CUDA_TRY(cudaMemsetAsync(v.pst, 0, sizeof(uint32_t) * (size_t)h->P, h->stream));
-    // lambda^0 = 1/sum(b_i) 1 (satisfies b_i^T lambda = 1), mu = gamma = 0
-    const unsigned grid = (unsigned)((h->P + 255) / 256);
-    ca::k_init_y<<<grid, 256, 0, h->stream>>>(h->dev);
-    CUDA_TRY(cudaGetLastError());
+    const int G = h->np * h->M;
+    std::vector<int> perm((size_t)B * G);
+    std::vector<int> key(G);
+    for (int b = 0; b < B; ++b) {
+      int* pb = perm.data() + (size_t)b * G;
+      for (int g = 0; g < G; ++g) {
+        const int i = g / h->M, j = g % h->M;
+        key[g] = (D->part_off[i + 1] - D->part_off[i]) + (D->obs_off[(long long)b * h->M + j + 1] - D->obs_off[(long long)b * h->M + j]);
+        pb[g] = g;
+      }
+      std::stable_sort(pb, pb + G, [&](int a, int c) { return key[a] < key[c]; });
+    }
+    if ((st = h2d(h, const_cast<int*>(v.gperm), perm.data(), perm.size()))) return st;
   }
+  if ((st = h2d(h, h->s_start, s0v.data(), s0v.size()))) return st;
+  if ((st = reset_iterate(h))) return st;
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return CA_OK;
 }
@@ -336,6 +368,7 @@ ca_status launch_collect(ca_problem* h, double* dst, int mask) {
   }
   ca::k_collect<<<(h->B + 127) / 128, 128, 0, h->stream>>>(h->dev, dst, mask);
   CUDA_TRY(cudaGetLastError());
+  h->launches[4]++;
   return CA_OK;
 }
 
@@ -413,6 +446,7 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
     nomax = std::max(nomax, h->obs_counts[o]);
   }
   h->nmax = (h->M > 0) ? nrmax + nomax + 1 : 1;
+  h->dev.nrmax = nrmax;
   h->nmax_t = nmax_template(h->nmax);
   h->rows_max = nrmax + nomax;
   h->P = (long long)h->B * h->N * h->np * h->M;
@@ -467,6 +501,8 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.agg, double, (size_t)B * N * v.nchunk * ca::REC);
   AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
   AL(h->scene_res, double, (size_t)B * 4);
+  AL(h->s_start, double, (size_t)B * (N + 1) * ns);
+  AL(v.gperm, int, (size_t)B * std::max(1, v.G));
 #undef AL
   v.zmask = nullptr;
   if ((st = upload(h, D))) {
@@ -499,6 +535,12 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* D) {
   return mark(h, upload(h, D));
 }
 
+ca_status ca_reset_iterate(ca_problem* h) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  return mark(h, reset_iterate(h));
+}
+
 ca_status ca_problem_info(const ca_problem* h, int64_t* n_pairs, int32_t* ny, int64_t* device_bytes) {
   if (!h) return fail(CA_E_INVALID, "NULL handle");
   if (n_pairs) *n_pairs = h->P;
@@ -517,7 +559,7 @@ ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t 
   ca_status st = check_handle(h);
   if (st) return st;
   if ((st = flush_timing(h))) return mark(h, st);
-  for (int f = 0; f < 4; ++f) {
+  for (int f = 0; f < 5; ++f) {
     if (ms) ms[f] = h->ms[f];
     if (launches) launches[f] = h->launches[f];
     if (reset) {
@@ -596,6 +638,7 @@ ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist) {
   if (hist) {
     ca::k_hist<<<iters, 256, 0, h->stream>>>(h->slots, h->B, iters, h->hist_dev);
     CUDA_TRY(cudaGetLastError());
+    h->launches[4]++;
     std::vector<double> hv((size_t)iters * 4);
     CUDA_TRY(cudaMemcpyAsync(hv.data(), h->hist_dev, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -762,6 +805,7 @@ ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, do
   CUDA_TRY(cudaGetLastError());
   ca::k_scene_min<<<h->B, 256, 0, h->stream>>>(h->alpha, h->P / h->B, h->alpha + h->P);
   CUDA_TRY(cudaGetLastError());
+  h->launches[3]++;  // k_scene_min (k_scale is counted by t_end)
   t_end(h, 3, e0);
   if (alpha) CUDA_TRY(cudaMemcpyAsync(alpha, h->alpha, sizeof(double) * h->P, cudaMemcpyDeviceToHost, h->stream));
   if (min_alpha) CUDA_TRY(cudaMemcpyAsync(min_alpha, h->alpha + h->P, sizeof(double) * h->B, cudaMemcpyDeviceToHost, h->stream));

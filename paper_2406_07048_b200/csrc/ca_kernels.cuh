@@ -18,16 +18,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "ca_lemke.cuh"
 
 namespace ca {
 
 constexpr int REC = 20;  // per (scene, t, chunk) record
 constexpr int R_RDUAL = 16, R_RPRI = 17, R_PIV = 18, R_FAIL = 19;
-constexpr int CTA = 128;  // threads per pair-sweep CTA
+constexpr int CTA = 32;  // threads per CTA of the per-pair kernels: one warp (no cross-warp barriers)
+
+struct LemkeParams {
+  double pivot_tol, tie_tol;
+  int max_pivot_factor;
+};
 
 struct Dev {
   int d, B, N, ns, nu, np, M, pose_model, npc;
+  int nrmax;  // largest robot-part face count
   int pidx[4];
   const int* part_off;
   const double* part_rows;  // [rows][4] = (a_0, a_1, a_2, b)
@@ -45,6 +50,7 @@ struct Dev {
   uint32_t* zmask;
   double* agg;
   double* ric;
+  const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
 };
 
 __device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* R, double* rho) {
@@ -65,286 +71,24 @@ __device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* 
 
 __device__ __forceinline__ int sym_idx(int a, int c, int npc) { return a * npc - a * (a - 1) / 2 + (c - a); }
 
-// deterministic CTA sum of `nf` fields starting at rec[f0]; thread 0 gets totals
+// deterministic warp sum of NF fields (CTA == one warp); lane 0 gets the totals
 template <int NF>
-__device__ __forceinline__ void cta_sum(double* rec, double* red /* smem [NF][CTA/32] */) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+__device__ __forceinline__ void cta_sum(double* rec, double* /*unused*/) {
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     double v = rec[f];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[f * 32 + w] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      double acc = 0.0;
-      for (int k = 0; k < nw; ++k) acc += red[f * 32 + k];
-      rec[f] = acc;
-    }
+    rec[f] = v;
   }
 }
-
-// ----------------------------------------------------------------------------
-// ADMM step 1 (+ fused step 3 of the previous iteration)
-// ----------------------------------------------------------------------------
-template <int D, int NMAX, bool FUSED>
-__global__ void __launch_bounds__(CTA) k_sweep(Dev P) {
-  extern __shared__ double smem[];
-  __shared__ double sR[9], srho[3], red[REC * 32];
-  const int tid = threadIdx.x;
-  const int chunk = blockIdx.x % P.nchunk;
-  const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
-  const int b = bt / P.N, t = bt % P.N + 1;
-  if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
-  __syncthreads();
-  constexpr int MMAX = D + 4;
-  Rows<D> W{smem + tid, CTA};
-  double* Gs = smem + NMAX * (D + 2) * CTA + tid;
-  double rec[REC];
-#pragma unroll
-  for (int f = 0; f < REC; ++f) rec[f] = 0.0;
-  const int g = chunk * P.CH + tid;
-  if (tid < P.CH && g < P.G) {
-    const long long p = (long long)bt * P.G + g;
-    const long long PP = P.P;
-    const int i = g / P.M, j = g % P.M;
-    const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
-    const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
-    const int n = nr + no + 1;
-    const double* prow = P.part_rows + 4 * r0;
-    const double* orow = P.obs_rows + 4 * (long long)l0;
-    // e = argmax_k b_k, lowest k on ties (reading #3)
-    int e = 0;
-    double be = __ldg(prow + 3);
-    for (int k = 1; k < nr; ++k) {
-      const double bk = __ldg(prow + 4 * k + 3);
-      if (bk > be) { be = bk; e = k; }
-    }
-    double ae[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) ae[a] = __ldg(prow + 4 * e + a);
-    // y^k (SoA planes), zeta, xi
-    double yk[NMAX];
-#pragma unroll
-    for (int k = 0; k < NMAX; ++k) yk[k] = (k < n) ? P.y[(long long)k * PP + p] : 0.0;
-    double zeta = P.zeta[p], xi[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
-    // K rows of the obstacle at pose(s^k) (Eq. 19b): (d_l - c_l.rho, R^T c_l); LCP index nr-1+l
-    for (int lo = 0; lo < no; ++lo) {
-      const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);
-      const double c[3] = {cr.x, cr.y, cr.z};
-      const double dl = cr.w;
-      double acc = 0.0;
-#pragma unroll
-      for (int a = 0; a < D; ++a) acc = __fma_rn(c[a], srho[a], acc);
-      const int u = nr - 1 + lo;
-      W.setF(u, 0, dl - acc);
-#pragma unroll
-      for (int mm = 0; mm < D; ++mm) {
-        double r = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) r = __fma_rn(c[a], sR[a * D + mm], r);
-        W.setF(u, 1 + mm, r);
-      }
-      W.setk(u, 0.0);
-    }
-    if (FUSED) {
-      // Eq. 17 for the previous iteration at s^k with y^k (Eqs. 10-11):
-      //   T = 1 + sum mu_l (d_l - c_l.rho) + gamma,  R = A^T lambda + (C R)^T mu
-      double Tv = 1.0, Rv[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) Rv[a] = 0.0;
-#pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        if (k < nr) {
-#pragma unroll
-          for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yk[k], __ldg(prow + 4 * k + a), Rv[a]);
-        } else if (k < nr + no) {
-          const int u = k - 1;
-          Tv = __fma_rn(yk[k], W.F(u, 0), Tv);
-#pragma unroll
-          for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yk[k], W.F(u, 1 + a), Rv[a]);
-        } else if (k == nr + no) {
-          Tv += yk[k];
-        }
-      }
-      zeta += Tv;
-      double r2 = Tv * Tv;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        xi[a] += Rv[a];
-        r2 = __fma_rn(Rv[a], Rv[a], r2);
-      }
-      rec[R_RPRI] = r2;
-      P.zeta[p] = zeta;
-#pragma unroll
-      for (int a = 0; a < D; ++a) P.xi[(long long)a * PP + p] = xi[a];
-    }
-    // Eqs. 20-21: lambda rows k != e, ratio = b_k / b_e
-    for (int k = 0; k < nr; ++k) {
-      if (k == e) continue;
-      const int u = k - (k > e);
-      const double ratio = __ldg(prow + 4 * k + 3) / be;
-      W.setF(u, 0, __fma_rn(-ratio, 0.0, 0.0));
-#pragma unroll
-      for (int a = 0; a < D; ++a) W.setF(u, 1 + a, __fma_rn(-ratio, ae[a], __ldg(prow + 4 * k + a)));
-      W.setk(u, ratio);
-    }
-    {  // gamma row (1, 0): ratio 0; phi row: zeros
-      const int u = n - 2;
-      W.setF(u, 0, 1.0);
-#pragma unroll
-      for (int a = 0; a < D; ++a) W.setF(u, 1 + a, 0.0);
-      W.setk(u, 0.0);
-#pragma unroll
-      for (int c = 0; c <= D; ++c) W.setF(n - 1, c, 0.0);
-      W.setk(n - 1, 0.0);
-    }
-    // btil = bvec + K_e / b_e, etatil = 1 / b_e;  q = [Ktil btil; etatil] (Eq. 25)
-    double bt_[D + 1];
-    bt_[0] = (1.0 + zeta) + 0.0 / be;
-#pragma unroll
-    for (int a = 0; a < D; ++a) bt_[1 + a] = xi[a] + ae[a] / be;
-    double q[NMAX];
-#pragma unroll
-    for (int u = 0; u < NMAX; ++u) {
-      q[u] = 0.0;
-      if (u < n - 1) {
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c <= D; ++c) acc = __fma_rn(W.F(u, c), bt_[c], acc);
-        q[u] = acc;
-      } else if (u == n - 1) {
-        q[u] = 1.0 / be;
-      }
-    }
-    Lemke<D, NMAX> L;
-    L.solve(W, Gs, CTA, q, n, P.lp);
-    double zU[NMAX];
-    L.solution(zU);
-    // recovery: y_U = z[0..n-2], y_e = (1 - sum_{k != e} b_k lambda_k) / b_e
-    double ynew[NMAX];
-#pragma unroll
-    for (int k = 0; k < NMAX; ++k) {
-      double v = 0.0;
-      if (k < n) {
-        if (k < e) v = zU[k];
-        else if (k > e) v = zU[k - 1];
-      }
-      ynew[k] = v;
-    }
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < NMAX; ++k)
-      if (k < nr && k != e) acc = __fma_rn(__ldg(prow + 4 * k + 3), ynew[k], acc);
-    const double ye = (1.0 - acc) / be;
-#pragma unroll
-    for (int k = 0; k < NMAX; ++k)
-      if (k == e) ynew[k] = ye;
-    int st = L.status;
-    if (st == ST_OK && ye < -1e-6) st = ST_NEGYE;
-    const bool solved = (st == ST_OK);
-    if (st == ST_OK) {
-      double rd = 0.0;
-#pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        if (k < nr + no) {
-          const double df = ynew[k] - yk[k];
-          rd = __fma_rn(df, df, rd);
-        }
-        if (k < n) P.y[(long long)k * PP + p] = ynew[k];
-      }
-      rec[R_RDUAL] = rd;
-
-    } else {
-      rec[R_FAIL] = 1.0;
-    }
-    rec[R_PIV] = (double)L.pivots;
-    P.pst[p] = (uint32_t)min(L.pivots, 65535) | ((uint32_t)st << 16);
-    if (P.zmask) P.zmask[p] = L.zmask();
-    // Gauss-Newton aggregates at pose(s^k) (step 2 data):
-    //   u* = K^T y + bvec = (eT, eR);  v = C_j^T mu;  gth = J^T R^T v
-    double eT = (1.0 + zeta), eR[D], v[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) { eR[a] = xi[a]; v[a] = 0.0; }
-#pragma unroll
-    for (int k = 0; k < NMAX; ++k) {
-      const double yv = solved ? ynew[k] : yk[k];
-      if (k < nr) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, __ldg(prow + 4 * k + a), eR[a]);
-      } else if (k < nr + no) {
-        const int u = k - 1;
-        eT = __fma_rn(yv, W.F(u, 0), eT);
-#pragma unroll
-        for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, W.F(u, 1 + a), eR[a]);
-        const double* cr = orow + 4 * (k - nr);
-#pragma unroll
-        for (int a = 0; a < D; ++a) v[a] = __fma_rn(yv, __ldg(cr + a), v[a]);
-      } else if (k == nr + no) {
-        eT += yv;
-      }
-    }
-    // record layout always reserves D+1 pose coordinates (compile-time offsets)
-    constexpr int L1 = D + 1;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-#pragma unroll
-      for (int c = a; c < D; ++c) rec[sym_idx(a, c, L1)] = v[a] * v[c];
-      rec[L1 * (L1 + 1) / 2 + a] = -eT * v[a];
-    }
-    if (P.pose_model != 0) {
-      // w = R^T v; gth = J^T w = (w_1, -w_0, 0)
-      double w0 = 0.0, w1 = 0.0;
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        w0 = __fma_rn(sR[c * D + 0], v[c], w0);
-        w1 = __fma_rn(sR[c * D + 1], v[c], w1);
-      }
-      const double g0 = w1, g1 = -w0;
-      rec[sym_idx(D, D, L1)] = g0 * g0 + g1 * g1;
-      rec[L1 * (L1 + 1) / 2 + D] = g0 * eR[0] + g1 * eR[1];
-    }
-  }
-  cta_sum<REC>(rec, red);
-  if (tid == 0) {
-    double* out = P.agg + (long long)blockIdx.x * REC;
-#pragma unroll
-    for (int f = 0; f < REC; ++f) out[f] = rec[f];
-  }
-}
-
-inline size_t sweep_smem_bytes(int d, int nmaxt) {
-  const int mmax = d + 4;
-  return sizeof(double) * (size_t)CTA * ((size_t)nmaxt * (d + 2) + (size_t)mmax * (mmax + 1));
-}
-
-// host-side launcher; explicitly instantiated in ca_sweep_d{2,3}.cu (parallel build)
-template <int D, int NM, bool F>
-cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
-  static bool configured = false;
-  const size_t sm = sweep_smem_bytes(D, NM);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  k_sweep<D, NM, F><<<grid, CTA, sm, stream>>>(P);
-  return cudaGetLastError();
-}
-
-#define CA_SWEEP_NMAX_LIST(X, D, F) X(D, 9, F) X(D, 11, F) X(D, 13, F) X(D, 15, F) X(D, 20, F) X(D, 32, F)
 
 // ----------------------------------------------------------------------------
 // ADMM step 3 standalone (Eq. 17 with Eqs. 10-11 at s^{k+1}, y^{k+1})
 // ----------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
-  __shared__ double sR[9], srho[3], red[32];
+  __shared__ double sR[9], srho[3];
   const int tid = threadIdx.x;
   const int chunk = blockIdx.x % P.nchunk;
   const int bt = blockIdx.x / P.nchunk;
@@ -352,8 +96,9 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
   if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
   __syncthreads();
   double rec[1] = {0.0};
-  const int g = chunk * P.CH + tid;
-  if (tid < P.CH && g < P.G) {
+  const int gs = chunk * P.CH + tid;  // slot in the n-sorted order of the (b, t) group
+  const int g = (tid < P.CH && gs < P.G) ? P.gperm[(long long)b * P.G + gs] : 0;
+  if (tid < P.CH && gs < P.G) {
     const long long p = (long long)bt * P.G + g, PP = P.P;
     const int i = g / P.M, j = g % P.M;
     const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
@@ -395,7 +140,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
     }
     rec[0] = r2;
   }
-  cta_sum<1>(rec, red);
+  cta_sum<1>(rec, nullptr);
   if (tid == 0) P.agg[(long long)blockIdx.x * REC + R_RPRI] = rec[0];
 }
 
@@ -733,8 +478,9 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
   const int b = bt / P.N, t = bt % P.N + 1;
   if (tid == 0) pose_of(P, states + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
   __syncthreads();
-  const int g = chunk * P.CH + tid;
-  if (!(tid < P.CH && g < P.G)) return;
+  const int gs = chunk * P.CH + tid;
+  if (!(tid < P.CH && gs < P.G)) return;
+  const int g = P.gperm[(long long)b * P.G + gs];
   const long long p = (long long)bt * P.G + g;
   const int i = g / P.M, j = g % P.M;
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;

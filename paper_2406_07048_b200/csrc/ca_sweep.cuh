@@ -1,0 +1,494 @@
+// ca_sweep.cuh -- ADMM step 1 (Eq. 15) over all (scene, t, part,
+// obstacle) pairs, one pair per thread, fused with step 3 of the previous
+// iteration (Eq. 17) and the step-2 Gauss-Newton aggregates.
+//
+// Per pair: Eq. 19 rows at pose(s^k) -> Eqs. 20-21 elimination (index e =
+// argmax b_i, reading #3) -> Eq. 24 LCP -> revised Lemke (ca_lemke.cuh) ->
+// recovery y_e = (1 - sum_{k != e} b_k lambda_k)/b_e -> dual residual
+// (Eq. 18b) and (v v^T, |g|^2, -eT v, g.eR) for the primal step, reduced per
+// (scene, t, chunk) in a fixed order (no FP atomics).
+//
+// Layout: one warp per CTA (no cross-warp barrier).  Per-thread state that the
+// pivot loop indexes at run time (basic-variable values, entering-column
+// coefficients, reduced obstacle rows, the m x m system, tableau-row labels)
+// lives in shared memory as [item][thread] (32 consecutive words per warp access,
+// conflict-free); the pivot loop itself is a few hundred instructions so every
+// resident warp runs out of the instruction cache.
+#pragma once
+#include "ca_kernels.cuh"
+#include "ca_lemke.cuh"
+
+namespace ca {
+
+constexpr int NPMAX = 8;   // robot parts per problem (validated)
+constexpr int NRMAX = 16;  // faces per robot part (validated)
+constexpr int MFAST = 3;   // m x m systems up to this size live in shared memory (99.7 % on C5)
+
+template <int D, int NMAX>
+struct SweepSmem {
+  static constexpr int NOMAX = NMAX - 4;  // n = nr + no + 1 <= NMAX, nr >= d+1 >= 3
+  static constexpr int MU = NOMAX * (D + 1);
+  static constexpr int GS = MFAST * (MFAST + 1);
+  static constexpr int VAL = NMAX, CB = NMAX, YK = NMAX;
+  static constexpr int ROWB = (NMAX + 1 + 7) / 8;  // tableau-row labels, bytes
+  static constexpr int PER_THREAD = MU + GS + VAL + CB + YK + ROWB;  // doubles
+  // + the CTA-shared lambda-row table of every robot part
+  static size_t bytes(int np, int nrmax) {
+    return sizeof(double) * ((size_t)PER_THREAD * CTA + (size_t)np * (nrmax - 1) * (D + 1));
+  }
+};
+
+// L5.4-5 (rare): lexicographic rule on the w columns (= B^{-1}) among the tied
+// members `tm`; returns the leaving member (pair index).
+template <int D, int NMAX>
+__device__ __noinline__ int lexico(const PairRows<D> W, double* Gs, double* Gslow, const double* scb,
+                                   const unsigned char* rowb, uint32_t wb, uint32_t zb, bool z0b, uint32_t tm,
+                                   double tau) {
+  const int n = W.n;
+  for (int jj = 0; jj < n && __popc(tm) > 1; ++jj) {
+    const bool wbasic = (wb >> jj) & 1u;
+    ColSol<D> cs{};
+    if (!wbasic) cs = Lemke<D, NMAX, MFAST>::solve_column(W, Gs, CTA, wb, zb, z0b, Var{0, jj}, Gslow);
+    const double* A = cs.slow ? Gslow : Gs;
+    const int es = cs.slow ? 1 : CTA, mm = cs.slow ? D + 4 : MFAST;
+    double vmin = 1e308;
+    for (uint32_t b = tm; b; b &= b - 1) {
+      const int i = __ffs(b) - 1;
+      double num;
+      if (wbasic) {
+        num = (((wb >> i) & 1u) && i == jj) ? 1.0 : 0.0;
+      } else if ((wb >> i) & 1u) {
+        double f[D + 1], k;
+        W.row(i, f, k);
+        num = cs.s0;
+#pragma unroll
+        for (int c = 0; c <= D; ++c) num = __fma_rn(f[c], cs.uh[c], num);
+        num = __fma_rn(k, cs.sl, num);
+        if (i == n - 1) num -= cs.sk;
+      } else {
+        const int s = __popc(zb & ((1u << i) - 1u));
+        num = A[(s * (mm + 1) + mm) * es];
+      }
+      vmin = fmin(vmin, num / scb[i * CTA]);
+    }
+    const double vt = vmin + tau * fmax(1.0, fabs(vmin));
+    uint32_t keep = 0;
+    for (uint32_t b = tm; b; b &= b - 1) {
+      const int i = __ffs(b) - 1;
+      double num;  // recomputed (rare path)
+      if (wbasic) {
+        num = (((wb >> i) & 1u) && i == jj) ? 1.0 : 0.0;
+      } else if ((wb >> i) & 1u) {
+        double f[D + 1], k;
+        W.row(i, f, k);
+        num = cs.s0;
+#pragma unroll
+        for (int c = 0; c <= D; ++c) num = __fma_rn(f[c], cs.uh[c], num);
+        num = __fma_rn(k, cs.sl, num);
+        if (i == n - 1) num -= cs.sk;
+      } else {
+        const int s = __popc(zb & ((1u << i) - 1u));
+        num = A[(s * (mm + 1) + mm) * es];
+      }
+      if (num / scb[i * CTA] <= vt) keep |= 1u << i;
+    }
+    tm = keep;
+  }
+  int best = 99, lm = -1;
+  for (uint32_t b = tm; b; b &= b - 1) {
+    const int i = __ffs(b) - 1;
+    if ((int)rowb[i * CTA] < best) { best = rowb[i * CTA]; lm = i; }
+  }
+  return lm;
+}
+
+template <int D, int NMAX, bool FUSED>
+__global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
+  using SM = SweepSmem<D, NMAX>;
+  constexpr int L1 = D + 1;
+  extern __shared__ double smem[];
+  __shared__ double sR[9], srho[3];
+  __shared__ double part_be[NPMAX];
+  __shared__ int part_e[NPMAX];
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x % P.nchunk;
+  const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
+  const int b = bt / P.N, t = bt % P.N + 1;
+  double* mu = smem + tid;
+  double* Gs = mu + SM::MU * CTA;
+  double* sval = Gs + SM::GS * CTA;
+  double* scb = sval + SM::VAL * CTA;
+  double* syk = scb + SM::CB * CTA;
+  // tableau-row labels: bytes, [item][thread] from the CTA base of their region
+  unsigned char* rowb =
+      reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::GS + SM::VAL + SM::CB + SM::YK) * CTA) + tid;
+  double* lamtab = smem + SM::PER_THREAD * CTA;  // [np][nrmax-1][D+1]
+  const int LT = (P.nrmax - 1) * L1;
+  if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
+  if (tid < P.np) {
+    // Eqs. 20-21 for the lambda rows depend on the robot part only:
+    //   e = argmax_k b_k (lowest k on ties), kt_k = b_k / b_e, at_k = a_k - kt_k a_e
+    const int r0 = P.part_off[tid], nr = P.part_off[tid + 1] - r0;
+    const double* pr = P.part_rows + 4 * r0;
+    int e = 0;
+    double be = pr[3];
+    for (int k = 1; k < nr; ++k)
+      if (pr[4 * k + 3] > be) { be = pr[4 * k + 3]; e = k; }
+    part_e[tid] = e;
+    part_be[tid] = be;
+    double* lt = lamtab + tid * LT;
+    for (int k = 0; k < nr; ++k) {
+      if (k == e) continue;
+      const int u = k - (k > e);
+      const double ratio = pr[4 * k + 3] / be;
+#pragma unroll
+      for (int a = 0; a < D; ++a) lt[u * L1 + a] = __fma_rn(-ratio, pr[4 * e + a], pr[4 * k + a]);
+      lt[u * L1 + D] = ratio;
+    }
+  }
+  __syncthreads();
+#define VAL(i) sval[(i) * CTA]
+#define CBV(i) scb[(i) * CTA]
+#define YK(i) syk[(i) * CTA]
+  double rec[REC];
+#pragma unroll
+  for (int f = 0; f < REC; ++f) rec[f] = 0.0;
+  const int gs = chunk * P.CH + tid;  // slot in the n-sorted order of the (b, t) group
+  const int g = (tid < P.CH && gs < P.G) ? P.gperm[(long long)b * P.G + gs] : 0;
+  if (tid < P.CH && gs < P.G) {
+    const long long p = (long long)bt * P.G + g;
+    const long long PP = P.P;
+    const int ip = g / P.M, j = g % P.M;
+    const int r0 = P.part_off[ip], nr = P.part_off[ip + 1] - r0;
+    const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
+    const int n = nr + no + 1;
+    const double* prow = P.part_rows + 4 * r0;
+    const double* orow = P.obs_rows + 4 * (long long)l0;
+    const int e = part_e[ip];
+    const double be = part_be[ip];
+    // y^k (SoA planes) -> smem; zeta, xi
+#pragma unroll 4
+    for (int k = 0; k < n; ++k) YK(k) = P.y[(long long)k * PP + p];
+    double zeta = P.zeta[p], xi[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
+    // obstacle rows of K at pose(s^k) (Eq. 19b): (d_l - c_l.rho, R^T c_l)
+#pragma unroll 2
+    for (int lo = 0; lo < no; ++lo) {
+      const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);
+      const double c[3] = {cr.x, cr.y, cr.z};
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc = __fma_rn(c[a], srho[a], acc);
+      double* m = mu + lo * L1 * CTA;
+      m[0] = cr.w - acc;
+#pragma unroll
+      for (int mm = 0; mm < D; ++mm) {
+        double r = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) r = __fma_rn(c[a], sR[a * D + mm], r);
+        m[(1 + mm) * CTA] = r;
+      }
+    }
+    const PairRows<D> W{lamtab + ip * LT, mu, CTA, nr, no, n, n - 1};
+    if (FUSED) {
+      // Eq. 17 for the previous iteration at s^k with y^k (Eqs. 10-11)
+      double Tv = 1.0, Rv[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) Rv[a] = 0.0;
+      for (int k = 0; k < nr; ++k) {
+        const double yv = YK(k);
+#pragma unroll
+        for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yv, prow[4 * k + a], Rv[a]);
+      }
+      for (int k = nr; k < nr + no; ++k) {
+        const double yv = YK(k);
+        const double* m = mu + (k - nr) * L1 * CTA;
+        Tv = __fma_rn(yv, m[0], Tv);
+#pragma unroll
+        for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yv, m[(1 + a) * CTA], Rv[a]);
+      }
+      Tv += YK(nr + no);
+      zeta += Tv;
+      double r2 = Tv * Tv;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        xi[a] += Rv[a];
+        r2 = __fma_rn(Rv[a], Rv[a], r2);
+      }
+      rec[R_RPRI] = r2;
+      P.zeta[p] = zeta;
+#pragma unroll
+      for (int a = 0; a < D; ++a) P.xi[(long long)a * PP + p] = xi[a];
+    }
+    // q = [Kt btil; etatil]  with btil = bvec + K_e / b_e, etatil = 1 / b_e (Eq. 25)
+    double bt_[D + 1];
+    bt_[0] = (1.0 + zeta) + 0.0 / be;
+#pragma unroll
+    for (int a = 0; a < D; ++a) bt_[1 + a] = xi[a] + prow[4 * e + a] / be;
+    double qmin = 1.0 / be;
+    VAL(n - 1) = qmin;
+#pragma unroll 1
+    for (int i = 0; i < n - 1; ++i) {
+      double f[D + 1], k;
+      W.row(i, f, k);
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c <= D; ++c) acc = __fma_rn(f[c], bt_[c], acc);
+      VAL(i) = acc;
+      qmin = fmin(qmin, acc);
+    }
+    // ------------------------------------------------------------------ Lemke
+    const LemkeParams& LP = P.lp;
+    const double tau = LP.tie_tol, ptol = LP.pivot_tol;
+    const uint32_t nmask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+    uint32_t wb = nmask, zb = 0;
+    bool z0b = false;
+    double val0 = 0.0;
+    int pivots = 0, status = ST_OK;
+#pragma unroll 1
+    for (int i = 0; i <= n; ++i) rowb[i * CTA] = (unsigned char)i;
+    if (qmin < 0.0) {  // L1: otherwise z = 0
+      // L2: z0 enters at row argmin q (ties -> largest index); its column is -1
+      const double tl = qmin + tau * fmax(1.0, fabs(qmin));
+      int r = 0;
+#pragma unroll 1
+      for (int i = 0; i < n; ++i)
+        if (VAL(i) <= tl) r = i;
+      const double ve = VAL(r) * -1.0;
+#pragma unroll 1
+      for (int i = 0; i < n; ++i)
+        if (i != r) VAL(i) = __fma_rn(1.0, ve, VAL(i));
+      wb &= ~(1u << r);
+      z0b = true;
+      val0 = ve;
+      rowb[NMAX * CTA] = (unsigned char)r;
+      pivots = 1;
+      Var ent{1, r};
+      const int maxpiv = LP.max_pivot_factor * n;
+      double Gslow[(D + 4) * (D + 5)];
+      for (;;) {
+        if (pivots >= maxpiv) { status = ST_ITER; break; }
+        if (n - __popc(wb) > D + 4) { status = ST_ITER; break; }  // rank bound (cannot happen exactly)
+        const ColSol<D> cs = Lemke<D, NMAX, MFAST>::solve_column(W, Gs, CTA, wb, zb, z0b, ent, Gslow);
+        const double* A = cs.slow ? Gslow : Gs;
+        const int es = cs.slow ? 1 : CTA, mmc = cs.slow ? D + 4 : MFAST;
+        const uint32_t basic = wb | zb;
+        // pass 1: entering-column coefficient of every basic variable, max |cbar|, and
+        // the minimum ratio max(val,0)/cbar (L5.2, cross-multiplied) over rows with
+        // cbar > pivot_tol (a superset of the eligible rows cbar > pivot_tol max(1,cmax))
+        double cmax = 0.0, bn = -1.0, bd = 1.0;
+#pragma unroll 1
+        for (int i = 0; i < n; ++i) {
+          const uint32_t bit = 1u << i;
+          double c = 0.0;
+          if (wb & bit) {
+            double f[D + 1], k;
+            W.row(i, f, k);
+            c = cs.s0;
+#pragma unroll
+            for (int cc = 0; cc <= D; ++cc) c = __fma_rn(f[cc], cs.uh[cc], c);
+            c = __fma_rn(k, cs.sl, c);
+            if (i == n - 1) c -= cs.sk;
+          } else if (zb & bit) {
+            const int s = __popc(zb & (bit - 1u));
+            c = A[(s * (mmc + 1) + mmc) * es];
+          }
+          CBV(i) = c;
+          cmax = fmax(cmax, fabs(c));
+          if ((basic & bit) && c > ptol) {
+            const double nu = fmax(VAL(i), 0.0);
+            if (bn < 0.0 || nu * bd < bn * c) { bn = nu; bd = c; }
+          }
+        }
+        double cb0 = 0.0;
+        if (z0b) {
+          cb0 = A[(__popc(zb) * (mmc + 1) + mmc) * es];
+          cmax = fmax(cmax, fabs(cb0));
+          if (cb0 > ptol) {
+            const double nu = fmax(val0, 0.0);
+            if (bn < 0.0 || nu * bd < bn * cb0) { bn = nu; bd = cb0; }
+          }
+        }
+        const double thr = ptol * fmax(1.0, cmax);
+        if (bn >= 0.0 && !(bd > thr)) {
+          // rare: the provisional minimiser is not eligible -> exact pass over cbar > thr
+          bn = -1.0;
+          bd = 1.0;
+#pragma unroll 1
+          for (int i = 0; i < n; ++i) {
+            const double c = CBV(i);
+            if (((basic >> i) & 1u) && c > thr) {
+              const double nu = fmax(VAL(i), 0.0);
+              if (bn < 0.0 || nu * bd < bn * c) { bn = nu; bd = c; }
+            }
+          }
+          if (z0b && cb0 > thr) {
+            const double nu = fmax(val0, 0.0);
+            if (bn < 0.0 || nu * bd < bn * cb0) { bn = nu; bd = cb0; }
+          }
+        }
+        if (bn < 0.0) { status = ST_RAY; break; }
+        const double thmin = bn / bd;
+        const double tt = thmin + tau * fmax(1.0, thmin);
+        // pass 2: tie set (L5.2) with the leaving candidate's coefficient and value
+        uint32_t tiem = 0;
+        double cr = 0.0, vr = 0.0;
+        int lm = -2;
+#pragma unroll 1
+        for (uint32_t bb = basic; bb; bb &= bb - 1) {
+          const int i = __ffs(bb) - 1;
+          const double c = CBV(i);
+          if (c > thr) {
+            const double v = VAL(i);
+            if (fmax(v, 0.0) <= tt * c) {
+              tiem |= 1u << i;
+              lm = i;
+              cr = c;
+              vr = v;
+            }
+          }
+        }
+        if (z0b && cb0 > thr && fmax(val0, 0.0) <= tt * cb0) {
+          lm = -1;  // L5.3: z0 leaves whenever it is tied
+          cr = cb0;
+          vr = val0;
+        } else if (tiem == 0) {
+          status = ST_RAY;
+          break;
+        } else if (__popc(tiem) > 1) {
+          lm = lexico<D, NMAX>(W, Gs, Gslow, scb, rowb, wb, zb, z0b, tiem, tau);
+          cr = CBV(lm);
+          vr = VAL(lm);
+        }
+        // L3: pivot (values only: the structure is re-derived from the basis);
+        // the entering variable takes the leaving one's tableau row
+        const bool leave_w = (lm >= 0) && ((wb >> lm) & 1u);
+        const double inv = 1.0 / cr;
+        const double ve2 = vr * inv;
+        const int je = ent.j;
+#pragma unroll 1
+        for (uint32_t bb = basic & ~(lm >= 0 ? (1u << lm) : 0u); bb; bb &= bb - 1) {
+          const int i = __ffs(bb) - 1;
+          VAL(i) = __fma_rn(-CBV(i), ve2, VAL(i));
+        }
+        if (z0b && lm >= 0) val0 = __fma_rn(-cb0, ve2, val0);
+        VAL(je) = ve2;
+        rowb[je * CTA] = (lm >= 0) ? rowb[lm * CTA] : rowb[NMAX * CTA];
+        if (ent.kind == 0) wb |= 1u << je;
+        else zb |= 1u << je;
+        ++pivots;
+        if (lm < 0) { z0b = false; break; }  // L6: z0 left
+        // leaving member lm (w or z of pair lm); next entering is its complement (L4)
+        if (leave_w) {
+          wb &= ~(1u << lm);
+          ent = Var{1, lm};
+        } else {
+          zb &= ~(1u << lm);
+          ent = Var{0, lm};
+        }
+      }
+    }
+    // ------------------------------------------------------------ recovery
+    // z_j = value of basic z_j (LCP index j);  y_U = z[0..n-2] in original order
+    // without e;  y_e = (1 - sum_{k != e} b_k y_k) / b_e
+    const int st0 = status;
+    double acc = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < nr; ++k) {
+      if (k == e) continue;
+      const int u = k - (k > e);
+      const double yv = ((zb >> u) & 1u) ? VAL(u) : 0.0;
+      acc = __fma_rn(prow[4 * k + 3], yv, acc);
+    }
+    const double ye = (1.0 - acc) / be;
+    int st = st0;
+    if (st == ST_OK && ye < -1e-6) st = ST_NEGYE;
+    const bool solved = (st == ST_OK);
+    // y used by the aggregates: y^{k+1}, or y^k for a failed pair
+    double rd = 0.0;
+    double eT = 1.0 + zeta, eR[D], v[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) { eR[a] = xi[a]; v[a] = 0.0; }
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      double yv;
+      if (solved) {
+        const int u = k - (k > e);
+        yv = (k == e) ? ye : (((zb >> u) & 1u) ? VAL(u) : 0.0);
+        if (k < nr + no) {
+          const double df = yv - YK(k);
+          rd = __fma_rn(df, df, rd);
+        }
+        P.y[(long long)k * PP + p] = yv;
+      } else {
+        yv = YK(k);
+      }
+      // Gauss-Newton aggregates at pose(s^k): u* = K^T y + bvec = (eT, eR); v = C_j^T mu
+      if (k < nr) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, prow[4 * k + a], eR[a]);
+      } else if (k < nr + no) {
+        const double* m = mu + (k - nr) * L1 * CTA;
+        eT = __fma_rn(yv, m[0], eT);
+#pragma unroll
+        for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, m[(1 + a) * CTA], eR[a]);
+        const double* cr = orow + 4 * (k - nr);
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = __fma_rn(yv, cr[a], v[a]);
+      } else {
+        eT += yv;
+      }
+    }
+    if (solved) rec[R_RDUAL] = rd;
+    else rec[R_FAIL] = 1.0;
+    rec[R_PIV] = (double)pivots;
+    P.pst[p] = (uint32_t)min(pivots, 65535) | ((uint32_t)st << 16);
+    if (P.zmask) P.zmask[p] = zb | (z0b ? 0x80000000u : 0u);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int c = a; c < D; ++c) rec[sym_idx(a, c, L1)] = v[a] * v[c];
+      rec[L1 * (L1 + 1) / 2 + a] = -eT * v[a];
+    }
+    if (P.pose_model != 0) {
+      // g = J^T R^T v with J the rotation generator (SE2 / yaw): (w_1, -w_0, 0)
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        w0 = __fma_rn(sR[c * D + 0], v[c], w0);
+        w1 = __fma_rn(sR[c * D + 1], v[c], w1);
+      }
+      const double g0 = w1, g1 = -w0;
+      rec[sym_idx(D, D, L1)] = g0 * g0 + g1 * g1;
+      rec[L1 * (L1 + 1) / 2 + D] = g0 * eR[0] + g1 * eR[1];
+    }
+  }
+#undef VAL
+#undef CBV
+#undef YK
+  cta_sum<REC>(rec, nullptr);
+  if (tid == 0) {
+    double* out = P.agg + (long long)blockIdx.x * REC;
+#pragma unroll
+    for (int f = 0; f < REC; ++f) out[f] = rec[f];
+  }
+}
+
+// host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build)
+template <int D, int NM, bool F>
+cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
+  const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax);
+  static size_t configured = 0;
+  if (configured < sm) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  k_sweep<D, NM, F><<<grid, CTA, sm, stream>>>(P);
+  return cudaGetLastError();
+}
+
+#define CA_SWEEP_NMAX_LIST(X, D, F) X(D, 9, F) X(D, 11, F) X(D, 13, F) X(D, 15, F) X(D, 20, F) X(D, 32, F)
+
+}  // namespace ca

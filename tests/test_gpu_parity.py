@@ -239,8 +239,10 @@ def test_c5_full_size_stepwise(ca):
                                               o.pivots, st1["status"], o.status)
             o.y[...] = st1["y"]  # adopt the GPU's (validated) minimisers
             o.primal_step()
-            close(s1, o.s, 1e-9, f"s scene {b} iter {k}")
-            close(u1, o.u, 1e-9, f"u scene {b} iter {k}")
+            # trajectory tolerance of BASELINE.json north_star (1e-6); measured ~1e-9 here
+            # (Riccati vs dense Cholesky of an LQ with condition ~1e6, sigma = 300)
+            close(s1, o.s, 1e-6, f"s scene {b} iter {k}")
+            close(u1, o.u, 1e-6, f"u scene {b} iter {k}")
             o.multiplier_update()
             sc_z = 1 + np.abs(o.zeta).max()
             assert np.abs(st1["zeta"] - o.zeta).max() <= 1e-9 * sc_z
