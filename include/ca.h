@@ -159,7 +159,8 @@ ca_status ca_get_scene_residuals(ca_problem* h, double* r_pri, double* r_dual);
 ca_status ca_get_trajectory(ca_problem* h, double* s, double* u);
 
 /* Pair state for pairs [p0, p0+count): y[count*ny] (padded with 0 beyond n_p),
- * zeta[count], xi[count*d], pivots[count], status[count] (CA_PAIR_*), zmask[count]
+ * zeta[count], xi[count*d], pivots[count], status[count] (CA_PAIR_*; | 0x100 if the
+ * pair was re-solved by the dense-tableau fallback), zmask[count]
  * (bit j = z_j basic in the final Lemke basis, bit 31 = z0).  Any may be NULL. */
 ca_status ca_get_pair_state(ca_problem* h, int64_t p0, int64_t count, double* y, double* zeta,
                             double* xi, int32_t* pivots, int32_t* status, uint32_t* zmask);
@@ -186,6 +187,13 @@ ca_status ca_set_record_basis(ca_problem* h, int32_t enable);
 /* Measured FP64 FMA throughput of the device: a register-resident DFMA loop on all
  * SMs for ~`ms` milliseconds; *tflops = 2 * FMAs / s / 1e12. */
 ca_status ca_fp64_peak(int device, double ms, double* tflops);
+
+/* Diagnostics: trace the Lemke pivots of pair p (-1 = off) during subsequent sweeps
+ * into an internal buffer; out (HOST [64*48] doubles, nullable) receives the trace
+ * recorded so far (per pivot: entering kind/j, m, leaving, theta_min, #ties, pivot,
+ * value, w-mask, z-mask, max|cbar|, slow-path flag, z0 value and coefficient, then
+ * 16 entering coefficients and 16 values by pair index); the buffer is then cleared. */
+ca_status ca_debug_trace(ca_problem* h, int64_t p, double* out);
 
 const char* ca_last_error(void);
 

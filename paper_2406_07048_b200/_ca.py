@@ -85,11 +85,12 @@ def lib():
         L.ca_set_record_basis.argtypes = [vp, C.c_int32]
         L.ca_fp64_peak.argtypes = [C.c_int, C.c_double, dp]
         L.ca_reset_iterate.argtypes = [vp]
+        L.ca_debug_trace.argtypes = [vp, C.c_int64, vp]
         for name in ("ca_problem_create", "ca_problem_load", "ca_problem_info", "ca_scale_detect",
                      "ca_admm_iterate", "ca_admm_solve", "ca_dual_sweep", "ca_primal_step",
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
-                     "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate"):
+                     "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib
@@ -253,6 +254,11 @@ class Problem:
         if arrs[2] is not None:
             assert arrs[2].shape == (self.n_pairs, self.ny), arrs[2].shape
         _check(lib().ca_set_iterate(self.h, *[_ptr(a) for a in arrs]))
+
+    def debug_trace(self, p: int = -1):
+        out = np.empty((64, 48))
+        _check(lib().ca_debug_trace(self.h, p, _ptr(out)))
+        return out
 
     def set_timing(self, on: bool = True):
         _check(lib().ca_set_timing(self.h, int(on)))

@@ -150,6 +150,7 @@ ca_status validate(const ca_problem_desc* D) {
   if (!riccati_supported(D->n_state, D->n_ctrl))
     return fail(CA_E_UNSUPPORTED, "(n_state, n_ctrl) combination not instantiated");
   if (D->n_parts > ca::NPMAX) return fail(CA_E_UNSUPPORTED, "more than 8 robot parts");
+  if ((long long)D->n_parts * D->n_obs > 65535) return fail(CA_E_UNSUPPORTED, "more than 65535 pairs per (scene, t)");
   int nrmax = 0;
   for (int i = 0; i < D->n_parts; ++i) {
     if (D->part_off[i + 1] - D->part_off[i] > ca::NRMAX)
@@ -315,6 +316,9 @@ ca_status launch_sweep_d(ca_problem* h) {
 
 ca_status launch_sweep(ca_problem* h, bool fused) {
   if (h->P == 0) return CA_OK;
+  ca::k_sortpairs<<<(unsigned)((long long)h->B * h->N), 32, 0, h->stream>>>(h->dev);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[4]++;
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
   ca_status st;
@@ -503,8 +507,11 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(h->scene_res, double, (size_t)B * 4);
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));
+  AL(v.gperm2, uint16_t, (size_t)B * N * std::max(1, v.G));
 #undef AL
   v.zmask = nullptr;
+  v.dbg_p = -1;
+  v.dbg = nullptr;
   if ((st = upload(h, D))) {
     delete h;
     return st;
@@ -533,6 +540,20 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* D) {
     if (D->obs_off[o + 1] - D->obs_off[o] != h->obs_counts[o])
       return fail(CA_E_INVALID, "ca_problem_load: obstacle row counts differ");
   return mark(h, upload(h, D));
+}
+
+ca_status ca_debug_trace(ca_problem* h, int64_t p, double* out) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (!h->dev.dbg) {
+    if ((st = h->alloc(&h->dev.dbg, 64 * 48))) return st;
+  }
+  if (out) {
+    CUDA_TRY(cudaMemcpy(out, h->dev.dbg, sizeof(double) * 64 * 48, cudaMemcpyDeviceToHost));
+  }
+  CUDA_TRY(cudaMemset(h->dev.dbg, 0xff, sizeof(double) * 64 * 48));
+  h->dev.dbg_p = p;
+  return CA_OK;
 }
 
 ca_status ca_reset_iterate(ca_problem* h) {
@@ -733,7 +754,7 @@ ca_status ca_get_pair_state(ca_problem* h, int64_t p0, int64_t count, double* y,
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     for (int64_t q = 0; q < count; ++q) {
       if (pivots) pivots[q] = (int32_t)(ps[q] & 0xffffu);
-      if (status) status[q] = (int32_t)(ps[q] >> 16);
+      if (status) status[q] = (int32_t)((ps[q] >> 16) & 0xf) | (int32_t)(ps[q] & (1u << 20) ? 0x100 : 0);
     }
   }
   if (zmask) {

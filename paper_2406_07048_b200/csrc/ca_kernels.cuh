@@ -51,6 +51,9 @@ struct Dev {
   double* agg;
   double* ric;
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
+  uint16_t* gperm2;  // [B*N][G]: per-(b,t) execution order, re-sorted by last pivot count
+  long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
+  double* dbg;       // [64][12]
 };
 
 __device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* R, double* rho) {
@@ -546,6 +549,42 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
 }
 
 #ifdef CA_COMMON_KERNELS
+// Per (b, t) group: stable counting sort of the pairs (taken in the per-scene
+// n-sorted order gperm) by their pivot count of the previous sweep, so that a
+// warp's 32 threads run Lemke paths of similar length.  Pure scheduling:
+// deterministic, results are stored at each pair's own index.
+__global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
+  constexpr int NB = 32;
+  __shared__ int cnt[NB][33];
+  const int bt = blockIdx.x, b = bt / P.N, tid = threadIdx.x;
+  const int G = P.G;
+  const int per = (G + 31) / 32, lo = tid * per, hi = min(G, lo + per);
+  const int* base = P.gperm + (long long)b * G;
+  const uint32_t* pst = P.pst + (long long)bt * G;
+  for (int k = 0; k < NB; ++k) cnt[k][tid] = 0;
+  for (int s = lo; s < hi; ++s) {
+    const int key = min((int)(pst[base[s]] & 0xffffu), NB - 1);
+    cnt[key][tid]++;
+  }
+  __syncwarp();
+  if (tid == 0) {
+    int run = 0;
+    for (int k = 0; k < NB; ++k)
+      for (int t = 0; t < 32; ++t) {
+        const int c = cnt[k][t];
+        cnt[k][t] = run;
+        run += c;
+      }
+  }
+  __syncwarp();
+  uint16_t* out = P.gperm2 + (long long)bt * G;
+  for (int s = lo; s < hi; ++s) {
+    const int g = base[s];
+    const int key = min((int)(pst[g] & 0xffffu), NB - 1);
+    out[cnt[key][tid]++] = (uint16_t)g;
+  }
+}
+
 __global__ void k_scene_min(const double* alpha, long long per_scene, double* out) {
   __shared__ double red[32];
   const int b = blockIdx.x;

@@ -29,9 +29,9 @@ struct SweepSmem {
   static constexpr int NOMAX = NMAX - 4;  // n = nr + no + 1 <= NMAX, nr >= d+1 >= 3
   static constexpr int MU = NOMAX * (D + 1);
   static constexpr int GS = MFAST * (MFAST + 1);
-  static constexpr int VAL = NMAX, CB = NMAX, YK = NMAX;
+  static constexpr int VAL = NMAX, CB = NMAX;
   static constexpr int ROWB = (NMAX + 1 + 7) / 8;  // tableau-row labels, bytes
-  static constexpr int PER_THREAD = MU + GS + VAL + CB + YK + ROWB;  // doubles
+  static constexpr int PER_THREAD = MU + GS + VAL + CB + ROWB;  // doubles
   // + the CTA-shared lambda-row table of every robot part
   static size_t bytes(int np, int nrmax) {
     return sizeof(double) * ((size_t)PER_THREAD * CTA + (size_t)np * (nrmax - 1) * (D + 1));
@@ -102,6 +102,133 @@ __device__ __noinline__ int lexico(const PairRows<D> W, double* Gs, double* Gslo
   return lm;
 }
 
+// Textbook dense-tableau Lemke (rules L1-L7, FMA policy of reading #18) on the
+// same reduced rows: the rare fallback when the revised path fails or its result
+// does not verify (near-degenerate, ill-conditioned bases where the revised
+// coefficients are rounding noise).  Tableau [I | -M | -1 | q] in local memory.
+// Writes the basic z values into sval (by LCP index) and returns the status;
+// *zb_out = basic-z mask, *piv_out = pivots.
+template <int D, int NMAX>
+__device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil, double be, LemkeParams LP,
+                                        double* sval, uint32_t* zb_out, int* piv_out) {
+  const int n = W.n, l = n - 1;
+  constexpr int WC = 2 * NMAX + 2;
+  double T[NMAX * WC];
+  int basis[NMAX];
+  const int Wd = 2 * n + 2, Z0 = 2 * n, RHS = 2 * n + 1;
+  for (int i = 0; i < n; ++i) {
+    double fi[D + 1], ki;
+    W.row(i, fi, ki);
+    for (int j = 0; j < Wd; ++j) T[i * WC + j] = 0.0;
+    T[i * WC + i] = 1.0;
+    for (int j = 0; j < n; ++j) {
+      double fj[D + 1], kj;
+      W.row(j, fj, kj);
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c <= D; ++c) acc = __fma_rn(fi[c], fj[c], acc);
+      if (j == l) acc = ki;
+      if (i == l) acc = -kj;
+      if (i == l && j == l) acc = 0.0;
+      T[i * WC + n + j] = -acc;
+    }
+    T[i * WC + Z0] = -1.0;
+    double q = 1.0 / be;
+    if (i < l) {
+      q = 0.0;
+#pragma unroll
+      for (int c = 0; c <= D; ++c) q = __fma_rn(fi[c], btil[c], q);
+    }
+    T[i * WC + RHS] = q;
+    basis[i] = i;
+  }
+  const double tau = LP.tie_tol;
+  int status = ST_OK, pivots = 0;
+  double qmin = T[RHS];
+  for (int i = 1; i < n; ++i) qmin = fmin(qmin, T[i * WC + RHS]);
+  auto pivot = [&](int r, int c) {
+    const double inv = 1.0 / T[r * WC + c];
+    for (int j = 0; j < Wd; ++j)
+      if (j != c) T[r * WC + j] = T[r * WC + j] * inv;
+    T[r * WC + c] = 1.0;
+    for (int i = 0; i < n; ++i) {
+      if (i == r) continue;
+      const double f = T[i * WC + c];
+      for (int j = 0; j < Wd; ++j)
+        if (j != c) T[i * WC + j] = __fma_rn(-f, T[r * WC + j], T[i * WC + j]);
+      T[i * WC + c] = 0.0;
+    }
+  };
+  if (qmin < 0.0) {
+    const double tl = qmin + tau * fmax(1.0, fabs(qmin));
+    int r = -1;
+    for (int i = 0; i < n; ++i)
+      if (T[i * WC + RHS] <= tl) r = i;
+    int leaving = basis[r];
+    pivot(r, Z0);
+    basis[r] = Z0;
+    ++pivots;
+    int entering = leaving + n;
+    const int maxpiv = LP.max_pivot_factor * n;
+    for (;;) {
+      if (pivots >= maxpiv) { status = ST_ITER; break; }
+      const int col = entering;
+      double cmax = 0.0;
+      for (int i = 0; i < n; ++i) cmax = fmax(cmax, fabs(T[i * WC + col]));
+      const double thr = LP.pivot_tol * fmax(1.0, cmax);
+      double thmin = 1e308;
+      for (int i = 0; i < n; ++i) {
+        const double ci = T[i * WC + col];
+        if (ci > thr) thmin = fmin(thmin, fmax(T[i * WC + RHS], 0.0) / ci);
+      }
+      if (!(thmin < 1e308)) { status = ST_RAY; break; }
+      const double ttol = thmin + tau * fmax(1.0, thmin);
+      uint32_t tie = 0;
+      int r2 = -1;
+      for (int i = 0; i < n; ++i) {
+        const double ci = T[i * WC + col];
+        if (ci > thr && fmax(T[i * WC + RHS], 0.0) / ci <= ttol) {
+          tie |= 1u << i;
+          if (basis[i] == Z0) r2 = i;
+        }
+      }
+      if (r2 < 0) {
+        for (int j = 0; j < n && __popc(tie) > 1; ++j) {
+          double vmin = 1e308;
+          for (uint32_t b = tie; b; b &= b - 1) {
+            const int i = __ffs(b) - 1;
+            vmin = fmin(vmin, T[i * WC + j] / T[i * WC + col]);
+          }
+          const double vt = vmin + tau * fmax(1.0, fabs(vmin));
+          uint32_t keep = 0;
+          for (uint32_t b = tie; b; b &= b - 1) {
+            const int i = __ffs(b) - 1;
+            if (T[i * WC + j] / T[i * WC + col] <= vt) keep |= 1u << i;
+          }
+          tie = keep;
+        }
+        r2 = __ffs(tie) - 1;
+      }
+      const int leaving2 = basis[r2];
+      pivot(r2, col);
+      basis[r2] = col;
+      ++pivots;
+      if (leaving2 == Z0) break;
+      entering = (leaving2 < n) ? leaving2 + n : leaving2 - n;
+    }
+  }
+  uint32_t zb = 0;
+  for (int i = 0; i < n; ++i)
+    if (basis[i] >= n && basis[i] < 2 * n) {
+      const int j = basis[i] - n;
+      zb |= 1u << j;
+      sval[j * CTA] = T[i * WC + RHS];
+    }
+  *zb_out = zb;
+  *piv_out = pivots;
+  return status;
+}
+
 template <int D, int NMAX, bool FUSED>
 __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
   using SM = SweepSmem<D, NMAX>;
@@ -118,10 +245,9 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
   double* Gs = mu + SM::MU * CTA;
   double* sval = Gs + SM::GS * CTA;
   double* scb = sval + SM::VAL * CTA;
-  double* syk = scb + SM::CB * CTA;
   // tableau-row labels: bytes, [item][thread] from the CTA base of their region
   unsigned char* rowb =
-      reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::GS + SM::VAL + SM::CB + SM::YK) * CTA) + tid;
+      reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::GS + SM::VAL + SM::CB) * CTA) + tid;
   double* lamtab = smem + SM::PER_THREAD * CTA;  // [np][nrmax-1][D+1]
   const int LT = (P.nrmax - 1) * L1;
   if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
@@ -149,12 +275,12 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
   __syncthreads();
 #define VAL(i) sval[(i) * CTA]
 #define CBV(i) scb[(i) * CTA]
-#define YK(i) syk[(i) * CTA]
+#define YK(i) P.y[(long long)(i) * PP + p]  // y^k from HBM (L1-resident re-reads)
   double rec[REC];
 #pragma unroll
   for (int f = 0; f < REC; ++f) rec[f] = 0.0;
   const int gs = chunk * P.CH + tid;  // slot in the n-sorted order of the (b, t) group
-  const int g = (tid < P.CH && gs < P.G) ? P.gperm[(long long)b * P.G + gs] : 0;
+  const int g = (tid < P.CH && gs < P.G) ? (int)P.gperm2[(long long)bt * P.G + gs] : 0;
   if (tid < P.CH && gs < P.G) {
     const long long p = (long long)bt * P.G + g;
     const long long PP = P.P;
@@ -166,9 +292,6 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
     const double* orow = P.obs_rows + 4 * (long long)l0;
     const int e = part_e[ip];
     const double be = part_be[ip];
-    // y^k (SoA planes) -> smem; zeta, xi
-#pragma unroll 4
-    for (int k = 0; k < n; ++k) YK(k) = P.y[(long long)k * PP + p];
     double zeta = P.zeta[p], xi[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
@@ -361,6 +484,13 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           cr = CBV(lm);
           vr = VAL(lm);
         }
+        if (p == P.dbg_p && pivots < 64) {
+          double* dd = P.dbg + pivots * 48;
+          dd[0] = ent.kind; dd[1] = ent.j; dd[2] = n - __popc(wb); dd[3] = lm; dd[4] = thmin;
+          dd[5] = __popc(tiem); dd[6] = cr; dd[7] = vr; dd[8] = wb; dd[9] = zb; dd[10] = cmax; dd[11] = cs.slow;
+          dd[12] = val0; dd[13] = cb0;
+          for (int i = 0; i < n && i < 16; ++i) { dd[14 + i] = CBV(i); dd[30 + i] = VAL(i); }
+        }
         // L3: pivot (values only: the structure is re-derived from the basis);
         // the entering variable takes the leaving one's tableau row
         const bool leave_w = (lm >= 0) && ((wb >> lm) & 1u);
@@ -388,6 +518,55 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           ent = Var{0, lm};
         }
       }
+    }
+    // ------------------------------------------------------- verification
+    // The revised path never forms the tableau, so check its answer against the
+    // LCP itself: w = M z + q (O(n d) with the low-rank M), w_i = value of basic
+    // w_i or 0, w >= 0, z >= 0.  Failure or RAY / ITER_LIMIT -> dense fallback.
+    bool fallback = (status != ST_OK);
+    if (!fallback && qmin < 0.0) {
+      double uz[D + 1], zl = 0.0, skz = 0.0, zsc = 0.0;
+#pragma unroll
+      for (int c = 0; c <= D; ++c) uz[c] = 0.0;
+#pragma unroll 1
+      for (uint32_t bb = zb; bb; bb &= bb - 1) {
+        const int jz = __ffs(bb) - 1;
+        const double z = VAL(jz);
+        zsc = fmax(zsc, fabs(z));
+        if (z < -1e-9) fallback = true;
+        double f[D + 1], k;
+        W.row(jz, f, k);
+#pragma unroll
+        for (int c = 0; c <= D; ++c) uz[c] = __fma_rn(z, f[c], uz[c]);
+        skz = __fma_rn(z, k, skz);
+        if (jz == n - 1) zl = z;
+      }
+#pragma unroll 1
+      for (int i = 0; i < n && !fallback; ++i) {
+        double f[D + 1], k;
+        W.row(i, f, k);
+        double q = 1.0 / be, w = 0.0, mag = 1.0 + zsc;
+        if (i < n - 1) {
+          q = 0.0;
+#pragma unroll
+          for (int c = 0; c <= D; ++c) {
+            q = __fma_rn(f[c], bt_[c], q);
+            w = __fma_rn(f[c], uz[c], w);
+          }
+        }
+        w = __fma_rn(k, zl, w);
+        if (i == n - 1) w -= skz;
+        w += q;
+        mag += fabs(q);
+        const double expect = ((wb >> i) & 1u) ? VAL(i) : 0.0;
+        if (fabs(w - expect) > 1e-7 * mag || w < -1e-7 * mag) fallback = true;
+      }
+    }
+    if (fallback) {
+      int piv2 = 0;
+      status = lemke_dense<D, NMAX>(W, bt_, be, LP, sval, &zb, &piv2);
+      pivots += piv2;
+      z0b = false;
     }
     // ------------------------------------------------------------ recovery
     // z_j = value of basic z_j (LCP index j);  y_U = z[0..n-2] in original order
@@ -443,7 +622,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
     if (solved) rec[R_RDUAL] = rd;
     else rec[R_FAIL] = 1.0;
     rec[R_PIV] = (double)pivots;
-    P.pst[p] = (uint32_t)min(pivots, 65535) | ((uint32_t)st << 16);
+    P.pst[p] = (uint32_t)min(pivots, 65535) | ((uint32_t)st << 16) | (fallback ? (1u << 20) : 0u);
     if (P.zmask) P.zmask[p] = zb | (z0b ? 0x80000000u : 0u);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
