@@ -340,6 +340,12 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
   ca_status st;
+  {
+    const long long nq = (long long)h->B * h->N;
+    ca::k_stage<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev);
+    CUDA_TRY(cudaGetLastError());
+    h->launches[1]++;
+  }
   const int ns = h->ns, nu = h->nu;
   if (ns == 4 && nu == 2) st = launch_riccati_t<4, 2>(h, cur, prev);
   else if (ns == 7 && nu == 4) st = launch_riccati_t<7, 4>(h, cur, prev);
@@ -504,6 +510,8 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.pst, uint32_t, std::max<long long>(h->P, 1));
   AL(v.agg, double, (size_t)B * N * v.nchunk * ca::REC);
   AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
+  AL(v.stg, double, (size_t)B * N * (ns * ns + ns));
+  AL(v.stg_stats, double, (size_t)B * N * 4);
   AL(h->scene_res, double, (size_t)B * 4);
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));

@@ -50,6 +50,8 @@ struct Dev {
   uint32_t* zmask;
   double* agg;
   double* ric;
+  double* stg;        // [B*N][ns*ns + ns] stage Hessians / gradients (k_stage -> k_riccati)
+  double* stg_stats;  // [B*N][4]
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
   uint16_t* gperm2;  // [B*N][G]: per-(b,t) execution order, re-sorted by last pivot count
   long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
@@ -175,59 +177,89 @@ __global__ void k_collect(Dev P, double* dst, int mask) {
 // Also collects per-scene statistics (rdual of this sweep -> dst_cur,
 // rpri of the fused multiplier update -> dst_prev) in fixed order.
 // ----------------------------------------------------------------------------
+#ifdef CA_COMMON_KERNELS
+// Stage assembly, one thread per (scene, t), t = 1..N (fully parallel): sums the
+// (scene, t) chunk records in fixed order and writes H_t (ns x ns), h_t (ns) and
+// the per-(scene, t) statistics to P.stg.
+__global__ void k_stage(Dev P) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + (t-1)
+  if (q >= (long long)P.B * P.N) return;
+  const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
+  const int N = P.N, NS = P.ns, npc = P.npc, L1 = P.d + 1;
+  const double sig = P.sigma;
+  double S[4][4], gv[4], st[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    gv[a] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) S[a][c] = 0.0;
+  }
+  for (int c = 0; c < P.nchunk; ++c) {
+    const double* rec = P.agg + (q * P.nchunk + c) * REC;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      if (a >= L1) continue;
+#pragma unroll
+      for (int cc = a; cc < 4; ++cc)
+        if (cc < L1) S[a][cc] += rec[sym_idx(a, cc, L1)];
+      gv[a] += rec[L1 * (L1 + 1) / 2 + a];
+    }
+    st[0] += rec[R_RDUAL];
+    st[1] += rec[R_RPRI];
+    st[2] += rec[R_PIV];
+    st[3] += rec[R_FAIL];
+  }
+  double* out = P.stg + q * (NS * NS + NS);
+  double* ho = out + NS * NS;
+  const double* sref = P.sref + ((long long)b * (N + 1) + t) * NS;
+  const double* sk = P.s + ((long long)b * (N + 1) + t) * NS;
+  for (int a = 0; a < NS; ++a) {
+    double acc = 0.0;
+    for (int c = 0; c < NS; ++c) {
+      out[a * NS + c] = 2.0 * P.Qs[a * NS + c];
+      acc += P.Qs[a * NS + c] * sref[c];
+    }
+    ho[a] = -2.0 * acc;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (a >= npc) continue;
+    double spv = gv[a];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= npc) continue;
+      const double Sac = (a <= c) ? S[a][c] : S[c][a];
+      spv -= Sac * sk[P.pidx[c]];
+      out[P.pidx[a] * NS + P.pidx[c]] += sig * Sac;
+    }
+    ho[P.pidx[a]] += sig * spv;
+  }
+  double* so = P.stg_stats + q * 4;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) so[f] = st[f];
+}
+#endif
+
 template <int NS, int NU>
 __global__ void k_riccati(Dev P, double* dst_cur, double* dst_prev) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= P.B) return;
-  const int N = P.N, npc = P.npc, L1 = P.d + 1;
-  const double sig = P.sigma;
+  const int N = P.N;
   double Pm[NS][NS], pv[NS];
   double st[4] = {0, 0, 0, 0};
-  // stage cost assembly for time t (1..N)
+  for (int t = 1; t <= N; ++t) {
+    const double* so = P.stg_stats + ((long long)b * N + (t - 1)) * 4;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) st[f] += so[f];
+  }
+  // stage cost of time t (1..N), assembled by k_stage
   auto stage = [&](int t, double H[NS][NS], double h[NS]) {
-    double S[16], gv[4];
-    for (int f = 0; f < 16; ++f) S[f] = 0.0;
-    for (int f = 0; f < 4; ++f) gv[f] = 0.0;
-    const long long base = ((long long)b * N + (t - 1)) * P.nchunk;
-    for (int c = 0; c < P.nchunk; ++c) {
-      const double* rec = P.agg + (base + c) * REC;
-      for (int f = 0; f < L1 * (L1 + 1) / 2; ++f) S[f] += rec[f];
-      for (int f = 0; f < L1; ++f) gv[f] += rec[L1 * (L1 + 1) / 2 + f];
-      st[0] += rec[R_RDUAL];
-      st[1] += rec[R_RPRI];
-      st[2] += rec[R_PIV];
-      st[3] += rec[R_FAIL];
-    }
-    const double* sref = P.sref + ((long long)b * (N + 1) + t) * NS;
-    const double* sk = P.s + ((long long)b * (N + 1) + t) * NS;
+    const double* in = P.stg + ((long long)b * N + (t - 1)) * (NS * NS + NS);
 #pragma unroll
     for (int a = 0; a < NS; ++a) {
-      double acc = 0.0;
+      h[a] = in[NS * NS + a];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        H[a][c] = 2.0 * P.Qs[a * NS + c];
-        acc += P.Qs[a * NS + c] * sref[c];
-      }
-      h[a] = -2.0 * acc;
-    }
-    for (int a = 0; a < npc; ++a) {
-      double spv = gv[a];
-      for (int c = 0; c < npc; ++c) {
-        const double Sac = (a <= c) ? S[sym_idx(a, c, L1)] : S[sym_idx(c, a, L1)];
-        spv -= Sac * sk[P.pidx[c]];
-      }
-      for (int c = 0; c < npc; ++c) {
-        const double Sac = (a <= c) ? S[sym_idx(a, c, L1)] : S[sym_idx(c, a, L1)];
-        // pose index writes (runtime indices into register arrays -> unrolled select)
-#pragma unroll
-        for (int aa = 0; aa < NS; ++aa)
-#pragma unroll
-          for (int cc = 0; cc < NS; ++cc)
-            if (aa == P.pidx[a] && cc == P.pidx[c]) H[aa][cc] += sig * Sac;
-      }
-#pragma unroll
-      for (int aa = 0; aa < NS; ++aa)
-        if (aa == P.pidx[a]) h[aa] += sig * spv;
+      for (int c = 0; c < NS; ++c) H[a][c] = in[a * NS + c];
     }
   };
   auto dynp = [&](const double* base, int t, int blk) {
@@ -567,14 +599,22 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
     cnt[key][tid]++;
   }
   __syncwarp();
-  if (tid == 0) {
+  {  // thread k owns bucket k: exclusive prefix over threads, then over buckets
+    const int k = tid;
     int run = 0;
-    for (int k = 0; k < NB; ++k)
-      for (int t = 0; t < 32; ++t) {
-        const int c = cnt[k][t];
-        cnt[k][t] = run;
-        run += c;
-      }
+    for (int t = 0; t < 32; ++t) {
+      const int c = cnt[k][t];
+      cnt[k][t] = run;
+      run += c;
+    }
+    int excl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, excl, o);
+      if (tid >= o) excl += v;
+    }
+    excl -= run;
+    for (int t = 0; t < 32; ++t) cnt[k][t] += excl;
   }
   __syncwarp();
   uint16_t* out = P.gperm2 + (long long)bt * G;

@@ -32,35 +32,40 @@ namespace ca {
 enum { ST_OK = 0, ST_RAY = 1, ST_ITER = 2, ST_NEGYE = 3 };
 
 // Reduced rows (Kt_i, kt_i) of one pair, i = 0..n-1 in LCP order:
-//   i <  nr-1      lambda rows: (0, at_i), kt_i = b_k / b_e    [CTA-shared, per part]
-//   i <  n-2       mu rows:     (d_l - c_l.rho, R^T c_l), 0    [per-thread smem]
-//   i == n-2       gamma row:   (1, 0), 0
-//   i == n-1       phi row:     0
+//   i <  nr-1      lambda rows: (0, at_i), kt_i = b_k / b_e  [CTA-shared, per part, D+2 doubles]
+//   i <  n-2       mu rows:     (d_l - c_l.rho, R^T c_l), 0  [per-thread table, D+1 doubles]
+//   i == n-2       gamma row:   (1, 0), 0                    [per-thread table]
+//   i == n-1       phi row:     0                            [per-thread table]
+// row() is branch-free: a pointer/stride select between the two tables.
 template <int D>
 struct PairRows {
-  const double* lam;  // [(nr-1)][D+1] = (at_1..at_D, kt)  (CTA smem)
-  double* mu;         // [no][D+1] with stride `ms` between doubles (thread smem)
+  const double* lam;  // [(nr-1)][D+2] = (0, at_1..at_D, kt)  (CTA smem)
+  const double* mu;   // [no+2][D+1], stride `ms` between doubles (thread smem)
   int ms;
   int nr, no, n, l;
   __device__ __forceinline__ void row(int i, double f[D + 1], double& k) const {
-    if (i < nr - 1) {
-      f[0] = 0.0;
+    const bool isl = i < nr - 1;
+    const double* base = isl ? lam + i * (D + 2) : mu + (i - (nr - 1)) * (D + 1) * ms;
+    const int st = isl ? 1 : ms;
 #pragma unroll
-      for (int c = 0; c < D; ++c) f[1 + c] = lam[i * (D + 1) + c];
-      k = lam[i * (D + 1) + D];
-    } else if (i < n - 2) {
-      const double* m = mu + (i - (nr - 1)) * (D + 1) * ms;
-#pragma unroll
-      for (int c = 0; c <= D; ++c) f[c] = m[c * ms];
-      k = 0.0;
-    } else {
-      f[0] = (i == n - 2) ? 1.0 : 0.0;
-#pragma unroll
-      for (int c = 1; c <= D; ++c) f[c] = 0.0;
-      k = 0.0;
-    }
+    for (int c = 0; c <= D; ++c) f[c] = base[c * st];
+    const double kl = lam[(isl ? i : 0) * (D + 2) + D + 1];
+    k = isl ? kl : 0.0;
   }
 };
+
+// M_ij of Eq. 24 from two reduced rows (row/col l = n-1 is the phi row)
+template <int D>
+__device__ __forceinline__ double m_entry(const double fi[D + 1], double ki, int i, const double fj[D + 1],
+                                          double kj, int j, int l) {
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) acc = __fma_rn(fi[c], fj[c], acc);
+  if (j == l) acc = ki;
+  if (i == l) acc = -kj;
+  if (i == l && j == l) acc = 0.0;
+  return acc;
+}
 
 // Gauss-Jordan with partial pivoting (rows physically swapped) on an m x (m+1)
 // system stored with element stride `es`: A[(p*(mm+1)+c)*es], mm = row capacity.
@@ -137,13 +142,7 @@ struct Lemke {
         const int j = __ffs(cb) - 1;
         double fj[D + 1], kj;
         W.row(j, fj, kj);
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c <= D; ++c) acc = __fma_rn(fi[c], fj[c], acc);
-        if (j == W.l) acc = ki;
-        if (i == W.l) acc = -kj;
-        if (i == W.l && j == W.l) acc = 0.0;
-        GA(p, s) = -acc;
+        GA(p, s) = -m_entry<D>(fi, ki, i, fj, kj, j, W.l);
       }
       if (z0b) GA(p, s) = -1.0;
       double a;
@@ -152,13 +151,7 @@ struct Lemke {
       } else if (e.kind == 2) {
         a = -1.0;
       } else {
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c <= D; ++c) acc = __fma_rn(fi[c], fe[c], acc);
-        if (e.j == W.l) acc = ki;
-        if (i == W.l) acc = -ke;
-        if (i == W.l && e.j == W.l) acc = 0.0;
-        a = -acc;
+        a = -m_entry<D>(fi, ki, i, fe, ke, e.j, W.l);
       }
       GA(p, mm) = a;
     }
@@ -192,5 +185,119 @@ struct Lemke {
     return out;
   }
 };
+
+// Fast path of solve_column for m <= 3 (99.7 % of bases on C5): the m x m
+// structural system lives in registers (padded to 3 x 3 with identity rows).
+template <int D>
+struct SmallSol {
+  double x[3];  // columns: basic z_j in increasing j, then z0
+  double uh[D + 1];
+  double sl, sk, s0;
+};
+
+template <int D>
+__device__ __forceinline__ bool solve_small(const PairRows<D>& W, uint32_t wb, uint32_t zb, bool z0b, Var e,
+                                            SmallSol<D>& out) {
+  const uint32_t nmask = (W.n >= 32) ? 0xffffffffu : ((1u << W.n) - 1u);
+  const uint32_t Rm = ~wb & nmask;
+  const int m = __popc(Rm);
+  if (m > 3) return false;
+  const int mz = __popc(zb);
+  const int l = W.l;
+  double fc[3][D + 1], kc[3];
+  int jc[3];
+  uint32_t zbits = zb;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    jc[s] = -1;
+    kc[s] = 0.0;
+#pragma unroll
+    for (int c = 0; c <= D; ++c) fc[s][c] = 0.0;
+    if (s < mz) {
+      const int j = __ffs(zbits) - 1;
+      zbits &= zbits - 1;
+      W.row(j, fc[s], kc[s]);
+      jc[s] = j;
+    }
+  }
+  double fe[D + 1], ke = 0.0;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) fe[c] = 0.0;
+  if (e.kind == 1) W.row(e.j, fe, ke);
+  double G[3][4];
+  uint32_t rbits = Rm;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) G[p][c] = 0.0;
+    if (p < m) {
+      const int i = __ffs(rbits) - 1;
+      rbits &= rbits - 1;
+      double fi[D + 1], ki;
+      W.row(i, fi, ki);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if (s < mz) G[p][s] = -m_entry<D>(fi, ki, i, fc[s], kc[s], jc[s], l);
+        else if (s == mz && z0b) G[p][s] = -1.0;
+      }
+      double a;
+      if (e.kind == 0) a = (i == e.j) ? 1.0 : 0.0;
+      else if (e.kind == 2) a = -1.0;
+      else a = -m_entry<D>(fi, ki, i, fe, ke, e.j, l);
+      G[p][3] = a;
+    } else {
+      G[p][p] = 1.0;
+    }
+  }
+  // Gauss-Jordan with partial pivoting, compile-time indices
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int r = c + 1; r < 3; ++r) {
+      if (fabs(G[r][c]) > fabs(G[c][c])) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const double t = G[c][cc];
+          G[c][cc] = G[r][cc];
+          G[r][cc] = t;
+        }
+      }
+    }
+    const double inv = 1.0 / G[c][c];
+#pragma unroll
+    for (int cc = c + 1; cc < 4; ++cc) G[c][cc] = G[c][cc] * inv;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      if (r == c) continue;
+      const double f = G[r][c];
+#pragma unroll
+      for (int cc = c + 1; cc < 4; ++cc) G[r][cc] = __fma_rn(-f, G[c][cc], G[r][cc]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c <= D; ++c) out.uh[c] = 0.0;
+  out.sl = out.sk = out.s0 = 0.0;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    out.x[s] = G[s][3];
+    if (s < mz) {
+#pragma unroll
+      for (int c = 0; c <= D; ++c) out.uh[c] = __fma_rn(out.x[s], fc[s][c], out.uh[c]);
+      out.sk = __fma_rn(out.x[s], kc[s], out.sk);
+      if (jc[s] == l) out.sl += out.x[s];
+    } else if (s == mz && z0b) {
+      out.s0 += out.x[s];
+    }
+  }
+  if (e.kind == 2) {
+    out.s0 -= 1.0;
+  } else if (e.kind == 1) {
+#pragma unroll
+    for (int c = 0; c <= D; ++c) out.uh[c] -= fe[c];
+    out.sk -= ke;
+    if (e.j == l) out.sl -= 1.0;
+  }
+  return true;
+}
 
 }  // namespace ca

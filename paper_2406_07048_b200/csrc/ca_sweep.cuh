@@ -27,30 +27,29 @@ constexpr int MFAST = 3;   // m x m systems up to this size live in shared memor
 template <int D, int NMAX>
 struct SweepSmem {
   static constexpr int NOMAX = NMAX - 4;  // n = nr + no + 1 <= NMAX, nr >= d+1 >= 3
-  static constexpr int MU = NOMAX * (D + 1);
-  static constexpr int GS = MFAST * (MFAST + 1);
+  static constexpr int MU = (NOMAX + 2) * (D + 1);  // mu rows + gamma + phi rows
   static constexpr int VAL = NMAX, CB = NMAX;
   static constexpr int ROWB = (NMAX + 1 + 7) / 8;  // tableau-row labels, bytes
-  static constexpr int PER_THREAD = MU + GS + VAL + CB + ROWB;  // doubles
+  static constexpr int PER_THREAD = MU + VAL + CB + ROWB;  // doubles
   // + the CTA-shared lambda-row table of every robot part
   static size_t bytes(int np, int nrmax) {
-    return sizeof(double) * ((size_t)PER_THREAD * CTA + (size_t)np * (nrmax - 1) * (D + 1));
+    return sizeof(double) * ((size_t)PER_THREAD * CTA + (size_t)np * (nrmax - 1) * (D + 2));
   }
 };
 
 // L5.4-5 (rare): lexicographic rule on the w columns (= B^{-1}) among the tied
 // members `tm`; returns the leaving member (pair index).
 template <int D, int NMAX>
-__device__ __noinline__ int lexico(const PairRows<D> W, double* Gs, double* Gslow, const double* scb,
+__device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const double* scb,
                                    const unsigned char* rowb, uint32_t wb, uint32_t zb, bool z0b, uint32_t tm,
                                    double tau) {
   const int n = W.n;
   for (int jj = 0; jj < n && __popc(tm) > 1; ++jj) {
     const bool wbasic = (wb >> jj) & 1u;
     ColSol<D> cs{};
-    if (!wbasic) cs = Lemke<D, NMAX, MFAST>::solve_column(W, Gs, CTA, wb, zb, z0b, Var{0, jj}, Gslow);
-    const double* A = cs.slow ? Gslow : Gs;
-    const int es = cs.slow ? 1 : CTA, mm = cs.slow ? D + 4 : MFAST;
+    if (!wbasic) cs = Lemke<D, NMAX, D + 4>::solve_column(W, Gslow, 1, wb, zb, z0b, Var{0, jj}, Gslow);
+    const double* A = Gslow;
+    const int es = 1, mm = D + 4;
     double vmin = 1e308;
     for (uint32_t b = tm; b; b &= b - 1) {
       const int i = __ffs(b) - 1;
@@ -242,14 +241,13 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
   const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
   const int b = bt / P.N, t = bt % P.N + 1;
   double* mu = smem + tid;
-  double* Gs = mu + SM::MU * CTA;
-  double* sval = Gs + SM::GS * CTA;
+  double* sval = mu + SM::MU * CTA;
   double* scb = sval + SM::VAL * CTA;
   // tableau-row labels: bytes, [item][thread] from the CTA base of their region
   unsigned char* rowb =
-      reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::GS + SM::VAL + SM::CB) * CTA) + tid;
+      reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::VAL + SM::CB) * CTA) + tid;
   double* lamtab = smem + SM::PER_THREAD * CTA;  // [np][nrmax-1][D+1]
-  const int LT = (P.nrmax - 1) * L1;
+  const int LT = (P.nrmax - 1) * (D + 2);
   if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
   if (tid < P.np) {
     // Eqs. 20-21 for the lambda rows depend on the robot part only:
@@ -267,9 +265,10 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
       if (k == e) continue;
       const int u = k - (k > e);
       const double ratio = pr[4 * k + 3] / be;
+      lt[u * (D + 2)] = __fma_rn(-ratio, 0.0, 0.0);
 #pragma unroll
-      for (int a = 0; a < D; ++a) lt[u * L1 + a] = __fma_rn(-ratio, pr[4 * e + a], pr[4 * k + a]);
-      lt[u * L1 + D] = ratio;
+      for (int a = 0; a < D; ++a) lt[u * (D + 2) + 1 + a] = __fma_rn(-ratio, pr[4 * e + a], pr[4 * k + a]);
+      lt[u * (D + 2) + D + 1] = ratio;
     }
   }
   __syncthreads();
@@ -311,6 +310,16 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
 #pragma unroll
         for (int a = 0; a < D; ++a) r = __fma_rn(c[a], sR[a * D + mm], r);
         m[(1 + mm) * CTA] = r;
+      }
+    }
+    {  // gamma row (1, 0) and phi row (0) complete the per-thread row table
+      double* m = mu + no * L1 * CTA;
+      m[0] = 1.0;
+      m[L1 * CTA] = 0.0;
+#pragma unroll
+      for (int a = 1; a <= D; ++a) {
+        m[a * CTA] = 0.0;
+        m[(L1 + a) * CTA] = 0.0;
       }
     }
     const PairRows<D> W{lamtab + ip * LT, mu, CTA, nr, no, n, n - 1};
@@ -393,9 +402,21 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
       for (;;) {
         if (pivots >= maxpiv) { status = ST_ITER; break; }
         if (n - __popc(wb) > D + 4) { status = ST_ITER; break; }  // rank bound (cannot happen exactly)
-        const ColSol<D> cs = Lemke<D, NMAX, MFAST>::solve_column(W, Gs, CTA, wb, zb, z0b, ent, Gslow);
-        const double* A = cs.slow ? Gslow : Gs;
-        const int es = cs.slow ? 1 : CTA, mmc = cs.slow ? D + 4 : MFAST;
+        // structural m x m system: registers for m <= 3, generic solver otherwise
+        SmallSol<D> ss;
+        const bool small = solve_small<D>(W, wb, zb, z0b, ent, ss);
+        if (!small) {
+          const ColSol<D> cg = Lemke<D, NMAX, D + 4>::solve_column(W, Gslow, 1, wb, zb, z0b, ent, Gslow);
+#pragma unroll
+          for (int c = 0; c <= D; ++c) ss.uh[c] = cg.uh[c];
+          ss.sl = cg.sl;
+          ss.sk = cg.sk;
+          ss.s0 = cg.s0;
+        }
+        auto xcol = [&](int s) -> double {
+          if (small) return (s == 0) ? ss.x[0] : ((s == 1) ? ss.x[1] : ss.x[2]);
+          return Gslow[s * (D + 5) + D + 4];
+        };
         const uint32_t basic = wb | zb;
         // pass 1: entering-column coefficient of every basic variable, max |cbar|, and
         // the minimum ratio max(val,0)/cbar (L5.2, cross-multiplied) over rows with
@@ -408,25 +429,26 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           if (wb & bit) {
             double f[D + 1], k;
             W.row(i, f, k);
-            c = cs.s0;
+            c = ss.s0;
 #pragma unroll
-            for (int cc = 0; cc <= D; ++cc) c = __fma_rn(f[cc], cs.uh[cc], c);
-            c = __fma_rn(k, cs.sl, c);
-            if (i == n - 1) c -= cs.sk;
+            for (int cc = 0; cc <= D; ++cc) c = __fma_rn(f[cc], ss.uh[cc], c);
+            c = __fma_rn(k, ss.sl, c);
+            if (i == n - 1) c -= ss.sk;
           } else if (zb & bit) {
-            const int s = __popc(zb & (bit - 1u));
-            c = A[(s * (mmc + 1) + mmc) * es];
+            c = xcol(__popc(zb & (bit - 1u)));
           }
           CBV(i) = c;
-          cmax = fmax(cmax, fabs(c));
+          const double ac = fabs(c);
+          cmax = (ac > cmax) ? ac : cmax;
           if ((basic & bit) && c > ptol) {
-            const double nu = fmax(VAL(i), 0.0);
+            const double v = VAL(i);
+            const double nu = (v > 0.0) ? v : 0.0;
             if (bn < 0.0 || nu * bd < bn * c) { bn = nu; bd = c; }
           }
         }
         double cb0 = 0.0;
         if (z0b) {
-          cb0 = A[(__popc(zb) * (mmc + 1) + mmc) * es];
+          cb0 = xcol(__popc(zb));
           cmax = fmax(cmax, fabs(cb0));
           if (cb0 > ptol) {
             const double nu = fmax(val0, 0.0);
@@ -480,14 +502,14 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           status = ST_RAY;
           break;
         } else if (__popc(tiem) > 1) {
-          lm = lexico<D, NMAX>(W, Gs, Gslow, scb, rowb, wb, zb, z0b, tiem, tau);
+          lm = lexico<D, NMAX>(W, Gslow, scb, rowb, wb, zb, z0b, tiem, tau);
           cr = CBV(lm);
           vr = VAL(lm);
         }
         if (p == P.dbg_p && pivots < 64) {
           double* dd = P.dbg + pivots * 48;
           dd[0] = ent.kind; dd[1] = ent.j; dd[2] = n - __popc(wb); dd[3] = lm; dd[4] = thmin;
-          dd[5] = __popc(tiem); dd[6] = cr; dd[7] = vr; dd[8] = wb; dd[9] = zb; dd[10] = cmax; dd[11] = cs.slow;
+          dd[5] = __popc(tiem); dd[6] = cr; dd[7] = vr; dd[8] = wb; dd[9] = zb; dd[10] = cmax; dd[11] = small ? 0 : 1;
           dd[12] = val0; dd[13] = cb0;
           for (int i = 0; i < n && i < 16; ++i) { dd[14 + i] = CBV(i); dd[30 + i] = VAL(i); }
         }
