@@ -544,11 +544,32 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
     GR(nr + lo, D) = 0.0;
     GR(nr + lo, D + 1) = __ldg(c + 3);
   }
+  // alpha = 0 is attained iff the body origin y = rho lies in the obstacle (alpha >= 0
+  // always for b > 0); otherwise an optimal vertex mixes robot and obstacle rows
+  // (no robot row: singular alpha column; only robot rows: x = rho, alpha = 0).
+  bool origin_in = true;
+  for (int lo = 0; lo < no; ++lo) {
+    double cr = 0.0, mag = fabs(GR(nr + lo, D + 1));
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double tc = GR(nr + lo, a) * srho[a];
+      cr += tc;
+      mag += fabs(tc);
+    }
+    if (cr - GR(nr + lo, D + 1) > 1e-9 * (1.0 + mag)) origin_in = false;
+  }
+  if (origin_in) {
+    alpha[p] = 0.0;
+    return;
+  }
   double best = 1e308;
   int sub[D + 1];
 #pragma unroll
   for (int k = 0; k <= D; ++k) sub[k] = k;
   for (;;) {
+    if (sub[0] >= nr) break;  // lexicographic order: no robot row from here on
+    if (sub[D] < nr) goto next;  // robot rows only
+    {
     double A[D + 1][D + 2], z[D + 1];
 #pragma unroll
     for (int r = 0; r <= D; ++r) {
@@ -570,6 +591,8 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
       }
       if (feas) best = z[D];
     }
+    }
+  next:
     int k = D;
     while (k >= 0 && sub[k] == m - (D + 1) + k) --k;
     if (k < 0) break;
