@@ -15,6 +15,8 @@ timer only).  Inputs (5.6 GB of resident iterate) exceed the 126 MB L2.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --config 4 --shard obstacles   # one problem split across GPUs by
+                                                   # obstacle blocks (ncclAllReduce/iter)
 
 Prints ONE JSON line (rank 0).
 """
@@ -31,6 +33,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# keep stdout for the single JSON line: NCCL's banner / warnings go to stderr
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 import scenes  # noqa: E402  (seeded generators: shared by both arms)
 
@@ -45,6 +50,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--shard", default="scenes", choices=["scenes", "obstacles"],
+                    help="multi-GPU split: independent scenes per rank (no collective, weak scaling) or the "
+                         "obstacles of one problem (one ncclAllReduce per iteration, strong scaling)")
     ap.add_argument("--scenes", type=int, default=scenes.C5_SCENES, help="C5 scenes per rank")
     ap.add_argument("--iters", type=int, default=0, help="ADMM iterations per solve (0 = config default)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -64,6 +72,23 @@ def make_scene(cfg, rank, n_scenes):
     if cfg == 5:
         return scenes.make_c5(scene_ids=range(rank * n_scenes, (rank + 1) * n_scenes))
     return scenes.make_config(cfg)
+
+
+def slice_obstacles(sc, j0, j1):
+    """The same problem restricted to obstacles [j0, j1) of every scene (rank-local view)."""
+    import dataclasses
+
+    M = sc.n_obs
+    offs, Cs, ds = [0], [], []
+    for b in range(sc.n_scenes):
+        for j in range(j0, j1):
+            lo, hi = sc.obs_off[b * M + j], sc.obs_off[b * M + j + 1]
+            Cs.append(sc.obs_C[lo:hi])
+            ds.append(sc.obs_d[lo:hi])
+            offs.append(offs[-1] + hi - lo)
+    return dataclasses.replace(sc, n_obs=j1 - j0, obs_off=np.asarray(offs, np.int32),
+                               obs_C=np.concatenate(Cs) if Cs else np.zeros((0, sc.dim)),
+                               obs_d=np.concatenate(ds) if ds else np.zeros(0))
 
 
 def workload_name(cfg, n_scenes, iters):
@@ -137,7 +162,7 @@ def algorithmic_bytes_per_sweep(sc):
     per_pair = 16.0 * n.sum() + sc.n_pairs * (16.0 * (1 + d) + 4.0)
     faces = float(sc.obs_off[-1]) * 8.0 * (d + 1)
     G = sc.n_parts * sc.n_obs
-    nchunk = max(1, -(-G // 128))
+    nchunk = max(1, -(-G // 32))  # one-warp CTAs
     recs = sc.n_scenes * sc.horizon * nchunk * 20 * 8.0
     return per_pair + faces + recs
 
@@ -260,9 +285,22 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     cfg = args.config
-    sc = make_scene(cfg, rank, args.scenes)
+    obstacle_shard = args.shard == "obstacles"
+    if obstacle_shard:
+        # every rank holds the same problem and solves its obstacle block
+        sc = make_scene(cfg, 0, args.scenes)
+        nid = ca.nccl_unique_id() if rank == 0 else None
+        if dist:
+            box = [nid]
+            dist.broadcast_object_list(box, src=0)
+            nid = box[0]
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid))
+        sc_local = slice_obstacles(sc, g.j0, g.j1)
+    else:
+        sc = make_scene(cfg, rank, args.scenes)
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream)
+        sc_local = sc
     iters = args.iters or sc.iters
-    g = ca.Problem(sc, device=local, stream=stream.cuda_stream)
     fp64 = ca.fp64_peak(local, 300.0) if rank == 0 else None
 
     def step():
@@ -300,11 +338,12 @@ def run_ours(args, rank, world, local):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    pairs_total = sc.n_pairs * iters * args.steps * world
+    units = 1 if obstacle_shard else world  # obstacle sharding splits ONE problem
+    pairs_total = sc.n_pairs * iters * args.steps * units
     value = pairs_total / (ms * 1e-3)
-    solves = sc.n_scenes * args.steps * world / (ms * 1e-3)
+    solves = sc.n_scenes * args.steps * units / (ms * 1e-3)
     launches = int(sum(v[1] for v in kt.values()))
-    # pivots of the last solve (for the algorithmic flop count)
+    # pivots of the last solve (for the algorithmic flop count; rank-local pairs)
     g.reset_iterate()
     rc, hist = g.admm_iterate(iters, hist=True)
     piv_per_sweep = float(hist["pivots"].mean())
@@ -335,7 +374,7 @@ def run_ours(args, rank, world, local):
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": sc.n_pairs * iters * args.e2e_steps * world / dt, "unit": "pair-QP/s",
+        e2e = {"value": sc.n_pairs * iters * args.e2e_steps * units / dt, "unit": "pair-QP/s",
                "h2d_bytes_per_step": h2d_bytes(sc),
                "d2h_bytes_per_step": int(8 * (sc.n_scenes * (sc.horizon + 1) * sc.n_state
                                               + sc.n_scenes * sc.horizon * sc.n_ctrl + 2 * sc.n_scenes)),
@@ -347,15 +386,15 @@ def run_ours(args, rank, world, local):
         return
     sweep_ms, sweep_n = kt["sweep"]
     avg_sweep_ms = sweep_ms / max(1, sweep_n)
-    nbytes = algorithmic_bytes_per_sweep(sc)
-    flops = algorithmic_flops_per_sweep(sc, piv_per_sweep)
+    nbytes = algorithmic_bytes_per_sweep(sc_local)
+    flops = algorithmic_flops_per_sweep(sc_local, piv_per_sweep)
     hbm, hbm_src = hbm_peak()
     achieved_gbs = nbytes / (avg_sweep_ms * 1e-3) / 1e9
     achieved_tf = flops / (avg_sweep_ms * 1e-3) / 1e12
     traffic = None
     try:
         prof = json.load(open(PROFILE_SUMMARY))
-        if prof.get("workload_key") == f"C{cfg}-{sc.n_scenes}":
+        if prof.get("workload_key") == f"C{cfg}-{sc.n_scenes}" and not obstacle_shard:
             traffic = prof.get("sweep_dram_bytes_per_launch")
     except Exception:
         pass
@@ -370,7 +409,7 @@ def run_ours(args, rank, world, local):
     roof.update({"kernel": "k_sweep (ADMM step 1 + fused step 3)", "launch_ms": avg_sweep_ms,
                  "algorithmic_bytes_per_launch": nbytes, "algorithmic_flops_per_launch": flops,
                  "hbm_frac": frac_hbm, "fp64_frac": frac_fp, "fp64_peak_tflops": fp64,
-                 "pivots_per_pair": piv_per_sweep / max(1, sc.n_pairs),
+                 "pivots_per_pair": piv_per_sweep / max(1, sc_local.n_pairs),
                  "share_of_step": sweep_ms / ms if ms else None})
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -380,11 +419,14 @@ def run_ours(args, rank, world, local):
                          f"+ 2 scale detections, {dt:.1f} s single-threaded on {cpu_model()}"}
     line = {
         "metric": "pair-QPs/sec", "value": value, "unit": "pair-QP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if obstacle_shard else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes/ generators)",
         "config": {"workload": workload_name(cfg, sc.n_scenes, iters), "scenes_per_gpu": sc.n_scenes,
                    "admm_iters": iters, "pair_qps_per_iter_per_gpu": sc.n_pairs,
-                   "parallelism": f"scene-sharded x{world}, no data-path collective",
+                   "parallelism": (f"obstacle-sharded x{world}, one ncclAllReduce of per-(scene,t) aggregates "
+                                   f"per iteration" if obstacle_shard else
+                                   f"scene-sharded x{world}, no data-path collective"),
                    "l2": "inputs larger than L2 (resident iterate %.1f GB)" % (g.device_bytes / 1e9)},
         "admm_solves_per_sec": solves,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},

@@ -120,6 +120,30 @@ typedef struct {
 ca_status ca_problem_create(const ca_problem_desc* desc, int device, void* stream, ca_problem** out);
 void ca_problem_destroy(ca_problem* h);
 
+/* ---- multi-GPU: obstacle sharding (one process per GPU, NCCL over NVLink) ----
+ * Rank r of W owns obstacles [j0, j1) of every scene (a contiguous block balanced by
+ * total face count, ca_obstacle_partition) and solves only those pairs; every rank
+ * holds the full trajectory.  Per iteration the per-(scene, t) aggregates of step 2
+ * and the residual partials are summed by ONE ncclAllReduce on
+ * the handle's stream; the primal step then runs replicated on identical bytes.
+ * Pair indices of the getters are rank-local (j counted from j0).
+ * Scene sharding needs no collective: give each rank its own scenes instead. */
+typedef struct {
+  int32_t world_size, rank;
+  const uint8_t* nccl_id; /* 128 bytes from ca_nccl_unique_id on one rank, broadcast */
+} ca_dist_desc;
+
+ca_status ca_nccl_unique_id(uint8_t* out128);
+
+/* Pure host function: the obstacle block [*j0, *j1) of `rank`. */
+ca_status ca_obstacle_partition(int32_t n_scenes, int32_t n_obs, const int32_t* obs_off, int32_t world_size,
+                                int32_t rank, int32_t* j0, int32_t* j1);
+
+/* ca_problem_create for rank dist->rank of an obstacle-sharded problem (desc is the
+ * FULL problem; the rank keeps its block).  world_size == 1 is allowed. */
+ca_status ca_problem_create_dist(const ca_problem_desc* desc, const ca_dist_desc* dist, int device, void* stream,
+                                 ca_problem** out);
+
 /* Re-upload every per-batch input of a problem with the SAME shapes (n_scenes,
  * horizon, parts, per-obstacle row counts) and reset the iterate.  The end-to-end
  * path: load -> ca_admm_iterate -> ca_get_trajectory. */

@@ -11,6 +11,8 @@ from ._ca import (  # noqa: F401
     CAError,
     Problem,
     fp64_peak,
+    nccl_unique_id,
+    obstacle_partition,
     lib,
     library_path,
 )

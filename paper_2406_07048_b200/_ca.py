@@ -40,6 +40,10 @@ class Desc(C.Structure):
     ]
 
 
+class DistDesc(C.Structure):
+    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p)]
+
+
 class Residuals(C.Structure):
     _fields_ = [("r_pri", C.c_double), ("r_dual", C.c_double), ("n_pairs", C.c_int64),
                 ("n_fail", C.c_int64), ("pivots", C.c_int64)]
@@ -86,11 +90,16 @@ def lib():
         L.ca_fp64_peak.argtypes = [C.c_int, C.c_double, dp]
         L.ca_reset_iterate.argtypes = [vp]
         L.ca_debug_trace.argtypes = [vp, C.c_int64, vp]
+        L.ca_nccl_unique_id.argtypes = [vp]
+        L.ca_obstacle_partition.argtypes = [C.c_int32, C.c_int32, vp, C.c_int32, C.c_int32,
+                                            C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.ca_problem_create_dist.argtypes = [C.POINTER(Desc), C.POINTER(DistDesc), C.c_int, vp, C.POINTER(vp)]
         for name in ("ca_problem_create", "ca_problem_load", "ca_problem_info", "ca_scale_detect",
                      "ca_admm_iterate", "ca_admm_solve", "ca_dual_sweep", "ca_primal_step",
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
-                     "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace"):
+                     "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace",
+                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib
@@ -153,13 +162,24 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
 class Problem:
     """A batched MPC problem resident on one B200 (ca_problem handle)."""
 
-    def __init__(self, sc, device: int = 0, stream: int | None = None, **params):
+    def __init__(self, sc, device: int = 0, stream: int | None = None, dist=None, **params):
+        """dist = (world_size, rank, nccl_id bytes): obstacle-sharded rank of the full
+        problem `sc` (include/ca.h ca_problem_create_dist); None = single GPU."""
         self.sc = sc
         self.params = params
         self._keep = {}
         desc = make_desc(sc, self._keep, **params)
         h = C.c_void_p()
-        _check(lib().ca_problem_create(C.byref(desc), device, stream, C.byref(h)), ok=(CA_OK,))
+        self.dist = dist
+        if dist is None:
+            _check(lib().ca_problem_create(C.byref(desc), device, stream, C.byref(h)), ok=(CA_OK,))
+            self.j0, self.j1 = 0, sc.n_obs
+        else:
+            world, rank, nid = dist
+            self._nid = C.create_string_buffer(bytes(nid), 128)
+            dd = DistDesc(world, rank, C.cast(self._nid, C.c_void_p))
+            _check(lib().ca_problem_create_dist(C.byref(desc), C.byref(dd), device, stream, C.byref(h)), ok=(CA_OK,))
+            self.j0, self.j1 = obstacle_partition(sc, world, rank)
         self.h = h
         n, ny, nb = C.c_int64(), C.c_int32(), C.c_int64()
         _check(lib().ca_problem_info(h, C.byref(n), C.byref(ny), C.byref(nb)))
@@ -214,7 +234,7 @@ class Problem:
 
     def scale_detect(self, states=None, want_alpha=True):
         st = None if states is None else _f64(states)
-        alpha = np.empty(self.n_pairs) if want_alpha else None
+        alpha = np.empty(max(self.n_pairs, 1)) if want_alpha else None
         amin = np.empty(self.sc.n_scenes)
         _check(lib().ca_scale_detect(self.h, _ptr(st), _ptr(alpha), _ptr(amin)))
         return alpha, amin
@@ -272,6 +292,21 @@ class Problem:
         _check(lib().ca_kernel_times(self.h, ms, ln, int(reset)))
         names = ("sweep", "primal", "multiplier", "scale", "other")
         return {n: (ms[i], ln[i]) for i, n in enumerate(names)}
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().ca_nccl_unique_id(buf))
+    return buf.raw
+
+
+def obstacle_partition(sc, world: int, rank: int):
+    """[j0, j1): the obstacle block of `rank` in an obstacle-sharded run (host only)."""
+    off = _i32(sc.obs_off)
+    j0, j1 = C.c_int32(), C.c_int32()
+    _check(lib().ca_obstacle_partition(sc.n_scenes, sc.n_obs, off.ctypes.data, world, rank, C.byref(j0),
+                                       C.byref(j1)))
+    return j0.value, j1.value
 
 
 def fp64_peak(device: int = 0, ms: float = 200.0) -> float:

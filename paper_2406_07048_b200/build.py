@@ -20,10 +20,22 @@ DEPS = SOURCES + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(
                                                                     os.path.abspath(__file__)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+
+def _nccl_dir():
+    """The NCCL bundled with torch (headers + libnccl.so.2), same image on the GPU box."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    base = os.path.join(list(spec.submodule_search_locations)[0], "nccl")
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+NCCL_INC, NCCL_LIB = _nccl_dir()
+
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + NCCL_INC,
 ]
 
 
@@ -62,7 +74,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(f"--- {src}\n{err[-6000:]}")
         raise RuntimeError(f"nvcc failed (see {log})")
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
-            *[r[1] for r in results], "-cudart", "static"]
+            *[r[1] for r in results], "-cudart", "static",
+            "-Xlinker", os.path.join(NCCL_LIB, "libnccl.so.2"), "-Xlinker", "-rpath," + NCCL_LIB]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stderr)

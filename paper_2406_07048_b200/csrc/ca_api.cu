@@ -2,6 +2,7 @@
 // Every step of the method runs in the kernels of ca_kernels.cuh; this file only
 // validates input, lays data out in HBM, launches, and copies results back.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -30,6 +31,12 @@ ca_status fail(ca_status s, const std::string& msg) {
   g_err = msg;
   return s;
 }
+
+#define NCCL_TRY(expr)                                                                        \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess) return fail(CA_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
 
 #define CUDA_TRY(expr)                                                                        \
   do {                                                                                        \
@@ -68,8 +75,14 @@ struct ca_problem {
   std::vector<cudaEvent_t> event_pool;
   bool sticky = false;
   long long bytes = 0;
+  // obstacle sharding
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
+  double* rb = nullptr;     // [B*N][REC] reduced records (allreduced)
+  double* tmpB4 = nullptr;  // [B][4]
 
   ~ca_problem() {
+    if (comm) ncclCommDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : event_pool) cudaEventDestroy(e);
     for (auto& pe : pending) {
@@ -342,9 +355,19 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
   ca_status st;
   {
     const long long nq = (long long)h->B * h->N;
-    ca::k_stage<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev);
+    const unsigned gq = (unsigned)((nq + 127) / 128);
+    if (h->comm) {
+      // a5: one allreduce of the per-(scene, t) aggregates + residual partials
+      ca::k_reduce_records<<<gq, 128, 0, h->stream>>>(h->dev, h->rb);
+      CUDA_TRY(cudaGetLastError());
+      NCCL_TRY(ncclAllReduce(h->rb, h->rb, (size_t)nq * ca::REC, ncclDouble, ncclSum, h->comm, h->stream));
+      ca::k_stage<<<gq, 128, 0, h->stream>>>(h->dev, h->rb, 1);
+      h->launches[1] += 2;
+    } else {
+      ca::k_stage<<<gq, 128, 0, h->stream>>>(h->dev, h->dev.agg, h->dev.nchunk);
+      h->launches[1]++;
+    }
     CUDA_TRY(cudaGetLastError());
-    h->launches[1]++;
   }
   const int ns = h->ns, nu = h->nu;
   if (ns == 4 && nu == 2) st = launch_riccati_t<4, 2>(h, cur, prev);
@@ -380,6 +403,47 @@ ca_status launch_collect(ca_problem* h, double* dst, int mask) {
   CUDA_TRY(cudaGetLastError());
   h->launches[4]++;
   return CA_OK;
+}
+
+// per-scene statistics of the local pairs -> fields `mask` of dst; in obstacle-sharded
+// runs summed over ranks (one small allreduce).  Other fields are left untouched.
+ca_status collect_global(ca_problem* h, double* dst, int mask) {
+  if (!h->comm) return launch_collect(h, dst, mask);
+  CUDA_TRY(cudaMemsetAsync(h->tmpB4, 0, sizeof(double) * 4 * h->B, h->stream));
+  ca_status st = launch_collect(h, h->tmpB4, mask);
+  if (st) return st;
+  NCCL_TRY(ncclAllReduce(h->tmpB4, h->tmpB4, (size_t)4 * h->B, ncclDouble, ncclSum, h->comm, h->stream));
+  for (int f = 0; f < 4; ++f)
+    if ((mask >> f) & 1)
+      CUDA_TRY(cudaMemcpy2DAsync(dst + f, 4 * sizeof(double), h->tmpB4 + f, 4 * sizeof(double), sizeof(double),
+                                 h->B, cudaMemcpyDeviceToDevice, h->stream));
+  return CA_OK;
+}
+
+// the rank-local slice [j0, j1) of every scene's obstacles
+struct LocalObs {
+  std::vector<int> off;
+  std::vector<double> C, d;
+};
+void slice_obstacles(const ca_problem_desc* D, int j0, int j1, LocalObs& L, ca_problem_desc& out) {
+  const int M = D->n_obs, dim = D->dim, Ml = j1 - j0;
+  L.off.assign(1, 0);
+  L.C.clear();
+  L.d.clear();
+  for (int b = 0; b < D->n_scenes; ++b)
+    for (int j = j0; j < j1; ++j) {
+      const int lo = D->obs_off[(long long)b * M + j], hi = D->obs_off[(long long)b * M + j + 1];
+      for (int r = lo; r < hi; ++r) {
+        for (int a = 0; a < dim; ++a) L.C.push_back(D->obs_C[(long long)r * dim + a]);
+        L.d.push_back(D->obs_d[r]);
+      }
+      L.off.push_back(L.off.back() + (hi - lo));
+    }
+  out = *D;
+  out.n_obs = Ml;
+  out.obs_off = L.off.data();
+  out.obs_C = L.C.empty() ? nullptr : L.C.data();
+  out.obs_d = L.d.empty() ? nullptr : L.d.data();
 }
 
 ca_status ensure_slots(ca_problem* h, int n) {
@@ -535,10 +599,18 @@ void ca_problem_destroy(ca_problem* h) {
   delete h;
 }
 
-ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* D) {
+ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
   ca_status st = check_handle(h);
   if (st) return st;
-  if ((st = validate(D))) return st;
+  if ((st = validate(Dfull))) return st;
+  LocalObs lobs;
+  ca_problem_desc Dl;
+  const ca_problem_desc* D = Dfull;
+  if (h->comm) {
+    if (Dfull->n_obs != h->n_obs_full) return fail(CA_E_INVALID, "ca_problem_load: obstacle count differs");
+    slice_obstacles(Dfull, h->j0, h->j1, lobs, Dl);
+    D = &Dl;
+  }
   if (D->dim != h->d || D->n_scenes != h->B || D->horizon != h->N || D->n_state != h->ns ||
       D->n_ctrl != h->nu || D->n_parts != h->np || D->n_obs != h->M)
     return fail(CA_E_INVALID, "ca_problem_load: shapes differ from the handle");
@@ -561,6 +633,80 @@ ca_status ca_debug_trace(ca_problem* h, int64_t p, double* out) {
   }
   CUDA_TRY(cudaMemset(h->dev.dbg, 0xff, sizeof(double) * 64 * 48));
   h->dev.dbg_p = p;
+  return CA_OK;
+}
+
+ca_status ca_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return fail(CA_E_INVALID, "out is NULL");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return CA_OK;
+}
+
+ca_status ca_obstacle_partition(int32_t n_scenes, int32_t n_obs, const int32_t* obs_off, int32_t world, int32_t rank,
+                                int32_t* j0, int32_t* j1) {
+  if (!j0 || !j1 || world < 1 || rank < 0 || rank >= world || n_obs < 0 || n_scenes < 1 || (n_obs > 0 && !obs_off))
+    return fail(CA_E_INVALID, "bad partition arguments");
+  std::vector<long long> cnt(n_obs, 0);
+  long long total = 0;
+  for (int b = 0; b < n_scenes; ++b)
+    for (int j = 0; j < n_obs; ++j) {
+      const long long c = obs_off[(long long)b * n_obs + j + 1] - obs_off[(long long)b * n_obs + j];
+      cnt[j] += c;
+      total += c;
+    }
+  auto bnd = [&](int k) -> int {
+    if (k <= 0) return 0;
+    if (k >= world) return n_obs;
+    long long acc = 0;
+    for (int j = 0; j < n_obs; ++j) {
+      if (acc * world >= (long long)k * total) return j;
+      acc += cnt[j];
+    }
+    return n_obs;
+  };
+  *j0 = bnd(rank);
+  *j1 = bnd(rank + 1);
+  return CA_OK;
+}
+
+ca_status ca_problem_create_dist(const ca_problem_desc* D, const ca_dist_desc* dist, int device, void* stream,
+                                 ca_problem** out) {
+  if (!dist) return ca_problem_create(D, device, stream, out);
+  if (!out) return fail(CA_E_INVALID, "out is NULL");
+  *out = nullptr;
+  ca_status st = validate(D);
+  if (st) return st;
+  if (!dist->nccl_id || dist->world_size < 1 || dist->rank < 0 || dist->rank >= dist->world_size)
+    return fail(CA_E_INVALID, "bad ca_dist_desc");
+  int j0 = 0, j1 = 0;
+  if ((st = ca_obstacle_partition(D->n_scenes, D->n_obs, D->obs_off, dist->world_size, dist->rank, &j0, &j1)))
+    return st;
+  LocalObs lobs;
+  ca_problem_desc Dl;
+  slice_obstacles(D, j0, j1, lobs, Dl);
+  ca_problem* h = nullptr;
+  if ((st = ca_problem_create(&Dl, device, stream, &h))) return st;
+  h->world = dist->world_size;
+  h->rank = dist->rank;
+  h->j0 = j0;
+  h->j1 = j1;
+  h->n_obs_full = D->n_obs;
+  if ((st = h->alloc(&h->rb, (size_t)h->B * h->N * ca::REC)) || (st = h->alloc(&h->tmpB4, (size_t)h->B * 4))) {
+    delete h;
+    return st;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, dist->nccl_id, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&h->comm, dist->world_size, id, dist->rank);
+  if (r != ncclSuccess) {
+    h->comm = nullptr;
+    delete h;
+    return fail(CA_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *out = h;
   return CA_OK;
 }
 
@@ -617,7 +763,8 @@ ca_status ca_dual_sweep(ca_problem* h, ca_residuals* out) {
   ca_status st = check_handle(h);
   if (st) return st;
   if ((st = launch_sweep(h, false))) return mark(h, st);
-  if ((st = launch_collect(h, h->scene_res, 1 | 4 | 8))) return mark(h, st);
+  CUDA_TRY(cudaMemsetAsync(h->scene_res, 0, sizeof(double) * 4 * h->B, h->stream));
+  if ((st = collect_global(h, h->scene_res, 1 | 4 | 8))) return mark(h, st);
   ca_residuals r{};
   if ((st = sums(h, h->scene_res, &r))) return mark(h, st);
   r.r_pri = 0.0;
@@ -637,7 +784,7 @@ ca_status ca_multiplier_update(ca_problem* h, ca_residuals* out) {
   ca_status st = check_handle(h);
   if (st) return st;
   if ((st = launch_mult(h))) return mark(h, st);
-  if ((st = launch_collect(h, h->scene_res, 2))) return mark(h, st);
+  if ((st = collect_global(h, h->scene_res, 2))) return mark(h, st);
   ca_residuals r{};
   if ((st = sums(h, h->scene_res, &r))) return mark(h, st);
   if (out) {
@@ -661,7 +808,7 @@ ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist) {
   }
   if ((st = launch_mult(h))) return mark(h, st);
   double* last = h->slots + (size_t)(iters - 1) * h->B * 4;
-  if ((st = launch_collect(h, last, 2))) return mark(h, st);
+  if ((st = collect_global(h, last, 2))) return mark(h, st);
   CUDA_TRY(cudaMemcpyAsync(h->scene_res, last, sizeof(double) * h->B * 4, cudaMemcpyDeviceToDevice, h->stream));
   int64_t fails = 0;
   if (hist) {
@@ -835,6 +982,8 @@ ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, do
   ca::k_scene_min<<<h->B, 256, 0, h->stream>>>(h->alpha, h->P / h->B, h->alpha + h->P);
   CUDA_TRY(cudaGetLastError());
   h->launches[3]++;  // k_scene_min (k_scale is counted by t_end)
+  if (h->comm)
+    NCCL_TRY(ncclAllReduce(h->alpha + h->P, h->alpha + h->P, h->B, ncclDouble, ncclMin, h->comm, h->stream));
   t_end(h, 3, e0);
   if (alpha) CUDA_TRY(cudaMemcpyAsync(alpha, h->alpha, sizeof(double) * h->P, cudaMemcpyDeviceToHost, h->stream));
   if (min_alpha) CUDA_TRY(cudaMemcpyAsync(min_alpha, h->alpha + h->P, sizeof(double) * h->B, cudaMemcpyDeviceToHost, h->stream));

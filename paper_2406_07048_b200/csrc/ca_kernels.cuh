@@ -178,10 +178,27 @@ __global__ void k_collect(Dev P, double* dst, int mask) {
 // rpri of the fused multiplier update -> dst_prev) in fixed order.
 // ----------------------------------------------------------------------------
 #ifdef CA_COMMON_KERNELS
+// Obstacle-sharded runs: per (scene, t), sum the rank-local chunk records in fixed
+// order into one record (the buffer that is then ncclAllReduce'd across ranks).
+__global__ void k_reduce_records(Dev P, double* out) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)P.B * P.N) return;
+  double acc[REC];
+#pragma unroll
+  for (int f = 0; f < REC; ++f) acc[f] = 0.0;
+  for (int c = 0; c < P.nchunk; ++c) {
+    const double* rec = P.agg + (q * P.nchunk + c) * REC;
+#pragma unroll
+    for (int f = 0; f < REC; ++f) acc[f] += rec[f];
+  }
+#pragma unroll
+  for (int f = 0; f < REC; ++f) out[q * REC + f] = acc[f];
+}
+
 // Stage assembly, one thread per (scene, t), t = 1..N (fully parallel): sums the
 // (scene, t) chunk records in fixed order and writes H_t (ns x ns), h_t (ns) and
 // the per-(scene, t) statistics to P.stg.
-__global__ void k_stage(Dev P) {
+__global__ void k_stage(Dev P, const double* recs, int nchunk) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + (t-1)
   if (q >= (long long)P.B * P.N) return;
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
@@ -194,8 +211,8 @@ __global__ void k_stage(Dev P) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) S[a][c] = 0.0;
   }
-  for (int c = 0; c < P.nchunk; ++c) {
-    const double* rec = P.agg + (q * P.nchunk + c) * REC;
+  for (int c = 0; c < nchunk; ++c) {
+    const double* rec = recs + (q * nchunk + c) * REC;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       if (a >= L1) continue;

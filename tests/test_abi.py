@@ -70,3 +70,19 @@ def test_validation_errors_precede_device(ca):
 def test_fails_loudly_without_gpu(ca):
     code, msg = _create(ca, scenes.make_config(1))
     assert code == -5 and "no CPU fallback" in msg
+
+
+def test_obstacle_partition_properties(ca):
+    """ca_obstacle_partition (host only): contiguous, disjoint, covering, face-balanced."""
+    for cfg, kw in ((4, {}), (2, {}), (5, {"n_scenes": 3})):
+        sc = scenes.make_config(cfg, **kw)
+        faces = np.diff(sc.obs_off).reshape(sc.n_scenes, sc.n_obs).sum(0)
+        for W in (1, 2, 3, 5, 8):
+            parts = [ca.obstacle_partition(sc, W, r) for r in range(W)]
+            assert parts[0][0] == 0 and parts[-1][1] == sc.n_obs
+            for (a0, a1), (b0, b1) in zip(parts, parts[1:]):
+                assert a1 == b0 and a0 <= a1
+            tot = faces.sum()
+            for r, (j0, j1) in enumerate(parts):
+                got = faces[j0:j1].sum()
+                assert abs(got - tot / W) <= faces.max() + 1e-9, (cfg, W, r, got, tot / W)

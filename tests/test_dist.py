@@ -73,3 +73,68 @@ def test_scene_sharding_world2_gloo():
     o = oracle.Oracle(ref)
     o.admm_iterate(iters)
     assert np.array_equal(s_sharded, o.s)
+
+
+def _worker_obs(rank, world, port, out):
+    """Obstacle sharding: each rank solves the pair QPs of its obstacle block; the
+    per-timestep partial sums are all-reduced (the a5 exchange of SURVEY §8(a))."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import paper_2406_07048_b200 as ca
+    import scenes
+    from parity_util import pair_geometry
+
+    sc = scenes.make_config(2)
+    j0, j1 = ca.obstacle_partition(sc, world, rank)
+    part = torch.zeros(sc.horizon, dtype=torch.float64)
+    M = sc.n_obs
+    for p in range(sc.n_pairs):
+        if not (j0 <= p % M < j1):
+            continue
+        b, t, A, bb, Cm, dv = pair_geometry(sc, p)
+        R, rho = oracle.pose(sc.pose_model, sc.pose_idx, sc.dim, sc.s_ref[b, t])
+        y, st, piv, _ = oracle.pair_solve(A, bb, Cm, dv, R, rho, 0.0, np.zeros(2))
+        K, bvec, *_ = oracle.pair_lcp(A, bb, Cm, dv, R, rho, 0.0, np.zeros(2))
+        u = K.T @ y + bvec
+        part[t - 1] += 0.5 * float(u @ u)
+    dist.all_reduce(part)
+    if rank == 0:
+        out.put(part.numpy())
+    dist.destroy_process_group()
+
+
+def test_obstacle_sharding_world2_gloo():
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle
+    import scenes
+    from parity_util import pair_geometry
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_obs, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sc = scenes.make_config(2)
+    ref = np.zeros(sc.horizon)
+    for p in range(sc.n_pairs):
+        b, t, A, bb, Cm, dv = pair_geometry(sc, p)
+        R, rho = oracle.pose(sc.pose_model, sc.pose_idx, sc.dim, sc.s_ref[b, t])
+        y, st, piv, _ = oracle.pair_solve(A, bb, Cm, dv, R, rho, 0.0, np.zeros(2))
+        K, bvec, *_ = oracle.pair_lcp(A, bb, Cm, dv, R, rho, 0.0, np.zeros(2))
+        u = K.T @ y + bvec
+        ref[t - 1] += 0.5 * float(u @ u)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)

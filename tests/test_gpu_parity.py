@@ -249,3 +249,24 @@ def test_c5_full_size_stepwise(ca):
             assert np.abs(st1["xi"] - o.xi).max() <= 1e-9 * sc_z
             prev[b] = (s1, u1, st1)
     print("C5 validated Lemke flips:", total_flips)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_obstacle_sharded_world1_nccl(ca, cfg):
+    """The obstacle-sharded path (record reduction + ncclAllReduce + replicated Riccati)
+    at world size 1 matches the unsharded solve (summation order differs)."""
+    sc = scene(cfg)
+    K = 20
+    a = ca.Problem(sc)
+    rca, ha = a.admm_iterate(K)
+    b = ca.Problem(sc, dist=(1, 0, ca.nccl_unique_id()))
+    rcb, hb = b.admm_iterate(K)
+    sa, ua = a.trajectory()
+    sb, ub = b.trajectory()
+    close(sb, sa, 1e-10, "s (sharded vs plain)")
+    close(ub, ua, 1e-10, "u (sharded vs plain)")
+    np.testing.assert_allclose(hb["r_pri"], ha["r_pri"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(hb["r_dual"], ha["r_dual"], rtol=1e-9, atol=1e-12)
+    _, ma = a.scale_detect(want_alpha=False)
+    _, mb = b.scale_detect(want_alpha=False)
+    np.testing.assert_allclose(mb, ma, rtol=1e-12)
