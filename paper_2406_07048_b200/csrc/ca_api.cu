@@ -231,6 +231,8 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
   ca_status st;
   if ((st = h2d(h, const_cast<double*>(v.part_rows), pr.data(), pr.size()))) return st;
   if ((st = h2d(h, const_cast<int*>(v.part_off), D->part_off, (size_t)h->np + 1))) return st;
+  ca::k_lamtab<<<1, 32, 0, h->stream>>>(v);
+  CUDA_TRY(cudaGetLastError());
   if (h->M > 0) {
     if ((st = h2d(h, const_cast<double*>(v.obs_rows), orr.data(), 4 * (size_t)orow))) return st;
     if ((st = h2d(h, const_cast<int*>(v.obs_off), D->obs_off, (size_t)B * h->M + 1))) return st;
@@ -580,6 +582,10 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));
   AL(v.gperm2, uint16_t, (size_t)B * N * std::max(1, v.G));
+  AL(v.pose, double, (size_t)B * N * 12);
+  AL(v.lam, double, (size_t)h->np * std::max(1, v.nrmax - 1) * (d + 2));
+  AL(v.part_e, int, (size_t)h->np);
+  AL(v.part_be, double, (size_t)h->np);
 #undef AL
   v.zmask = nullptr;
   v.dbg_p = -1;

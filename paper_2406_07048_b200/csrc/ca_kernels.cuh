@@ -54,6 +54,10 @@ struct Dev {
   double* stg_stats;  // [B*N][4]
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
   uint16_t* gperm2;  // [B*N][G]: per-(b,t) execution order, re-sorted by last pivot count
+  double* pose;      // [B*N][12]: R(s_t) (d x d, row-major) at [0..8], rho(s_t) at [9..11] (k_sortpairs)
+  double* lam;       // [np][nrmax-1][d+2]: lambda rows (0, at_u, kt_u) of Eqs. 20-21 (k_lamtab)
+  int* part_e;       // [np]: eliminated index e = argmax b (reading #3)
+  double* part_be;   // [np]: b_e
   long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
   double* dbg;       // [64][12]
 };
@@ -625,10 +629,39 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
 // n-sorted order gperm) by their pivot count of the previous sweep, so that a
 // warp's 32 threads run Lemke paths of similar length.  Pure scheduling:
 // deterministic, results are stored at each pair's own index.
+// Eqs. 20-21 for the lambda rows depend on the robot part only (once per load):
+//   e = argmax_k b_k (lowest k on ties), kt_k = b_k / b_e, at_k = a_k - kt_k a_e
+__global__ void k_lamtab(Dev P) {
+  const int ip = threadIdx.x;
+  if (ip >= P.np) return;
+  const int d = P.d, LT = (P.nrmax - 1) * (d + 2);
+  const int r0 = P.part_off[ip], nr = P.part_off[ip + 1] - r0;
+  const double* pr = P.part_rows + 4 * r0;
+  int e = 0;
+  double be = pr[3];
+  for (int k = 1; k < nr; ++k)
+    if (pr[4 * k + 3] > be) { be = pr[4 * k + 3]; e = k; }
+  P.part_e[ip] = e;
+  P.part_be[ip] = be;
+  double* lt = P.lam + ip * LT;
+  for (int k = 0; k < nr; ++k) {
+    if (k == e) continue;
+    const int u = k - (k > e);
+    const double ratio = pr[4 * k + 3] / be;
+    lt[u * (d + 2)] = __fma_rn(-ratio, 0.0, 0.0);
+    for (int a = 0; a < d; ++a) lt[u * (d + 2) + 1 + a] = __fma_rn(-ratio, pr[4 * e + a], pr[4 * k + a]);
+    lt[u * (d + 2) + d + 1] = ratio;
+  }
+}
+
 __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   constexpr int NB = 32;
   __shared__ int cnt[NB][33];
   const int bt = blockIdx.x, b = bt / P.N, tid = threadIdx.x;
+  if (tid == 0) {  // pose(s_t^k) of this (b, t) for the sweep
+    double* po = P.pose + (long long)bt * 12;
+    pose_of(P, P.s + ((long long)b * (P.N + 1) + bt % P.N + 1) * P.ns, po, po + 9);
+  }
   const int G = P.G;
   const int per = (G + 31) / 32, lo = tid * per, hi = min(G, lo + per);
   const int* base = P.gperm + (long long)b * G;

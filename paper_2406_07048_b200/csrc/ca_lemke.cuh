@@ -38,7 +38,7 @@ enum { ST_OK = 0, ST_RAY = 1, ST_ITER = 2, ST_NEGYE = 3 };
 //   i == n-1       phi row:     0                            [per-thread table]
 // row() is branch-free: a pointer/stride select between the two tables.
 template <int D>
-struct PairRows {
+struct PairRows {  // @region row_fetch
   const double* lam;  // [(nr-1)][D+2] = (0, at_1..at_D, kt)  (CTA smem)
   const double* mu;   // [no+2][D+1], stride `ms` between doubles (thread smem)
   int ms;
@@ -56,7 +56,7 @@ struct PairRows {
 
 // M_ij of Eq. 24 from two reduced rows (row/col l = n-1 is the phi row)
 template <int D>
-__device__ __forceinline__ double m_entry(const double fi[D + 1], double ki, int i, const double fj[D + 1],
+__device__ __forceinline__ double m_entry(const double fi[D + 1], double ki, int i, const double fj[D + 1],  // @region m_entry
                                           double kj, int j, int l) {
   double acc = 0.0;
 #pragma unroll
@@ -70,7 +70,7 @@ __device__ __forceinline__ double m_entry(const double fi[D + 1], double ki, int
 // Gauss-Jordan with partial pivoting (rows physically swapped) on an m x (m+1)
 // system stored with element stride `es`: A[(p*(mm+1)+c)*es], mm = row capacity.
 // Solution left in column m: x_s = A[s][m].
-__device__ __forceinline__ void gj_solve(double* A, int es, int mm, int m) {
+__device__ __forceinline__ void gj_solve(double* A, int es, int mm, int m) {  // @region gj_solve
 #define GA(p_, c_) A[((p_) * (mm + 1) + (c_)) * es]
   for (int c = 0; c < m; ++c) {
     int pb = c;
@@ -116,7 +116,7 @@ struct Lemke {
   //   coef(w_i) = F_i.uh + kt_i sl - [i=l] sk + s0
   // and writes x_s for the structural columns into xcol (smem, stride es).
   // Columns: basic z_j in increasing j, then z0 if basic.  Rows: R increasing.
-  __device__ __noinline__ static ColSol<D> solve_column(const PairRows<D> W, double* Gs, int gs, uint32_t wb,
+  __device__ __noinline__ static ColSol<D> solve_column(const PairRows<D> W, double* Gs, int gs, uint32_t wb,  // @region solve_column
                                                        uint32_t zb, bool z0b, Var e, double* Gslow) {
     ColSol<D> out;
     double* uh = out.uh;
@@ -197,70 +197,57 @@ struct SmallSol {
 
 template <int D>
 __device__ __forceinline__ bool solve_small(const PairRows<D>& W, uint32_t wb, uint32_t zb, bool z0b, Var e,
-                                            SmallSol<D>& out) {
+                                            SmallSol<D>& out) {  // @region small_build
   const uint32_t nmask = (W.n >= 32) ? 0xffffffffu : ((1u << W.n) - 1u);
   const uint32_t Rm = ~wb & nmask;
   const int m = __popc(Rm);
   if (m > 3) return false;
   const int mz = __popc(zb);
   const int l = W.l;
+  // Branch-free: every row fetch uses a valid index (clamped), the results of the
+  // padding slots are discarded by selects.
   double fc[3][D + 1], kc[3];
   int jc[3];
   uint32_t zbits = zb;
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    jc[s] = -1;
-    kc[s] = 0.0;
-#pragma unroll
-    for (int c = 0; c <= D; ++c) fc[s][c] = 0.0;
-    if (s < mz) {
-      const int j = __ffs(zbits) - 1;
-      zbits &= zbits - 1;
-      W.row(j, fc[s], kc[s]);
-      jc[s] = j;
-    }
+    const int j = __ffs(zbits) - 1;  // -1 when exhausted
+    zbits &= zbits - 1;
+    W.row(j < 0 ? 0 : j, fc[s], kc[s]);
+    jc[s] = j;
   }
-  double fe[D + 1], ke = 0.0;
-#pragma unroll
-  for (int c = 0; c <= D; ++c) fe[c] = 0.0;
-  if (e.kind == 1) W.row(e.j, fe, ke);
+  double fe[D + 1], ke;
+  W.row(e.kind == 1 ? e.j : 0, fe, ke);
   double G[3][4];
   uint32_t rbits = Rm;
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
+    const int i = __ffs(rbits) - 1;
+    rbits &= rbits - 1;
+    double fi[D + 1], ki;
+    W.row(i < 0 ? 0 : i, fi, ki);
+    const bool real = p < m;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) G[p][c] = 0.0;
-    if (p < m) {
-      const int i = __ffs(rbits) - 1;
-      rbits &= rbits - 1;
-      double fi[D + 1], ki;
-      W.row(i, fi, ki);
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        if (s < mz) G[p][s] = -m_entry<D>(fi, ki, i, fc[s], kc[s], jc[s], l);
-        else if (s == mz && z0b) G[p][s] = -1.0;
-      }
-      double a;
-      if (e.kind == 0) a = (i == e.j) ? 1.0 : 0.0;
-      else if (e.kind == 2) a = -1.0;
-      else a = -m_entry<D>(fi, ki, i, fe, ke, e.j, l);
-      G[p][3] = a;
-    } else {
-      G[p][p] = 1.0;
+    for (int s = 0; s < 3; ++s) {
+      const double me = -m_entry<D>(fi, ki, i, fc[s], kc[s], jc[s], l);
+      const double v = (s < mz) ? me : ((s == mz && z0b) ? -1.0 : 0.0);
+      G[p][s] = real ? v : ((p == s) ? 1.0 : 0.0);
     }
+    const double me = -m_entry<D>(fi, ki, i, fe, ke, e.j, l);
+    const double a = (e.kind == 0) ? ((i == e.j) ? 1.0 : 0.0) : ((e.kind == 2) ? -1.0 : me);
+    G[p][3] = real ? a : 0.0;
   }
-  // Gauss-Jordan with partial pivoting, compile-time indices
+  // Gauss-Jordan with partial pivoting, compile-time indices  // @region small_gj
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
 #pragma unroll
     for (int r = c + 1; r < 3; ++r) {
-      if (fabs(G[r][c]) > fabs(G[c][c])) {
+      const bool sw = fabs(G[r][c]) > fabs(G[c][c]);
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const double t = G[c][cc];
-          G[c][cc] = G[r][cc];
-          G[r][cc] = t;
-        }
+      for (int cc = c; cc < 4; ++cc) {
+        const double t = G[c][cc];
+        G[c][cc] = sw ? G[r][cc] : t;
+        G[r][cc] = sw ? t : G[r][cc];
       }
     }
     const double inv = 1.0 / G[c][c];
@@ -274,29 +261,28 @@ __device__ __forceinline__ bool solve_small(const PairRows<D>& W, uint32_t wb, u
       for (int cc = c + 1; cc < 4; ++cc) G[r][cc] = __fma_rn(-f, G[c][cc], G[r][cc]);
     }
   }
+  double uh[D + 1], sl = 0.0, sk = 0.0, s0 = 0.0;
 #pragma unroll
-  for (int c = 0; c <= D; ++c) out.uh[c] = 0.0;
-  out.sl = out.sk = out.s0 = 0.0;
+  for (int c = 0; c <= D; ++c) uh[c] = 0.0;
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
-    out.x[s] = G[s][3];
-    if (s < mz) {
+    const double x = G[s][3];
+    out.x[s] = x;
+    const bool col = s < mz;
+    const double xz = col ? x : 0.0;  // contributes exact zeros otherwise
 #pragma unroll
-      for (int c = 0; c <= D; ++c) out.uh[c] = __fma_rn(out.x[s], fc[s][c], out.uh[c]);
-      out.sk = __fma_rn(out.x[s], kc[s], out.sk);
-      if (jc[s] == l) out.sl += out.x[s];
-    } else if (s == mz && z0b) {
-      out.s0 += out.x[s];
-    }
+    for (int c = 0; c <= D; ++c) uh[c] = col ? __fma_rn(x, fc[s][c], uh[c]) : uh[c];
+    sk = col ? __fma_rn(x, kc[s], sk) : sk;
+    sl = (col && jc[s] == l) ? sl + xz : sl;
+    s0 = (s == mz && z0b) ? s0 + x : s0;
   }
-  if (e.kind == 2) {
-    out.s0 -= 1.0;
-  } else if (e.kind == 1) {
+  if (e.kind == 2) s0 -= 1.0;
+  const bool ez = e.kind == 1;
 #pragma unroll
-    for (int c = 0; c <= D; ++c) out.uh[c] -= fe[c];
-    out.sk -= ke;
-    if (e.j == l) out.sl -= 1.0;
-  }
+  for (int c = 0; c <= D; ++c) out.uh[c] = ez ? uh[c] - fe[c] : uh[c];
+  out.sk = ez ? sk - ke : sk;
+  out.sl = (ez && e.j == l) ? sl - 1.0 : sl;
+  out.s0 = s0;
   return true;
 }
 

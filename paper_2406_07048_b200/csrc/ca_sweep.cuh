@@ -31,6 +31,7 @@ struct SweepSmem {
   static constexpr int VAL = NMAX, CB = NMAX;
   static constexpr int ROWB = (NMAX + 1 + 7) / 8;  // tableau-row labels, bytes
   static constexpr int PER_THREAD = MU + VAL + CB + ROWB;  // doubles
+  static_assert(PER_THREAD >= REC, "the record reduction reuses the per-thread column");
   // + the CTA-shared lambda-row table of every robot part
   static size_t bytes(int np, int nrmax) {
     return sizeof(double) * ((size_t)PER_THREAD * CTA + (size_t)np * (nrmax - 1) * (D + 2));
@@ -40,7 +41,7 @@ struct SweepSmem {
 // L5.4-5 (rare): lexicographic rule on the w columns (= B^{-1}) among the tied
 // members `tm`; returns the leaving member (pair index).
 template <int D, int NMAX>
-__device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const double* scb,
+__device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const double* scb,  // @region lexico
                                    const unsigned char* rowb, uint32_t wb, uint32_t zb, bool z0b, uint32_t tm,
                                    double tau) {
   const int n = W.n;
@@ -108,7 +109,7 @@ __device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const dou
 // Writes the basic z values into sval (by LCP index) and returns the status;
 // *zb_out = basic-z mask, *piv_out = pivots.
 template <int D, int NMAX>
-__device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil, double be, LemkeParams LP,
+__device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil, double be, LemkeParams LP,  // @region lemke_dense
                                         double* sval, uint32_t* zb_out, int* piv_out) {
   const int n = W.n, l = n - 1;
   constexpr int WC = 2 * NMAX + 2;
@@ -229,7 +230,7 @@ __device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil,
 }
 
 template <int D, int NMAX, bool FUSED>
-__global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
+__global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setup
   using SM = SweepSmem<D, NMAX>;
   constexpr int L1 = D + 1;
   extern __shared__ double smem[];
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
   const int tid = threadIdx.x;
   const int chunk = blockIdx.x % P.nchunk;
   const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
-  const int b = bt / P.N, t = bt % P.N + 1;
+  const int b = bt / P.N;
   double* mu = smem + tid;
   double* sval = mu + SM::MU * CTA;
   double* scb = sval + SM::VAL * CTA;
@@ -248,28 +249,13 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
       reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::VAL + SM::CB) * CTA) + tid;
   double* lamtab = smem + SM::PER_THREAD * CTA;  // [np][nrmax-1][D+1]
   const int LT = (P.nrmax - 1) * (D + 2);
-  if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
+  // pose(s_t^k) (k_sortpairs) and the lambda-row table (k_lamtab): plain copies
+  if (tid < 9) sR[tid] = P.pose[(long long)bt * 12 + tid];
+  else if (tid < 12) srho[tid - 9] = P.pose[(long long)bt * 12 + tid];
+  for (int k = tid; k < P.np * LT; k += CTA) lamtab[k] = P.lam[k];
   if (tid < P.np) {
-    // Eqs. 20-21 for the lambda rows depend on the robot part only:
-    //   e = argmax_k b_k (lowest k on ties), kt_k = b_k / b_e, at_k = a_k - kt_k a_e
-    const int r0 = P.part_off[tid], nr = P.part_off[tid + 1] - r0;
-    const double* pr = P.part_rows + 4 * r0;
-    int e = 0;
-    double be = pr[3];
-    for (int k = 1; k < nr; ++k)
-      if (pr[4 * k + 3] > be) { be = pr[4 * k + 3]; e = k; }
-    part_e[tid] = e;
-    part_be[tid] = be;
-    double* lt = lamtab + tid * LT;
-    for (int k = 0; k < nr; ++k) {
-      if (k == e) continue;
-      const int u = k - (k > e);
-      const double ratio = pr[4 * k + 3] / be;
-      lt[u * (D + 2)] = __fma_rn(-ratio, 0.0, 0.0);
-#pragma unroll
-      for (int a = 0; a < D; ++a) lt[u * (D + 2) + 1 + a] = __fma_rn(-ratio, pr[4 * e + a], pr[4 * k + a]);
-      lt[u * (D + 2) + D + 1] = ratio;
-    }
+    part_e[tid] = P.part_e[tid];
+    part_be[tid] = P.part_be[tid];
   }
   __syncthreads();
 #define VAL(i) sval[(i) * CTA]
@@ -291,7 +277,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
     const double* orow = P.obs_rows + 4 * (long long)l0;
     const int e = part_e[ip];
     const double be = part_be[ip];
-    double zeta = P.zeta[p], xi[D];
+    double zeta = P.zeta[p], xi[D];  // @region pair_setup
 #pragma unroll
     for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
     // obstacle rows of K at pose(s^k) (Eq. 19b): (d_l - c_l.rho, R^T c_l)
@@ -323,24 +309,27 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
       }
     }
     const PairRows<D> W{lamtab + ip * LT, mu, CTA, nr, no, n, n - 1};
-    if (FUSED) {
-      // Eq. 17 for the previous iteration at s^k with y^k (Eqs. 10-11)
+    if (FUSED) {  // @region fused_mult
+      // Eq. 17 for the previous iteration at s^k with y^k (Eqs. 10-11); y^k is
+      // staged in the (still unused) cbar scratch with batched loads
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) CBV(k) = YK(k);
       double Tv = 1.0, Rv[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) Rv[a] = 0.0;
       for (int k = 0; k < nr; ++k) {
-        const double yv = YK(k);
+        const double yv = CBV(k);
 #pragma unroll
         for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yv, prow[4 * k + a], Rv[a]);
       }
       for (int k = nr; k < nr + no; ++k) {
-        const double yv = YK(k);
+        const double yv = CBV(k);
         const double* m = mu + (k - nr) * L1 * CTA;
         Tv = __fma_rn(yv, m[0], Tv);
 #pragma unroll
         for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yv, m[(1 + a) * CTA], Rv[a]);
       }
-      Tv += YK(nr + no);
+      Tv += CBV(nr + no);
       zeta += Tv;
       double r2 = Tv * Tv;
 #pragma unroll
@@ -353,7 +342,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
 #pragma unroll
       for (int a = 0; a < D; ++a) P.xi[(long long)a * PP + p] = xi[a];
     }
-    // q = [Kt btil; etatil]  with btil = bvec + K_e / b_e, etatil = 1 / b_e (Eq. 25)
+    // q = [Kt btil; etatil]  with btil = bvec + K_e / b_e, etatil = 1 / b_e (Eq. 25)  // @region q_build
     double bt_[D + 1];
     bt_[0] = (1.0 + zeta) + 0.0 / be;
 #pragma unroll
@@ -370,7 +359,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
       VAL(i) = acc;
       qmin = fmin(qmin, acc);
     }
-    // ------------------------------------------------------------------ Lemke
+    // ------------------------------------------------------------------ Lemke  // @region lemke_init
     const LemkeParams& LP = P.lp;
     const double tau = LP.tie_tol, ptol = LP.pivot_tol;
     const uint32_t nmask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
@@ -399,11 +388,17 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
       Var ent{1, r};
       const int maxpiv = LP.max_pivot_factor * n;
       double Gslow[(D + 4) * (D + 5)];
+      const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+      const double kSlack = 1.0 + 1e-12;  // candidate superset margin (filtered exactly below)
+      const double* lt = lamtab + ip * LT;
+      const int nr1 = nr - 1;
+      uint32_t pend = 0;  // rows still owing the previous pivot's value update
+      double ve2p = 0.0;
       for (;;) {
         if (pivots >= maxpiv) { status = ST_ITER; break; }
         if (n - __popc(wb) > D + 4) { status = ST_ITER; break; }  // rank bound (cannot happen exactly)
         // structural m x m system: registers for m <= 3, generic solver otherwise
-        SmallSol<D> ss;
+        SmallSol<D> ss;  // @region solve_call
         const bool small = solve_small<D>(W, wb, zb, z0b, ent, ss);
         if (!small) {
           const ColSol<D> cg = Lemke<D, NMAX, D + 4>::solve_column(W, Gslow, 1, wb, zb, z0b, ent, Gslow);
@@ -418,82 +413,103 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           return Gslow[s * (D + 5) + D + 4];
         };
         const uint32_t basic = wb | zb;
-        // pass 1: entering-column coefficient of every basic variable, max |cbar|, and
-        // the minimum ratio max(val,0)/cbar (L5.2, cross-multiplied) over rows with
-        // cbar > pivot_tol (a superset of the eligible rows cbar > pivot_tol max(1,cmax))
-        double cmax = 0.0, bn = -1.0, bd = 1.0;
-#pragma unroll 1
-        for (int i = 0; i < n; ++i) {
+        // pass 1 (one sweep over the rows, segment by segment so every row fetch is a  // @region pass1
+        // fixed-stride load): apply the previous pivot's value update (deferred from
+        // L3), store the entering-column coefficient cbar_i of row i, and run the
+        // L5.2 ratio test on the fly -- provisional minimum over cbar > pivot_tol (a
+        // superset of the eligible rows cbar > pivot_tol max(1, cmax)) plus a
+        // superset `cand` of the final tie set (rows within the tie tolerance of
+        // the running minimum, which only shrinks).
+        double cmax = 0.0, bn = kInf, bd = 1.0, tn = kInf;
+        uint32_t cand = 0;
+        auto ratio = [&](bool el, double c, double v) -> bool {  // branch-free
+          const double nu = (v > 0.0) ? v : 0.0;
+          const bool lt = el && (nu * bd < bn * c);
+          const double tnn = __fma_rn(tau, (c > nu) ? c : nu, nu) * kSlack;  // (theta + tau max(1,theta)) bd
+          bn = lt ? nu : bn;
+          bd = lt ? c : bd;
+          tn = lt ? tnn : tn;
+          return el && (nu * bd <= tn * c);
+        };
+        auto rowc = [&](int i, double c) {
           const uint32_t bit = 1u << i;
-          double c = 0.0;
-          if (wb & bit) {
-            double f[D + 1], k;
-            W.row(i, f, k);
-            c = ss.s0;
-#pragma unroll
-            for (int cc = 0; cc <= D; ++cc) c = __fma_rn(f[cc], ss.uh[cc], c);
-            c = __fma_rn(k, ss.sl, c);
-            if (i == n - 1) c -= ss.sk;
-          } else if (zb & bit) {
-            c = xcol(__popc(zb & (bit - 1u)));
-          }
+          const double vo = VAL(i), co = CBV(i);
+          const double vu = __fma_rn(-co, ve2p, vo);
+          const double v = (pend & bit) ? vu : vo;
+          VAL(i) = v;
           CBV(i) = c;
+          const bool wbas = (wb & bit) != 0u;
           const double ac = fabs(c);
-          cmax = (ac > cmax) ? ac : cmax;
-          if ((basic & bit) && c > ptol) {
-            const double v = VAL(i);
-            const double nu = (v > 0.0) ? v : 0.0;
-            if (bn < 0.0 || nu * bd < bn * c) { bn = nu; bd = c; }
+          cmax = (wbas && ac > cmax) ? ac : cmax;
+          cand |= ratio(wbas && c > ptol, c, v) ? bit : 0u;
+        };
+        // lambda rows (0, at_u, kt_u): CTA-shared table of part ip
+#pragma unroll 1
+        for (int i = 0; i < nr1; ++i) {
+          const double* r = lt + i * (D + 2);
+          double c = ss.s0;
+#pragma unroll
+          for (int cc = 0; cc <= D; ++cc) c = __fma_rn(r[cc], ss.uh[cc], c);
+          rowc(i, __fma_rn(r[D + 1], ss.sl, c));
+        }
+        // mu rows (d_l - c_l.rho, R^T c_l) and the gamma row (1, 0): kt = 0
+#pragma unroll 1
+        for (int l = 0; l <= no; ++l) {
+          const double* m = mu + l * L1 * CTA;
+          double c = ss.s0;
+#pragma unroll
+          for (int cc = 0; cc <= D; ++cc) c = __fma_rn(m[cc * CTA], ss.uh[cc], c);
+          rowc(nr1 + l, c);
+        }
+        rowc(n - 1, ss.s0 - ss.sk);  // phi row (0, 0)
+        pend = 0;
+        // basic z rows: cbar is the structural solution itself
+        {
+          int s = 0;
+#pragma unroll 1
+          for (uint32_t bb = zb; bb; bb &= bb - 1, ++s) {
+            const int i = __ffs(bb) - 1;
+            const double c = xcol(s);
+            CBV(i) = c;
+            const double ac = fabs(c);
+            cmax = (ac > cmax) ? ac : cmax;
+            cand |= ratio(c > ptol, c, VAL(i)) ? (1u << i) : 0u;
           }
         }
         double cb0 = 0.0;
         if (z0b) {
           cb0 = xcol(__popc(zb));
           cmax = fmax(cmax, fabs(cb0));
-          if (cb0 > ptol) {
-            const double nu = fmax(val0, 0.0);
-            if (bn < 0.0 || nu * bd < bn * cb0) { bn = nu; bd = cb0; }
-          }
+          ratio(cb0 > ptol, cb0, val0);
         }
         const double thr = ptol * fmax(1.0, cmax);
-        if (bn >= 0.0 && !(bd > thr)) {
+        if (bn < kInf && !(bd > thr)) {
           // rare: the provisional minimiser is not eligible -> exact pass over cbar > thr
-          bn = -1.0;
+          bn = kInf;
           bd = 1.0;
+          tn = kInf;
+          cand = 0;
 #pragma unroll 1
-          for (int i = 0; i < n; ++i) {
+          for (uint32_t bb = basic; bb; bb &= bb - 1) {
+            const int i = __ffs(bb) - 1;
             const double c = CBV(i);
-            if (((basic >> i) & 1u) && c > thr) {
-              const double nu = fmax(VAL(i), 0.0);
-              if (bn < 0.0 || nu * bd < bn * c) { bn = nu; bd = c; }
-            }
+            cand |= ratio(c > thr, c, VAL(i)) ? (1u << i) : 0u;
           }
-          if (z0b && cb0 > thr) {
-            const double nu = fmax(val0, 0.0);
-            if (bn < 0.0 || nu * bd < bn * cb0) { bn = nu; bd = cb0; }
-          }
+          ratio(z0b && cb0 > thr, cb0, val0);
         }
-        if (bn < 0.0) { status = ST_RAY; break; }
+        if (!(bn < kInf)) { status = ST_RAY; break; }
         const double thmin = bn / bd;
         const double tt = thmin + tau * fmax(1.0, thmin);
-        // pass 2: tie set (L5.2) with the leaving candidate's coefficient and value
+        // tie set (L5.2): filter the candidates against the final minimum  // @region tie_filter
         uint32_t tiem = 0;
-        double cr = 0.0, vr = 0.0;
-        int lm = -2;
 #pragma unroll 1
-        for (uint32_t bb = basic; bb; bb &= bb - 1) {
+        for (uint32_t bb = cand; bb; bb &= bb - 1) {
           const int i = __ffs(bb) - 1;
           const double c = CBV(i);
-          if (c > thr) {
-            const double v = VAL(i);
-            if (fmax(v, 0.0) <= tt * c) {
-              tiem |= 1u << i;
-              lm = i;
-              cr = c;
-              vr = v;
-            }
-          }
+          if (c > thr && fmax(VAL(i), 0.0) <= tt * c) tiem |= 1u << i;
         }
+        int lm;
+        double cr, vr;
         if (z0b && cb0 > thr && fmax(val0, 0.0) <= tt * cb0) {
           lm = -1;  // L5.3: z0 leaves whenever it is tied
           cr = cb0;
@@ -501,8 +517,8 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
         } else if (tiem == 0) {
           status = ST_RAY;
           break;
-        } else if (__popc(tiem) > 1) {
-          lm = lexico<D, NMAX>(W, Gslow, scb, rowb, wb, zb, z0b, tiem, tau);
+        } else {
+          lm = (__popc(tiem) > 1) ? lexico<D, NMAX>(W, Gslow, scb, rowb, wb, zb, z0b, tiem, tau) : (__ffs(tiem) - 1);
           cr = CBV(lm);
           vr = VAL(lm);
         }
@@ -513,17 +529,14 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           dd[12] = val0; dd[13] = cb0;
           for (int i = 0; i < n && i < 16; ++i) { dd[14 + i] = CBV(i); dd[30 + i] = VAL(i); }
         }
-        // L3: pivot (values only: the structure is re-derived from the basis);
+        // L3: pivot (values only: the structure is re-derived from the basis); the  // @region pivot_update
+        // update of the other basic values is deferred to the next pass 1 (`pend`);
         // the entering variable takes the leaving one's tableau row
         const bool leave_w = (lm >= 0) && ((wb >> lm) & 1u);
-        const double inv = 1.0 / cr;
-        const double ve2 = vr * inv;
+        const double ve2 = vr * (1.0 / cr);
         const int je = ent.j;
-#pragma unroll 1
-        for (uint32_t bb = basic & ~(lm >= 0 ? (1u << lm) : 0u); bb; bb &= bb - 1) {
-          const int i = __ffs(bb) - 1;
-          VAL(i) = __fma_rn(-CBV(i), ve2, VAL(i));
-        }
+        pend = basic & ~(lm >= 0 ? (1u << lm) : 0u);
+        ve2p = ve2;
         if (z0b && lm >= 0) val0 = __fma_rn(-cb0, ve2, val0);
         VAL(je) = ve2;
         rowb[je * CTA] = (lm >= 0) ? rowb[lm * CTA] : rowb[NMAX * CTA];
@@ -540,8 +553,14 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
           ent = Var{0, lm};
         }
       }
+#pragma unroll 1
+      for (uint32_t bb = pend; bb; bb &= bb - 1) {  // the last pivot's deferred update
+        const int i = __ffs(bb) - 1;
+        VAL(i) = __fma_rn(-CBV(i), ve2p, VAL(i));
+      }
     }
-    // ------------------------------------------------------- verification
+
+    // ------------------------------------------------------- verification  // @region verify
     // The revised path never forms the tableau, so check its answer against the
     // LCP itself: w = M z + q (O(n d) with the low-rank M), w_i = value of basic
     // w_i or 0, w >= 0, z >= 0.  Failure or RAY / ITER_LIMIT -> dense fallback.
@@ -584,13 +603,13 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
         if (fabs(w - expect) > 1e-7 * mag || w < -1e-7 * mag) fallback = true;
       }
     }
-    if (fallback) {
+    if (fallback) {  // @region fallback
       int piv2 = 0;
       status = lemke_dense<D, NMAX>(W, bt_, be, LP, sval, &zb, &piv2);
       pivots += piv2;
       z0b = false;
     }
-    // ------------------------------------------------------------ recovery
+    // ------------------------------------------------------------ recovery  // @region recover
     // z_j = value of basic z_j (LCP index j);  y_U = z[0..n-2] in original order
     // without e;  y_e = (1 - sum_{k != e} b_k y_k) / b_e
     const int st0 = status;
@@ -606,7 +625,10 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
     int st = st0;
     if (st == ST_OK && ye < -1e-6) st = ST_NEGYE;
     const bool solved = (st == ST_OK);
-    // y used by the aggregates: y^{k+1}, or y^k for a failed pair
+    // y used by the aggregates: y^{k+1}, or y^k for a failed pair;
+    // y^k re-staged in the cbar scratch (free again) with batched loads
+#pragma unroll 4
+    for (int k = 0; k < n; ++k) CBV(k) = YK(k);
     double rd = 0.0;
     double eT = 1.0 + zeta, eR[D], v[D];
 #pragma unroll
@@ -618,14 +640,14 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
         const int u = k - (k > e);
         yv = (k == e) ? ye : (((zb >> u) & 1u) ? VAL(u) : 0.0);
         if (k < nr + no) {
-          const double df = yv - YK(k);
+          const double df = yv - CBV(k);
           rd = __fma_rn(df, df, rd);
         }
         P.y[(long long)k * PP + p] = yv;
       } else {
-        yv = YK(k);
+        yv = CBV(k);
       }
-      // Gauss-Newton aggregates at pose(s^k): u* = K^T y + bvec = (eT, eR); v = C_j^T mu
+      // Gauss-Newton aggregates at pose(s^k): u* = K^T y + bvec = (eT, eR); v = C_j^T mu  // @region aggregates
       if (k < nr) {
 #pragma unroll
         for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, prow[4 * k + a], eR[a]);
@@ -668,11 +690,20 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {
 #undef VAL
 #undef CBV
 #undef YK
-  cta_sum<REC>(rec, nullptr);
-  if (tid == 0) {
-    double* out = P.agg + (long long)blockIdx.x * REC;
+  {  // @region cta_reduce
+    // deterministic warp sum of the record (butterfly, lane 0's order), staged through
+    // this thread's own smem column so the reduction is one compact loop
+    double* red = smem + tid;
 #pragma unroll
-    for (int f = 0; f < REC; ++f) out[f] = rec[f];
+    for (int f = 0; f < REC; ++f) red[f * CTA] = rec[f];
+    double* out = P.agg + (long long)blockIdx.x * REC;
+#pragma unroll 1
+    for (int f = 0; f < REC; ++f) {
+      double v = red[f * CTA];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) out[f] = v;
+    }
   }
 }
 
