@@ -523,6 +523,7 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   }
   h->nmax = (h->M > 0) ? nrmax + nomax + 1 : 1;
   h->dev.nrmax = nrmax;
+  h->dev.nomax = nomax;
   h->nmax_t = nmax_template(h->nmax);
   h->rows_max = nrmax + nomax;
   h->P = (long long)h->B * h->N * h->np * h->M;

@@ -33,6 +33,7 @@ struct LemkeParams {
 struct Dev {
   int d, B, N, ns, nu, np, M, pose_model, npc;
   int nrmax;  // largest robot-part face count
+  int nomax;  // largest obstacle face count
   int pidx[4];
   const int* part_off;
   const double* part_rows;  // [rows][4] = (a_0, a_1, a_2, b)

@@ -34,23 +34,26 @@ enum { ST_OK = 0, ST_RAY = 1, ST_ITER = 2, ST_NEGYE = 3 };
 // Reduced rows (Kt_i, kt_i) of one pair, i = 0..n-1 in LCP order:
 //   i <  nr-1      lambda rows: (0, at_i), kt_i = b_k / b_e  [CTA-shared, per part, D+2 doubles]
 //   i <  n-2       mu rows:     (d_l - c_l.rho, R^T c_l), 0  [per-thread table, D+1 doubles]
-//   i == n-2       gamma row:   (1, 0), 0                    [per-thread table]
-//   i == n-1       phi row:     0                            [per-thread table]
-// row() is branch-free: a pointer/stride select between the two tables.
+//   i == n-2       gamma row:   (1, 0), 0                    [CTA-shared constant row]
+//   i == n-1       phi row:     0                            [CTA-shared constant row]
+// row() is branch-free: a pointer/stride select between the tables.
 template <int D>
 struct PairRows {  // @region row_fetch
   const double* lam;  // [(nr-1)][D+2] = (0, at_1..at_D, kt)  (CTA smem)
-  const double* mu;   // [no+2][D+1], stride `ms` between doubles (thread smem)
+  const double* cst;  // [2][D+2]: gamma row, phi row            (CTA smem)
+  const double* mu;   // [no][D+1], stride `ms` between doubles (thread smem)
   int ms;
   int nr, no, n, l;
   __device__ __forceinline__ void row(int i, double f[D + 1], double& k) const {
     const bool isl = i < nr - 1;
-    const double* base = isl ? lam + i * (D + 2) : mu + (i - (nr - 1)) * (D + 1) * ms;
-    const int st = isl ? 1 : ms;
+    const bool sh = isl || i >= n - 2;
+    const double* sb = isl ? lam + i * (D + 2) : cst + (i - (n - 2)) * (D + 2);
+    const double* base = sh ? sb : mu + (i - (nr - 1)) * (D + 1) * ms;
+    const int st = sh ? 1 : ms;
 #pragma unroll
     for (int c = 0; c <= D; ++c) f[c] = base[c * st];
-    const double kl = lam[(isl ? i : 0) * (D + 2) + D + 1];
-    k = isl ? kl : 0.0;
+    const double ks = sb[D + 1];
+    k = sh ? ks : 0.0;
   }
 };
 

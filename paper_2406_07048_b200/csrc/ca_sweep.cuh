@@ -24,17 +24,41 @@ constexpr int NPMAX = 8;   // robot parts per problem (validated)
 constexpr int NRMAX = 16;  // faces per robot part (validated)
 constexpr int MFAST = 3;   // m x m systems up to this size live in shared memory (99.7 % on C5)
 
+// Tableau-row labels (L5.5 final tie-break): 4-bit fields of one register when
+// they fit (NMAX <= 15: labels <= 14, slot NMAX holds z0's row), else bytes in smem.
+template <int NMAX, bool REG = (NMAX <= 15)>
+struct RowLab {
+  uint64_t v;
+  __device__ __forceinline__ void init(int) { v = 0xFEDCBA9876543210ull; }
+  __device__ __forceinline__ int get(int i) const { return (int)((v >> (4 * i)) & 15u); }
+  __device__ __forceinline__ void set(int i, int x) {
+    v = (v & ~(0xFull << (4 * i))) | ((uint64_t)x << (4 * i));
+  }
+};
+template <int NMAX>
+struct RowLab<NMAX, false> {
+  unsigned char* p;  // [item][thread] bytes
+  __device__ __forceinline__ void init(int n) {
+#pragma unroll 1
+    for (int i = 0; i <= n; ++i) p[i * CTA] = (unsigned char)i;
+  }
+  __device__ __forceinline__ int get(int i) const { return p[i * CTA]; }
+  __device__ __forceinline__ void set(int i, int x) { p[i * CTA] = (unsigned char)x; }
+};
+
+// Per-thread shared-memory column ([item][thread], conflict-free): the obstacle
+// rows (sized by the problem's largest obstacle, `nomax`), basic values, entering-
+// column coefficients, and the row labels when they do not fit a register; then the
+// CTA-shared lambda-row table and the gamma / phi constant rows.
 template <int D, int NMAX>
 struct SweepSmem {
-  static constexpr int NOMAX = NMAX - 4;  // n = nr + no + 1 <= NMAX, nr >= d+1 >= 3
-  static constexpr int MU = (NOMAX + 2) * (D + 1);  // mu rows + gamma + phi rows
   static constexpr int VAL = NMAX, CB = NMAX;
-  static constexpr int ROWB = (NMAX + 1 + 7) / 8;  // tableau-row labels, bytes
-  static constexpr int PER_THREAD = MU + VAL + CB + ROWB;  // doubles
-  static_assert(PER_THREAD >= REC, "the record reduction reuses the per-thread column");
-  // + the CTA-shared lambda-row table of every robot part
-  static size_t bytes(int np, int nrmax) {
-    return sizeof(double) * ((size_t)PER_THREAD * CTA + (size_t)np * (nrmax - 1) * (D + 2));
+  static constexpr int ROWB = (NMAX <= 15) ? 0 : (NMAX + 1 + 7) / 8;  // label bytes, in doubles
+  static_assert(VAL + CB + (D + 1) * (D + 1) >= REC, "the record reduction reuses the per-thread column");
+  static __host__ __device__ int mu(int nomax) { return nomax * (D + 1); }
+  static __host__ __device__ int per_thread(int nomax) { return mu(nomax) + VAL + CB + ROWB; }
+  static size_t bytes(int np, int nrmax, int nomax) {
+    return sizeof(double) * ((size_t)per_thread(nomax) * CTA + (size_t)np * (nrmax - 1) * (D + 2) + 2 * (D + 2));
   }
 };
 
@@ -42,7 +66,7 @@ struct SweepSmem {
 // members `tm`; returns the leaving member (pair index).
 template <int D, int NMAX>
 __device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const double* scb,  // @region lexico
-                                   const unsigned char* rowb, uint32_t wb, uint32_t zb, bool z0b, uint32_t tm,
+                                   const RowLab<NMAX> rowb, uint32_t wb, uint32_t zb, bool z0b, uint32_t tm,
                                    double tau) {
   const int n = W.n;
   for (int jj = 0; jj < n && __popc(tm) > 1; ++jj) {
@@ -97,7 +121,7 @@ __device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const dou
   int best = 99, lm = -1;
   for (uint32_t b = tm; b; b &= b - 1) {
     const int i = __ffs(b) - 1;
-    if ((int)rowb[i * CTA] < best) { best = rowb[i * CTA]; lm = i; }
+    if (rowb.get(i) < best) { best = rowb.get(i); lm = i; }
   }
   return lm;
 }
@@ -242,17 +266,19 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
   const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
   const int b = bt / P.N;
   double* mu = smem + tid;
-  double* sval = mu + SM::MU * CTA;
+  double* sval = mu + SM::mu(P.nomax) * CTA;
   double* scb = sval + SM::VAL * CTA;
-  // tableau-row labels: bytes, [item][thread] from the CTA base of their region
-  unsigned char* rowb =
-      reinterpret_cast<unsigned char*>(smem + (SM::MU + SM::VAL + SM::CB) * CTA) + tid;
-  double* lamtab = smem + SM::PER_THREAD * CTA;  // [np][nrmax-1][D+1]
+  RowLab<NMAX> rowb;
+  if constexpr (NMAX > 15)  // tableau-row labels as bytes, [item][thread] from the region base
+    rowb.p = reinterpret_cast<unsigned char*>(smem + (SM::mu(P.nomax) + SM::VAL + SM::CB) * CTA) + tid;
+  double* lamtab = smem + SM::per_thread(P.nomax) * CTA;  // [np][nrmax-1][D+2]
   const int LT = (P.nrmax - 1) * (D + 2);
+  double* cst = lamtab + P.np * LT;  // gamma row (1, 0, .., 0), phi row 0
   // pose(s_t^k) (k_sortpairs) and the lambda-row table (k_lamtab): plain copies
   if (tid < 9) sR[tid] = P.pose[(long long)bt * 12 + tid];
   else if (tid < 12) srho[tid - 9] = P.pose[(long long)bt * 12 + tid];
   for (int k = tid; k < P.np * LT; k += CTA) lamtab[k] = P.lam[k];
+  if (tid < 2 * (D + 2)) cst[tid] = (tid == 0) ? 1.0 : 0.0;
   if (tid < P.np) {
     part_e[tid] = P.part_e[tid];
     part_be[tid] = P.part_be[tid];
@@ -298,17 +324,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
         m[(1 + mm) * CTA] = r;
       }
     }
-    {  // gamma row (1, 0) and phi row (0) complete the per-thread row table
-      double* m = mu + no * L1 * CTA;
-      m[0] = 1.0;
-      m[L1 * CTA] = 0.0;
-#pragma unroll
-      for (int a = 1; a <= D; ++a) {
-        m[a * CTA] = 0.0;
-        m[(L1 + a) * CTA] = 0.0;
-      }
-    }
-    const PairRows<D> W{lamtab + ip * LT, mu, CTA, nr, no, n, n - 1};
+    const PairRows<D> W{lamtab + ip * LT, cst, mu, CTA, nr, no, n, n - 1};
     if (FUSED) {  // @region fused_mult
       // Eq. 17 for the previous iteration at s^k with y^k (Eqs. 10-11); y^k is
       // staged in the (still unused) cbar scratch with batched loads
@@ -367,8 +383,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
     bool z0b = false;
     double val0 = 0.0;
     int pivots = 0, status = ST_OK;
-#pragma unroll 1
-    for (int i = 0; i <= n; ++i) rowb[i * CTA] = (unsigned char)i;
+    rowb.init(n);
     if (qmin < 0.0) {  // L1: otherwise z = 0
       // L2: z0 enters at row argmin q (ties -> largest index); its column is -1
       const double tl = qmin + tau * fmax(1.0, fabs(qmin));
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
       wb &= ~(1u << r);
       z0b = true;
       val0 = ve;
-      rowb[NMAX * CTA] = (unsigned char)r;
+      rowb.set(NMAX, r);
       pivots = 1;
       Var ent{1, r};
       const int maxpiv = LP.max_pivot_factor * n;
@@ -452,16 +467,17 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
           for (int cc = 0; cc <= D; ++cc) c = __fma_rn(r[cc], ss.uh[cc], c);
           rowc(i, __fma_rn(r[D + 1], ss.sl, c));
         }
-        // mu rows (d_l - c_l.rho, R^T c_l) and the gamma row (1, 0): kt = 0
+        // mu rows (d_l - c_l.rho, R^T c_l): kt = 0
 #pragma unroll 1
-        for (int l = 0; l <= no; ++l) {
+        for (int l = 0; l < no; ++l) {
           const double* m = mu + l * L1 * CTA;
           double c = ss.s0;
 #pragma unroll
           for (int cc = 0; cc <= D; ++cc) c = __fma_rn(m[cc * CTA], ss.uh[cc], c);
           rowc(nr1 + l, c);
         }
-        rowc(n - 1, ss.s0 - ss.sk);  // phi row (0, 0)
+        rowc(n - 2, __fma_rn(1.0, ss.uh[0], ss.s0));  // gamma row (1, 0)
+        rowc(n - 1, ss.s0 - ss.sk);                    // phi row (0, 0)
         pend = 0;
         // basic z rows: cbar is the structural solution itself
         {
@@ -539,7 +555,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
         ve2p = ve2;
         if (z0b && lm >= 0) val0 = __fma_rn(-cb0, ve2, val0);
         VAL(je) = ve2;
-        rowb[je * CTA] = (lm >= 0) ? rowb[lm * CTA] : rowb[NMAX * CTA];
+        rowb.set(je, rowb.get(lm >= 0 ? lm : NMAX));
         if (ent.kind == 0) wb |= 1u << je;
         else zb |= 1u << je;
         ++pivots;
@@ -630,9 +646,9 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
 #pragma unroll 4
     for (int k = 0; k < n; ++k) CBV(k) = YK(k);
     double rd = 0.0;
-    double eT = 1.0 + zeta, eR[D], v[D];
+    double eT = 1.0 + zeta, eR[D], vb[D];  // vb = R^T v = sum_l mu_l R^T c_l (body frame)
 #pragma unroll
-    for (int a = 0; a < D; ++a) { eR[a] = xi[a]; v[a] = 0.0; }
+    for (int a = 0; a < D; ++a) { eR[a] = xi[a]; vb[a] = 0.0; }
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
       double yv;
@@ -656,12 +672,19 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
         eT = __fma_rn(yv, m[0], eT);
 #pragma unroll
         for (int a = 0; a < D; ++a) eR[a] = __fma_rn(yv, m[(1 + a) * CTA], eR[a]);
-        const double* cr = orow + 4 * (k - nr);
 #pragma unroll
-        for (int a = 0; a < D; ++a) v[a] = __fma_rn(yv, cr[a], v[a]);
+        for (int a = 0; a < D; ++a) vb[a] = __fma_rn(yv, m[(1 + a) * CTA], vb[a]);
       } else {
         eT += yv;
       }
+    }
+    double v[D];  // v = C_j^T mu = R vb (world frame)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc = __fma_rn(sR[c * D + a], vb[a], acc);
+      v[c] = acc;
     }
     if (solved) rec[R_RDUAL] = rd;
     else rec[R_FAIL] = 1.0;
@@ -675,14 +698,8 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
       rec[L1 * (L1 + 1) / 2 + a] = -eT * v[a];
     }
     if (P.pose_model != 0) {
-      // g = J^T R^T v with J the rotation generator (SE2 / yaw): (w_1, -w_0, 0)
-      double w0 = 0.0, w1 = 0.0;
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        w0 = __fma_rn(sR[c * D + 0], v[c], w0);
-        w1 = __fma_rn(sR[c * D + 1], v[c], w1);
-      }
-      const double g0 = w1, g1 = -w0;
+      // g = J^T R^T v = J^T vb with J the rotation generator (SE2 / yaw): (vb_1, -vb_0, 0)
+      const double g0 = vb[1], g1 = -vb[0];
       rec[sym_idx(D, D, L1)] = g0 * g0 + g1 * g1;
       rec[L1 * (L1 + 1) / 2 + D] = g0 * eR[0] + g1 * eR[1];
     }
@@ -710,7 +727,7 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
 // host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build)
 template <int D, int NM, bool F>
 cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
-  const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax);
+  const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax, P.nomax);
   static size_t configured = 0;
   if (configured < sm) {
     cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
