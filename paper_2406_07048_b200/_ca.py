@@ -9,7 +9,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "libca.so")
+# CA_LIBRARY: a tuning variant built by profiles/tune.py (default: the in-tree library)
+LIB = os.environ.get("CA_LIBRARY") or os.path.join(HERE, "libca.so")
 
 CA_OK = 0
 CA_W_NOT_CONVERGED = 1

@@ -46,23 +46,26 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
+    """Build libca.so in-tree.  `out` / `defines` (-D flags) build a tuning variant
+    elsewhere (profiles/tune.py); the product library is always the in-tree one."""
+    lib = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if out is None else out + ".objs"
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *FLAGS, "-c", "-o", obj, src]
+        cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-c", "-o", obj, src]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, res
 
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         results = list(ex.map(compile_one, SOURCES))
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build.log") if out is None else out + ".log"
     bad = []
     with open(log, "w") as f:
         for src, obj, cmd, res in results:
@@ -73,17 +76,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for src, err in bad:
             sys.stderr.write(f"--- {src}\n{err[-6000:]}")
         raise RuntimeError(f"nvcc failed (see {log})")
-    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib + ".tmp",
             *[r[1] for r in results], "-cudart", "static",
             "-Xlinker", os.path.join(NCCL_LIB, "libnccl.so.2"), "-Xlinker", "-rpath," + NCCL_LIB]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stderr)
         raise RuntimeError("link failed")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     if verbose:
         print(open(log).read()[-3000:])
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -18,6 +18,13 @@
 #include "ca_kernels.cuh"
 #include "ca_lemke.cuh"
 
+#ifndef CA_EXP_MU_UNROLL
+#define CA_EXP_MU_UNROLL 1
+#endif
+#ifndef CA_SWEEP_MINB
+#define CA_SWEEP_MINB 16  // resident one-warp CTAs per SM the register budget targets
+#endif
+
 namespace ca {
 
 constexpr int NPMAX = 8;   // robot parts per problem (validated)
@@ -254,7 +261,7 @@ __device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil,
 }
 
 template <int D, int NMAX, bool FUSED>
-__global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setup
+__global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @region cta_setup
   using SM = SweepSmem<D, NMAX>;
   constexpr int L1 = D + 1;
   extern __shared__ double smem[];
@@ -468,7 +475,11 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
           rowc(i, __fma_rn(r[D + 1], ss.sl, c));
         }
         // mu rows (d_l - c_l.rho, R^T c_l): kt = 0
+#if CA_EXP_MU_UNROLL == 2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
         for (int l = 0; l < no; ++l) {
           const double* m = mu + l * L1 * CTA;
           double c = ss.s0;
@@ -516,13 +527,18 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
         if (!(bn < kInf)) { status = ST_RAY; break; }
         const double thmin = bn / bd;
         const double tt = thmin + tau * fmax(1.0, thmin);
-        // tie set (L5.2): filter the candidates against the final minimum  // @region tie_filter
-        uint32_t tiem = 0;
+        // tie set (L5.2): filter the candidates against the final minimum.  A lone
+        // candidate is the minimising row itself (eligible: checked above), so the
+        // filter only runs on real near-ties.
+        uint32_t tiem = cand;
+        if (__popc(cand) > 1) {
+          tiem = 0;
 #pragma unroll 1
-        for (uint32_t bb = cand; bb; bb &= bb - 1) {
-          const int i = __ffs(bb) - 1;
-          const double c = CBV(i);
-          if (c > thr && fmax(VAL(i), 0.0) <= tt * c) tiem |= 1u << i;
+          for (uint32_t bb = cand; bb; bb &= bb - 1) {
+            const int i = __ffs(bb) - 1;
+            const double c = CBV(i);
+            if (c > thr && fmax(VAL(i), 0.0) <= tt * c) tiem |= 1u << i;
+          }
         }
         int lm;
         double cr, vr;
@@ -727,10 +743,16 @@ __global__ void __launch_bounds__(CTA, 16) k_sweep(Dev P) {  // @region cta_setu
 // host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build)
 template <int D, int NM, bool F>
 cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
-  const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax, P.nomax);
+#ifndef CA_EXP_SMEM_PAD
+#define CA_EXP_SMEM_PAD 0
+#endif
+  const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax, P.nomax) + CA_EXP_SMEM_PAD;
   static size_t configured = 0;
   if (configured < sm) {
     cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    // all of the unified L1/shared array as shared memory: residency is smem-bound
+    e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = sm;
   }
