@@ -33,9 +33,15 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# keep stdout for the single JSON line: NCCL's banner / warnings go to stderr
-os.environ.setdefault("NCCL_DEBUG", "WARN")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# stdout carries exactly one JSON line: main() moves file descriptor 1 onto stderr
+# (NCCL's version banner, library chatter) and keeps a private handle for emit()
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 import scenes  # noqa: E402  (seeded generators: shared by both arms)
 
@@ -263,7 +269,7 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": "pair-QP/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "pair-QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------------------
@@ -433,10 +439,14 @@ def run_ours(args, rank, world, local):
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
         "lemke_failures": fails, "min_alpha_final": float(np.min(amin)),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
