@@ -162,6 +162,8 @@ ca_status validate(const ca_problem_desc* D) {
     if (D->pose_idx[a] < 0 || D->pose_idx[a] >= D->n_state) return fail(CA_E_DIM, "pose index out of range");
   if (!riccati_supported(D->n_state, D->n_ctrl))
     return fail(CA_E_UNSUPPORTED, "(n_state, n_ctrl) combination not instantiated");
+  if (ca::riccati_smem_doubles(D->horizon, D->n_state, D->n_ctrl, D->dyn_per_time != 0) * 8 > 227 * 1024)
+    return fail(CA_E_UNSUPPORTED, "horizon too long for the shared-memory Riccati step");
   if (D->n_parts > ca::NPMAX) return fail(CA_E_UNSUPPORTED, "more than 8 robot parts");
   if ((long long)D->n_parts * D->n_obs > 65535) return fail(CA_E_UNSUPPORTED, "more than 65535 pairs per (scene, t)");
   int nrmax = 0;
@@ -344,9 +346,14 @@ ca_status launch_sweep(ca_problem* h, bool fused) {
 }
 
 template <int NS, int NU>
-ca_status launch_riccati_t(ca_problem* h, double* cur, double* prev) {
-  const int thr = 64;
-  ca::k_riccati<NS, NU><<<(h->B + thr - 1) / thr, thr, 0, h->stream>>>(h->dev, cur, prev);
+ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double* cur, double* prev) {
+  const size_t sm = sizeof(double) * (size_t)ca::riccati_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
+  static size_t configured = 48 * 1024;
+  if (sm > configured) {
+    CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    configured = sm;
+  }
+  ca::k_riccati<NS, NU><<<(unsigned)h->B, 32, sm, h->stream>>>(h->dev, recs, nchunk, cur, prev);
   CUDA_TRY(cudaGetLastError());
   return CA_OK;
 }
@@ -355,31 +362,28 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
   ca_status st;
-  {
+  const double* recs = h->dev.agg;
+  int nchunk = h->dev.nchunk;
+  if (h->comm) {
+    // a5: one allreduce of the per-(scene, t) aggregates + residual partials
     const long long nq = (long long)h->B * h->N;
     const unsigned gq = (unsigned)((nq + 127) / 128);
-    if (h->comm) {
-      // a5: one allreduce of the per-(scene, t) aggregates + residual partials
-      ca::k_reduce_records<<<gq, 128, 0, h->stream>>>(h->dev, h->rb);
-      CUDA_TRY(cudaGetLastError());
-      NCCL_TRY(ncclAllReduce(h->rb, h->rb, (size_t)nq * ca::REC, ncclDouble, ncclSum, h->comm, h->stream));
-      ca::k_stage<<<gq, 128, 0, h->stream>>>(h->dev, h->rb, 1);
-      h->launches[1] += 2;
-    } else {
-      ca::k_stage<<<gq, 128, 0, h->stream>>>(h->dev, h->dev.agg, h->dev.nchunk);
-      h->launches[1]++;
-    }
+    ca::k_reduce_records<<<gq, 128, 0, h->stream>>>(h->dev, h->rb);
     CUDA_TRY(cudaGetLastError());
+    NCCL_TRY(ncclAllReduce(h->rb, h->rb, (size_t)nq * ca::REC, ncclDouble, ncclSum, h->comm, h->stream));
+    h->launches[1]++;
+    recs = h->rb;
+    nchunk = 1;
   }
   const int ns = h->ns, nu = h->nu;
-  if (ns == 4 && nu == 2) st = launch_riccati_t<4, 2>(h, cur, prev);
-  else if (ns == 7 && nu == 4) st = launch_riccati_t<7, 4>(h, cur, prev);
-  else if (ns == 2 && nu == 1) st = launch_riccati_t<2, 1>(h, cur, prev);
-  else if (ns == 4 && nu == 1) st = launch_riccati_t<4, 1>(h, cur, prev);
-  else if (ns == 6 && nu == 3) st = launch_riccati_t<6, 3>(h, cur, prev);
-  else if (ns == 3 && nu == 2) st = launch_riccati_t<3, 2>(h, cur, prev);
-  else if (ns == 4 && nu == 3) st = launch_riccati_t<4, 3>(h, cur, prev);
-  else st = launch_riccati_t<6, 2>(h, cur, prev);
+  if (ns == 4 && nu == 2) st = launch_riccati_t<4, 2>(h, recs, nchunk, cur, prev);
+  else if (ns == 7 && nu == 4) st = launch_riccati_t<7, 4>(h, recs, nchunk, cur, prev);
+  else if (ns == 2 && nu == 1) st = launch_riccati_t<2, 1>(h, recs, nchunk, cur, prev);
+  else if (ns == 4 && nu == 1) st = launch_riccati_t<4, 1>(h, recs, nchunk, cur, prev);
+  else if (ns == 6 && nu == 3) st = launch_riccati_t<6, 3>(h, recs, nchunk, cur, prev);
+  else if (ns == 3 && nu == 2) st = launch_riccati_t<3, 2>(h, recs, nchunk, cur, prev);
+  else if (ns == 4 && nu == 3) st = launch_riccati_t<4, 3>(h, recs, nchunk, cur, prev);
+  else st = launch_riccati_t<6, 2>(h, recs, nchunk, cur, prev);
   t_end(h, 1, e0);
   return st;
 }
@@ -576,9 +580,6 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.xi, double, (size_t)d * std::max<long long>(h->P, 1));
   AL(v.pst, uint32_t, std::max<long long>(h->P, 1));
   AL(v.agg, double, (size_t)B * N * v.nchunk * ca::REC);
-  AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
-  AL(v.stg, double, (size_t)B * N * (ns * ns + ns));
-  AL(v.stg_stats, double, (size_t)B * N * 4);
   AL(h->scene_res, double, (size_t)B * 4);
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));

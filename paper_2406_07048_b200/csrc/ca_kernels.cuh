@@ -50,9 +50,6 @@ struct Dev {
   uint32_t* pst;
   uint32_t* zmask;
   double* agg;
-  double* ric;
-  double* stg;        // [B*N][ns*ns + ns] stage Hessians / gradients (k_stage -> k_riccati)
-  double* stg_stats;  // [B*N][4]
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
   uint16_t* gperm2;  // [B*N][G]: per-(b,t) execution order, re-sorted by last pivot count
   double* pose;      // [B*N][12]: R(s_t) (d x d, row-major) at [0..8], rho(s_t) at [9..11] (k_sortpairs)
@@ -200,12 +197,12 @@ __global__ void k_reduce_records(Dev P, double* out) {
   for (int f = 0; f < REC; ++f) out[q * REC + f] = acc[f];
 }
 
-// Stage assembly, one thread per (scene, t), t = 1..N (fully parallel): sums the
-// (scene, t) chunk records in fixed order and writes H_t (ns x ns), h_t (ns) and
-// the per-(scene, t) statistics to P.stg.
-__global__ void k_stage(Dev P, const double* recs, int nchunk) {
-  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + (t-1)
-  if (q >= (long long)P.B * P.N) return;
+#endif  // CA_COMMON_KERNELS
+
+// Stage assembly of one (scene, t), t = 1..N: sums the (scene, t) chunk records in
+// fixed order and writes H_t (ns x ns), h_t (ns) and the (scene, t) statistics.
+static __device__ void stage_block(const Dev& P, const double* recs, int nchunk, long long q, double* out,
+                            double* so) {
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
   const int N = P.N, NS = P.ns, npc = P.npc, L1 = P.d + 1;
   const double sig = P.sigma;
@@ -231,7 +228,6 @@ __global__ void k_stage(Dev P, const double* recs, int nchunk) {
     st[2] += rec[R_PIV];
     st[3] += rec[R_FAIL];
   }
-  double* out = P.stg + q * (NS * NS + NS);
   double* ho = out + NS * NS;
   const double* sref = P.sref + ((long long)b * (N + 1) + t) * NS;
   const double* sk = P.s + ((long long)b * (N + 1) + t) * NS;
@@ -256,229 +252,229 @@ __global__ void k_stage(Dev P, const double* recs, int nchunk) {
     }
     ho[P.pidx[a]] += sig * spv;
   }
-  double* so = P.stg_stats + q * 4;
 #pragma unroll
   for (int f = 0; f < 4; ++f) so[f] = st[f];
 }
-#endif
 
+// shared-memory footprint of k_riccati (doubles): stage blocks, stats, dynamics, gains
+__host__ __device__ inline long long riccati_smem_doubles(int N, int NS, int NU, bool dyn_pt) {
+  return (long long)N * (NS * NS + NS) + 4LL * N + (dyn_pt ? N : 1) * (NS * NS + NS * NU + NS) +
+         (long long)N * NU * (NS + 1);
+}
+
+// One CTA (one warp) per scene: the lanes assemble the N stage blocks from the
+// sweep records (fixed order per (scene, t)) and stage this scene's dynamics in
+// shared memory with coalesced loads; lane 0 then runs the O(N) recursion out of
+// shared memory (no global-memory latency on the dependent chain).
 template <int NS, int NU>
-__global__ void k_riccati(Dev P, double* dst_cur, double* dst_prev) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= P.B) return;
+__global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int nchunk, double* dst_cur,
+                                               double* dst_prev) {
+  extern __shared__ double rsm[];
+  const int b = blockIdx.x, lane = threadIdx.x;
   const int N = P.N;
-  double Pm[NS][NS], pv[NS];
-  double st[4] = {0, 0, 0, 0};
-  for (int t = 1; t <= N; ++t) {
-    const double* so = P.stg_stats + ((long long)b * N + (t - 1)) * 4;
-#pragma unroll
-    for (int f = 0; f < 4; ++f) st[f] += so[f];
-  }
-  // stage cost of time t (1..N), assembled by k_stage
-  auto stage = [&](int t, double H[NS][NS], double h[NS]) {
-    const double* in = P.stg + ((long long)b * N + (t - 1)) * (NS * NS + NS);
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      h[a] = in[NS * NS + a];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) H[a][c] = in[a * NS + c];
-    }
-  };
-  auto dynp = [&](const double* base, int t, int blk) {
-    const long long nt = P.dyn_pt ? N : 1;
-    const long long idx = (P.dyn_ps ? (long long)b * nt : 0) + (P.dyn_pt ? t : 0);
-    return base + idx * blk;
-  };
+  constexpr int SB = NS * NS + NS, DB = NS * NS + NS * NU + NS;
+  double* sstg = rsm;                      // [N][SB]: H_t, h_t
+  double* sst = sstg + (long long)N * SB;  // [N][4]
+  double* sdyn = sst + 4LL * N;            // [nd][DB]: A, B, c
+  const int nd = P.dyn_pt ? N : 1;
+  double* ric = sdyn + (long long)nd * DB;  // [N][NU][NS+1]: feedback K_t | k_t
+  // recursion work area (static): value function, products, gains
+  __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Quu[NU][NU], Qux[NU][NS + 1],
+      Pn[NS][NS], xs[NS], us[NU];
+  for (int t = lane; t < N; t += 32)
+    stage_block(P, recs, nchunk, (long long)b * N + t, sstg + (long long)t * SB, sst + 4LL * t);
   {
-    double H[NS][NS], h[NS];
-    stage(N, H, h);
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      pv[a] = h[a];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) Pm[a][c] = H[a][c];
-    }
+    const long long idx0 = P.dyn_ps ? (long long)b * nd : 0;
+    for (int k = lane; k < nd * NS * NS; k += 32) sdyn[(k / (NS * NS)) * DB + k % (NS * NS)] = P.dynA[idx0 * NS * NS + k];
+    for (int k = lane; k < nd * NS * NU; k += 32)
+      sdyn[(k / (NS * NU)) * DB + NS * NS + k % (NS * NU)] = P.dynB[idx0 * NS * NU + k];
+    for (int k = lane; k < nd * NS; k += 32) sdyn[(k / NS) * DB + NS * NS + NS * NU + k % NS] = P.dync[idx0 * NS + k];
   }
-  double* ric = P.ric + (long long)b * N * NU * (NS + 1);
+  __syncwarp();
+  // 2 Qu of this lane's phase-2 entry (kept in a register)
+  const double qu2 = (lane < NU * NU) ? 2.0 * P.Qu[lane] : 0.0;
+  // P_N = H_N, p_N = h_N
+  for (int k = lane; k < SB; k += 32) {
+    const double v = sstg[(long long)(N - 1) * SB + k];
+    if (k < NS * NS) Pm[k / NS][k % NS] = v;
+    else pv[k - NS * NS] = v;
+  }
+  __syncwarp();
+  // Backward Riccati recursion, warp-cooperative: every phase assigns one matrix
+  // entry per lane and keeps the serial summation order of that entry.
   for (int t = N - 1; t >= 0; --t) {
-    const double* A = dynp(P.dynA, t, NS * NS);
-    const double* Bm = dynp(P.dynB, t, NS * NU);
-    const double* cv = dynp(P.dync, t, NS);
-    double H[NS][NS], h[NS];
-    if (t >= 1) {
-      stage(t, H, h);
-    } else {
+    const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
+    const double* Bm = A + NS * NS;
+    const double* cv = Bm + NS * NU;
+    // phase 1: PA = P A, PB = P B, w = P c + p
+    for (int k = lane; k < NS * NS + NS * NU + NS; k += 32) {
+      if (k < NS * NS) {
+        const int a_ = k / NS, c = k % NS;
+        double s_ = 0.0;
 #pragma unroll
-      for (int a = 0; a < NS; ++a) {
-        h[a] = 0.0;
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Pm[a_][q], A[q * NS + c], s_);
+        PA[a_][c] = s_;
+      } else if (k < NS * NS + NS * NU) {
+        const int kk = k - NS * NS, a_ = kk / NU, c = kk % NU;
+        double s_ = 0.0;
 #pragma unroll
-        for (int c = 0; c < NS; ++c) H[a][c] = 0.0;
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Pm[a_][q], Bm[q * NU + c], s_);
+        PB[a_][c] = s_;
+      } else {
+        const int a_ = k - NS * NS - NS * NU;
+        double acc = pv[a_];
+#pragma unroll
+        for (int c = 0; c < NS; ++c) acc = __fma_rn(Pm[a_][c], cv[c], acc);
+        w[a_] = acc;
       }
     }
-    // PA = P A, PB = P B, w = P c + p
-    double PA[NS][NS], PB[NS][NU], w[NS];
+    __syncwarp();
+    // phase 2: Quu = 2Qu + B^T P B, [Qux | qu] = B^T [P A | w]
+    for (int k = lane; k < NU * NU + NU * (NS + 1); k += 32) {
+      if (k < NU * NU) {
+        const int a_ = k / NU, c = k % NU;
+        double s_ = qu2;  // 2 Qu[a][c], k = a NU + c < 32
 #pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      double acc = pv[a];
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], PB[q][c], s_);
+        Quu[a_][c] = s_;
+      } else {
+        const int kk = k - NU * NU, a_ = kk / (NS + 1), c = kk % (NS + 1);
+        double s_ = 0.0;
 #pragma unroll
-      for (int c = 0; c < NS; ++c) acc = __fma_rn(Pm[a][c], cv[c], acc);
-      w[a] = acc;
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(Pm[a][k], A[k * NS + c], s);
-        PA[a][c] = s;
-      }
-#pragma unroll
-      for (int c = 0; c < NU; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(Pm[a][k], Bm[k * NU + c], s);
-        PB[a][c] = s;
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], (c < NS) ? PA[q][c] : w[q], s_);
+        Qux[a_][c] = s_;
       }
     }
-    double Quu[NU][NU], Qux[NU][NS], qu[NU];
+    __syncwarp();
+    // phase 3: Cholesky Quu = L L^T (each lane, redundantly), then lane c solves
+    // column c of -Quu^{-1} [Qux | qu] into the gains
+    double Kc[NU];
+    if (lane <= NS) {
+      double Lc[NU][NU], Li[NU];  // factor and reciprocal diagonal
 #pragma unroll
-    for (int a = 0; a < NU; ++a) {
+      for (int a_ = 0; a_ < NU; ++a_)
 #pragma unroll
-      for (int c = 0; c < NU; ++c) {
-        double s = 2.0 * P.Qu[a * NU + c];
+        for (int c = 0; c < NU; ++c) Lc[a_][c] = 0.0;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PB[k][c], s);
-        Quu[a][c] = s;
+      for (int jj = 0; jj < NU; ++jj) {
+        double s_ = Quu[jj][jj];
+#pragma unroll
+        for (int q = 0; q < jj; ++q) s_ -= Lc[jj][q] * Lc[jj][q];
+        const double ljj = sqrt(s_);
+        Lc[jj][jj] = ljj;
+        Li[jj] = 1.0 / ljj;
+#pragma unroll
+        for (int ii = jj + 1; ii < NU; ++ii) {
+          double a2 = Quu[ii][jj];
+#pragma unroll
+          for (int q = 0; q < jj; ++q) a2 -= Lc[ii][q] * Lc[jj][q];
+          Lc[ii][jj] = a2 * Li[jj];
+        }
       }
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PA[k][c], s);
-        Qux[a][c] = s;
-      }
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
-      qu[a] = s;
-    }
-    // Cholesky Quu = L L^T
-    double Lc[NU][NU];
-#pragma unroll
-    for (int a = 0; a < NU; ++a)
-#pragma unroll
-      for (int c = 0; c < NU; ++c) Lc[a][c] = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < NU; ++jj) {
-      double s = Quu[jj][jj];
-#pragma unroll
-      for (int k = 0; k < jj; ++k) s -= Lc[jj][k] * Lc[jj][k];
-      const double ljj = sqrt(s);
-      Lc[jj][jj] = ljj;
-#pragma unroll
-      for (int ii = jj + 1; ii < NU; ++ii) {
-        double a = Quu[ii][jj];
-#pragma unroll
-        for (int k = 0; k < jj; ++k) a -= Lc[ii][k] * Lc[jj][k];
-        Lc[ii][jj] = a / ljj;
-      }
-    }
-    // K = -Quu^{-1} Qux, k = -Quu^{-1} qu (columns solved with the factor)
-    double Kg[NU][NS + 1];
-#pragma unroll
-    for (int c = 0; c <= NS; ++c) {
       double rhs[NU];
 #pragma unroll
-      for (int a = 0; a < NU; ++a) rhs[a] = (c < NS) ? Qux[a][c] : qu[a];
+      for (int a_ = 0; a_ < NU; ++a_) rhs[a_] = Qux[a_][lane];
 #pragma unroll
-      for (int a = 0; a < NU; ++a) {
-        double s = rhs[a];
+      for (int a_ = 0; a_ < NU; ++a_) {
+        double s_ = rhs[a_];
 #pragma unroll
-        for (int k = 0; k < a; ++k) s -= Lc[a][k] * rhs[k];
-        rhs[a] = s / Lc[a][a];
+        for (int q = 0; q < a_; ++q) s_ -= Lc[a_][q] * rhs[q];
+        rhs[a_] = s_ * Li[a_];
       }
 #pragma unroll
-      for (int a = NU - 1; a >= 0; --a) {
-        double s = rhs[a];
+      for (int a_ = NU - 1; a_ >= 0; --a_) {
+        double s_ = rhs[a_];
 #pragma unroll
-        for (int k = a + 1; k < NU; ++k) s -= Lc[k][a] * rhs[k];
-        rhs[a] = s / Lc[a][a];
+        for (int q = a_ + 1; q < NU; ++q) s_ -= Lc[q][a_] * rhs[q];
+        rhs[a_] = s_ * Li[a_];
       }
 #pragma unroll
-      for (int a = 0; a < NU; ++a) Kg[a][c] = -rhs[a];
-    }
-#pragma unroll
-    for (int a = 0; a < NU; ++a)
-#pragma unroll
-      for (int c = 0; c <= NS; ++c) ric[((long long)t * NU + a) * (NS + 1) + c] = Kg[a][c];
-    // P <- H + A^T P A + Qux^T K ;  p <- h + A^T w + Qux^T k
-    double Pn[NS][NS], pn[NS];
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      double s = h[a];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) s = __fma_rn(A[k * NS + a], w[k], s);
-#pragma unroll
-      for (int k = 0; k < NU; ++k) s = __fma_rn(Qux[k][a], Kg[k][NS], s);
-      pn[a] = s;
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double v = H[a][c];
-#pragma unroll
-        for (int k = 0; k < NS; ++k) v = __fma_rn(A[k * NS + a], PA[k][c], v);
-#pragma unroll
-        for (int k = 0; k < NU; ++k) v = __fma_rn(Qux[k][a], Kg[k][c], v);
-        Pn[a][c] = v;
+      for (int a_ = 0; a_ < NU; ++a_) {
+        Kc[a_] = -rhs[a_];
+        ric[((long long)t * NU + a_) * (NS + 1) + lane] = Kc[a_];
       }
     }
+    __syncwarp();
+    // phase 4: P <- H + A^T P A + Qux^T K ;  p <- h + A^T w + Qux^T k
+    const double* H = sstg + (long long)(t - 1) * SB;  // stage t (zero at t = 0)
+    const double* Kt = ric + (long long)t * NU * (NS + 1);
+    for (int k = lane; k < NS * NS + NS; k += 32) {
+      if (k < NS * NS) {
+        const int a_ = k / NS, c = k % NS;
+        double v = (t >= 1) ? H[a_ * NS + c] : 0.0;
 #pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      pv[a] = pn[a];
+        for (int q = 0; q < NS; ++q) v = __fma_rn(A[q * NS + a_], PA[q][c], v);
 #pragma unroll
-      for (int c = 0; c < NS; ++c) Pm[a][c] = 0.5 * (Pn[a][c] + Pn[c][a]);
+        for (int q = 0; q < NU; ++q) v = __fma_rn(Qux[q][a_], Kt[q * (NS + 1) + c], v);
+        Pn[a_][c] = v;
+      } else {
+        const int a_ = k - NS * NS;
+        double s_ = (t >= 1) ? H[NS * NS + a_] : 0.0;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(A[q * NS + a_], w[q], s_);
+#pragma unroll
+        for (int q = 0; q < NU; ++q) s_ = __fma_rn(Qux[q][a_], Kt[q * (NS + 1) + NS], s_);
+        pv[a_] = s_;
+      }
     }
+    __syncwarp();
+    for (int k = lane; k < NS * NS; k += 32) {
+      const int a_ = k / NS, c = k % NS;
+      Pm[a_][c] = 0.5 * (Pn[a_][c] + Pn[c][a_]);
+    }
+    __syncwarp();
   }
-  // forward rollout from s_0 (Eq. 13b holds exactly)
-  double x[NS];
+  // forward rollout from s_0 (Eq. 13b holds exactly): u_t = K_t x_t + k_t (lanes
+  // < NU), x_{t+1} = A x + B u + c (lanes < NS)
   double* sb = P.s + (long long)b * (N + 1) * NS;
-#pragma unroll
-  for (int a = 0; a < NS; ++a) {
-    x[a] = P.s0[b * NS + a];
-    sb[a] = x[a];
+  if (lane < NS) {
+    xs[lane] = P.s0[b * NS + lane];
+    sb[lane] = xs[lane];
   }
+  __syncwarp();
   for (int t = 0; t < N; ++t) {
-    const double* A = dynp(P.dynA, t, NS * NS);
-    const double* Bm = dynp(P.dynB, t, NS * NU);
-    const double* cv = dynp(P.dync, t, NS);
-    double uu[NU];
+    const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
+    const double* Bm = A + NS * NS;
+    const double* cv = Bm + NS * NU;
+    if (lane < NU) {
+      const double* kr = ric + ((long long)t * NU + lane) * (NS + 1);
+      double s_ = kr[NS];
 #pragma unroll
-    for (int a = 0; a < NU; ++a) {
-      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], x[c], s);
-      uu[a] = s;
-      P.u[((long long)b * N + t) * NU + a] = s;
+      for (int c = 0; c < NS; ++c) s_ = __fma_rn(kr[c], xs[c], s_);
+      us[lane] = s_;
+      P.u[((long long)b * N + t) * NU + lane] = s_;
     }
-    double xn[NS];
+    __syncwarp();
+    double xn = 0.0;
+    if (lane < NS) {
+      double s_ = cv[lane];
 #pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      double s = cv[a];
+      for (int c = 0; c < NS; ++c) s_ = __fma_rn(A[lane * NS + c], xs[c], s_);
 #pragma unroll
-      for (int c = 0; c < NS; ++c) s = __fma_rn(A[a * NS + c], x[c], s);
-#pragma unroll
-      for (int c = 0; c < NU; ++c) s = __fma_rn(Bm[a * NU + c], uu[c], s);
-      xn[a] = s;
+      for (int c = 0; c < NU; ++c) s_ = __fma_rn(Bm[lane * NU + c], us[c], s_);
+      xn = s_;
     }
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      x[a] = xn[a];
-      sb[(t + 1) * NS + a] = xn[a];
+    __syncwarp();
+    if (lane < NS) {
+      xs[lane] = xn;
+      sb[(t + 1) * NS + lane] = xn;
     }
+    __syncwarp();
   }
-  if (dst_cur) {
-    dst_cur[b * 4 + 0] = st[0];
-    dst_cur[b * 4 + 2] = st[2];
-    dst_cur[b * 4 + 3] = st[3];
+  if (lane == 0) {
+    double st[4] = {0, 0, 0, 0};
+    for (int t = 1; t <= N; ++t) {
+      const double* so = sst + 4LL * (t - 1);
+#pragma unroll
+      for (int f = 0; f < 4; ++f) st[f] += so[f];
+    }
+    if (dst_cur) {
+      dst_cur[b * 4 + 0] = st[0];
+      dst_cur[b * 4 + 2] = st[2];
+      dst_cur[b * 4 + 3] = st[3];
+    }
+    if (dst_prev) dst_prev[b * 4 + 1] = st[1];
   }
-  if (dst_prev) dst_prev[b * 4 + 1] = st[1];
 }
 
 // ----------------------------------------------------------------------------
