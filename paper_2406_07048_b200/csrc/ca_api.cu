@@ -345,8 +345,22 @@ ca_status launch_sweep(ca_problem* h, bool fused) {
   return st;
 }
 
+// Scenes per batch above which the thread-per-scene Riccati (throughput) beats the
+// warp-per-scene one (latency): the warp version runs ~1 scene-recursion per resident
+// CTA at a time, the thread version 32 per warp.
+constexpr int RIC_THREAD_MIN_B = 1024;
+
 template <int NS, int NU>
 ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double* cur, double* prev) {
+  if (h->B > RIC_THREAD_MIN_B) {
+    const long long nq = (long long)h->B * h->N;
+    ca::k_stage<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev, recs, nchunk);
+    CUDA_TRY(cudaGetLastError());
+    ca::k_riccati_thread<NS, NU><<<(h->B + 63) / 64, 64, 0, h->stream>>>(h->dev, cur, prev);
+    CUDA_TRY(cudaGetLastError());
+    h->launches[1]++;
+    return CA_OK;
+  }
   const size_t sm = sizeof(double) * (size_t)ca::riccati_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
   static size_t configured = 48 * 1024;
   if (sm > configured) {
@@ -585,6 +599,11 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));
   AL(v.gperm2, uint16_t, (size_t)B * N * std::max(1, v.G));
   AL(v.pose, double, (size_t)B * N * 12);
+  AL(v.work, int, 1);
+  AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
+  AL(v.stg, double, (size_t)B * N * (ns * ns + ns));
+  AL(v.stg_stats, double, (size_t)B * N * 4);
+  v.nitems = (int)std::min<long long>((long long)B * N * v.nchunk, 0x7fffffff);
   AL(v.lam, double, (size_t)h->np * std::max(1, v.nrmax - 1) * (d + 2));
   AL(v.part_e, int, (size_t)h->np);
   AL(v.part_be, double, (size_t)h->np);

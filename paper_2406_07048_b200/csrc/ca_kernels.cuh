@@ -50,12 +50,17 @@ struct Dev {
   uint32_t* pst;
   uint32_t* zmask;
   double* agg;
+  double* ric;        // [B][N][nu][ns+1] gains (thread-per-scene Riccati)
+  double* stg;        // [B*N][ns*ns + ns] stage blocks (k_stage -> k_riccati_thread)
+  double* stg_stats;  // [B*N][4]
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
   uint16_t* gperm2;  // [B*N][G]: per-(b,t) execution order, re-sorted by last pivot count
   double* pose;      // [B*N][12]: R(s_t) (d x d, row-major) at [0..8], rho(s_t) at [9..11] (k_sortpairs)
   double* lam;       // [np][nrmax-1][d+2]: lambda rows (0, at_u, kt_u) of Eqs. 20-21 (k_lamtab)
   int* part_e;       // [np]: eliminated index e = argmax b (reading #3)
   double* part_be;   // [np]: b_e
+  int* work;         // persistent-sweep work counter (reset by k_sortpairs)
+  int nitems;        // B*N*nchunk work items of one sweep
   long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
   double* dbg;       // [64][12]
 };
@@ -254,6 +259,238 @@ static __device__ void stage_block(const Dev& P, const double* recs, int nchunk,
   }
 #pragma unroll
   for (int f = 0; f < 4; ++f) so[f] = st[f];
+}
+
+
+#ifdef CA_COMMON_KERNELS
+// Stage assembly for the thread-per-scene Riccati: one thread per (scene, t).
+__global__ void k_stage(Dev P, const double* recs, int nchunk) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + (t-1)
+  if (q >= (long long)P.B * P.N) return;
+  stage_block(P, recs, nchunk, q, P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * 4);
+}
+#endif  // CA_COMMON_KERNELS
+
+// Large batches: one thread per scene (throughput), stage blocks from k_stage in
+// global memory; the same arithmetic per entry as the warp version below.
+template <int NS, int NU>
+__global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  const int N = P.N;
+  double Pm[NS][NS], pv[NS];
+  double st[4] = {0, 0, 0, 0};
+  for (int t = 1; t <= N; ++t) {
+    const double* so = P.stg_stats + ((long long)b * N + (t - 1)) * 4;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) st[f] += so[f];
+  }
+  // stage cost of time t (1..N), assembled by k_stage
+  auto stage = [&](int t, double H[NS][NS], double h[NS]) {
+    const double* in = P.stg + ((long long)b * N + (t - 1)) * (NS * NS + NS);
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      h[a] = in[NS * NS + a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) H[a][c] = in[a * NS + c];
+    }
+  };
+  auto dynp = [&](const double* base, int t, int blk) {
+    const long long nt = P.dyn_pt ? N : 1;
+    const long long idx = (P.dyn_ps ? (long long)b * nt : 0) + (P.dyn_pt ? t : 0);
+    return base + idx * blk;
+  };
+  {
+    double H[NS][NS], h[NS];
+    stage(N, H, h);
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      pv[a] = h[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) Pm[a][c] = H[a][c];
+    }
+  }
+  double* ric = P.ric + (long long)b * N * NU * (NS + 1);
+  for (int t = N - 1; t >= 0; --t) {
+    const double* A = dynp(P.dynA, t, NS * NS);
+    const double* Bm = dynp(P.dynB, t, NS * NU);
+    const double* cv = dynp(P.dync, t, NS);
+    double H[NS][NS], h[NS];
+    if (t >= 1) {
+      stage(t, H, h);
+    } else {
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        h[a] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NS; ++c) H[a][c] = 0.0;
+      }
+    }
+    // PA = P A, PB = P B, w = P c + p
+    double PA[NS][NS], PB[NS][NU], w[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double acc = pv[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) acc = __fma_rn(Pm[a][c], cv[c], acc);
+      w[a] = acc;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Pm[a][k], A[k * NS + c], s);
+        PA[a][c] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < NU; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Pm[a][k], Bm[k * NU + c], s);
+        PB[a][c] = s;
+      }
+    }
+    double Quu[NU][NU], Qux[NU][NS], qu[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+#pragma unroll
+      for (int c = 0; c < NU; ++c) {
+        double s = 2.0 * P.Qu[a * NU + c];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PB[k][c], s);
+        Quu[a][c] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PA[k][c], s);
+        Qux[a][c] = s;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
+      qu[a] = s;
+    }
+    // Cholesky Quu = L L^T
+    double Lc[NU][NU], Li[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a)
+#pragma unroll
+      for (int c = 0; c < NU; ++c) Lc[a][c] = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < NU; ++jj) {
+      double s = Quu[jj][jj];
+#pragma unroll
+      for (int k = 0; k < jj; ++k) s -= Lc[jj][k] * Lc[jj][k];
+      const double ljj = sqrt(s);
+      Lc[jj][jj] = ljj;
+      Li[jj] = 1.0 / ljj;
+#pragma unroll
+      for (int ii = jj + 1; ii < NU; ++ii) {
+        double a = Quu[ii][jj];
+#pragma unroll
+        for (int k = 0; k < jj; ++k) a -= Lc[ii][k] * Lc[jj][k];
+        Lc[ii][jj] = a * Li[jj];
+      }
+    }
+    // K = -Quu^{-1} Qux, k = -Quu^{-1} qu (columns solved with the factor)
+    double Kg[NU][NS + 1];
+#pragma unroll
+    for (int c = 0; c <= NS; ++c) {
+      double rhs[NU];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) rhs[a] = (c < NS) ? Qux[a][c] : qu[a];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) {
+        double s = rhs[a];
+#pragma unroll
+        for (int k = 0; k < a; ++k) s -= Lc[a][k] * rhs[k];
+        rhs[a] = s * Li[a];
+      }
+#pragma unroll
+      for (int a = NU - 1; a >= 0; --a) {
+        double s = rhs[a];
+#pragma unroll
+        for (int k = a + 1; k < NU; ++k) s -= Lc[k][a] * rhs[k];
+        rhs[a] = s * Li[a];
+      }
+#pragma unroll
+      for (int a = 0; a < NU; ++a) Kg[a][c] = -rhs[a];
+    }
+#pragma unroll
+    for (int a = 0; a < NU; ++a)
+#pragma unroll
+      for (int c = 0; c <= NS; ++c) ric[((long long)t * NU + a) * (NS + 1) + c] = Kg[a][c];
+    // P <- H + A^T P A + Qux^T K ;  p <- h + A^T w + Qux^T k
+    double Pn[NS][NS], pn[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double s = h[a];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s = __fma_rn(A[k * NS + a], w[k], s);
+#pragma unroll
+      for (int k = 0; k < NU; ++k) s = __fma_rn(Qux[k][a], Kg[k][NS], s);
+      pn[a] = s;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double v = H[a][c];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) v = __fma_rn(A[k * NS + a], PA[k][c], v);
+#pragma unroll
+        for (int k = 0; k < NU; ++k) v = __fma_rn(Qux[k][a], Kg[k][c], v);
+        Pn[a][c] = v;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      pv[a] = pn[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) Pm[a][c] = 0.5 * (Pn[a][c] + Pn[c][a]);
+    }
+  }
+  // forward rollout from s_0 (Eq. 13b holds exactly)
+  double x[NS];
+  double* sb = P.s + (long long)b * (N + 1) * NS;
+#pragma unroll
+  for (int a = 0; a < NS; ++a) {
+    x[a] = P.s0[b * NS + a];
+    sb[a] = x[a];
+  }
+  for (int t = 0; t < N; ++t) {
+    const double* A = dynp(P.dynA, t, NS * NS);
+    const double* Bm = dynp(P.dynB, t, NS * NU);
+    const double* cv = dynp(P.dync, t, NS);
+    double uu[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], x[c], s);
+      uu[a] = s;
+      P.u[((long long)b * N + t) * NU + a] = s;
+    }
+    double xn[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double s = cv[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(A[a * NS + c], x[c], s);
+#pragma unroll
+      for (int c = 0; c < NU; ++c) s = __fma_rn(Bm[a * NU + c], uu[c], s);
+      xn[a] = s;
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      x[a] = xn[a];
+      sb[(t + 1) * NS + a] = xn[a];
+    }
+  }
+  if (dst_cur) {
+    dst_cur[b * 4 + 0] = st[0];
+    dst_cur[b * 4 + 2] = st[2];
+    dst_cur[b * 4 + 3] = st[3];
+  }
+  if (dst_prev) dst_prev[b * 4 + 1] = st[1];
 }
 
 // shared-memory footprint of k_riccati (doubles): stage blocks, stats, dynamics, gains
@@ -655,6 +892,7 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   constexpr int NB = 32;
   __shared__ int cnt[NB][33];
   const int bt = blockIdx.x, b = bt / P.N, tid = threadIdx.x;
+  if (bt == 0 && tid == 0 && P.work) *P.work = 0;  // persistent-sweep work counter
   if (tid == 0) {  // pose(s_t^k) of this (b, t) for the sweep
     double* po = P.pose + (long long)bt * 12;
     pose_of(P, P.s + ((long long)b * (P.N + 1) + bt % P.N + 1) * P.ns, po, po + 9);

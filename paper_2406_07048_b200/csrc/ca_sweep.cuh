@@ -21,6 +21,9 @@
 #ifndef CA_EXP_MU_UNROLL
 #define CA_EXP_MU_UNROLL 1
 #endif
+#ifndef CA_SWEEP_PERSIST
+#define CA_SWEEP_PERSIST 1  // persistent warps pulling work items (no per-CTA launch / retire gaps)
+#endif
 #ifndef CA_SWEEP_MINB
 #define CA_SWEEP_MINB 16  // resident one-warp CTAs per SM the register budget targets
 #endif
@@ -269,9 +272,6 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   __shared__ double part_be[NPMAX];
   __shared__ int part_e[NPMAX];
   const int tid = threadIdx.x;
-  const int chunk = blockIdx.x % P.nchunk;
-  const int bt = blockIdx.x / P.nchunk;  // b*N + (t-1)
-  const int b = bt / P.N;
   double* mu = smem + tid;
   double* sval = mu + SM::mu(P.nomax) * CTA;
   double* scb = sval + SM::VAL * CTA;
@@ -281,19 +281,37 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   double* lamtab = smem + SM::per_thread(P.nomax) * CTA;  // [np][nrmax-1][D+2]
   const int LT = (P.nrmax - 1) * (D + 2);
   double* cst = lamtab + P.np * LT;  // gamma row (1, 0, .., 0), phi row 0
-  // pose(s_t^k) (k_sortpairs) and the lambda-row table (k_lamtab): plain copies
-  if (tid < 9) sR[tid] = P.pose[(long long)bt * 12 + tid];
-  else if (tid < 12) srho[tid - 9] = P.pose[(long long)bt * 12 + tid];
+  // the lambda-row table (k_lamtab) and the constant rows: plain copies
   for (int k = tid; k < P.np * LT; k += CTA) lamtab[k] = P.lam[k];
   if (tid < 2 * (D + 2)) cst[tid] = (tid == 0) ? 1.0 : 0.0;
   if (tid < P.np) {
     part_e[tid] = P.part_e[tid];
     part_be[tid] = P.part_be[tid];
   }
-  __syncthreads();
 #define VAL(i) sval[(i) * CTA]
 #define CBV(i) scb[(i) * CTA]
 #define YK(i) P.y[(long long)(i) * PP + p]  // y^k from HBM (L1-resident re-reads)
+#if CA_SWEEP_PERSIST
+  // persistent warps: each CTA (one warp) pulls (b, t, chunk) work items from a
+  // counter (reset by k_sortpairs); results depend only on the item, not on which
+  // warp ran it, so the order of the pulls does not change any output bit
+  for (;;) {
+  int item = 0;
+  if (tid == 0) item = atomicAdd(P.work, 1);
+  item = __shfl_sync(0xffffffffu, item, 0);
+  if (item >= P.nitems) break;
+#else
+  {
+  const int item = blockIdx.x;
+#endif
+  const int chunk = item % P.nchunk;
+  const int bt = item / P.nchunk;  // b*N + (t-1)
+  const int b = bt / P.N;
+  __syncwarp();  // the previous item's readers of sR / srho are done
+  // pose(s_t^k) (k_sortpairs): plain copy
+  if (tid < 9) sR[tid] = P.pose[(long long)bt * 12 + tid];
+  else if (tid < 12) srho[tid - 9] = P.pose[(long long)bt * 12 + tid];
+  __syncthreads();
   double rec[REC];
 #pragma unroll
   for (int f = 0; f < REC; ++f) rec[f] = 0.0;
@@ -729,7 +747,7 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
     double* red = smem + tid;
 #pragma unroll
     for (int f = 0; f < REC; ++f) red[f * CTA] = rec[f];
-    double* out = P.agg + (long long)blockIdx.x * REC;
+    double* out = P.agg + (long long)item * REC;
 #pragma unroll 1
     for (int f = 0; f < REC; ++f) {
       double v = red[f * CTA];
@@ -738,6 +756,7 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
       if (tid == 0) out[f] = v;
     }
   }
+  }  // work item
 }
 
 // host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build)
@@ -756,6 +775,17 @@ cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = sm;
   }
+#if CA_SWEEP_PERSIST
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F>, CTA, sm);
+    resident = nsm * (per > 0 ? per : 1);
+  }
+  grid = (unsigned)resident < grid ? (unsigned)resident : grid;
+#endif
   k_sweep<D, NM, F><<<grid, CTA, sm, stream>>>(P);
   return cudaGetLastError();
 }
