@@ -13,6 +13,12 @@
 
 #include "../../include/ca.h"
 #define CA_COMMON_KERNELS 1
+#ifndef CA_SWEEP_POOL
+#define CA_SWEEP_POOL 800  // pairs per sweep sort pool (whole timesteps of one scene)
+#endif
+#ifndef CA_SWEEP_POOL_MIN_ITEMS
+#define CA_SWEEP_POOL_MIN_ITEMS 10000  // ~4 waves of resident warps on 148 SMs
+#endif
 #include "ca_kernels.cuh"
 #include "ca_sweep.cuh"
 
@@ -314,7 +320,7 @@ int nmax_template(int nmax) {
 
 template <int D, int NM, bool F>
 ca_status launch_sweep_t(ca_problem* h) {
-  const long long grid = (long long)h->B * h->N * h->dev.nchunk;
+  const long long grid = (long long)h->dev.nitems;
   CUDA_TRY((ca::sweep_launch<D, NM, F>(h->dev, (unsigned)grid, h->stream)));
   return CA_OK;
 }
@@ -333,7 +339,7 @@ ca_status launch_sweep_d(ca_problem* h) {
 
 ca_status launch_sweep(ca_problem* h, bool fused) {
   if (h->P == 0) return CA_OK;
-  ca::k_sortpairs<<<(unsigned)((long long)h->B * h->N), 32, 0, h->stream>>>(h->dev);
+  ca::k_sortpairs<<<(unsigned)((long long)h->B * h->dev.NG), 32, 0, h->stream>>>(h->dev);
   CUDA_TRY(cudaGetLastError());
   h->launches[4]++;
   cudaEvent_t e0 = nullptr;
@@ -377,7 +383,7 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
   t_begin(h, &e0);
   ca_status st;
   const double* recs = h->dev.agg;
-  int nchunk = h->dev.nchunk;
+  int nchunk = h->dev.nchunkG;
   if (h->comm) {
     // a5: one allreduce of the per-(scene, t) aggregates + residual partials
     const long long nq = (long long)h->B * h->N;
@@ -387,7 +393,7 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
     NCCL_TRY(ncclAllReduce(h->rb, h->rb, (size_t)nq * ca::REC, ncclDouble, ncclSum, h->comm, h->stream));
     h->launches[1]++;
     recs = h->rb;
-    nchunk = 1;
+    nchunk = 0;  // one reduced record per (scene, t)
   }
   const int ns = h->ns, nu = h->nu;
   if (ns == 4 && nu == 2) st = launch_riccati_t<4, 2>(h, recs, nchunk, cur, prev);
@@ -406,7 +412,7 @@ ca_status launch_mult(ca_problem* h) {
   if (h->P == 0) return CA_OK;
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
-  const long long grid = (long long)h->B * h->N * h->dev.nchunk;
+  const long long grid = (long long)h->dev.nitems;
   if (h->d == 2) ca::k_mult<2><<<(unsigned)grid, ca::CTA, 0, h->stream>>>(h->dev);
   else ca::k_mult<3><<<(unsigned)grid, ca::CTA, 0, h->stream>>>(h->dev);
   CUDA_TRY(cudaGetLastError());
@@ -561,6 +567,18 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   v.G = h->np * h->M;
   v.nchunk = std::max(1, (v.G + ca::CTA - 1) / ca::CTA);
   v.CH = std::max(1, (v.G + v.nchunk - 1) / v.nchunk);
+  // sweep sort pools: TG consecutive timesteps (~CA_SWEEP_POOL pairs) per (scene,
+  // group) when the sweep spans many waves (lane utilisation); one timestep per
+  // pool for small problems, whose sweep is one latency-bound wave
+  {
+    const long long items1 = (long long)h->B * h->N * v.nchunk;
+    const int tg = std::max(1, std::min(h->N, CA_SWEEP_POOL / std::max(1, v.G)));
+    v.TG = (items1 >= CA_SWEEP_POOL_MIN_ITEMS) ? tg : 1;
+  }
+  v.NG = (h->N + v.TG - 1) / v.TG;
+  v.GG = v.TG * std::max(1, v.G);
+  v.nchunkG = (v.GG + 31) / 32;
+  v.CHG = (v.GG + v.nchunkG - 1) / v.nchunkG;  // balanced: lanes used per chunk
   h->eps_pri = D->eps_pri;
   h->eps_dual = D->eps_dual;
   h->max_iters = D->max_iters > 0 ? D->max_iters : 100;
@@ -593,17 +611,17 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.zeta, double, std::max<long long>(h->P, 1));
   AL(v.xi, double, (size_t)d * std::max<long long>(h->P, 1));
   AL(v.pst, uint32_t, std::max<long long>(h->P, 1));
-  AL(v.agg, double, (size_t)B * N * v.nchunk * ca::REC);
+  AL(v.agg, double, (size_t)B * v.NG * v.nchunkG * v.TG * ca::REC);
   AL(h->scene_res, double, (size_t)B * 4);
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));
-  AL(v.gperm2, uint16_t, (size_t)B * N * std::max(1, v.G));
+  AL(v.gperm2, uint16_t, (size_t)B * v.NG * v.GG);
   AL(v.pose, double, (size_t)B * N * 12);
   AL(v.work, int, 1);
   AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
   AL(v.stg, double, (size_t)B * N * (ns * ns + ns));
   AL(v.stg_stats, double, (size_t)B * N * 4);
-  v.nitems = (int)std::min<long long>((long long)B * N * v.nchunk, 0x7fffffff);
+  v.nitems = (int)std::min<long long>((long long)B * v.NG * v.nchunkG, 0x7fffffff);
   AL(v.lam, double, (size_t)h->np * std::max(1, v.nrmax - 1) * (d + 2));
   AL(v.part_e, int, (size_t)h->np);
   AL(v.part_be, double, (size_t)h->np);

@@ -54,13 +54,17 @@ struct Dev {
   double* stg;        // [B*N][ns*ns + ns] stage blocks (k_stage -> k_riccati_thread)
   double* stg_stats;  // [B*N][4]
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
-  uint16_t* gperm2;  // [B*N][G]: per-(b,t) execution order, re-sorted by last pivot count
+  uint16_t* gperm2;  // [B*NG][GG]: per-(scene, timestep group) execution order u = tl*G + g,
+                     //   re-sorted by last pivot count
   double* pose;      // [B*N][12]: R(s_t) (d x d, row-major) at [0..8], rho(s_t) at [9..11] (k_sortpairs)
   double* lam;       // [np][nrmax-1][d+2]: lambda rows (0, at_u, kt_u) of Eqs. 20-21 (k_lamtab)
   int* part_e;       // [np]: eliminated index e = argmax b (reading #3)
   double* part_be;   // [np]: b_e
   int* work;         // persistent-sweep work counter (reset by k_sortpairs)
-  int nitems;        // B*N*nchunk work items of one sweep
+  // sweep work decomposition: the pairs of TG consecutive timesteps of a scene form
+  // one sort pool of up to GG = TG*G pairs, cut into nchunkG warp items of 32
+  int TG, NG, GG, nchunkG, CHG;  // CHG: lanes used per chunk (balanced)
+  int nitems;        // B*NG*nchunkG work items of one sweep
   long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
   double* dbg;       // [64][12]
 };
@@ -83,6 +87,51 @@ __device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* 
 
 __device__ __forceinline__ int sym_idx(int a, int c, int npc) { return a * npc - a * (a - 1) / 2 + (c - a); }
 
+// Record of (scene b, timestep t = 1..N, chunk c) in agg: each sweep work item
+// (b, group, chunk) writes one record per timestep of its group.
+__host__ __device__ __forceinline__ long long rec_index(const Dev& P, int b, int t, int c) {
+  const int grp = (t - 1) / P.TG, tl = (t - 1) % P.TG;
+  return (((long long)b * P.NG + grp) * P.nchunkG + c) * P.TG + tl;
+}
+
+// Work item -> (scene, group, chunk), group size and the pair of slot gs
+struct Item {
+  int b, grp, chunk, nt, size;
+};
+__device__ __forceinline__ Item item_of(const Dev& P, int item) {
+  Item it;
+  it.chunk = item % P.nchunkG;
+  const int bg = item / P.nchunkG;
+  it.b = bg / P.NG;
+  it.grp = bg % P.NG;
+  it.nt = min(P.TG, P.N - it.grp * P.TG);
+  it.size = it.nt * P.G;
+  return it;
+}
+
+// Deterministic grouped record reduction of one warp: lane l holds rec[REC] for its
+// pair's timestep slot tl (-1: no pair), staged in its smem column red[f*32];
+// out[tt*REC + f] = sum over lanes l = 0..31 with tl(l) == tt, in lane order.
+template <int NFIELD>
+__device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int TG, double* out, const double* rec,
+                                             int f0) {
+  __syncwarp();  // every lane is done with its columns (stl below crosses columns)
+  double* red = col0 + lane;
+#pragma unroll
+  for (int f = 0; f < NFIELD; ++f) red[f * 32] = rec[f];
+  int* stl = reinterpret_cast<int*>(col0 + NFIELD * 32);
+  stl[lane] = tl;
+  __syncwarp();
+  for (int o = lane; o < TG * NFIELD; o += 32) {
+    const int tt = o / NFIELD, f = o % NFIELD;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) acc += (stl[l] == tt) ? col0[f * 32 + l] : 0.0;
+    out[tt * REC + f0 + f] = acc;
+  }
+  __syncwarp();
+}
+
 // deterministic warp sum of NF fields (CTA == one warp); lane 0 gets the totals
 template <int NF>
 __device__ __forceinline__ void cta_sum(double* rec, double* /*unused*/) {
@@ -100,21 +149,23 @@ __device__ __forceinline__ void cta_sum(double* rec, double* /*unused*/) {
 // ----------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
-  __shared__ double sR[9], srho[3];
+  __shared__ double sred[2 * CTA];
   const int tid = threadIdx.x;
-  const int chunk = blockIdx.x % P.nchunk;
-  const int bt = blockIdx.x / P.nchunk;
-  const int b = bt / P.N, t = bt % P.N + 1;
-  if (tid == 0) pose_of(P, P.s + ((long long)b * (P.N + 1) + t) * P.ns, sR, srho);
-  __syncthreads();
+  const Item it = item_of(P, blockIdx.x);
   double rec[1] = {0.0};
-  const int gs = chunk * P.CH + tid;  // slot in the n-sorted order of the (b, t) group
-  const int g = (tid < P.CH && gs < P.G) ? P.gperm[(long long)b * P.G + gs] : 0;
-  if (tid < P.CH && gs < P.G) {
-    const long long p = (long long)bt * P.G + g, PP = P.P;
+  const int gs = it.chunk * P.CHG + tid;  // slot in the execution order of the group
+  int tl = -1;
+  if (tid < P.CHG && gs < it.size) {
+    const int u = P.gperm2[((long long)it.b * P.NG + it.grp) * P.GG + gs];
+    tl = u / P.G;
+    const int g = u % P.G, t = it.grp * P.TG + tl + 1;
+    const long long bt = (long long)it.b * P.N + t - 1;
+    const long long p = bt * P.G + g, PP = P.P;
+    double sR[9], srho[3];  // pose(s_t^{k+1}): the trajectory the last primal step produced
+    pose_of(P, P.s + ((long long)it.b * (P.N + 1) + t) * P.ns, sR, srho);
     const int i = g / P.M, j = g % P.M;
     const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
-    const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
+    const int o = it.b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
     const double* prow = P.part_rows + 4 * r0;
     const double* orow = P.obs_rows + 4 * (long long)l0;
     double Tv = 1.0, Rv[D];
@@ -152,8 +203,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
     }
     rec[0] = r2;
   }
-  cta_sum<1>(rec, nullptr);
-  if (tid == 0) P.agg[(long long)blockIdx.x * REC + R_RPRI] = rec[0];
+  group_reduce<1>(sred, tid, tl, P.TG, P.agg + (long long)blockIdx.x * P.TG * REC, rec, R_RPRI);
 }
 
 #ifdef CA_COMMON_KERNELS
@@ -163,8 +213,9 @@ __global__ void k_collect(Dev P, double* dst, int mask) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= P.B) return;
   double acc[4] = {0, 0, 0, 0};
-  const long long base = (long long)b * P.N * P.nchunk;
-  for (long long r = 0; r < (long long)P.N * P.nchunk; ++r) {
+  const long long per = (long long)P.NG * P.nchunkG * P.TG;  // records of one scene (contiguous)
+  const long long base = (long long)b * per;
+  for (long long r = 0; r < per; ++r) {
     const double* rec = P.agg + (base + r) * REC;
     acc[0] += rec[R_RDUAL];
     acc[1] += rec[R_RPRI];
@@ -193,8 +244,9 @@ __global__ void k_reduce_records(Dev P, double* out) {
   double acc[REC];
 #pragma unroll
   for (int f = 0; f < REC; ++f) acc[f] = 0.0;
-  for (int c = 0; c < P.nchunk; ++c) {
-    const double* rec = P.agg + (q * P.nchunk + c) * REC;
+  const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
+  for (int c = 0; c < P.nchunkG; ++c) {
+    const double* rec = P.agg + rec_index(P, b, t, c) * REC;
 #pragma unroll
     for (int f = 0; f < REC; ++f) acc[f] += rec[f];
   }
@@ -209,6 +261,7 @@ __global__ void k_reduce_records(Dev P, double* out) {
 static __device__ void stage_block(const Dev& P, const double* recs, int nchunk, long long q, double* out,
                             double* so) {
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
+  const int nrec = nchunk ? nchunk : 1;
   const int N = P.N, NS = P.ns, npc = P.npc, L1 = P.d + 1;
   const double sig = P.sigma;
   double S[4][4], gv[4], st[4] = {0, 0, 0, 0};
@@ -218,8 +271,9 @@ static __device__ void stage_block(const Dev& P, const double* recs, int nchunk,
 #pragma unroll
     for (int c = 0; c < 4; ++c) S[a][c] = 0.0;
   }
-  for (int c = 0; c < nchunk; ++c) {
-    const double* rec = recs + (q * nchunk + c) * REC;
+  for (int c = 0; c < nrec; ++c) {
+    // nchunk == 0: one reduced record per (scene, t) (obstacle-sharded rb buffer)
+    const double* rec = recs + (nchunk ? rec_index(P, b, t, c) : q) * REC;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       if (a >= L1) continue;
@@ -891,20 +945,29 @@ __global__ void k_lamtab(Dev P) {
 __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   constexpr int NB = 32;
   __shared__ int cnt[NB][33];
-  const int bt = blockIdx.x, b = bt / P.N, tid = threadIdx.x;
-  if (bt == 0 && tid == 0 && P.work) *P.work = 0;  // persistent-sweep work counter
-  if (tid == 0) {  // pose(s_t^k) of this (b, t) for the sweep
-    double* po = P.pose + (long long)bt * 12;
-    pose_of(P, P.s + ((long long)b * (P.N + 1) + bt % P.N + 1) * P.ns, po, po + 9);
+  const int bg = blockIdx.x, b = bg / P.NG, grp = bg % P.NG, tid = threadIdx.x;
+  const int t0 = grp * P.TG + 1, nt = min(P.TG, P.N - grp * P.TG);
+  if (bg == 0 && tid == 0 && P.work) *P.work = 0;  // persistent-sweep work counter
+  for (int tl = tid; tl < nt; tl += 32) {  // pose(s_t^k) of the group's timesteps
+    const long long bt = (long long)b * P.N + t0 - 1 + tl;
+    double* po = P.pose + bt * 12;
+    pose_of(P, P.s + ((long long)b * (P.N + 1) + t0 + tl) * P.ns, po, po + 9);
   }
-  const int G = P.G;
-  const int per = (G + 31) / 32, lo = tid * per, hi = min(G, lo + per);
+  // slots s = tl*G + (position in the n-sorted order gperm), keyed by the pair's
+  // pivot count of the previous sweep; stable counting sort over the group
+  const int G = P.G, S = nt * G;
+  const int per = (S + 31) / 32, lo = tid * per, hi = min(S, lo + per);
   const int* base = P.gperm + (long long)b * G;
-  const uint32_t* pst = P.pst + (long long)bt * G;
+  const uint32_t* pst = P.pst + ((long long)b * P.N + t0 - 1) * G;
+  auto key_of = [&](int s_, int& u) {
+    const int tl = s_ / G, g = base[s_ % G];
+    u = tl * G + g;
+    return min((int)(pst[(long long)tl * G + g] & 0xffffu), NB - 1);
+  };
   for (int k = 0; k < NB; ++k) cnt[k][tid] = 0;
-  for (int s = lo; s < hi; ++s) {
-    const int key = min((int)(pst[base[s]] & 0xffffu), NB - 1);
-    cnt[key][tid]++;
+  for (int s_ = lo; s_ < hi; ++s_) {
+    int u;
+    cnt[key_of(s_, u)][tid]++;
   }
   __syncwarp();
   {  // thread k owns bucket k: exclusive prefix over threads, then over buckets
@@ -925,11 +988,11 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
     for (int t = 0; t < 32; ++t) cnt[k][t] += excl;
   }
   __syncwarp();
-  uint16_t* out = P.gperm2 + (long long)bt * G;
-  for (int s = lo; s < hi; ++s) {
-    const int g = base[s];
-    const int key = min((int)(pst[g] & 0xffffu), NB - 1);
-    out[cnt[key][tid]++] = (uint16_t)g;
+  uint16_t* out = P.gperm2 + (long long)bg * P.GG;
+  for (int s_ = lo; s_ < hi; ++s_) {
+    int u;
+    const int key = key_of(s_, u);
+    out[cnt[key][tid]++] = (uint16_t)u;
   }
 }
 

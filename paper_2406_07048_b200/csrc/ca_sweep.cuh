@@ -64,7 +64,7 @@ template <int D, int NMAX>
 struct SweepSmem {
   static constexpr int VAL = NMAX, CB = NMAX;
   static constexpr int ROWB = (NMAX <= 15) ? 0 : (NMAX + 1 + 7) / 8;  // label bytes, in doubles
-  static_assert(VAL + CB + (D + 1) * (D + 1) >= REC, "the record reduction reuses the per-thread column");
+  static_assert(VAL + CB + (D + 1) * (D + 1) >= REC + 1, "the record reduction reuses the per-thread columns");
   static __host__ __device__ int mu(int nomax) { return nomax * (D + 1); }
   static __host__ __device__ int per_thread(int nomax) { return mu(nomax) + VAL + CB + ROWB; }
   static size_t bytes(int np, int nrmax, int nomax) {
@@ -268,9 +268,6 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   using SM = SweepSmem<D, NMAX>;
   constexpr int L1 = D + 1;
   extern __shared__ double smem[];
-  __shared__ double sR[9], srho[3];
-  __shared__ double part_be[NPMAX];
-  __shared__ int part_e[NPMAX];
   const int tid = threadIdx.x;
   double* mu = smem + tid;
   double* sval = mu + SM::mu(P.nomax) * CTA;
@@ -284,15 +281,12 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   // the lambda-row table (k_lamtab) and the constant rows: plain copies
   for (int k = tid; k < P.np * LT; k += CTA) lamtab[k] = P.lam[k];
   if (tid < 2 * (D + 2)) cst[tid] = (tid == 0) ? 1.0 : 0.0;
-  if (tid < P.np) {
-    part_e[tid] = P.part_e[tid];
-    part_be[tid] = P.part_be[tid];
-  }
+  __syncthreads();
 #define VAL(i) sval[(i) * CTA]
 #define CBV(i) scb[(i) * CTA]
 #define YK(i) P.y[(long long)(i) * PP + p]  // y^k from HBM (L1-resident re-reads)
 #if CA_SWEEP_PERSIST
-  // persistent warps: each CTA (one warp) pulls (b, t, chunk) work items from a
+  // persistent warps: each CTA (one warp) pulls (b, group, chunk) work items from a
   // counter (reset by k_sortpairs); results depend only on the item, not on which
   // warp ran it, so the order of the pulls does not change any output bit
   for (;;) {
@@ -304,21 +298,21 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   {
   const int item = blockIdx.x;
 #endif
-  const int chunk = item % P.nchunk;
-  const int bt = item / P.nchunk;  // b*N + (t-1)
-  const int b = bt / P.N;
-  __syncwarp();  // the previous item's readers of sR / srho are done
-  // pose(s_t^k) (k_sortpairs): plain copy
-  if (tid < 9) sR[tid] = P.pose[(long long)bt * 12 + tid];
-  else if (tid < 12) srho[tid - 9] = P.pose[(long long)bt * 12 + tid];
-  __syncthreads();
+  // item = (scene b, group of TG timesteps, chunk of 32 slots of its sort pool)
+  const Item it = item_of(P, item);
+  const int b = it.b;
   double rec[REC];
 #pragma unroll
   for (int f = 0; f < REC; ++f) rec[f] = 0.0;
-  const int gs = chunk * P.CH + tid;  // slot in the n-sorted order of the (b, t) group
-  const int g = (tid < P.CH && gs < P.G) ? (int)P.gperm2[(long long)bt * P.G + gs] : 0;
-  if (tid < P.CH && gs < P.G) {
-    const long long p = (long long)bt * P.G + g;
+  const int gs = it.chunk * P.CHG + tid;  // slot in the group's execution order
+  int tl = -1;                            // this lane's timestep within the group
+  if (tid < P.CHG && gs < it.size) {
+    const int u = P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs];
+    tl = u / P.G;
+    const int g = u % P.G;
+    const long long bt = (long long)b * P.N + it.grp * P.TG + tl;  // b*N + (t-1)
+    const double* po = P.pose + bt * 12;                          // pose(s_t^k) (k_sortpairs)
+    const long long p = bt * P.G + g;
     const long long PP = P.P;
     const int ip = g / P.M, j = g % P.M;
     const int r0 = P.part_off[ip], nr = P.part_off[ip + 1] - r0;
@@ -326,12 +320,17 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
     const int n = nr + no + 1;
     const double* prow = P.part_rows + 4 * r0;
     const double* orow = P.obs_rows + 4 * (long long)l0;
-    const int e = part_e[ip];
-    const double be = part_be[ip];
+    const int e = P.part_e[ip];
+    const double be = P.part_be[ip];
     double zeta = P.zeta[p], xi[D];  // @region pair_setup
 #pragma unroll
     for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
     // obstacle rows of K at pose(s^k) (Eq. 19b): (d_l - c_l.rho, R^T c_l)
+    double sR[D * D], srho[D];
+#pragma unroll
+    for (int a = 0; a < D * D; ++a) sR[a] = po[a];
+#pragma unroll
+    for (int a = 0; a < D; ++a) srho[a] = po[9 + a];
 #pragma unroll 2
     for (int lo = 0; lo < no; ++lo) {
       const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);
@@ -717,7 +716,7 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
     for (int c = 0; c < D; ++c) {
       double acc = 0.0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) acc = __fma_rn(sR[c * D + a], vb[a], acc);
+      for (int a = 0; a < D; ++a) acc = __fma_rn(po[c * D + a], vb[a], acc);
       v[c] = acc;
     }
     if (solved) rec[R_RDUAL] = rd;
@@ -742,19 +741,9 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
 #undef CBV
 #undef YK
   {  // @region cta_reduce
-    // deterministic warp sum of the record (butterfly, lane 0's order), staged through
-    // this thread's own smem column so the reduction is one compact loop
-    double* red = smem + tid;
-#pragma unroll
-    for (int f = 0; f < REC; ++f) red[f * CTA] = rec[f];
-    double* out = P.agg + (long long)item * REC;
-#pragma unroll 1
-    for (int f = 0; f < REC; ++f) {
-      double v = red[f * CTA];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (tid == 0) out[f] = v;
-    }
+    // deterministic grouped reduction: one record per timestep of the group, lanes
+    // summed in lane order, staged through the (now free) per-thread columns
+    group_reduce<REC>(smem, tid, tl, P.TG, P.agg + (long long)item * P.TG * REC, rec, 0);
   }
   }  // work item
 }
