@@ -25,11 +25,18 @@
 #define CA_SWEEP_PERSIST 1  // persistent warps pulling work items (no per-CTA launch / retire gaps)
 #endif
 #ifndef CA_SWEEP_MINB
-#define CA_SWEEP_MINB 16  // resident one-warp CTAs per SM the register budget targets
+#define CA_SWEEP_MINB 16  // resident warps per SM the register budget targets
+#endif
+#ifndef CA_SWEEP_WPC
+#define CA_SWEEP_WPC 2  // independent warps per CTA (halves the per-CTA shared-memory reserve)
+#endif
+#ifndef CA_SWEEP_GSLOTS
+#define CA_SWEEP_GSLOTS 2  // per warp: lanes whose m > 3 system lives in shared memory
 #endif
 
 namespace ca {
 
+constexpr int WPC = CA_SWEEP_WPC, GSLOTS = CA_SWEEP_GSLOTS;
 constexpr int NPMAX = 8;   // robot parts per problem (validated)
 constexpr int NRMAX = 16;  // faces per robot part (validated)
 constexpr int MFAST = 3;   // m x m systems up to this size live in shared memory (99.7 % on C5)
@@ -66,9 +73,12 @@ struct SweepSmem {
   static constexpr int ROWB = (NMAX <= 15) ? 0 : (NMAX + 1 + 7) / 8;  // label bytes, in doubles
   static_assert(VAL + CB + (D + 1) * (D + 1) >= REC + 1, "the record reduction reuses the per-thread columns");
   static __host__ __device__ int mu(int nomax) { return nomax * (D + 1); }
+  static __host__ __device__ int rowb_off(int nomax) { return mu(nomax) + VAL + CB; }
   static __host__ __device__ int per_thread(int nomax) { return mu(nomax) + VAL + CB + ROWB; }
+  static constexpr int GN = (D + 4) * (D + 5);  // one generic m x m system (m > 3)
   static size_t bytes(int np, int nrmax, int nomax) {
-    return sizeof(double) * ((size_t)per_thread(nomax) * CTA + (size_t)np * (nrmax - 1) * (D + 2) + 2 * (D + 2));
+    return sizeof(double) * ((size_t)WPC * per_thread(nomax) * CTA + (size_t)np * (nrmax - 1) * (D + 2) +
+                             2 * (D + 2) + (size_t)WPC * GSLOTS * GN);
   }
 };
 
@@ -264,29 +274,32 @@ __device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil,
 }
 
 template <int D, int NMAX, bool FUSED>
-__global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @region cta_setup
+__global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P) {  // @region cta_setup
   using SM = SweepSmem<D, NMAX>;
   constexpr int L1 = D + 1;
   extern __shared__ double smem[];
-  const int tid = threadIdx.x;
-  double* mu = smem + tid;
+  const int tid = threadIdx.x & 31, warp = threadIdx.x >> 5;  // lane; warps are independent
+  const int PT = SM::per_thread(P.nomax);
+  double* wcol = smem + (long long)warp * PT * CTA;  // this warp's [item][lane] columns
+  double* mu = wcol + tid;
   double* sval = mu + SM::mu(P.nomax) * CTA;
   double* scb = sval + SM::VAL * CTA;
   RowLab<NMAX> rowb;
-  if constexpr (NMAX > 15)  // tableau-row labels as bytes, [item][thread] from the region base
-    rowb.p = reinterpret_cast<unsigned char*>(smem + (SM::mu(P.nomax) + SM::VAL + SM::CB) * CTA) + tid;
-  double* lamtab = smem + SM::per_thread(P.nomax) * CTA;  // [np][nrmax-1][D+2]
+  if constexpr (NMAX > 15)  // tableau-row labels as bytes, [item][lane] from the region base
+    rowb.p = reinterpret_cast<unsigned char*>(wcol + SM::rowb_off(P.nomax) * CTA) + tid;
+  double* lamtab = smem + (long long)WPC * PT * CTA;  // [np][nrmax-1][D+2]
   const int LT = (P.nrmax - 1) * (D + 2);
   double* cst = lamtab + P.np * LT;  // gamma row (1, 0, .., 0), phi row 0
+  double* gpool = cst + 2 * (D + 2) + (long long)warp * GSLOTS * SM::GN;  // m > 3 systems
   // the lambda-row table (k_lamtab) and the constant rows: plain copies
-  for (int k = tid; k < P.np * LT; k += CTA) lamtab[k] = P.lam[k];
-  if (tid < 2 * (D + 2)) cst[tid] = (tid == 0) ? 1.0 : 0.0;
+  for (int k = threadIdx.x; k < P.np * LT; k += CTA * WPC) lamtab[k] = P.lam[k];
+  if (threadIdx.x < 2 * (D + 2)) cst[threadIdx.x] = (threadIdx.x == 0) ? 1.0 : 0.0;
   __syncthreads();
 #define VAL(i) sval[(i) * CTA]
 #define CBV(i) scb[(i) * CTA]
 #define YK(i) P.y[(long long)(i) * PP + p]  // y^k from HBM (L1-resident re-reads)
 #if CA_SWEEP_PERSIST
-  // persistent warps: each CTA (one warp) pulls (b, group, chunk) work items from a
+  // persistent warps: every warp pulls (b, group, chunk) work items from a
   // counter (reset by k_sortpairs); results depend only on the item, not on which
   // warp ran it, so the order of the pulls does not change any output bit
   for (;;) {
@@ -295,8 +308,7 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   item = __shfl_sync(0xffffffffu, item, 0);
   if (item >= P.nitems) break;
 #else
-  {
-  const int item = blockIdx.x;
+  for (int item = blockIdx.x * WPC + warp, once = 1; once && item < P.nitems; once = 0) {
 #endif
   // item = (scene b, group of TG timesteps, chunk of 32 slots of its sort pool)
   const Item it = item_of(P, item);
@@ -439,8 +451,13 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
         // structural m x m system: registers for m <= 3, generic solver otherwise
         SmallSol<D> ss;  // @region solve_call
         const bool small = solve_small<D>(W, wb, zb, z0b, ent, ss);
+        double* Gp = Gslow;
         if (!small) {
-          const ColSol<D> cg = Lemke<D, NMAX, D + 4>::solve_column(W, Gslow, 1, wb, zb, z0b, ent, Gslow);
+          // the first GSLOTS lanes of the warp needing it use shared memory
+          const unsigned am = __activemask();
+          const int slot = __popc(am & ((1u << tid) - 1u));
+          if (slot < GSLOTS) Gp = gpool + slot * SM::GN;
+          const ColSol<D> cg = Lemke<D, NMAX, D + 4>::solve_column(W, Gp, 1, wb, zb, z0b, ent, Gp);
 #pragma unroll
           for (int c = 0; c <= D; ++c) ss.uh[c] = cg.uh[c];
           ss.sl = cg.sl;
@@ -449,7 +466,7 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
         }
         auto xcol = [&](int s) -> double {
           if (small) return (s == 0) ? ss.x[0] : ((s == 1) ? ss.x[1] : ss.x[2]);
-          return Gslow[s * (D + 5) + D + 4];
+          return Gp[s * (D + 5) + D + 4];
         };
         const uint32_t basic = wb | zb;
         // pass 1 (one sweep over the rows, segment by segment so every row fetch is a  // @region pass1
@@ -743,7 +760,7 @@ __global__ void __launch_bounds__(CTA, CA_SWEEP_MINB) k_sweep(Dev P) {  // @regi
   {  // @region cta_reduce
     // deterministic grouped reduction: one record per timestep of the group, lanes
     // summed in lane order, staged through the (now free) per-thread columns
-    group_reduce<REC>(smem, tid, tl, P.TG, P.agg + (long long)item * P.TG * REC, rec, 0);
+    group_reduce<REC>(wcol, tid, tl, P.TG, P.agg + (long long)item * P.TG * REC, rec, 0);
   }
   }  // work item
 }
@@ -756,7 +773,9 @@ cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
 #endif
   const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax, P.nomax) + CA_EXP_SMEM_PAD;
   static size_t configured = 0;
+  static int resident = 0;
   if (configured < sm) {
+    resident = 0;
     cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // all of the unified L1/shared array as shared memory: residency is smem-bound
@@ -765,17 +784,18 @@ cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
     configured = sm;
   }
 #if CA_SWEEP_PERSIST
-  static int resident = 0;
   if (!resident) {
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F>, CTA, sm);
-    resident = nsm * (per > 0 ? per : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F>, CTA * WPC, sm);
+    resident = nsm * (per > 0 ? per : 1) * WPC;  // in warps
   }
-  grid = (unsigned)resident < grid ? (unsigned)resident : grid;
+  unsigned warps = (unsigned)resident < grid ? (unsigned)resident : grid;
+#else
+  unsigned warps = grid;
 #endif
-  k_sweep<D, NM, F><<<grid, CTA, sm, stream>>>(P);
+  k_sweep<D, NM, F><<<(warps + WPC - 1) / WPC, CTA * WPC, sm, stream>>>(P);
   return cudaGetLastError();
 }
 
