@@ -241,9 +241,19 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
   if ((st = h2d(h, const_cast<int*>(v.part_off), D->part_off, (size_t)h->np + 1))) return st;
   ca::k_lamtab<<<1, 32, 0, h->stream>>>(v);
   CUDA_TRY(cudaGetLastError());
+  if (d == 2) {  // polygon vertices for the separating-axis scale detection
+    ca::k_vertices2d<<<1, 32, 0, h->stream>>>(v.part_rows, v.part_off, h->np, v.part_vert, v.part_nv);
+    CUDA_TRY(cudaGetLastError());
+  }
   if (h->M > 0) {
     if ((st = h2d(h, const_cast<double*>(v.obs_rows), orr.data(), 4 * (size_t)orow))) return st;
     if ((st = h2d(h, const_cast<int*>(v.obs_off), D->obs_off, (size_t)B * h->M + 1))) return st;
+    if (d == 2) {
+      const long long no = (long long)B * h->M;
+      ca::k_vertices2d<<<(unsigned)((no + 127) / 128), 128, 0, h->stream>>>(v.obs_rows, v.obs_off, (int)no, v.obs_vert,
+                                                                           v.obs_nv);
+      CUDA_TRY(cudaGetLastError());
+    }
   }
   const long long nd = (long long)(D->dyn_per_scene ? B : 1) * (D->dyn_per_time ? N : 1);
   if ((st = h2d(h, const_cast<double*>(v.dynA), D->dyn_A, (size_t)nd * ns * ns))) return st;
@@ -618,6 +628,10 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.gperm2, uint16_t, (size_t)B * v.NG * v.GG);
   AL(v.pose, double, (size_t)B * N * 12);
   AL(v.work, int, 1);
+  AL(v.obs_vert, double, 2 * (size_t)std::max<long long>(orow, 1));
+  AL(v.obs_nv, int, (size_t)B * h->M + 1);
+  AL(v.part_vert, double, 2 * (size_t)D->part_off[h->np]);
+  AL(v.part_nv, int, (size_t)h->np);
   AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
   AL(v.stg, double, (size_t)B * N * (ns * ns + ns));
   AL(v.stg_stats, double, (size_t)B * N * 4);
@@ -1017,8 +1031,7 @@ ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, do
   const size_t sm = sizeof(double) * (size_t)ca::CTA * h->rows_max * (h->d + 2);
   const long long grid = (long long)h->B * h->N * h->dev.nchunk;
   if (h->d == 2) {
-    CUDA_TRY(cudaFuncSetAttribute(ca::k_scale<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ca::k_scale<2><<<(unsigned)grid, ca::CTA, sm, h->stream>>>(h->dev, sd, h->alpha);
+    ca::k_scale2<<<(unsigned)((h->P + 127) / 128), 128, 0, h->stream>>>(h->dev, sd, h->alpha);
   } else {
     CUDA_TRY(cudaFuncSetAttribute(ca::k_scale<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     ca::k_scale<3><<<(unsigned)grid, ca::CTA, sm, h->stream>>>(h->dev, sd, h->alpha);

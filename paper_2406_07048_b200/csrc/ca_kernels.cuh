@@ -65,6 +65,10 @@ struct Dev {
   // one sort pool of up to GG = TG*G pairs, cut into nchunkG warp items of 32
   int TG, NG, GG, nchunkG, CHG;  // CHG: lanes used per chunk (balanced)
   int nitems;        // B*NG*nchunkG work items of one sweep
+  double* obs_vert;  // d = 2: vertices of every obstacle polygon, [obs row][2] (k_vertices2d)
+  int* obs_nv;       //        vertex count per obstacle
+  double* part_vert; // d = 2: robot-part vertices (body frame), [part row][2]
+  int* part_nv;
   long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
   double* dbg;       // [64][12]
 };
@@ -811,6 +815,82 @@ __device__ __forceinline__ bool solve_sq(double A[D + 1][D + 2], double x[D + 1]
   }
   return true;
 }
+
+#ifdef CA_COMMON_KERNELS
+// 2-D polygon vertices from the H-representation (once per load): pairwise facet
+// intersections that satisfy every facet (1e-9 relative), de-duplicated.  rows use
+// the [r][4] = (n_0, n_1, -, offset) layout of part_rows / obs_rows.
+__global__ void k_vertices2d(const double* rows, const int* off, int count, double* vert, int* nv) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= count) return;
+  const int r0 = off[o], m = off[o + 1] - r0;
+  const double* R = rows + 4LL * r0;
+  int k = 0;
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) {
+      const double a0 = R[4 * i], a1 = R[4 * i + 1], ad = R[4 * i + 3];
+      const double b0 = R[4 * j], b1 = R[4 * j + 1], bd = R[4 * j + 3];
+      const double det = a0 * b1 - a1 * b0;
+      if (!(fabs(det) > 1e-12 * (fabs(a0) + fabs(a1)) * (fabs(b0) + fabs(b1)))) continue;
+      const double x = (ad * b1 - a1 * bd) / det, y = (a0 * bd - ad * b0) / det;
+      bool ok = true;
+      for (int l = 0; l < m && ok; ++l) {
+        const double t0 = R[4 * l] * x, t1 = R[4 * l + 1] * y;
+        if (t0 + t1 - R[4 * l + 3] > 1e-9 * (1.0 + fabs(t0) + fabs(t1) + fabs(R[4 * l + 3]))) ok = false;
+      }
+      for (int q = 0; q < k && ok; ++q) {
+        const double* v = vert + 2LL * (r0 + q);
+        if (fabs(x - v[0]) + fabs(y - v[1]) <= 1e-9 * (1.0 + fabs(x) + fabs(y))) ok = false;
+      }
+      if (ok && k < m) {
+        vert[2LL * (r0 + k)] = x;
+        vert[2LL * (r0 + k) + 1] = y;
+        ++k;
+      }
+    }
+  nv[o] = k;
+}
+
+// Eq. 3 for convex polygons (d = 2) by the separating-axis characterisation: the
+// scaled robot rho + alpha R P and the obstacle O touch at
+//   alpha* = max(0, max_u (min_{o in O} u.(o - rho)) / h_{RP}(u)),
+// u over the outward robot facet normals R a_k (h = b_k) and the inward obstacle
+// facet normals -c_l (min = c_l.rho - d_l, h = max_v -c_l.(R v)), the edge normals
+// of O (+) (-alpha R P).  Redundant facets only contribute lower bounds.  Same
+// value as the LP (unique), O(n_r n_o) per pair instead of subset enumeration.
+__global__ void __launch_bounds__(128) k_scale2(Dev P, const double* states, double* alpha) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // pair index p
+  if (q >= P.P) return;
+  const int g = (int)(q % P.G);
+  const long long bt = q / P.G;
+  const int b = (int)(bt / P.N), t = (int)(bt % P.N) + 1;
+  double R[9], rho[3];
+  pose_of(P, states + ((long long)b * (P.N + 1) + t) * P.ns, R, rho);
+  const int i = g / P.M, j = g % P.M;
+  const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
+  const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
+  const double* ov = P.obs_vert + 2LL * l0;
+  const double* pv = P.part_vert + 2LL * r0;
+  const int nvo = P.obs_nv[o], nvp = P.part_nv[i];
+  double best = 0.0;
+  for (int k = 0; k < nr; ++k) {  // robot facets: u = R a_k
+    const double* a = P.part_rows + 4 * (r0 + k);
+    const double u0 = R[0] * a[0] + R[1] * a[1], u1 = R[2] * a[0] + R[3] * a[1];
+    double mn = 1e308;
+    for (int v = 0; v < nvo; ++v) mn = fmin(mn, u0 * (ov[2 * v] - rho[0]) + u1 * (ov[2 * v + 1] - rho[1]));
+    best = fmax(best, mn / a[3]);
+  }
+  for (int l = 0; l < no; ++l) {  // obstacle facets: u = -c_l
+    const double* c = P.obs_rows + 4 * ((long long)l0 + l);
+    const double num = (c[0] * rho[0] + c[1] * rho[1]) - c[3];
+    const double w0 = -(R[0] * c[0] + R[2] * c[1]), w1 = -(R[1] * c[0] + R[3] * c[1]);  // -R^T c
+    double h = 0.0;
+    for (int v = 0; v < nvp; ++v) h = fmax(h, w0 * pv[2 * v] + w1 * pv[2 * v + 1]);
+    best = fmax(best, num / h);
+  }
+  alpha[q] = best;
+}
+#endif  // CA_COMMON_KERNELS
 
 template <int D>
 __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, double* alpha) {
