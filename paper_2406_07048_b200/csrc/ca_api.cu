@@ -370,7 +370,12 @@ template <int NS, int NU>
 ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double* cur, double* prev) {
   if (h->B > RIC_THREAD_MIN_B) {
     const long long nq = (long long)h->B * h->N;
-    ca::k_stage<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev, recs, nchunk);
+    if (nchunk) {
+      const long long nbg = (long long)h->B * h->dev.NG;
+      ca::k_stage_grouped<<<(unsigned)((nbg + 3) / 4), 128, 0, h->stream>>>(h->dev);
+    } else {
+      ca::k_stage<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev, recs, nchunk);
+    }
     CUDA_TRY(cudaGetLastError());
     ca::k_riccati_thread<NS, NU><<<(h->B + 63) / 64, 64, 0, h->stream>>>(h->dev, cur, prev);
     CUDA_TRY(cudaGetLastError());
@@ -583,7 +588,7 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   {
     const long long items1 = (long long)h->B * h->N * v.nchunk;
     const int tg = std::max(1, std::min(h->N, CA_SWEEP_POOL / std::max(1, v.G)));
-    v.TG = (items1 >= CA_SWEEP_POOL_MIN_ITEMS) ? tg : 1;
+    v.TG = (items1 >= CA_SWEEP_POOL_MIN_ITEMS) ? std::min(tg, 8) : 1;  // <= 8: k_stage_grouped smem
   }
   v.NG = (h->N + v.TG - 1) / v.TG;
   v.GG = v.TG * std::max(1, v.G);

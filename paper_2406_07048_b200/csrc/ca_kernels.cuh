@@ -262,34 +262,17 @@ __global__ void k_reduce_records(Dev P, double* out) {
 
 // Stage assembly of one (scene, t), t = 1..N: sums the (scene, t) chunk records in
 // fixed order and writes H_t (ns x ns), h_t (ns) and the (scene, t) statistics.
-static __device__ void stage_block(const Dev& P, const double* recs, int nchunk, long long q, double* out,
-                            double* so) {
+// H_t, h_t and the statistics of (scene, t) = q from its summed record
+static __device__ void stage_assemble(const Dev& P, long long q, const double* rec, double* out, double* so) {
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
-  const int nrec = nchunk ? nchunk : 1;
   const int N = P.N, NS = P.ns, npc = P.npc, L1 = P.d + 1;
   const double sig = P.sigma;
-  double S[4][4], gv[4], st[4] = {0, 0, 0, 0};
+  double S[4][4], gv[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    gv[a] = 0.0;
+    gv[a] = (a < L1) ? rec[L1 * (L1 + 1) / 2 + a] : 0.0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) S[a][c] = 0.0;
-  }
-  for (int c = 0; c < nrec; ++c) {
-    // nchunk == 0: one reduced record per (scene, t) (obstacle-sharded rb buffer)
-    const double* rec = recs + (nchunk ? rec_index(P, b, t, c) : q) * REC;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      if (a >= L1) continue;
-#pragma unroll
-      for (int cc = a; cc < 4; ++cc)
-        if (cc < L1) S[a][cc] += rec[sym_idx(a, cc, L1)];
-      gv[a] += rec[L1 * (L1 + 1) / 2 + a];
-    }
-    st[0] += rec[R_RDUAL];
-    st[1] += rec[R_RPRI];
-    st[2] += rec[R_PIV];
-    st[3] += rec[R_FAIL];
+    for (int c = 0; c < 4; ++c) S[a][c] = (a < L1 && c >= a && c < L1) ? rec[sym_idx(a, c, L1)] : 0.0;
   }
   double* ho = out + NS * NS;
   const double* sref = P.sref + ((long long)b * (N + 1) + t) * NS;
@@ -315,8 +298,26 @@ static __device__ void stage_block(const Dev& P, const double* recs, int nchunk,
     }
     ho[P.pidx[a]] += sig * spv;
   }
+  so[0] = rec[R_RDUAL];
+  so[1] = rec[R_RPRI];
+  so[2] = rec[R_PIV];
+  so[3] = rec[R_FAIL];
+}
+
+// Stage assembly of one (scene, t): sum its chunk records in fixed chunk order
+// (nchunk == 0: one reduced record per (scene, t), the obstacle-sharded rb buffer)
+static __device__ void stage_block(const Dev& P, const double* recs, int nchunk, long long q, double* out,
+                                   double* so) {
+  const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
+  double rec[REC];
 #pragma unroll
-  for (int f = 0; f < 4; ++f) so[f] = st[f];
+  for (int f = 0; f < REC; ++f) rec[f] = 0.0;
+  for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
+    const double* r = recs + (nchunk ? rec_index(P, b, t, c) : q) * REC;
+#pragma unroll
+    for (int f = 0; f < REC; ++f) rec[f] += r[f];
+  }
+  stage_assemble(P, q, rec, out, so);
 }
 
 
@@ -326,6 +327,28 @@ __global__ void k_stage(Dev P, const double* recs, int nchunk) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + (t-1)
   if (q >= (long long)P.B * P.N) return;
   stage_block(P, recs, nchunk, q, P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * 4);
+}
+
+// Same from the sweep's grouped records, one warp per (scene, timestep group): the
+// group's records are contiguous, so lane o sums output (timestep o / REC, field
+// o % REC) over the chunks with coalesced loads (same chunk order as stage_block).
+__global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
+  __shared__ double sums[4][8 * REC];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long bg = (long long)blockIdx.x * 4 + w;
+  if (bg >= (long long)P.B * P.NG) return;
+  const int b = (int)(bg / P.NG), grp = (int)(bg % P.NG), nt = min(P.TG, P.N - grp * P.TG);
+  const double* base = P.agg + bg * P.nchunkG * P.TG * REC;
+  for (int o = lane; o < nt * REC; o += 32) {
+    double acc = 0.0;
+    for (int c = 0; c < P.nchunkG; ++c) acc += base[(long long)c * P.TG * REC + o];
+    sums[w][o] = acc;
+  }
+  __syncwarp();
+  if (lane < nt) {
+    const long long q = (long long)b * P.N + grp * P.TG + lane;
+    stage_assemble(P, q, &sums[w][lane * REC], P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * 4);
+  }
 }
 #endif  // CA_COMMON_KERNELS
 
