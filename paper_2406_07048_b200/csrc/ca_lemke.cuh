@@ -29,7 +29,7 @@
 
 namespace ca {
 
-enum { ST_OK = 0, ST_RAY = 1, ST_ITER = 2, ST_NEGYE = 3 };
+enum { ST_OK = 0, ST_RAY = 1, ST_ITER = 2, ST_NEGYE = 3, ST_TIE = 4 /* internal: re-solve densely */ };
 
 // Reduced rows (Kt_i, kt_i) of one pair, i = 0..n-1 in LCP order:
 //   i <  nr-1      lambda rows: (0, at_i), kt_i = b_k / b_e  [CTA-shared, per part, D+2 doubles]

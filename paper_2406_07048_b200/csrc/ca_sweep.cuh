@@ -82,68 +82,17 @@ struct SweepSmem {
   }
 };
 
-// L5.4-5 (rare): lexicographic rule on the w columns (= B^{-1}) among the tied
-// members `tm`; returns the leaving member (pair index).
-template <int D, int NMAX>
-__device__ __noinline__ int lexico(const PairRows<D> W, double* Gslow, const double* scb,  // @region lexico
-                                   const RowLab<NMAX> rowb, uint32_t wb, uint32_t zb, bool z0b, uint32_t tm,
-                                   double tau) {
-  const int n = W.n;
-  for (int jj = 0; jj < n && __popc(tm) > 1; ++jj) {
-    const bool wbasic = (wb >> jj) & 1u;
-    ColSol<D> cs{};
-    if (!wbasic) cs = Lemke<D, NMAX, D + 4>::solve_column(W, Gslow, 1, wb, zb, z0b, Var{0, jj}, Gslow);
-    const double* A = Gslow;
-    const int es = 1, mm = D + 4;
-    double vmin = 1e308;
-    for (uint32_t b = tm; b; b &= b - 1) {
-      const int i = __ffs(b) - 1;
-      double num;
-      if (wbasic) {
-        num = (((wb >> i) & 1u) && i == jj) ? 1.0 : 0.0;
-      } else if ((wb >> i) & 1u) {
-        double f[D + 1], k;
-        W.row(i, f, k);
-        num = cs.s0;
-#pragma unroll
-        for (int c = 0; c <= D; ++c) num = __fma_rn(f[c], cs.uh[c], num);
-        num = __fma_rn(k, cs.sl, num);
-        if (i == n - 1) num -= cs.sk;
-      } else {
-        const int s = __popc(zb & ((1u << i) - 1u));
-        num = A[(s * (mm + 1) + mm) * es];
-      }
-      vmin = fmin(vmin, num / scb[i * CTA]);
-    }
-    const double vt = vmin + tau * fmax(1.0, fabs(vmin));
-    uint32_t keep = 0;
-    for (uint32_t b = tm; b; b &= b - 1) {
-      const int i = __ffs(b) - 1;
-      double num;  // recomputed (rare path)
-      if (wbasic) {
-        num = (((wb >> i) & 1u) && i == jj) ? 1.0 : 0.0;
-      } else if ((wb >> i) & 1u) {
-        double f[D + 1], k;
-        W.row(i, f, k);
-        num = cs.s0;
-#pragma unroll
-        for (int c = 0; c <= D; ++c) num = __fma_rn(f[c], cs.uh[c], num);
-        num = __fma_rn(k, cs.sl, num);
-        if (i == n - 1) num -= cs.sk;
-      } else {
-        const int s = __popc(zb & ((1u << i) - 1u));
-        num = A[(s * (mm + 1) + mm) * es];
-      }
-      if (num / scb[i * CTA] <= vt) keep |= 1u << i;
-    }
-    tm = keep;
+// One pivot of the diagnostic trace (ca_debug_trace); kept out of line so the
+// pivot loop's instruction footprint does not carry it.
+struct TraceRow {
+  double v[14];
+};
+static __device__ __noinline__ void trace_pivot(double* dd, const TraceRow tr, const double* sval, const double* scb, int n) {
+  for (int k = 0; k < 14; ++k) dd[k] = tr.v[k];
+  for (int i = 0; i < n && i < 16; ++i) {
+    dd[14 + i] = scb[i * CTA];
+    dd[30 + i] = sval[i * CTA];
   }
-  int best = 99, lm = -1;
-  for (uint32_t b = tm; b; b &= b - 1) {
-    const int i = __ffs(b) - 1;
-    if (rowb.get(i) < best) { best = rowb.get(i); lm = i; }
-  }
-  return lm;
 }
 
 // Textbook dense-tableau Lemke (rules L1-L7, FMA policy of reading #18) on the
@@ -273,7 +222,7 @@ __device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil,
   return status;
 }
 
-template <int D, int NMAX, bool FUSED>
+template <int D, int NMAX, bool FUSED, bool TRACE>
 __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P) {  // @region cta_setup
   using SM = SweepSmem<D, NMAX>;
   constexpr int L1 = D + 1;
@@ -584,16 +533,19 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
           status = ST_RAY;
           break;
         } else {
-          lm = (__popc(tiem) > 1) ? lexico<D, NMAX>(W, Gslow, scb, rowb, wb, zb, z0b, tiem, tau) : (__ffs(tiem) - 1);
+          // a multi-way tie (L5.4-5, lexicographic rule) is left to the dense-tableau
+          // solve, which applies the oracle's rules verbatim; ties are rare (none in
+          // 3000 sampled C5 pairs) and keeping the rule out of the pivot loop keeps
+          // its register footprint small
+          if (__popc(tiem) > 1) { status = ST_TIE; break; }
+          lm = __ffs(tiem) - 1;
           cr = CBV(lm);
           vr = VAL(lm);
         }
-        if (p == P.dbg_p && pivots < 64) {
-          double* dd = P.dbg + pivots * 48;
-          dd[0] = ent.kind; dd[1] = ent.j; dd[2] = n - __popc(wb); dd[3] = lm; dd[4] = thmin;
-          dd[5] = __popc(tiem); dd[6] = cr; dd[7] = vr; dd[8] = wb; dd[9] = zb; dd[10] = cmax; dd[11] = small ? 0 : 1;
-          dd[12] = val0; dd[13] = cb0;
-          for (int i = 0; i < n && i < 16; ++i) { dd[14 + i] = CBV(i); dd[30 + i] = VAL(i); }
+        if (TRACE && p == P.dbg_p && pivots < 64) {  // diagnostics (ca_debug_trace) build only
+          const TraceRow tr{{(double)ent.kind, (double)ent.j, (double)(n - __popc(wb)), (double)lm, thmin,
+                             (double)__popc(tiem), cr, vr, (double)wb, (double)zb, cmax, small ? 0.0 : 1.0, val0, cb0}};
+          trace_pivot(P.dbg + pivots * 48, tr, sval, scb, n);
         }
         // L3: pivot (values only: the structure is re-derived from the basis); the  // @region pivot_update
         // update of the other basic values is deferred to the next pass 1 (`pend`);
@@ -672,7 +624,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     if (fallback) {  // @region fallback
       int piv2 = 0;
       status = lemke_dense<D, NMAX>(W, bt_, be, LP, sval, &zb, &piv2);
-      pivots += piv2;
+      pivots = piv2;  // the returned solution's own path
       z0b = false;
     }
     // ------------------------------------------------------------ recovery  // @region recover
@@ -765,9 +717,12 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   }  // work item
 }
 
-// host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build)
-template <int D, int NM, bool F>
-cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
+// host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build).
+// The pivot-trace variant (TRACE) is a separate kernel, launched only while a
+// ca_debug_trace request is armed, so the production pivot loop carries no
+// diagnostic code.
+template <int D, int NM, bool F, bool T>
+cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 #ifndef CA_EXP_SMEM_PAD
 #define CA_EXP_SMEM_PAD 0
 #endif
@@ -776,10 +731,10 @@ cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
   static int resident = 0;
   if (configured < sm) {
     resident = 0;
-    cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // all of the unified L1/shared array as shared memory: residency is smem-bound
-    e = cudaFuncSetAttribute(k_sweep<D, NM, F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(k_sweep<D, NM, F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = sm;
   }
@@ -788,15 +743,21 @@ cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F>, CTA * WPC, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F, T>, CTA * WPC, sm);
     resident = nsm * (per > 0 ? per : 1) * WPC;  // in warps
   }
   unsigned warps = (unsigned)resident < grid ? (unsigned)resident : grid;
 #else
   unsigned warps = grid;
 #endif
-  k_sweep<D, NM, F><<<(warps + WPC - 1) / WPC, CTA * WPC, sm, stream>>>(P);
+  k_sweep<D, NM, F, T><<<(warps + WPC - 1) / WPC, CTA * WPC, sm, stream>>>(P);
   return cudaGetLastError();
+}
+
+template <int D, int NM, bool F>
+cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
+  return (P.dbg_p >= 0) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
+                        : sweep_launch_v<D, NM, F, false>(P, grid, stream);
 }
 
 #define CA_SWEEP_NMAX_LIST(X, D, F) X(D, 9, F) X(D, 11, F) X(D, 13, F) X(D, 15, F) X(D, 20, F) X(D, 32, F)
