@@ -27,6 +27,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef CA_EXP_INLINE_GEN
+#define CA_EXP_INLINE_GEN 1  // generic m > 3 solve inlined (no call-site register saves)
+#endif
+
 namespace ca {
 
 enum { ST_OK = 0, ST_RAY = 1, ST_ITER = 2, ST_NEGYE = 3, ST_TIE = 4 /* internal: re-solve densely */ };
@@ -119,7 +123,12 @@ struct Lemke {
   //   coef(w_i) = F_i.uh + kt_i sl - [i=l] sk + s0
   // and writes x_s for the structural columns into xcol (smem, stride es).
   // Columns: basic z_j in increasing j, then z0 if basic.  Rows: R increasing.
-  __device__ __noinline__ static ColSol<D> solve_column(const PairRows<D> W, double* Gs, int gs, uint32_t wb,  // @region solve_column
+#if CA_EXP_INLINE_GEN
+  __device__ __forceinline__ static ColSol<D> solve_column(
+#else
+  __device__ __noinline__ static ColSol<D> solve_column(
+#endif
+      const PairRows<D> W, double* Gs, int gs, uint32_t wb,  // @region solve_column
                                                        uint32_t zb, bool z0b, Var e, double* Gslow) {
     ColSol<D> out;
     double* uh = out.uh;
