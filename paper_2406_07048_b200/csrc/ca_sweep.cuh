@@ -493,20 +493,9 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
           ratio(cb0 > ptol, cb0, val0);
         }
         const double thr = ptol * fmax(1.0, cmax);
-        if (bn < kInf && !(bd > thr)) {
-          // rare: the provisional minimiser is not eligible -> exact pass over cbar > thr
-          bn = kInf;
-          bd = 1.0;
-          tn = kInf;
-          cand = 0;
-#pragma unroll 1
-          for (uint32_t bb = basic; bb; bb &= bb - 1) {
-            const int i = __ffs(bb) - 1;
-            const double c = CBV(i);
-            cand |= ratio(c > thr, c, VAL(i)) ? (1u << i) : 0u;
-          }
-          ratio(z0b && cb0 > thr, cb0, val0);
-        }
+        // rare: the provisional minimiser is not eligible (pivot_tol < cbar <= thr):
+        // the dense-tableau solve takes the exact L5 decision
+        if (bn < kInf && !(bd > thr)) { status = ST_TIE; break; }
         if (!(bn < kInf)) { status = ST_RAY; break; }
         const double thmin = bn / bd;
         const double tt = thmin + tau * fmax(1.0, thmin);
