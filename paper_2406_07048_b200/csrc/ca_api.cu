@@ -630,7 +630,7 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(h->scene_res, double, (size_t)B * 4);
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));
-  AL(v.gperm2, uint16_t, (size_t)B * v.NG * v.GG);
+  AL(v.gperm2, uint32_t, (size_t)B * v.NG * v.GG);
   AL(v.pose, double, (size_t)B * N * 12);
   AL(v.work, int, 1);
   AL(v.obs_vert, double, 2 * (size_t)std::max<long long>(orow, 1));

@@ -54,8 +54,8 @@ struct Dev {
   double* stg;        // [B*N][ns*ns + ns] stage blocks (k_stage -> k_riccati_thread)
   double* stg_stats;  // [B*N][4]
   const int* gperm;  // [B][G]: pairs of a (b, t) group sorted by LCP size n (warp uniformity)
-  uint16_t* gperm2;  // [B*NG][GG]: per-(scene, timestep group) execution order u = tl*G + g,
-                     //   re-sorted by last pivot count
+  uint32_t* gperm2;  // [B*NG][GG]: per-(scene, timestep group) execution order, re-sorted by
+                     //   last pivot count; packed pair = tl << 19 | part << 16 | obstacle (no division)
   double* pose;      // [B*N][12]: R(s_t) (d x d, row-major) at [0..8], rho(s_t) at [9..11] (k_sortpairs)
   double* lam;       // [np][nrmax-1][d+2]: lambda rows (0, at_u, kt_u) of Eqs. 20-21 (k_lamtab)
   int* part_e;       // [np]: eliminated index e = argmax b (reading #3)
@@ -93,6 +93,14 @@ __device__ __forceinline__ int sym_idx(int a, int c, int npc) { return a * npc -
 
 // Record of (scene b, timestep t = 1..N, chunk c) in agg: each sweep work item
 // (b, group, chunk) writes one record per timestep of its group.
+// packed execution-order entry: timestep slot tl (< 8), robot part ip (< 8), obstacle j
+__device__ __forceinline__ uint32_t pack_pair(int tl, int ip, int j) { return (uint32_t)(tl << 19 | ip << 16 | j); }
+__device__ __forceinline__ void unpack_pair(uint32_t u, int& tl, int& ip, int& j) {
+  tl = (int)(u >> 19);
+  ip = (int)((u >> 16) & 7u);
+  j = (int)(u & 0xffffu);
+}
+
 __host__ __device__ __forceinline__ long long rec_index(const Dev& P, int b, int t, int c) {
   const int grp = (t - 1) / P.TG, tl = (t - 1) % P.TG;
   return (((long long)b * P.NG + grp) * P.nchunkG + c) * P.TG + tl;
@@ -160,14 +168,13 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
   const int gs = it.chunk * P.CHG + tid;  // slot in the execution order of the group
   int tl = -1;
   if (tid < P.CHG && gs < it.size) {
-    const int u = P.gperm2[((long long)it.b * P.NG + it.grp) * P.GG + gs];
-    tl = u / P.G;
-    const int g = u % P.G, t = it.grp * P.TG + tl + 1;
+    int i, j;
+    unpack_pair(P.gperm2[((long long)it.b * P.NG + it.grp) * P.GG + gs], tl, i, j);
+    const int g = i * P.M + j, t = it.grp * P.TG + tl + 1;
     const long long bt = (long long)it.b * P.N + t - 1;
     const long long p = bt * P.G + g, PP = P.P;
     double sR[9], srho[3];  // pose(s_t^{k+1}): the trajectory the last primal step produced
     pose_of(P, P.s + ((long long)it.b * (P.N + 1) + t) * P.ns, sR, srho);
-    const int i = g / P.M, j = g % P.M;
     const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
     const int o = it.b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
     const double* prow = P.part_rows + 4 * r0;
@@ -1062,14 +1069,14 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   const int per = (S + 31) / 32, lo = tid * per, hi = min(S, lo + per);
   const int* base = P.gperm + (long long)b * G;
   const uint32_t* pst = P.pst + ((long long)b * P.N + t0 - 1) * G;
-  auto key_of = [&](int s_, int& u) {
+  auto key_of = [&](int s_, uint32_t& u) {
     const int tl = s_ / G, g = base[s_ % G];
-    u = tl * G + g;
+    u = pack_pair(tl, g / P.M, g % P.M);
     return min((int)(pst[(long long)tl * G + g] & 0xffffu), NB - 1);
   };
   for (int k = 0; k < NB; ++k) cnt[k][tid] = 0;
   for (int s_ = lo; s_ < hi; ++s_) {
-    int u;
+    uint32_t u;
     cnt[key_of(s_, u)][tid]++;
   }
   __syncwarp();
@@ -1091,11 +1098,11 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
     for (int t = 0; t < 32; ++t) cnt[k][t] += excl;
   }
   __syncwarp();
-  uint16_t* out = P.gperm2 + (long long)bg * P.GG;
+  uint32_t* out = P.gperm2 + (long long)bg * P.GG;
   for (int s_ = lo; s_ < hi; ++s_) {
-    int u;
+    uint32_t u;
     const int key = key_of(s_, u);
-    out[cnt[key][tid]++] = (uint16_t)u;
+    out[cnt[key][tid]++] = u;
   }
 }
 

@@ -268,14 +268,13 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   const int gs = it.chunk * P.CHG + tid;  // slot in the group's execution order
   int tl = -1;                            // this lane's timestep within the group
   if (tid < P.CHG && gs < it.size) {
-    const int u = P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs];
-    tl = u / P.G;
-    const int g = u % P.G;
+    int ip, j;
+    unpack_pair(P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs], tl, ip, j);
+    const int g = ip * P.M + j;
     const long long bt = (long long)b * P.N + it.grp * P.TG + tl;  // b*N + (t-1)
     const double* po = P.pose + bt * 12;                          // pose(s_t^k) (k_sortpairs)
     const long long p = bt * P.G + g;
     const long long PP = P.P;
-    const int ip = g / P.M, j = g % P.M;
     const int r0 = P.part_off[ip], nr = P.part_off[ip + 1] - r0;
     const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
     const int n = nr + no + 1;
@@ -292,7 +291,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     for (int a = 0; a < D * D; ++a) sR[a] = po[a];
 #pragma unroll
     for (int a = 0; a < D; ++a) srho[a] = po[9 + a];
-#pragma unroll 2
+#pragma unroll 1
     for (int lo = 0; lo < no; ++lo) {
       const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);
       const double c[3] = {cr.x, cr.y, cr.z};
@@ -318,11 +317,13 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       double Tv = 1.0, Rv[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) Rv[a] = 0.0;
+#pragma unroll 1
       for (int k = 0; k < nr; ++k) {
         const double yv = CBV(k);
 #pragma unroll
         for (int a = 0; a < D; ++a) Rv[a] = __fma_rn(yv, prow[4 * k + a], Rv[a]);
       }
+#pragma unroll 1
       for (int k = nr; k < nr + no; ++k) {
         const double yv = CBV(k);
         const double* m = mu + (k - nr) * L1 * CTA;
