@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   double* cst = lamtab + P.np * LT;  // gamma row (1, 0, .., 0), phi row 0
   double* gpool = cst + 2 * (D + 2) + (long long)warp * GSLOTS * SM::GN;  // m > 3 systems
   // the lambda-row table (k_lamtab) and the constant rows: plain copies
+#pragma unroll 1
   for (int k = threadIdx.x; k < P.np * LT; k += CTA * WPC) lamtab[k] = P.lam[k];
   if (threadIdx.x < 2 * (D + 2)) cst[threadIdx.x] = (threadIdx.x == 0) ? 1.0 : 0.0;
   __syncthreads();
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       const int maxpiv = LP.max_pivot_factor * n;
       double Gslow[(D + 4) * (D + 5)];
       const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-      const double kSlack = 1.0 + 1e-12;  // candidate superset margin (filtered exactly below)
+      const double tauS = tau + 1e-12;  // candidate band: tie tolerance + superset margin (filtered exactly)
       const double* lt = lamtab + ip * LT;
       const int nr1 = nr - 1;
       uint32_t pend = 0;  // rows still owing the previous pivot's value update
@@ -430,12 +431,16 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         uint32_t cand = 0;
         auto ratio = [&](bool el, double c, double v) -> bool {  // branch-free
           const double nu = (v > 0.0) ? v : 0.0;
-          const bool lt = el && (nu * bd < bn * c);
-          const double tnn = __fma_rn(tau, (c > nu) ? c : nu, nu) * kSlack;  // (theta + tau max(1,theta)) bd
+          const double nbd = nu * bd;
+          const bool lt = el && (nbd < bn * c);
+          // a new minimum is its own candidate; otherwise compare with the band of the
+          // running minimum: nu/c <= theta + tau' max(1, theta), tau' = tau + 1e-12 (superset)
+          const bool cnd = lt || (el && nbd <= tn * c);
+          const double tnn = __fma_rn(tauS, (c > nu) ? c : nu, nu);  // (theta + tau' max(1,theta)) c
           bn = lt ? nu : bn;
           bd = lt ? c : bd;
           tn = lt ? tnn : tn;
-          return el && (nu * bd <= tn * c);
+          return cnd;
         };
         auto rowc = [&](int i, double c) {
           const uint32_t bit = 1u << i;
