@@ -96,24 +96,28 @@ static __device__ __noinline__ void trace_pivot(double* dd, const TraceRow tr, c
 }
 
 // Textbook dense-tableau Lemke (rules L1-L7, FMA policy of reading #18) on the
-// same reduced rows: the rare fallback when the revised path fails or its result
-// does not verify (near-degenerate, ill-conditioned bases where the revised
-// coefficients are rounding noise).  Tableau [I | -M | -1 | q] in local memory.
-// Writes the basic z values into sval (by LCP index) and returns the status;
-// *zb_out = basic-z mask, *piv_out = pivots.
+// same reduced rows, solved by a whole warp for one pair: lane i owns tableau row
+// i of [I | -M | -1 | q] (local memory), the pivot row is broadcast by shuffles,
+// reductions (min / max / ballots) are exact, so the arithmetic is element for
+// element that of a sequential dense Lemke.  The rare fallback when the revised
+// path fails, meets a multi-way tie (lexicographic rule) or an ineligible
+// provisional minimum, or its result does not verify.  Called by all 32 lanes;
+// writes the basic z values of the pair into svalL (by LCP index, stride CTA).
 template <int D, int NMAX>
-__device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil, double be, LemkeParams LP,  // @region lemke_dense
-                                        double* sval, uint32_t* zb_out, int* piv_out) {
+__device__ __noinline__ int lemke_warp(const PairRows<D> W, const double btil[D + 1], double be,  // @region lemke_dense
+                                       LemkeParams LP, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
+  constexpr unsigned FULL = 0xffffffffu;
   const int n = W.n, l = n - 1;
-  constexpr int WC = 2 * NMAX + 2;
-  double T[NMAX * WC];
-  int basis[NMAX];
   const int Wd = 2 * n + 2, Z0 = 2 * n, RHS = 2 * n + 1;
-  for (int i = 0; i < n; ++i) {
+  const bool own = lane < n;
+  double T[2 * NMAX + 2];
+  int basis = lane;
+  if (own) {
+    const int i = lane;
     double fi[D + 1], ki;
     W.row(i, fi, ki);
-    for (int j = 0; j < Wd; ++j) T[i * WC + j] = 0.0;
-    T[i * WC + i] = 1.0;
+    for (int j = 0; j < Wd; ++j) T[j] = 0.0;
+    T[i] = 1.0;
     for (int j = 0; j < n; ++j) {
       double fj[D + 1], kj;
       W.row(j, fj, kj);
@@ -123,101 +127,84 @@ __device__ __noinline__ int lemke_dense(const PairRows<D> W, const double* btil,
       if (j == l) acc = ki;
       if (i == l) acc = -kj;
       if (i == l && j == l) acc = 0.0;
-      T[i * WC + n + j] = -acc;
+      T[n + j] = -acc;
     }
-    T[i * WC + Z0] = -1.0;
+    T[Z0] = -1.0;
     double q = 1.0 / be;
     if (i < l) {
       q = 0.0;
 #pragma unroll
       for (int c = 0; c <= D; ++c) q = __fma_rn(fi[c], btil[c], q);
     }
-    T[i * WC + RHS] = q;
-    basis[i] = i;
+    T[RHS] = q;
   }
+  auto wmin = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+  };
+  // L3 pivot on (row r, column c): row r / T[r][c]; other rows fma(-T_ic, T_rj, T_ij)
+  auto pivot = [&](int r, int c) {
+    const double inv = 1.0 / __shfl_sync(FULL, own ? T[c] : 0.0, r);
+    if (lane == r)
+      for (int j = 0; j < Wd; ++j)
+        if (j != c) T[j] = T[j] * inv;
+    const double f = own ? T[c] : 0.0;
+    for (int j = 0; j < Wd; ++j) {
+      const double rj = __shfl_sync(FULL, own ? T[j] : 0.0, r);
+      if (own && lane != r && j != c) T[j] = __fma_rn(-f, rj, T[j]);
+    }
+    if (own) T[c] = (lane == r) ? 1.0 : 0.0;
+  };
   const double tau = LP.tie_tol;
   int status = ST_OK, pivots = 0;
-  double qmin = T[RHS];
-  for (int i = 1; i < n; ++i) qmin = fmin(qmin, T[i * WC + RHS]);
-  auto pivot = [&](int r, int c) {
-    const double inv = 1.0 / T[r * WC + c];
-    for (int j = 0; j < Wd; ++j)
-      if (j != c) T[r * WC + j] = T[r * WC + j] * inv;
-    T[r * WC + c] = 1.0;
-    for (int i = 0; i < n; ++i) {
-      if (i == r) continue;
-      const double f = T[i * WC + c];
-      for (int j = 0; j < Wd; ++j)
-        if (j != c) T[i * WC + j] = __fma_rn(-f, T[r * WC + j], T[i * WC + j]);
-      T[i * WC + c] = 0.0;
-    }
-  };
+  const double qmin = wmin(own ? T[RHS] : 1e308);
   if (qmin < 0.0) {
     const double tl = qmin + tau * fmax(1.0, fabs(qmin));
-    int r = -1;
-    for (int i = 0; i < n; ++i)
-      if (T[i * WC + RHS] <= tl) r = i;
-    int leaving = basis[r];
+    const int r = 31 - __clz(__ballot_sync(FULL, own && T[RHS] <= tl));  // ties -> largest index
+    const int leaving = r;                                               // basis[r] = w_r
     pivot(r, Z0);
-    basis[r] = Z0;
+    if (lane == r) basis = Z0;
     ++pivots;
     int entering = leaving + n;
     const int maxpiv = LP.max_pivot_factor * n;
     for (;;) {
       if (pivots >= maxpiv) { status = ST_ITER; break; }
       const int col = entering;
-      double cmax = 0.0;
-      for (int i = 0; i < n; ++i) cmax = fmax(cmax, fabs(T[i * WC + col]));
+      const double cmax = -wmin(own ? -fabs(T[col]) : 0.0);
       const double thr = LP.pivot_tol * fmax(1.0, cmax);
-      double thmin = 1e308;
-      for (int i = 0; i < n; ++i) {
-        const double ci = T[i * WC + col];
-        if (ci > thr) thmin = fmin(thmin, fmax(T[i * WC + RHS], 0.0) / ci);
-      }
+      const double ci = own ? T[col] : 0.0;
+      const bool el = own && ci > thr;
+      const double th = el ? fmax(T[RHS], 0.0) / ci : 1e308;
+      const double thmin = wmin(th);
       if (!(thmin < 1e308)) { status = ST_RAY; break; }
       const double ttol = thmin + tau * fmax(1.0, thmin);
-      uint32_t tie = 0;
-      int r2 = -1;
-      for (int i = 0; i < n; ++i) {
-        const double ci = T[i * WC + col];
-        if (ci > thr && fmax(T[i * WC + RHS], 0.0) / ci <= ttol) {
-          tie |= 1u << i;
-          if (basis[i] == Z0) r2 = i;
-        }
-      }
-      if (r2 < 0) {
-        for (int j = 0; j < n && __popc(tie) > 1; ++j) {
-          double vmin = 1e308;
-          for (uint32_t b = tie; b; b &= b - 1) {
-            const int i = __ffs(b) - 1;
-            vmin = fmin(vmin, T[i * WC + j] / T[i * WC + col]);
-          }
+      uint32_t tie = __ballot_sync(FULL, el && th <= ttol);
+      const uint32_t z0t = __ballot_sync(FULL, ((tie >> lane) & 1u) && basis == Z0);
+      int r2;
+      if (z0t) {
+        r2 = __ffs(z0t) - 1;  // L5.3: z0 leaves whenever it is tied
+      } else {
+        for (int j = 0; j < n && __popc(tie) > 1; ++j) {  // L5.4: lexicographic on B^{-1}
+          const bool in = (tie >> lane) & 1u;
+          const double v = in ? T[j] / T[col] : 1e308;
+          const double vmin = wmin(v);
           const double vt = vmin + tau * fmax(1.0, fabs(vmin));
-          uint32_t keep = 0;
-          for (uint32_t b = tie; b; b &= b - 1) {
-            const int i = __ffs(b) - 1;
-            if (T[i * WC + j] / T[i * WC + col] <= vt) keep |= 1u << i;
-          }
-          tie = keep;
+          tie = __ballot_sync(FULL, in && v <= vt);
         }
-        r2 = __ffs(tie) - 1;
+        r2 = __ffs(tie) - 1;  // L5.5: smallest row
       }
-      const int leaving2 = basis[r2];
+      const int leaving2 = __shfl_sync(FULL, basis, r2);
       pivot(r2, col);
-      basis[r2] = col;
+      if (lane == r2) basis = col;
       ++pivots;
       if (leaving2 == Z0) break;
       entering = (leaving2 < n) ? leaving2 + n : leaving2 - n;
     }
   }
-  uint32_t zb = 0;
-  for (int i = 0; i < n; ++i)
-    if (basis[i] >= n && basis[i] < 2 * n) {
-      const int j = basis[i] - n;
-      zb |= 1u << j;
-      sval[j * CTA] = T[i * WC + RHS];
-    }
-  *zb_out = zb;
+  const bool zbas = own && basis >= n && basis < 2 * n;
+  if (zbas) svalL[(basis - n) * CTA] = T[RHS];
+  *zb_out = __reduce_or_sync(FULL, zbas ? (1u << (basis - n)) : 0u);
   *piv_out = pivots;
   return status;
 }
@@ -268,22 +255,34 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   for (int f = 0; f < REC; ++f) rec[f] = 0.0;
   const int gs = it.chunk * P.CHG + tid;  // slot in the group's execution order
   int tl = -1;                            // this lane's timestep within the group
-  if (tid < P.CHG && gs < it.size) {
-    int ip, j;
+  // pair state shared by the two halves of the pair's work (around the warp's
+  // dense re-solves)
+  const long long PP = P.P;
+  long long p = 0;
+  int ip = 0, nr = 0, no = 0, n = 0, e = 0, pivots = 0, status = ST_OK;
+  double be = 1.0, zeta = 0.0, xi[D], bt_[D + 1];
+  const double* po = P.pose;
+  const double* prow = P.part_rows;
+  uint32_t zb = 0;
+  bool z0b = false, fallback = false;
+  const bool act = tid < P.CHG && gs < it.size;
+  if (act) {
+    int j;
     unpack_pair(P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs], tl, ip, j);
     const int g = ip * P.M + j;
     const long long bt = (long long)b * P.N + it.grp * P.TG + tl;  // b*N + (t-1)
-    const double* po = P.pose + bt * 12;                          // pose(s_t^k) (k_sortpairs)
-    const long long p = bt * P.G + g;
-    const long long PP = P.P;
-    const int r0 = P.part_off[ip], nr = P.part_off[ip + 1] - r0;
-    const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
-    const int n = nr + no + 1;
-    const double* prow = P.part_rows + 4 * r0;
+    po = P.pose + bt * 12;                                        // pose(s_t^k) (k_sortpairs)
+    p = bt * P.G + g;
+    const int r0 = P.part_off[ip];
+    nr = P.part_off[ip + 1] - r0;
+    const int o = b * P.M + j, l0 = P.obs_off[o];
+    no = P.obs_off[o + 1] - l0;
+    n = nr + no + 1;
+    prow = P.part_rows + 4 * r0;
     const double* orow = P.obs_rows + 4 * (long long)l0;
-    const int e = P.part_e[ip];
-    const double be = P.part_be[ip];
-    double zeta = P.zeta[p], xi[D];  // @region pair_setup
+    e = P.part_e[ip];
+    be = P.part_be[ip];
+    zeta = P.zeta[p];  // @region pair_setup
 #pragma unroll
     for (int a = 0; a < D; ++a) xi[a] = P.xi[(long long)a * PP + p];
     // obstacle rows of K at pose(s^k) (Eq. 19b): (d_l - c_l.rho, R^T c_l)
@@ -346,7 +345,6 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       for (int a = 0; a < D; ++a) P.xi[(long long)a * PP + p] = xi[a];
     }
     // q = [Kt btil; etatil]  with btil = bvec + K_e / b_e, etatil = 1 / b_e (Eq. 25)  // @region q_build
-    double bt_[D + 1];
     bt_[0] = (1.0 + zeta) + 0.0 / be;
 #pragma unroll
     for (int a = 0; a < D; ++a) bt_[1 + a] = xi[a] + prow[4 * e + a] / be;
@@ -366,10 +364,12 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     const LemkeParams& LP = P.lp;
     const double tau = LP.tie_tol, ptol = LP.pivot_tol;
     const uint32_t nmask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
-    uint32_t wb = nmask, zb = 0;
-    bool z0b = false;
+    uint32_t wb = nmask;
+    zb = 0;
+    z0b = false;
     double val0 = 0.0;
-    int pivots = 0, status = ST_OK;
+    pivots = 0;
+    status = ST_OK;
     rowb.init(n);
     if (qmin < 0.0) {  // L1: otherwise z = 0
       // L2: z0 enters at row argmin q (ties -> largest index); its column is -1
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     // The revised path never forms the tableau, so check its answer against the
     // LCP itself: w = M z + q (O(n d) with the low-rank M), w_i = value of basic
     // w_i or 0, w >= 0, z >= 0.  Failure or RAY / ITER_LIMIT -> dense fallback.
-    bool fallback = (status != ST_OK);
+    fallback = (status != ST_OK);
     if (!fallback && qmin < 0.0) {
       double uz[D + 1], zl = 0.0, skz = 0.0, zsc = 0.0;
 #pragma unroll
@@ -616,12 +616,29 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         if (fabs(w - expect) > 1e-7 * mag || w < -1e-7 * mag) fallback = true;
       }
     }
-    if (fallback) {  // @region fallback
-      int piv2 = 0;
-      status = lemke_dense<D, NMAX>(W, bt_, be, LP, sval, &zb, &piv2);
-      pivots = piv2;  // the returned solution's own path
+  }
+  // dense-tableau re-solves (rules L1-L7 verbatim, lexicographic ties included), one
+  // pair at a time by the whole warp: lane i owns tableau row i
+  for (uint32_t need = __ballot_sync(0xffffffffu, act && fallback); need; need &= need - 1) {  // @region fallback
+    const int L = __ffs(need) - 1;
+    const int nrL = __shfl_sync(0xffffffffu, nr, L), noL = __shfl_sync(0xffffffffu, no, L);
+    const int ipL = __shfl_sync(0xffffffffu, ip, L);
+    double btL[D + 1];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) btL[c] = __shfl_sync(0xffffffffu, bt_[c], L);
+    const double beL = __shfl_sync(0xffffffffu, be, L);
+    const PairRows<D> WL{lamtab + ipL * LT, cst, wcol + L, CTA, nrL, noL, nrL + noL + 1, nrL + noL};
+    uint32_t zbL;
+    int pivL;
+    const int stL = lemke_warp<D, NMAX>(WL, btL, beL, P.lp, sval - tid + L, tid, &zbL, &pivL);
+    if (tid == L) {
+      status = stL;
+      zb = zbL;
+      pivots = pivL;  // the returned solution's own path
       z0b = false;
     }
+  }
+  if (act) {
     // ------------------------------------------------------------ recovery  // @region recover
     // z_j = value of basic z_j (LCP index j);  y_U = z[0..n-2] in original order
     // without e;  y_e = (1 - sum_{k != e} b_k y_k) / b_e
