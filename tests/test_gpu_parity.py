@@ -270,3 +270,47 @@ def test_obstacle_sharded_world1_nccl(ca, cfg):
     _, ma = a.scale_detect(want_alpha=False)
     _, mb = b.scale_detect(want_alpha=False)
     np.testing.assert_allclose(mb, ma, rtol=1e-12)
+
+
+def symmetric_scene():
+    """Degenerate geometry: an obstacle with a duplicated face (two identical LCP rows:
+    exact ratio-test ties -> the lexicographic rule, solved by the warp-cooperative
+    dense re-solve), obstacles centred on the reference line, one touching the car
+    at t = 0, a diamond whose vertex points at the car."""
+    def dup(poly):  # every face twice: exact ties between the copies' LCP rows
+        return np.repeat(poly[0], 2, axis=0), np.repeat(poly[1], 2)
+
+    polys = [
+        dup(scenes.box_hrep([6.0, 0.0], [1.0, 1.0])),
+        dup(scenes.box_hrep([10.0, 0.0], [0.5, 2.0])),
+        scenes.polygon_hrep([14.0, 0.0], 1.5, np.array([0.0, 0.5, 1.0, 1.5]) * np.pi),
+        scenes.box_hrep([3.25, 0.0], [1.0, 1.0]),  # face at x = 2.25: touches the car body at t = 0
+    ]
+    return scenes._car_common("SYM", 0, 0, N=20, iters=20, speed=4.0, polys_per_scene=[polys])
+
+
+@pytest.mark.parametrize("k0", [0, 2, 6])
+def test_t1_symmetric_degenerate(ca, k0):
+    sc = symmetric_scene()
+    o = warm(sc, k0)
+    g = ca.Problem(sc)
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    s, zeta, xi = o.s.copy(), o.zeta.copy(), o.xi.copy()
+    rc, r = g.dual_sweep()
+    o.dual_sweep()
+    st = g.pair_state()
+    compare_dual_sweep(sc, s, zeta, xi, st["y"], o.y, st["pivots"], o.pivots, st["status"], o.status)
+    # the duplicated faces produce lexicographic ties, re-solved by the dense path
+    assert np.count_nonzero(st["status"] & 0x100) > 0
+
+
+def test_t2_symmetric_degenerate(ca):
+    sc = symmetric_scene()
+    g = ca.Problem(sc)
+    o = oracle.Oracle(sc)
+    K = 20
+    rc, h = g.admm_iterate(K)
+    o.admm_iterate(K)
+    s, u = g.trajectory()
+    close(s, o.s, 1e-6, "s")
+    close(u, o.u, 1e-6, "u")
