@@ -89,7 +89,7 @@ class _Problem(C.Structure):
         ("dyn_A", C.c_void_p), ("dyn_B", C.c_void_p), ("dyn_c", C.c_void_p),
         ("Qs", C.c_void_p), ("Qu", C.c_void_p), ("s0", C.c_void_p), ("s_ref", C.c_void_p),
         ("sigma", C.c_double), ("pivot_tol", C.c_double), ("tie_tol", C.c_double),
-        ("max_pivot_factor", C.c_int), ("ny", C.c_int), ("prox_eps", C.c_double),
+        ("max_pivot_factor", C.c_int), ("ny", C.c_int), ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
     ]
 
 
@@ -133,6 +133,8 @@ class Oracle:
         P.sigma = sc.sigma if sigma is None else sigma
         P.pivot_tol, P.tie_tol, P.max_pivot_factor = pivot_tol, tie_tol, max_pivot_factor
         P.prox_eps = prox_eps
+        step = getattr(sc, "obs_step", None)  # NEXT f3: moving obstacles (None = static)
+        P.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
         self.ny = P.ny = sc.n_max if sc.n_obs > 0 else 1
         self.P = P
         B, N, ns, nu, d = sc.n_scenes, sc.horizon, sc.n_state, sc.n_ctrl, sc.dim

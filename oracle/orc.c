@@ -57,6 +57,16 @@ void orc_pose(int model, const int* idx, int d, const double* s, double* R, doub
   }
 }
 
+/* Pair (t, obstacle j) with a moving obstacle (NEXT f3): by translation invariance the
+ * robot posed at rho meets O_j + t*step_j exactly as the robot posed at
+ * rho - t*step_j meets O_j, so every pair computation takes this shifted origin. */
+static void obstacle_frame(const orc_problem* P, int b, int j, int t, const double* rho, double* rho_j) {
+  for (int a = 0; a < P->dim; ++a) rho_j[a] = rho[a];
+  if (!P->obs_step) return;
+  const double* st = P->obs_step + ((long long)b * P->n_obs + j) * P->dim;
+  for (int a = 0; a < P->dim; ++a) rho_j[a] = rho[a] - (double)t * st[a];
+}
+
 /* ---------------------------------------------------------------------------
  * Eq. 3: alpha* = min alpha s.t. A x <= b alpha, C x <= d, with the
  * robot posed: x = R^T (y - rho) in world coordinates y, so the robot
@@ -464,8 +474,10 @@ long long orc_dual_sweep(const orc_problem* P, orc_iterate* I, double* rdual) {
     int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
     double ynew[MAXN];
     int piv;
+    double rj[3];
+    obstacle_frame(P, b, j, t, rho, rj);
     int st = orc_pair_solve(d, nr, P->part_A + (long long)r0 * d, P->part_b + r0, no,
-                            P->obs_C + (long long)l0 * d, P->obs_d + l0, R, rho, I->zeta[p],
+                            P->obs_C + (long long)l0 * d, P->obs_d + l0, R, rj, I->zeta[p],
                             I->xi + p * d, P->prox_eps, I->y + p * P->ny, P->pivot_tol,
                             P->tie_tol, P->max_pivot_factor, ynew, &piv, NULL);
     if (I->pivots) I->pivots[p] = piv;
@@ -536,9 +548,10 @@ static void scene_aggregates(const orc_problem* P, const orc_iterate* I, int b, 
         long long p = (((long long)b * N + (t - 1)) * P->n_parts + i) * P->n_obs + j;
         int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
         int n = nr + no + 1;
-        double K[MAXN * (MAXD + 1)];
+        double K[MAXN * (MAXD + 1)], rj[3];
+        obstacle_frame(P, b, j, t, rho, rj);
         orc_build_K(d, nr, P->part_A + (long long)r0 * d, no, P->obs_C + (long long)l0 * d,
-                    P->obs_d + l0, R, rho, K);
+                    P->obs_d + l0, R, rj, K);
         const double* y = I->y + p * P->ny;
         double us[MAXD + 1];
         us[0] = 1.0 + I->zeta[p];
@@ -698,10 +711,11 @@ void orc_multiplier_update(const orc_problem* P, orc_iterate* I, double* rpri) {
     const double* lam = y;
     const double* mu = y + nr;
     double gam = y[nr + no];
-    double T = 1.0;
+    double T = 1.0, rj[3];
+    obstacle_frame(P, b, j, t, rho, rj);
     for (int l = 0; l < no; ++l) {
       double cr = 0.0;
-      for (int a = 0; a < d; ++a) cr += P->obs_C[(long long)(l0 + l) * d + a] * rho[a];
+      for (int a = 0; a < d; ++a) cr += P->obs_C[(long long)(l0 + l) * d + a] * rj[a];
       T += (P->obs_d[l0 + l] - cr) * mu[l];
     }
     T += gam;
@@ -762,7 +776,9 @@ long long orc_scale_detect(const orc_problem* P, const double* s, double* alpha)
     orc_pose(P->pose_model, P->pose_idx, d, s + ((long long)b * (N + 1) + t) * ns, R, rho);
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
     int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
-    if (orc_scale_lp(d, nr, P->part_A + (long long)r0 * d, P->part_b + r0, R, rho, no,
+    double rj[3];
+    obstacle_frame(P, b, j, t, rho, rj);
+    if (orc_scale_lp(d, nr, P->part_A + (long long)r0 * d, P->part_b + r0, R, rj, no,
                      P->obs_C + (long long)l0 * d, P->obs_d + l0, alpha + p, NULL) != 0) {
       alpha[p] = NAN;
       ++bad;

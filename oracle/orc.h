@@ -43,6 +43,10 @@ typedef struct {
   int max_pivot_factor;
   int ny;
   double prox_eps; /* 0 = paper-exact Eq. 19 (reading #2) */
+  /* NULL = static obstacles (reading #15).  Else [n_scenes*n_obs][dim]:
+   * per-timestep displacement of each obstacle (NEXT f3, moving traffic): obstacle j
+   * at timestep t is O_j + t*step_j, i.e. C_j x <= d_j + t C_j step_j. */
+  const double* obs_step;
 } orc_problem;
 
 typedef struct {

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
-from typing import Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 
@@ -40,6 +40,7 @@ CONFIG_NAMES = {
     3: "C3: 3D quadrotor (3 boxes) through a gap in 8 polyhedra, N=40, K=100",
     4: "C4: dense traffic, ego car vs 100 vehicles, N=60, K=300",
     5: "C5: 4096 scenes x 200 obstacles x N=50, K=100",
+    6: "C4m: C4 with moving traffic (vehicles at 12-18 m/s, NEXT f3), N=60, K=300",
 }
 
 
@@ -90,6 +91,9 @@ class Scene:
     dt: float = DT
     seed: int = 0
     config: int = 0
+    # NEXT f3 (moving obstacles): None = static (reading #15), else [B*M, d] displacement
+    # of each obstacle per timestep (obstacle j at timestep t is O_j + t*obs_step[j])
+    obs_step: Optional[np.ndarray] = None
 
     @property
     def n_parts(self) -> int:
@@ -144,6 +148,8 @@ class Scene:
             dyn_c=np.ascontiguousarray(dc),
             s0=np.ascontiguousarray(self.s0[ids]),
             s_ref=np.ascontiguousarray(self.s_ref[ids]),
+            obs_step=None if self.obs_step is None else np.ascontiguousarray(
+                np.concatenate([self.obs_step[b * M:(b + 1) * M] for b in ids])),
         )
 
 
@@ -333,11 +339,14 @@ def make_c3(seed: int = 3) -> Scene:
     )
 
 
-def make_c4(seed: int = 4) -> Scene:
+def make_c4(seed: int = 4, moving: bool = False) -> Scene:
+    """C4 dense traffic; moving=True (NEXT f3, config 6): the vehicles drive along +x at
+    U(12, 18) m/s (the ego at 20 m/s overtakes them), the polygonal barriers stay."""
     rng = np.random.default_rng(seed)
     lanes = [-3.5, 0.0, 3.5]
     placed = {0: [], 1: [], 2: []}
     polys = []
+    moves = []
     while len(polys) < 100:
         lane = int(rng.integers(0, 3))
         x = rng.uniform(0.0, 600.0)
@@ -350,11 +359,18 @@ def make_c4(seed: int = 4) -> Scene:
         if rng.uniform() < 0.1:
             nv = int(rng.integers(5, 7))
             polys.append(polygon_hrep([x, y], rng.uniform(0.8, 1.2), random_polygon_angles(rng, nv)))
+            moves.append(False)
         else:
             L, W = rng.uniform(4.0, 5.0), rng.uniform(1.7, 2.0)
             yaw = math.radians(rng.uniform(-3.0, 3.0))
             polys.append(box_hrep([x, y], [L / 2, W / 2], yaw))
-    return _car_common("C4", 4, seed, N=60, iters=300, speed=20.0, polys_per_scene=[polys])
+            moves.append(True)
+    if not moving:
+        return _car_common("C4", 4, seed, N=60, iters=300, speed=20.0, polys_per_scene=[polys])
+    # speeds drawn after the static recipe so the geometry equals C4's
+    v = rng.uniform(12.0, 18.0, len(polys)) * np.asarray(moves, float)
+    sc = _car_common("C4m", 6, seed, N=60, iters=300, speed=20.0, polys_per_scene=[polys])
+    return dataclasses.replace(sc, obs_step=np.stack([v * DT, np.zeros_like(v)], 1))
 
 
 C5_SEED_BASE = 5_000_000
@@ -409,4 +425,6 @@ def make_c5(n_scenes: int | None = None, scene_ids: Sequence[int] | None = None)
 
 
 def make_config(cfg: int, **kw) -> Scene:
+    if cfg == 6:
+        return make_c4(moving=True, **kw)
     return {1: make_c1, 2: make_c2, 3: make_c3, 4: make_c4, 5: make_c5}[cfg](**kw)
