@@ -92,9 +92,12 @@ def slice_obstacles(sc, j0, j1):
             Cs.append(sc.obs_C[lo:hi])
             ds.append(sc.obs_d[lo:hi])
             offs.append(offs[-1] + hi - lo)
+    step = None
+    if sc.obs_step is not None:
+        step = np.concatenate([sc.obs_step[b * M + j0:b * M + j1] for b in range(sc.n_scenes)])
     return dataclasses.replace(sc, n_obs=j1 - j0, obs_off=np.asarray(offs, np.int32),
                                obs_C=np.concatenate(Cs) if Cs else np.zeros((0, sc.dim)),
-                               obs_d=np.concatenate(ds) if ds else np.zeros(0))
+                               obs_d=np.concatenate(ds) if ds else np.zeros(0), obs_step=step)
 
 
 def workload_name(cfg, n_scenes, iters):

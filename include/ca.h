@@ -100,6 +100,10 @@ typedef struct {
   double lemke_pivot_tol, lemke_tie_tol;
   int32_t lemke_max_pivot_factor;
   double prox_eps;
+  /* NEXT f3, moving obstacles (nullable: NULL = static, reading #15):
+   * HOST [n_scenes*n_obs][dim], the displacement of each obstacle per timestep --
+   * obstacle j of scene b at timestep t is {x : C_j x <= d_j + t C_j step_bj}. */
+  const double* obs_step;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;

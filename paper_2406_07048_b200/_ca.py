@@ -37,7 +37,7 @@ class Desc(C.Structure):
         ("s_init", C.c_void_p),
         ("sigma", C.c_double), ("eps_pri", C.c_double), ("eps_dual", C.c_double), ("max_iters", C.c_int32),
         ("lemke_pivot_tol", C.c_double), ("lemke_tie_tol", C.c_double), ("lemke_max_pivot_factor", C.c_int32),
-        ("prox_eps", C.c_double),
+        ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
     ]
 
 
@@ -157,6 +157,8 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
     D.eps_pri, D.eps_dual, D.max_iters = eps_pri, eps_dual, max_iters
     D.lemke_pivot_tol, D.lemke_tie_tol, D.lemke_max_pivot_factor = pivot_tol, tie_tol, max_pivot_factor
     D.prox_eps = prox_eps
+    step = getattr(sc, "obs_step", None)
+    D.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
     return D
 
 

@@ -84,6 +84,7 @@ struct ca_problem {
   // obstacle sharding
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
+  double* obs_step_buf = nullptr;  // moving obstacles (allocated on first use)
   double* rb = nullptr;     // [B*N][REC] reduced records (allreduced)
   double* tmpB4 = nullptr;  // [B][4]
 
@@ -189,6 +190,9 @@ ca_status validate(const ca_problem_desc* D) {
     nomax = std::max(nomax, no);
   }
   if (nrmax + nomax + 1 > 32) return fail(CA_E_DIM, "n = n_r + n_o + 1 > 32");
+  if (D->obs_step)
+    for (long long k = 0; k < (long long)D->n_scenes * D->n_obs * d; ++k)
+      if (!std::isfinite(D->obs_step[k])) return fail(CA_E_INVALID, "obs_step must be finite");
   if (!spd(D->Qs, D->n_state) || !spd(D->Qu, D->n_ctrl)) return fail(CA_E_INVALID, "Qs/Qu must be SPD");
   return CA_OK;
 }
@@ -248,6 +252,11 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
   if (h->M > 0) {
     if ((st = h2d(h, const_cast<double*>(v.obs_rows), orr.data(), 4 * (size_t)orow))) return st;
     if ((st = h2d(h, const_cast<int*>(v.obs_off), D->obs_off, (size_t)B * h->M + 1))) return st;
+    if (D->obs_step) {  // moving obstacles (NEXT f3)
+      if (!h->obs_step_buf && (st = h->alloc(&h->obs_step_buf, (size_t)B * h->M * d))) return st;
+      if ((st = h2d(h, h->obs_step_buf, D->obs_step, (size_t)B * h->M * d))) return st;
+    }
+    v.obs_step = D->obs_step ? h->obs_step_buf : nullptr;
     if (d == 2) {
       const long long no = (long long)B * h->M;
       ca::k_vertices2d<<<(unsigned)((no + 127) / 128), 128, 0, h->stream>>>(v.obs_rows, v.obs_off, (int)no, v.obs_vert,
@@ -464,15 +473,18 @@ ca_status collect_global(ca_problem* h, double* dst, int mask) {
 // the rank-local slice [j0, j1) of every scene's obstacles
 struct LocalObs {
   std::vector<int> off;
-  std::vector<double> C, d;
+  std::vector<double> C, d, step;
 };
 void slice_obstacles(const ca_problem_desc* D, int j0, int j1, LocalObs& L, ca_problem_desc& out) {
   const int M = D->n_obs, dim = D->dim, Ml = j1 - j0;
   L.off.assign(1, 0);
   L.C.clear();
   L.d.clear();
+  L.step.clear();
   for (int b = 0; b < D->n_scenes; ++b)
     for (int j = j0; j < j1; ++j) {
+      if (D->obs_step)
+        for (int a = 0; a < dim; ++a) L.step.push_back(D->obs_step[((long long)b * M + j) * dim + a]);
       const int lo = D->obs_off[(long long)b * M + j], hi = D->obs_off[(long long)b * M + j + 1];
       for (int r = lo; r < hi; ++r) {
         for (int a = 0; a < dim; ++a) L.C.push_back(D->obs_C[(long long)r * dim + a]);
@@ -485,6 +497,7 @@ void slice_obstacles(const ca_problem_desc* D, int j0, int j1, LocalObs& L, ca_p
   out.obs_off = L.off.data();
   out.obs_C = L.C.empty() ? nullptr : L.C.data();
   out.obs_d = L.d.empty() ? nullptr : L.d.data();
+  out.obs_step = (D->obs_step && !L.step.empty()) ? L.step.data() : nullptr;
 }
 
 ca_status ensure_slots(ca_problem* h, int n) {

@@ -65,6 +65,7 @@ struct Dev {
   // one sort pool of up to GG = TG*G pairs, cut into nchunkG warp items of 32
   int TG, NG, GG, nchunkG, CHG;  // CHG: lanes used per chunk (balanced)
   int nitems;        // B*NG*nchunkG work items of one sweep
+  const double* obs_step;  // NULL or [B*M][d]: per-timestep obstacle displacement (NEXT f3)
   double* obs_vert;  // d = 2: vertices of every obstacle polygon, [obs row][2] (k_vertices2d)
   int* obs_nv;       //        vertex count per obstacle
   double* part_vert; // d = 2: robot-part vertices (body frame), [part row][2]
@@ -87,6 +88,17 @@ __device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* 
     sincos(st[P.pidx[3]], &sn, &cs);
     R[0] = cs; R[1] = -sn; R[3] = sn; R[4] = cs;
   }
+}
+
+// Moving obstacle j of scene b at timestep t (NEXT f3): the pair is evaluated with the
+// robot origin shifted into the obstacle's frame, rho - t*step (translation invariance;
+// the oracle's obstacle_frame, same two roundings: multiply, then subtract)
+template <int DD>
+__device__ __forceinline__ void obstacle_frame(const Dev& P, int b, int j, int t, double* rho) {
+  if (!P.obs_step) return;
+  const double* st = P.obs_step + ((long long)b * P.M + j) * DD;
+#pragma unroll
+  for (int a = 0; a < DD; ++a) rho[a] = rho[a] - (double)t * st[a];
 }
 
 __device__ __forceinline__ int sym_idx(int a, int c, int npc) { return a * npc - a * (a - 1) / 2 + (c - a); }
@@ -175,6 +187,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
     const long long p = bt * P.G + g, PP = P.P;
     double sR[9], srho[3];  // pose(s_t^{k+1}): the trajectory the last primal step produced
     pose_of(P, P.s + ((long long)it.b * (P.N + 1) + t) * P.ns, sR, srho);
+    obstacle_frame<D>(P, it.b, j, t, srho);
     const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
     const int o = it.b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
     const double* prow = P.part_rows + 4 * r0;
@@ -897,6 +910,7 @@ __global__ void __launch_bounds__(128) k_scale2(Dev P, const double* states, dou
   double R[9], rho[3];
   pose_of(P, states + ((long long)b * (P.N + 1) + t) * P.ns, R, rho);
   const int i = g / P.M, j = g % P.M;
+  obstacle_frame<2>(P, b, j, t, rho);
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
   const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
   const double* ov = P.obs_vert + 2LL * l0;
@@ -940,6 +954,8 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
   const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
   const int m = nr + no;
+  double rho[3] = {srho[0], srho[1], srho[2]};  // this pair's origin (moving obstacles)
+  obstacle_frame<D>(P, b, j, t, rho);
   double* Gr = smem + tid;  // rows [m][D+2] (g_0..g_D, h), stride CTA
 #define GR(r_, c_) Gr[((r_) * (D + 2) + (c_)) * CTA]
   for (int k = 0; k < nr; ++k) {
@@ -951,7 +967,7 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
 #pragma unroll
       for (int c = 0; c < D; ++c) ra += sR[aa * D + c] * __ldg(a + c);
       GR(k, aa) = ra;
-      h += ra * srho[aa];
+      h += ra * rho[aa];
     }
     GR(k, D) = -__ldg(a + 3);
     GR(k, D + 1) = h;
@@ -971,7 +987,7 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
     double cr = 0.0, mag = fabs(GR(nr + lo, D + 1));
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const double tc = GR(nr + lo, a) * srho[a];
+      const double tc = GR(nr + lo, a) * rho[a];
       cr += tc;
       mag += fabs(tc);
     }

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     for (int a = 0; a < D * D; ++a) sR[a] = po[a];
 #pragma unroll
     for (int a = 0; a < D; ++a) srho[a] = po[9 + a];
+    obstacle_frame<D>(P, b, j, it.grp * P.TG + tl + 1, srho);  // moving obstacles (NEXT f3)
 #pragma unroll 1
     for (int lo = 0; lo < no; ++lo) {
       const double4 cr = *reinterpret_cast<const double4*>(orow + 4 * lo);

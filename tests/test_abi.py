@@ -64,6 +64,10 @@ def test_validation_errors_precede_device(ca):
     assert _create(ca, sc, prox_eps=1e-3)[0] == -4  # CA_E_UNSUPPORTED
     bad = dataclasses.replace(sc, Qs=-sc.Qs)
     assert _create(ca, bad)[0] == -1  # CA_E_INVALID (not SPD)
+    step = np.zeros((sc.n_scenes * sc.n_obs, sc.dim))
+    step[0, 0] = np.nan
+    bad = dataclasses.replace(sc, obs_step=step)
+    assert _create(ca, bad)[0] == -1  # CA_E_INVALID (moving obstacles: finite steps)
 
 
 @pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="GPU present")
