@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -85,10 +86,23 @@ struct ca_problem {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
   double* obs_step_buf = nullptr;  // moving obstacles (allocated on first use)
+  // CUDA graph of one ca_admm_iterate(g_iters) call (single GPU, timing off)
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private stream to capture on (the handle's may be legacy)
+  int g_iters = 0;
+  long long g_launches[5] = {0, 0, 0, 0, 0};
+  bool use_graphs = std::getenv("CA_NO_GRAPHS") == nullptr;  // diagnostics: CA_NO_GRAPHS=1 disables
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+    g_iters = 0;
+  }
   double* rb = nullptr;     // [B*N][REC] reduced records (allreduced)
   double* tmpB4 = nullptr;  // [B][4]
 
   ~ca_problem() {
+    drop_graph();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     if (comm) ncclCommDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : event_pool) cudaEventDestroy(e);
@@ -679,6 +693,7 @@ void ca_problem_destroy(ca_problem* h) {
 ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
   ca_status st = check_handle(h);
   if (st) return st;
+  h->drop_graph();  // captured kernel parameters may change
   if ((st = validate(Dfull))) return st;
   LocalObs lobs;
   ca_problem_desc Dl;
@@ -702,6 +717,7 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
 ca_status ca_debug_trace(ca_problem* h, int64_t p, double* out) {
   ca_status st = check_handle(h);
   if (st) return st;
+  h->drop_graph();  // captured kernel parameters may change
   if (!h->dev.dbg) {
     if ((st = h->alloc(&h->dev.dbg, 64 * 48))) return st;
   }
@@ -825,6 +841,7 @@ ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t 
 ca_status ca_set_record_basis(ca_problem* h, int32_t enable) {
   ca_status st = check_handle(h);
   if (st) return st;
+  h->drop_graph();
   if (enable && !h->dev.zmask) {
     uint32_t* z = nullptr;
     if ((st = h->alloc(&z, std::max<long long>(h->P, 1)))) return st;
@@ -871,27 +888,79 @@ ca_status ca_multiplier_update(ca_problem* h, ca_residuals* out) {
   return CA_OK;
 }
 
+// The device work of one ca_admm_iterate(iters): K sweeps + primal steps, the final
+// multiplier update, residual collection and the per-iteration history.
+ca_status enqueue_iterations(ca_problem* h, int iters) {
+  ca_status st;
+  CUDA_TRY(cudaMemsetAsync(h->slots, 0, sizeof(double) * (size_t)iters * h->B * 4, h->stream));
+  for (int it = 0; it < iters; ++it) {
+    if ((st = launch_sweep(h, it > 0))) return st;
+    double* cur = h->slots + (size_t)it * h->B * 4;
+    double* prev = it > 0 ? h->slots + (size_t)(it - 1) * h->B * 4 : nullptr;
+    if ((st = launch_riccati(h, cur, prev))) return st;
+  }
+  if ((st = launch_mult(h))) return st;
+  double* last = h->slots + (size_t)(iters - 1) * h->B * 4;
+  if ((st = collect_global(h, last, 2))) return st;
+  CUDA_TRY(cudaMemcpyAsync(h->scene_res, last, sizeof(double) * h->B * 4, cudaMemcpyDeviceToDevice, h->stream));
+  ca::k_hist<<<iters, 256, 0, h->stream>>>(h->slots, h->B, iters, h->hist_dev);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[4]++;
+  return CA_OK;
+}
+
+// Replay (capturing on first use) the CUDA graph of enqueue_iterations(iters):
+// single-GPU handles with timing off (small configurations are
+// launch-bound).  The launch counters advance as if the kernels had been enqueued.
+ca_status launch_iterations_graph(ca_problem* h, int iters) {
+  if (!h->gexec || h->g_iters != iters) {
+    h->drop_graph();
+    long long before[5];
+    for (int f = 0; f < 5; ++f) before[f] = h->launches[f];
+    if (!h->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    const cudaStream_t user = h->stream;
+    h->stream = h->cap_stream;  // the launch helpers enqueue on h->stream
+    const cudaError_t be = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+    if (be != cudaSuccess) {
+      h->stream = user;
+      return fail(CA_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(be));
+    }
+    ca_status st = enqueue_iterations(h, iters);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    h->stream = user;
+    if (st) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (ce != cudaSuccess) return fail(CA_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&h->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      h->gexec = nullptr;
+      return fail(CA_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    }
+    h->g_iters = iters;
+    for (int f = 0; f < 5; ++f) {
+      h->g_launches[f] = h->launches[f] - before[f];
+      h->launches[f] = before[f];
+    }
+  }
+  CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+  for (int f = 0; f < 5; ++f) h->launches[f] += h->g_launches[f];
+  return CA_OK;
+}
+
 ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist) {
   ca_status st = check_handle(h);
   if (st) return st;
   if (iters <= 0) return fail(CA_E_INVALID, "iters must be > 0");
+  if (iters > h->slots_cap) h->drop_graph();  // slot buffers are reallocated
   if ((st = ensure_slots(h, iters))) return mark(h, st);
-  CUDA_TRY(cudaMemsetAsync(h->slots, 0, sizeof(double) * (size_t)iters * h->B * 4, h->stream));
-  for (int it = 0; it < iters; ++it) {
-    if ((st = launch_sweep(h, it > 0))) return mark(h, st);
-    double* cur = h->slots + (size_t)it * h->B * 4;
-    double* prev = it > 0 ? h->slots + (size_t)(it - 1) * h->B * 4 : nullptr;
-    if ((st = launch_riccati(h, cur, prev))) return mark(h, st);
-  }
-  if ((st = launch_mult(h))) return mark(h, st);
-  double* last = h->slots + (size_t)(iters - 1) * h->B * 4;
-  if ((st = collect_global(h, last, 2))) return mark(h, st);
-  CUDA_TRY(cudaMemcpyAsync(h->scene_res, last, sizeof(double) * h->B * 4, cudaMemcpyDeviceToDevice, h->stream));
+  const bool graph = h->use_graphs && !h->timing && !h->comm && h->dev.dbg_p < 0;
+  if ((st = graph ? launch_iterations_graph(h, iters) : enqueue_iterations(h, iters))) return mark(h, st);
   int64_t fails = 0;
   if (hist) {
-    ca::k_hist<<<iters, 256, 0, h->stream>>>(h->slots, h->B, iters, h->hist_dev);
-    CUDA_TRY(cudaGetLastError());
-    h->launches[4]++;
     std::vector<double> hv((size_t)iters * 4);
     CUDA_TRY(cudaMemcpyAsync(hv.data(), h->hist_dev, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
