@@ -617,8 +617,7 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   const int nd = P.dyn_pt ? N : 1;
   double* ric = sdyn + (long long)nd * DB;  // [N][NU][NS+1]: feedback K_t | k_t
   // recursion work area (static): value function, products, gains
-  __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Quu[NU][NU], Qux[NU][NS + 1],
-      Pn[NS][NS], xs[NS], us[NU];
+  __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Qux[NU][NS + 1], xs[NS], xs2[NS];
   for (int t = lane; t < N; t += 32)
     stage_block(P, recs, nchunk, (long long)b * N + t, sstg + (long long)t * SB, sst + 4LL * t);
   {
@@ -630,7 +629,20 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   }
   __syncwarp();
   // 2 Qu of this lane's phase-2 entry (kept in a register)
-  const double qu2 = (lane < NU * NU) ? 2.0 * P.Qu[lane] : 0.0;
+  // this lane's upper-triangle entries (row-major order), decoded once
+  int tri_row[2] = {0, 0}, tri_col[2] = {0, 0};
+  for (int k = lane, u = 0; k < NS * (NS + 1) / 2 && u < 2; k += 32, ++u) {
+    int a_ = 0, r = k;
+    while (r >= NS - a_) { r -= NS - a_; ++a_; }
+    tri_row[u] = a_;
+    tri_col[u] = a_ + r;
+  }
+  static_assert(NS * (NS + 1) / 2 <= 64, "two upper-triangle entries per lane at most");
+  double qu2[NU][NU];  // 2 Qu, kept in registers
+#pragma unroll
+  for (int a_ = 0; a_ < NU; ++a_)
+#pragma unroll
+    for (int c = 0; c < NU; ++c) qu2[a_][c] = 2.0 * P.Qu[a_ * NU + c];
   // P_N = H_N, p_N = h_N
   for (int k = lane; k < SB; k += 32) {
     const double v = sstg[(long long)(N - 1) * SB + k];
@@ -638,8 +650,8 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
     else pv[k - NS * NS] = v;
   }
   __syncwarp();
-  // Backward Riccati recursion, warp-cooperative: every phase assigns one matrix
-  // entry per lane and keeps the serial summation order of that entry.
+  // Backward Riccati recursion, warp-cooperative, three phases per step; every
+  // matrix entry keeps the serial summation order (bitwise equal to k_riccati_thread).
   for (int t = N - 1; t >= 0; --t) {
     const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
     const double* Bm = A + NS * NS;
@@ -667,35 +679,35 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
       }
     }
     __syncwarp();
-    // phase 2: Quu = 2Qu + B^T P B, [Qux | qu] = B^T [P A | w]
-    for (int k = lane; k < NU * NU + NU * (NS + 1); k += 32) {
-      if (k < NU * NU) {
-        const int a_ = k / NU, c = k % NU;
-        double s_ = qu2;  // 2 Qu[a][c], k = a NU + c < 32
+    // phase 2: lane c <= NS forms Quu = 2Qu + B^T P B (every lane the same, no
+    // exchange), its column c of [Qux | qu] = B^T [P A | w], factors Quu = L L^T and
+    // solves column c of the gains -Quu^{-1} [Qux | qu]
+    if (lane <= NS) {
+      const int c = lane;
+      double Qm[NU][NU], qx[NU];
 #pragma unroll
-        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], PB[q][c], s_);
-        Quu[a_][c] = s_;
-      } else {
-        const int kk = k - NU * NU, a_ = kk / (NS + 1), c = kk % (NS + 1);
+      for (int a_ = 0; a_ < NU; ++a_) {
+#pragma unroll
+        for (int cc = 0; cc < NU; ++cc) {
+          double s_ = qu2[a_][cc];
+#pragma unroll
+          for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], PB[q][cc], s_);
+          Qm[a_][cc] = s_;
+        }
         double s_ = 0.0;
 #pragma unroll
         for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], (c < NS) ? PA[q][c] : w[q], s_);
+        qx[a_] = s_;
         Qux[a_][c] = s_;
       }
-    }
-    __syncwarp();
-    // phase 3: Cholesky Quu = L L^T (each lane, redundantly), then lane c solves
-    // column c of -Quu^{-1} [Qux | qu] into the gains
-    double Kc[NU];
-    if (lane <= NS) {
       double Lc[NU][NU], Li[NU];  // factor and reciprocal diagonal
 #pragma unroll
       for (int a_ = 0; a_ < NU; ++a_)
 #pragma unroll
-        for (int c = 0; c < NU; ++c) Lc[a_][c] = 0.0;
+        for (int cc = 0; cc < NU; ++cc) Lc[a_][cc] = 0.0;
 #pragma unroll
       for (int jj = 0; jj < NU; ++jj) {
-        double s_ = Quu[jj][jj];
+        double s_ = Qm[jj][jj];
 #pragma unroll
         for (int q = 0; q < jj; ++q) s_ -= Lc[jj][q] * Lc[jj][q];
         const double ljj = sqrt(s_);
@@ -703,50 +715,51 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
         Li[jj] = 1.0 / ljj;
 #pragma unroll
         for (int ii = jj + 1; ii < NU; ++ii) {
-          double a2 = Quu[ii][jj];
+          double a2 = Qm[ii][jj];
 #pragma unroll
           for (int q = 0; q < jj; ++q) a2 -= Lc[ii][q] * Lc[jj][q];
           Lc[ii][jj] = a2 * Li[jj];
         }
       }
-      double rhs[NU];
-#pragma unroll
-      for (int a_ = 0; a_ < NU; ++a_) rhs[a_] = Qux[a_][lane];
 #pragma unroll
       for (int a_ = 0; a_ < NU; ++a_) {
-        double s_ = rhs[a_];
+        double s_ = qx[a_];
 #pragma unroll
-        for (int q = 0; q < a_; ++q) s_ -= Lc[a_][q] * rhs[q];
-        rhs[a_] = s_ * Li[a_];
+        for (int q = 0; q < a_; ++q) s_ -= Lc[a_][q] * qx[q];
+        qx[a_] = s_ * Li[a_];
       }
 #pragma unroll
       for (int a_ = NU - 1; a_ >= 0; --a_) {
-        double s_ = rhs[a_];
+        double s_ = qx[a_];
 #pragma unroll
-        for (int q = a_ + 1; q < NU; ++q) s_ -= Lc[q][a_] * rhs[q];
-        rhs[a_] = s_ * Li[a_];
+        for (int q = a_ + 1; q < NU; ++q) s_ -= Lc[q][a_] * qx[q];
+        qx[a_] = s_ * Li[a_];
       }
 #pragma unroll
-      for (int a_ = 0; a_ < NU; ++a_) {
-        Kc[a_] = -rhs[a_];
-        ric[((long long)t * NU + a_) * (NS + 1) + lane] = Kc[a_];
-      }
+      for (int a_ = 0; a_ < NU; ++a_) ric[((long long)t * NU + a_) * (NS + 1) + c] = -qx[a_];
     }
     __syncwarp();
-    // phase 4: P <- H + A^T P A + Qux^T K ;  p <- h + A^T w + Qux^T k
+    // phase 3: P <- sym(H + A^T P A + Qux^T K) (both triangle entries by one lane),
+    // p <- h + A^T w + Qux^T k
     const double* H = sstg + (long long)(t - 1) * SB;  // stage t (zero at t = 0)
     const double* Kt = ric + (long long)t * NU * (NS + 1);
-    for (int k = lane; k < NS * NS + NS; k += 32) {
-      if (k < NS * NS) {
-        const int a_ = k / NS, c = k % NS;
-        double v = (t >= 1) ? H[a_ * NS + c] : 0.0;
+    auto pn_entry = [&](int a_, int c) {
+      double v = (t >= 1) ? H[a_ * NS + c] : 0.0;
 #pragma unroll
-        for (int q = 0; q < NS; ++q) v = __fma_rn(A[q * NS + a_], PA[q][c], v);
+      for (int q = 0; q < NS; ++q) v = __fma_rn(A[q * NS + a_], PA[q][c], v);
 #pragma unroll
-        for (int q = 0; q < NU; ++q) v = __fma_rn(Qux[q][a_], Kt[q * (NS + 1) + c], v);
-        Pn[a_][c] = v;
+      for (int q = 0; q < NU; ++q) v = __fma_rn(Qux[q][a_], Kt[q * (NS + 1) + c], v);
+      return v;
+    };
+    // (phase 3 reads PA, w, Qux, K only, so P and p are written in place)
+    for (int k = lane; k < NS * (NS + 1) / 2 + NS; k += 32) {
+      if (k < NS * (NS + 1) / 2) {
+        const int a_ = tri_row[k >> 5], c = tri_col[k >> 5];  // this lane's upper-triangle entry
+        const double v = 0.5 * (pn_entry(a_, c) + pn_entry(c, a_));
+        Pm[a_][c] = v;
+        Pm[c][a_] = v;
       } else {
-        const int a_ = k - NS * NS;
+        const int a_ = k - NS * (NS + 1) / 2;
         double s_ = (t >= 1) ? H[NS * NS + a_] : 0.0;
 #pragma unroll
         for (int q = 0; q < NS; ++q) s_ = __fma_rn(A[q * NS + a_], w[q], s_);
@@ -756,48 +769,45 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
       }
     }
     __syncwarp();
-    for (int k = lane; k < NS * NS; k += 32) {
-      const int a_ = k / NS, c = k % NS;
-      Pm[a_][c] = 0.5 * (Pn[a_][c] + Pn[c][a_]);
-    }
-    __syncwarp();
   }
-  // forward rollout from s_0 (Eq. 13b holds exactly): u_t = K_t x_t + k_t (lanes
-  // < NU), x_{t+1} = A x + B u + c (lanes < NS)
+  // forward rollout from s_0 (Eq. 13b holds exactly): every lane forms u_t = K_t x_t
+  // + k_t (same arithmetic), lane a < NS then x_{t+1}[a] = A x + B u + c: one
+  // exchange per step (double-buffered state)
   double* sb = P.s + (long long)b * (N + 1) * NS;
   if (lane < NS) {
     xs[lane] = P.s0[b * NS + lane];
     sb[lane] = xs[lane];
   }
   __syncwarp();
+  double* xc = xs;
+  double* xn = xs2;
   for (int t = 0; t < N; ++t) {
     const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
     const double* Bm = A + NS * NS;
     const double* cv = Bm + NS * NU;
-    if (lane < NU) {
-      const double* kr = ric + ((long long)t * NU + lane) * (NS + 1);
+    double uu[NU];
+#pragma unroll
+    for (int a_ = 0; a_ < NU; ++a_) {
+      const double* kr = ric + ((long long)t * NU + a_) * (NS + 1);
       double s_ = kr[NS];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) s_ = __fma_rn(kr[c], xs[c], s_);
-      us[lane] = s_;
-      P.u[((long long)b * N + t) * NU + lane] = s_;
+      for (int c = 0; c < NS; ++c) s_ = __fma_rn(kr[c], xc[c], s_);
+      uu[a_] = s_;
     }
-    __syncwarp();
-    double xn = 0.0;
+    if (lane < NU) P.u[((long long)b * N + t) * NU + lane] = uu[lane];
     if (lane < NS) {
       double s_ = cv[lane];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) s_ = __fma_rn(A[lane * NS + c], xs[c], s_);
+      for (int c = 0; c < NS; ++c) s_ = __fma_rn(A[lane * NS + c], xc[c], s_);
 #pragma unroll
-      for (int c = 0; c < NU; ++c) s_ = __fma_rn(Bm[lane * NU + c], us[c], s_);
-      xn = s_;
+      for (int c = 0; c < NU; ++c) s_ = __fma_rn(Bm[lane * NU + c], uu[c], s_);
+      xn[lane] = s_;
+      sb[(t + 1) * NS + lane] = s_;
     }
     __syncwarp();
-    if (lane < NS) {
-      xs[lane] = xn;
-      sb[(t + 1) * NS + lane] = xn;
-    }
-    __syncwarp();
+    double* tmp = xc;
+    xc = xn;
+    xn = tmp;
   }
   if (lane == 0) {
     double st[4] = {0, 0, 0, 0};
