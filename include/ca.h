@@ -104,6 +104,13 @@ typedef struct {
    * HOST [n_scenes*n_obs][dim], the displacement of each obstacle per timestep --
    * obstacle j of scene b at timestep t is {x : C_j x <= d_j + t C_j step_bj}. */
   const double* obs_step;
+  /* Nullable caller-owned DEVICE workspace (e.g. a torch uint8 tensor) of
+   * workspace_bytes >= ca_workspace_size(): every buffer of the handle is carved out of
+   * it (256-byte aligned) instead of cudaMalloc; the caller keeps it alive until
+   * ca_problem_destroy.  Buffers needed later beyond it (more iterations than
+   * max_iters, tracing, basis recording) fall back to cudaMalloc. */
+  void* workspace;
+  size_t workspace_bytes;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;
@@ -117,6 +124,12 @@ typedef struct {
   int32_t iterations, converged;
   ca_residuals last;
 } ca_solve_report;
+
+/* Device bytes a handle for `desc` (and, if dist is non-NULL, rank dist->rank of an
+ * obstacle-sharded problem) takes from a caller workspace: every buffer allocated at
+ * creation plus the scale factors and max_iters iterations of statistics.  Host only. */
+struct ca_dist_desc_s;
+ca_status ca_workspace_size(const ca_problem_desc* desc, const struct ca_dist_desc_s* dist, size_t* bytes);
 
 /* Validate, allocate device state (~(2n_max + 2d + 8) * 8 bytes per pair), upload the
  * problem and initialise the iterate (reading #11).  device: CUDA ordinal; stream:
@@ -132,7 +145,7 @@ void ca_problem_destroy(ca_problem* h);
  * the handle's stream; the primal step then runs replicated on identical bytes.
  * Pair indices of the getters are rank-local (j counted from j0).
  * Scene sharding needs no collective: give each rank its own scenes instead. */
-typedef struct {
+typedef struct ca_dist_desc_s {
   int32_t world_size, rank;
   const uint8_t* nccl_id; /* 128 bytes from ca_nccl_unique_id on one rank, broadcast */
 } ca_dist_desc;

@@ -38,6 +38,7 @@ class Desc(C.Structure):
         ("sigma", C.c_double), ("eps_pri", C.c_double), ("eps_dual", C.c_double), ("max_iters", C.c_int32),
         ("lemke_pivot_tol", C.c_double), ("lemke_tie_tol", C.c_double), ("lemke_max_pivot_factor", C.c_int32),
         ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
     ]
 
 
@@ -72,6 +73,7 @@ def lib():
         L.ca_last_error.restype = C.c_char_p
         L.ca_problem_create.argtypes = [C.POINTER(Desc), C.c_int, vp, C.POINTER(vp)]
         L.ca_problem_destroy.argtypes = [vp]
+        L.ca_workspace_size.argtypes = [C.POINTER(Desc), vp, C.POINTER(C.c_size_t)]
         L.ca_problem_destroy.restype = None
         L.ca_problem_load.argtypes = [vp, C.POINTER(Desc)]
         L.ca_problem_info.argtypes = [vp, i64p, C.POINTER(C.c_int32), i64p]
@@ -100,7 +102,7 @@ def lib():
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
                      "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace",
-                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist"):
+                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib
@@ -165,22 +167,36 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
 class Problem:
     """A batched MPC problem resident on one B200 (ca_problem handle)."""
 
-    def __init__(self, sc, device: int = 0, stream: int | None = None, dist=None, **params):
+    def __init__(self, sc, device: int = 0, stream: int | None = None, dist=None, workspace: str | None = None,
+                 **params):
         """dist = (world_size, rank, nccl_id bytes): obstacle-sharded rank of the full
-        problem `sc` (include/ca.h ca_problem_create_dist); None = single GPU."""
+        problem `sc` (include/ca.h ca_problem_create_dist); None = single GPU.
+        workspace = "torch": every device buffer is carved out of one torch uint8 tensor
+        of ca_workspace_size bytes (device memory owned by PyTorch's allocator)."""
         self.sc = sc
         self.params = params
         self._keep = {}
         desc = make_desc(sc, self._keep, **params)
         h = C.c_void_p()
         self.dist = dist
+        if dist is not None:
+            world, rank, nid = dist
+            self._nid = C.create_string_buffer(bytes(nid), 128)
+            dd = DistDesc(world, rank, C.cast(self._nid, C.c_void_p))
+        if workspace == "torch":
+            import torch
+
+            nbytes = C.c_size_t()
+            _check(lib().ca_workspace_size(C.byref(desc), C.byref(dd) if dist is not None else None,
+                                           C.byref(nbytes)))
+            self._ws = torch.empty(nbytes.value, dtype=torch.uint8, device=torch.device("cuda", device))
+            desc.workspace, desc.workspace_bytes = self._ws.data_ptr(), nbytes.value
+        elif workspace is not None:
+            raise ValueError("workspace must be None or 'torch'")
         if dist is None:
             _check(lib().ca_problem_create(C.byref(desc), device, stream, C.byref(h)), ok=(CA_OK,))
             self.j0, self.j1 = 0, sc.n_obs
         else:
-            world, rank, nid = dist
-            self._nid = C.create_string_buffer(bytes(nid), 128)
-            dd = DistDesc(world, rank, C.cast(self._nid, C.c_void_p))
             _check(lib().ca_problem_create_dist(C.byref(desc), C.byref(dd), device, stream, C.byref(h)), ok=(CA_OK,))
             self.j0, self.j1 = obstacle_partition(sc, world, rank)
         self.h = h

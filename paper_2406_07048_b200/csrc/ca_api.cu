@@ -86,6 +86,11 @@ struct ca_problem {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
   double* obs_step_buf = nullptr;  // moving obstacles (allocated on first use)
+  // caller-provided device workspace (bump allocation, 256-B aligned); count_only:
+  // ca_workspace_size's planning pass (no device calls)
+  char* ws = nullptr;
+  size_t ws_size = 0, ws_used = 0;
+  bool count_only = false;
   // CUDA graph of one ca_admm_iterate(g_iters) call (single GPU, timing off)
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream to capture on (the handle's may be legacy)
@@ -115,6 +120,18 @@ struct ca_problem {
   ca_status alloc(T** p, size_t count) {
     void* q = nullptr;
     size_t nb = std::max<size_t>(count, 1) * sizeof(T);
+    const size_t na = (nb + 255) & ~size_t(255);
+    if (count_only) {  // ca_workspace_size: plan only
+      ws_used += na;
+      *p = reinterpret_cast<T*>(uintptr_t(256));
+      return CA_OK;
+    }
+    if (ws && ws_used + na <= ws_size) {  // the caller's workspace (e.g. a torch tensor)
+      *p = reinterpret_cast<T*>(ws + ws_used);
+      ws_used += na;
+      bytes += (long long)na;
+      return CA_OK;
+    }
     cudaError_t e = cudaMalloc(&q, nb);
     if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? CA_E_OOM : CA_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     allocs.push_back(q);
@@ -557,21 +574,9 @@ extern "C" {
 
 const char* ca_last_error(void) { return g_err.c_str(); }
 
-ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, ca_problem** out) {
-  if (!out) return fail(CA_E_INVALID, "out is NULL");
-  *out = nullptr;
-  ca_status st = validate(D);
-  if (st) return st;
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
-    return fail(CA_E_CUDA, "no CUDA device (this library has no CPU fallback)");
-  cudaDeviceProp prop;
-  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10) return fail(CA_E_CUDA, "built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
-  CUDA_TRY(cudaSetDevice(device));
-  ca_problem* h = new ca_problem();
-  h->device = device;
-  h->stream = static_cast<cudaStream_t>(stream);
+// Host-side setup of a handle: shapes, work decomposition and every device buffer
+// (through h->alloc, so a planning pass can size the caller's workspace).
+ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   h->d = D->dim;
   h->B = D->n_scenes;
   h->N = D->horizon;
@@ -627,14 +632,14 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   const int d = h->d, B = h->B, N = h->N, ns = h->ns, nu = h->nu;
   const long long nd = (long long)(D->dyn_per_scene ? B : 1) * (D->dyn_per_time ? N : 1);
   const long long orow = (h->M > 0) ? D->obs_off[(long long)B * h->M] : 0;
-#define AL(ptr, T, cnt)                                  \
-  do {                                                   \
-    T* tmp_ = nullptr;                                   \
-    if ((st = h->alloc(&tmp_, (size_t)(cnt)))) {         \
-      delete h;                                          \
-      return st;                                         \
-    }                                                    \
-    ptr = tmp_;                                          \
+  ca_status st;
+#define AL(ptr, T, cnt)                          \
+  do {                                           \
+    T* tmp_ = nullptr;                           \
+    if ((st = h->alloc(&tmp_, (size_t)(cnt)))) { \
+      return st;                                 \
+    }                                            \
+    ptr = tmp_;                                  \
   } while (0)
   AL(v.part_rows, double, 4 * (size_t)D->part_off[h->np]);
   AL(v.part_off, int, h->np + 1);
@@ -672,6 +677,38 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   AL(v.part_e, int, (size_t)h->np);
   AL(v.part_be, double, (size_t)h->np);
 #undef AL
+  // lazily used buffers that also live in the workspace: scale factors, per-iteration
+  // statistics for max_iters iterations, moving-obstacle steps
+  if ((st = h->alloc(&h->alpha, (size_t)h->P + h->B))) return st;
+  if ((st = ensure_slots(h, h->max_iters))) return st;
+  if (D->obs_step && (st = h->alloc(&h->obs_step_buf, (size_t)B * h->M * d))) return st;
+  return CA_OK;
+}
+
+ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, ca_problem** out) {
+  if (!out) return fail(CA_E_INVALID, "out is NULL");
+  *out = nullptr;
+  ca_status st = validate(D);
+  if (st) return st;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
+    return fail(CA_E_CUDA, "no CUDA device (this library has no CPU fallback)");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(CA_E_CUDA, "built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
+  CUDA_TRY(cudaSetDevice(device));
+  ca_problem* h = new ca_problem();
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(stream);
+  if (D->workspace) {
+    h->ws = static_cast<char*>(D->workspace);
+    h->ws_size = D->workspace_bytes;
+  }
+  if ((st = setup_handle(h, D))) {
+    delete h;
+    return st;
+  }
+  ca::Dev& v = h->dev;
   v.zmask = nullptr;
   v.dbg_p = -1;
   v.dbg = nullptr;
@@ -680,6 +717,30 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
     return st;
   }
   *out = h;
+  return CA_OK;
+}
+
+ca_status ca_workspace_size(const ca_problem_desc* D, const ca_dist_desc* dist, size_t* bytes) {
+  if (!bytes) return fail(CA_E_INVALID, "bytes is NULL");
+  *bytes = 0;
+  ca_status st = validate(D);
+  if (st) return st;
+  LocalObs lobs;
+  ca_problem_desc Dl;
+  const ca_problem_desc* Du = D;
+  long long extra = 0;
+  if (dist && dist->world_size > 1) {
+    int j0 = 0, j1 = 0;
+    if ((st = ca_obstacle_partition(D->n_scenes, D->n_obs, D->obs_off, dist->world_size, dist->rank, &j0, &j1)))
+      return st;
+    slice_obstacles(D, j0, j1, lobs, Dl);
+    Du = &Dl;
+  }
+  if (dist) extra = (((long long)D->n_scenes * D->horizon * ca::REC * 8 + 255) / 256 + ((long long)D->n_scenes * 32 + 255) / 256) * 256;
+  ca_problem h;
+  h.count_only = true;
+  if ((st = setup_handle(&h, Du))) return st;
+  *bytes = h.ws_used + (size_t)extra;
   return CA_OK;
 }
 

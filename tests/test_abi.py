@@ -90,3 +90,25 @@ def test_obstacle_partition_properties(ca):
             for r, (j0, j1) in enumerate(parts):
                 got = faces[j0:j1].sum()
                 assert abs(got - tot / W) <= faces.max() + 1e-9, (cfg, W, r, got, tot / W)
+
+
+def test_workspace_size_host_only(ca):
+    """ca_workspace_size is a host planning pass: positive, grows with the batch, and
+    covers at least the pair state (y, zeta, xi, status) of every pair."""
+    import ctypes as C
+
+    from paper_2406_07048_b200._ca import make_desc
+
+    def size(sc):
+        keep = {}
+        desc = make_desc(sc, keep)
+        nb = C.c_size_t()
+        rc = ca.lib().ca_workspace_size(C.byref(desc), None, C.byref(nb))
+        assert rc == 0
+        return nb.value
+
+    small, big = scenes.make_c5(n_scenes=2), scenes.make_c5(n_scenes=8)
+    s2, s8 = size(small), size(big)
+    assert 0 < s2 < s8
+    per_pair = 8 * (big.n_max + 1 + big.dim) + 4
+    assert s8 >= big.n_pairs * per_pair

@@ -314,3 +314,23 @@ def test_t2_symmetric_degenerate(ca):
     s, u = g.trajectory()
     close(s, o.s, 1e-6, "s")
     close(u, o.u, 1e-6, "u")
+
+
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_torch_workspace_bitwise(ca, cfg):
+    """Every device buffer carved out of one torch tensor (ca_workspace_size bytes):
+    the same results bit for bit as library-allocated memory."""
+    sc = scene(cfg)
+    a = ca.Problem(sc)
+    b = ca.Problem(sc, workspace="torch")
+    assert b._ws.numel() >= b.device_bytes > 0
+    a.admm_iterate(10)
+    b.admm_iterate(10)
+    (sa, ua), (sb, ub) = a.trajectory(), b.trajectory()
+    assert np.array_equal(sa, sb) and np.array_equal(ua, ub)
+    pa, pb = a.pair_state(), b.pair_state()
+    for k in ("y", "zeta", "xi", "pivots", "status"):
+        assert np.array_equal(pa[k], pb[k]), k
+    aa, ma = a.scale_detect()
+    ab, mb = b.scale_detect()
+    assert np.array_equal(aa, ab) and np.array_equal(ma, mb)
