@@ -303,11 +303,11 @@ def run_ours(args, rank, world, local):
             box = [nid]
             dist.broadcast_object_list(box, src=0)
             nid = box[0]
-        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid))
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid), workspace="torch")
         sc_local = slice_obstacles(sc, g.j0, g.j1)
     else:
         sc = make_scene(cfg, rank, args.scenes)
-        g = ca.Problem(sc, device=local, stream=stream.cuda_stream)
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, workspace="torch")
         sc_local = sc
     iters = args.iters or sc.iters
     fp64 = ca.fp64_peak(local, 300.0) if rank == 0 else None
