@@ -57,3 +57,20 @@ def compare_dual_sweep(sc, s, zeta, xi, y_gpu, y_orc, piv_gpu, piv_orc, st_gpu, 
     for p in bad:
         validate_pair_choice(sc, s, zeta, xi, p, y_gpu[p], y_orc[p])
     return len(bad)
+
+
+class OracleSolver:
+    """The CPU oracle behind the solver interface of paper_2406_07048_b200.mpc."""
+
+    def load(self, sc):
+        self.o = oracle.Oracle(sc)
+
+    def set_iterate(self, s, u, y, zeta, xi):
+        self.o.set_iterate(s, u, y, zeta, xi)
+
+    def admm_iterate(self, K):
+        self.o.admm_iterate(K)
+
+    def state(self):
+        o = self.o
+        return o.s.copy(), o.u.copy(), o.y.copy(), o.zeta.copy(), o.xi.copy()
