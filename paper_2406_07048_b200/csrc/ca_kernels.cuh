@@ -1,16 +1,23 @@
 // ca_kernels.cuh -- sm_100a FP64 kernels of the ADMM hot path (arXiv 2406.07048).
 //
-//   k_sweep<D,NMAX,FUSED>  ADMM step 1 (Eq. 15) for one pair per thread:
-//                          [FUSED: step 3 of the previous iteration, Eq. 17, first]
-//                          Eq. 19 build -> Eqs. 20-21 elimination -> Eq. 24 LCP ->
-//                          revised Lemke (ca_lemke.cuh) -> y recovery,
-//                          dual-residual partial (Eq. 18b) and the Gauss-Newton
-//                          aggregates of step 2, reduced per (scene, t, chunk).
-//   k_riccati<NS,NU>       ADMM step 2 (Eq. 16, one SQP QP)
-//                          as a Riccati recursion per scene.
+//   k_sweep<D,NMAX,FUSED,TRACE>  (ca_sweep.cuh) ADMM step 1 (Eq. 15), one
+//                          pair per thread, persistent warps over (scene, timestep
+//                          group, chunk) items: [FUSED: step 3 of the previous
+//                          iteration, Eq. 17, first] Eq. 19 build -> Eqs. 20-21
+//                          elimination -> Eq. 24 LCP -> revised Lemke (ca_lemke.cuh)
+//                          -> y recovery, dual-residual partial (Eq. 18b)
+//                          and the Gauss-Newton aggregates of step 2, one record per
+//                          (item, timestep).
+//   k_sortpairs            per sweep: poses of s^k and the execution order of every
+//                          sort pool (stable counting sort by last pivot count).
+//   k_stage_grouped / k_stage + k_riccati_thread (large batches), k_riccati (small:
+//                          warp per scene)  ADMM step 2 (Eq. 16, one SQP QP,
+//                          P:349-351) as a Riccati recursion per scene.
 //   k_mult<D>              ADMM step 3 (Eq. 17) standalone + r_pri.
-//   k_scale<D>             Eq. 3 scale LP per pair (vertex enumeration).
-//   k_collect / k_scene_min / k_hist  small deterministic reductions.
+//   k_scale2 (d = 2, separating axes) / k_scale<3> (vertex enumeration)  Eq. 3
+//                           per pair; k_vertices2d polygon vertices.
+//   k_lamtab               per load: the lambda rows of Eqs. 20-21 per robot part.
+//   k_collect / k_reduce_records / k_scene_min / k_hist  deterministic reductions.
 //   k_dfma                 FP64 FMA peak microbenchmark.
 // No floating-point atomics anywhere: every reduction has a fixed order, so results
 // are bitwise reproducible run to run.
@@ -156,17 +163,6 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
   __syncwarp();
 }
 
-// deterministic warp sum of NF fields (CTA == one warp); lane 0 gets the totals
-template <int NF>
-__device__ __forceinline__ void cta_sum(double* rec, double* /*unused*/) {
-#pragma unroll
-  for (int f = 0; f < NF; ++f) {
-    double v = rec[f];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    rec[f] = v;
-  }
-}
 
 // ----------------------------------------------------------------------------
 // ADMM step 3 standalone (Eq. 17 with Eqs. 10-11 at s^{k+1}, y^{k+1})

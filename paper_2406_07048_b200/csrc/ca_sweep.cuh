@@ -6,14 +6,18 @@
 // argmax b_i, reading #3) -> Eq. 24 LCP -> revised Lemke (ca_lemke.cuh) ->
 // recovery y_e = (1 - sum_{k != e} b_k lambda_k)/b_e -> dual residual
 // (Eq. 18b) and (v v^T, |g|^2, -eT v, g.eR) for the primal step, reduced per
-// (scene, t, chunk) in a fixed order (no FP atomics).
+// (scene, t) work-item records in a fixed order (no FP atomics).
 //
-// Layout: one warp per CTA (no cross-warp barrier).  Per-thread state that the
-// pivot loop indexes at run time (basic-variable values, entering-column
-// coefficients, reduced obstacle rows, the m x m system, tableau-row labels)
-// lives in shared memory as [item][thread] (32 consecutive words per warp access,
-// conflict-free); the pivot loop itself is a few hundred instructions so every
-// resident warp runs out of the instruction cache.
+// Scheduling: persistent, independent warps (WPC per CTA) pull work items -- 32
+// slots of a scene's sort pool of TG timesteps, ordered by last pivot count -- from
+// a counter.  Per-thread state that the pivot loop indexes at run time (basic-
+// variable values, entering-column coefficients, reduced obstacle rows) lives in
+// shared memory as [item][lane] (conflict-free); tableau-row labels are 4-bit
+// fields of a register; the m x m structural system is in registers (m <= 3) or a
+// shared-memory slot / local memory.  Rare cases (multi-way ties, an ineligible
+// provisional minimum, failures, unverified answers) leave the pivot loop for the
+// warp-cooperative dense Lemke, so the loop's instruction footprint and register
+// pressure stay small; the pivot trace is a separate kernel variant (TRACE).
 #pragma once
 #include "ca_kernels.cuh"
 #include "ca_lemke.cuh"
