@@ -90,6 +90,7 @@ class _Problem(C.Structure):
         ("Qs", C.c_void_p), ("Qu", C.c_void_p), ("s0", C.c_void_p), ("s_ref", C.c_void_p),
         ("sigma", C.c_double), ("pivot_tol", C.c_double), ("tie_tol", C.c_double),
         ("max_pivot_factor", C.c_int), ("ny", C.c_int), ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
+        ("dyn_model", C.c_int), ("dt", C.c_double),
     ]
 
 
@@ -135,6 +136,7 @@ class Oracle:
         P.prox_eps = prox_eps
         step = getattr(sc, "obs_step", None)  # NEXT f3: moving obstacles (None = static)
         P.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
+        P.dyn_model, P.dt = int(getattr(sc, "dyn_model", 0)), float(sc.dt)  # NEXT f2: SQP relinearisation
         self.ny = P.ny = sc.n_max if sc.n_obs > 0 else 1
         self.P = P
         B, N, ns, nu, d = sc.n_scenes, sc.horizon, sc.n_state, sc.n_ctrl, sc.dim

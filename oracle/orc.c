@@ -414,6 +414,27 @@ static const double* dyn_ptr(const orc_problem* P, const double* base, int b, in
   return base + idx * blk;
 }
 
+/* dyn_model 1: the unicycle linearised at (sbar, ubar) (f is linear in u, so c does
+ * not depend on ubar):  A = I + dt d(v cos th, v sin th, 0, 0)/ds,  B = dt [e_3 | e_2]
+ * for u = (a, om),  c = sbar + dt (v cos th, v sin th, 0, 0) - A sbar. */
+static void unicycle_ltv(double dt, const double* sb, double* A, double* B, double* c) {
+  const double th = sb[2], v = sb[3], cs = cos(th), sn = sin(th);
+  for (int a = 0; a < 16; ++a) A[a] = (a % 5 == 0) ? 1.0 : 0.0;
+  A[0 * 4 + 2] += -dt * v * sn;
+  A[0 * 4 + 3] += dt * cs;
+  A[1 * 4 + 2] += dt * v * cs;
+  A[1 * 4 + 3] += dt * sn;
+  for (int a = 0; a < 8; ++a) B[a] = 0.0;
+  B[2 * 2 + 1] = dt;
+  B[3 * 2 + 0] = dt;
+  const double f[4] = {dt * v * cs, dt * v * sn, 0.0, 0.0};
+  for (int a = 0; a < 4; ++a) {
+    double acc = 0.0;
+    for (int k = 0; k < 4; ++k) acc += A[a * 4 + k] * sb[k];
+    c[a] = sb[a] + f[a] - acc;
+  }
+}
+
 static int n_pose_coords(const orc_problem* P) {
   return P->pose_model == ORC_POSE_TRANSLATION ? P->dim : P->dim + 1;
 }
@@ -599,8 +620,17 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
   double f[16], f2[16], H[256], h[16];
   int pidx[4];
   for (int a = 0; a < npc; ++a) pidx[a] = P->pose_idx[a];
+  /* dyn_model 1: this scene's LTV at the current iterate, computed before the update */
+  double* Lin = P->dyn_model ? (double*)malloc(sizeof(double) * N * (16 + 8 + 4)) : NULL;
   int rc = 0;
   for (int b = 0; b < P->n_scenes && rc == 0; ++b) {
+    if (Lin)
+      for (int t = 0; t < N; ++t)
+        unicycle_ltv(P->dt, I->s + ((long long)b * (N + 1) + t) * ns, Lin + t * 28, Lin + t * 28 + 16,
+                     Lin + t * 28 + 24);
+#define DYN_A(b_, t_) (Lin ? Lin + (t_) * 28 : dyn_ptr(P, P->dyn_A, b_, t_, ns * ns))
+#define DYN_B(b_, t_) (Lin ? Lin + (t_) * 28 + 16 : dyn_ptr(P, P->dyn_B, b_, t_, ns * nu))
+#define DYN_C(b_, t_) (Lin ? Lin + (t_) * 28 + 24 : dyn_ptr(P, P->dyn_c, b_, t_, ns))
     scene_aggregates(P, I, b, S, g);
     memset(Hc, 0, sizeof(double) * m * m);
     memset(gc, 0, sizeof(double) * m);
@@ -611,9 +641,9 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
     for (int a = 0; a < ns; ++a) f[a] = P->s0[b * ns + a];
     for (int t = 0; t < N; ++t) {
       /* propagate: s_{t+1} = A_t s_t + B_t u_t + c_t */
-      const double* At = dyn_ptr(P, P->dyn_A, b, t, ns * ns);
-      const double* Bt = dyn_ptr(P, P->dyn_B, b, t, ns * nu);
-      const double* ct = dyn_ptr(P, P->dyn_c, b, t, ns);
+      const double* At = DYN_A(b, t);
+      const double* Bt = DYN_B(b, t);
+      const double* ct = DYN_C(b, t);
       for (int a = 0; a < ns; ++a) {
         double acc = ct[a];
         for (int c = 0; c < ns; ++c) acc += At[a * ns + c] * f[c];
@@ -675,9 +705,9 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
     for (int t = 0; t < N; ++t) {
       double* ut = I->u + ((long long)b * N + t) * nu;
       for (int a = 0; a < nu; ++a) ut[a] = gc[t * nu + a];
-      const double* At = dyn_ptr(P, P->dyn_A, b, t, ns * ns);
-      const double* Bt = dyn_ptr(P, P->dyn_B, b, t, ns * nu);
-      const double* ct = dyn_ptr(P, P->dyn_c, b, t, ns);
+      const double* At = DYN_A(b, t);
+      const double* Bt = DYN_B(b, t);
+      const double* ct = DYN_C(b, t);
       for (int a = 0; a < ns; ++a) {
         double acc = ct[a];
         for (int c = 0; c < ns; ++c) acc += At[a * ns + c] * sb[t * ns + c];
@@ -686,7 +716,10 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
       }
     }
   }
-  free(S); free(g); free(F); free(F2); free(HF); free(Hc); free(gc);
+#undef DYN_A
+#undef DYN_B
+#undef DYN_C
+  free(S); free(g); free(F); free(F2); free(HF); free(Hc); free(gc); free(Lin);
   return rc;
 }
 

@@ -47,6 +47,12 @@ typedef struct {
    * per-timestep displacement of each obstacle (NEXT f3, moving traffic): obstacle j
    * at timestep t is O_j + t*step_j, i.e. C_j x <= d_j + t C_j step_j. */
   const double* obs_step;
+  /* 0: the LTV model dyn_A/B/c as given (reading #8).  1: the SE2 unicycle of the car
+   * scenes, s = (x, y, th, v), u = (a, om), s' = s + dt (v cos th, v sin th, om, a),
+   * relinearised at the current iterate (s^k, u^k) in every primal step -- the SQP
+   * step of P:272, P:349-351 (NEXT f2). */
+  int dyn_model;
+  double dt;
 } orc_problem;
 
 typedef struct {

@@ -41,6 +41,7 @@ CONFIG_NAMES = {
     4: "C4: dense traffic, ego car vs 100 vehicles, N=60, K=300",
     5: "C5: 4096 scenes x 200 obstacles x N=50, K=100",
     6: "C4m: C4 with moving traffic (vehicles at 12-18 m/s, NEXT f3), N=60, K=300",
+    7: "C2n: C2 with the unicycle relinearised at every ADMM iterate (SQP, NEXT f2), N=50, K=200",
 }
 
 
@@ -94,6 +95,9 @@ class Scene:
     # NEXT f3 (moving obstacles): None = static (reading #15), else [B*M, d] displacement
     # of each obstacle per timestep (obstacle j at timestep t is O_j + t*obs_step[j])
     obs_step: Optional[np.ndarray] = None
+    # 0: dyn_A/B/c as given; 1: the car's unicycle relinearised at every ADMM iterate
+    # (SQP step; NEXT f2) -- dyn_A/B/c then only seed nothing
+    dyn_model: int = 0
 
     @property
     def n_parts(self) -> int:
@@ -427,4 +431,6 @@ def make_c5(n_scenes: int | None = None, scene_ids: Sequence[int] | None = None)
 def make_config(cfg: int, **kw) -> Scene:
     if cfg == 6:
         return make_c4(moving=True, **kw)
+    if cfg == 7:
+        return dataclasses.replace(make_c2(**kw), name="C2n", config=7, dyn_model=1)
     return {1: make_c1, 2: make_c2, 3: make_c3, 4: make_c4, 5: make_c5}[cfg](**kw)
