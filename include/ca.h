@@ -111,6 +111,13 @@ typedef struct {
    * max_iters, tracing, basis recording) fall back to cudaMalloc. */
   void* workspace;
   size_t workspace_bytes;
+  /* NEXT f2: 0 = the LTV model dyn_A/B/c as given (reading #8); 1 = the car's unicycle,
+   * s = (x, y, th, v), u = (a, om), s' = s + dt (v cos th, v sin th, om, a), relinearised
+   * at the current iterate (s^k, u^k) in every primal step (the SQP step of P:272,
+   * P:349-351); requires n_state 4, n_ctrl 2, SE2 pose (0, 1, 2), dt > 0; dyn_A/B/c
+   * are then ignored (may be NULL). */
+  int32_t dyn_model;
+  double dt;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;

@@ -39,6 +39,7 @@ class Desc(C.Structure):
         ("lemke_pivot_tol", C.c_double), ("lemke_tie_tol", C.c_double), ("lemke_max_pivot_factor", C.c_int32),
         ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+        ("dyn_model", C.c_int32), ("dt", C.c_double),
     ]
 
 
@@ -161,6 +162,7 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
     D.prox_eps = prox_eps
     step = getattr(sc, "obs_step", None)
     D.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
+    D.dyn_model, D.dt = int(getattr(sc, "dyn_model", 0)), float(sc.dt)
     return D
 
 

@@ -184,9 +184,14 @@ ca_status validate(const ca_problem_desc* D) {
   if (D->n_scenes <= 0 || D->horizon <= 0 || D->n_state <= 0 || D->n_ctrl <= 0 || D->n_parts <= 0 ||
       D->n_obs < 0)
     return fail(CA_E_INVALID, "non-positive size");
-  if (!D->part_off || !D->part_A || !D->part_b || !D->dyn_A || !D->dyn_B || !D->dyn_c || !D->Qs || !D->Qu ||
-      !D->s0 || !D->s_ref)
+  if (!D->part_off || !D->part_A || !D->part_b || !D->Qs || !D->Qu || !D->s0 || !D->s_ref)
     return fail(CA_E_INVALID, "NULL input array");
+  if (D->dyn_model == 0 && (!D->dyn_A || !D->dyn_B || !D->dyn_c)) return fail(CA_E_INVALID, "NULL dynamics array");
+  if (D->dyn_model != 0 && D->dyn_model != 1) return fail(CA_E_UNSUPPORTED, "unknown dyn_model");
+  if (D->dyn_model == 1 &&
+      (D->n_state != 4 || D->n_ctrl != 2 || D->pose_model != CA_POSE_SE2 || D->pose_idx[0] != 0 ||
+       D->pose_idx[1] != 1 || D->pose_idx[2] != 2 || !(D->dt > 0.0)))
+    return fail(CA_E_INVALID, "dyn_model 1 (unicycle): n_state 4, n_ctrl 2, SE2 pose (0, 1, 2), dt > 0");
   if (D->n_obs > 0 && (!D->obs_off || !D->obs_C || !D->obs_d)) return fail(CA_E_INVALID, "NULL obstacle array");
   if (!(D->sigma > 0.0)) return fail(CA_E_INVALID, "sigma must be > 0");
   if (D->prox_eps != 0.0) return fail(CA_E_UNSUPPORTED, "prox_eps > 0 (reading #2) is oracle-only in this build");
@@ -296,9 +301,11 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
     }
   }
   const long long nd = (long long)(D->dyn_per_scene ? B : 1) * (D->dyn_per_time ? N : 1);
-  if ((st = h2d(h, const_cast<double*>(v.dynA), D->dyn_A, (size_t)nd * ns * ns))) return st;
-  if ((st = h2d(h, const_cast<double*>(v.dynB), D->dyn_B, (size_t)nd * ns * nu))) return st;
-  if ((st = h2d(h, const_cast<double*>(v.dync), D->dyn_c, (size_t)nd * ns))) return st;
+  if (!D->dyn_model) {  // dyn_model 1: written by k_relin_unicycle every primal step
+    if ((st = h2d(h, const_cast<double*>(v.dynA), D->dyn_A, (size_t)nd * ns * ns))) return st;
+    if ((st = h2d(h, const_cast<double*>(v.dynB), D->dyn_B, (size_t)nd * ns * nu))) return st;
+    if ((st = h2d(h, const_cast<double*>(v.dync), D->dyn_c, (size_t)nd * ns))) return st;
+  }
   if ((st = h2d(h, const_cast<double*>(v.Qs), D->Qs, (size_t)ns * ns))) return st;
   if ((st = h2d(h, const_cast<double*>(v.Qu), D->Qu, (size_t)nu * nu))) return st;
   if ((st = h2d(h, const_cast<double*>(v.s0), D->s0, (size_t)B * ns))) return st;
@@ -437,6 +444,12 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
   ca_status st;
+  if (h->dev.dyn_model == 1) {  // SQP step: linearise the unicycle at the current iterate
+    const long long nq = (long long)h->B * h->N;
+    ca::k_relin_unicycle<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev);
+    CUDA_TRY(cudaGetLastError());
+    h->launches[1]++;
+  }
   const double* recs = h->dev.agg;
   int nchunk = h->dev.nchunkG;
   if (h->comm) {
@@ -603,8 +616,10 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   v.pose_model = D->pose_model;
   v.npc = (D->pose_model == CA_POSE_TRANSLATION) ? h->d : h->d + 1;
   for (int a = 0; a < 4; ++a) v.pidx[a] = D->pose_idx[a];
-  v.dyn_ps = D->dyn_per_scene ? 1 : 0;
-  v.dyn_pt = D->dyn_per_time ? 1 : 0;
+  v.dyn_ps = (D->dyn_per_scene || D->dyn_model) ? 1 : 0;  // relinearised: one block per (scene, t)
+  v.dyn_pt = (D->dyn_per_time || D->dyn_model) ? 1 : 0;
+  v.dyn_model = D->dyn_model;
+  v.dt = D->dt;
   v.sigma = D->sigma;
   v.lp.pivot_tol = D->lemke_pivot_tol > 0 ? D->lemke_pivot_tol : 1e-11;
   v.lp.tie_tol = D->lemke_tie_tol > 0 ? D->lemke_tie_tol : 1e-9;
@@ -630,7 +645,7 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   h->eps_dual = D->eps_dual;
   h->max_iters = D->max_iters > 0 ? D->max_iters : 100;
   const int d = h->d, B = h->B, N = h->N, ns = h->ns, nu = h->nu;
-  const long long nd = (long long)(D->dyn_per_scene ? B : 1) * (D->dyn_per_time ? N : 1);
+  const long long nd = (long long)(v.dyn_ps ? B : 1) * (v.dyn_pt ? N : 1);  // device layout
   const long long orow = (h->M > 0) ? D->obs_off[(long long)B * h->M] : 0;
   ca_status st;
 #define AL(ptr, T, cnt)                          \
@@ -769,6 +784,9 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
     return fail(CA_E_INVALID, "ca_problem_load: shapes differ from the handle");
   for (int i = 0; i <= h->np; ++i)
     if (D->part_off[i] != h->part_off[i]) return fail(CA_E_INVALID, "ca_problem_load: robot part rows differ");
+  if (D->dyn_model != h->dev.dyn_model ||
+      (!D->dyn_model && ((D->dyn_per_scene ? 1 : 0) != h->dev.dyn_ps || (D->dyn_per_time ? 1 : 0) != h->dev.dyn_pt)))
+    return fail(CA_E_INVALID, "ca_problem_load: dynamics model / layout differs from the handle");
   for (long long o = 0; o < (long long)h->B * h->M; ++o)
     if (D->obs_off[o + 1] - D->obs_off[o] != h->obs_counts[o])
       return fail(CA_E_INVALID, "ca_problem_load: obstacle row counts differ");

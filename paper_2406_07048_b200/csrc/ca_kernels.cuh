@@ -73,6 +73,8 @@ struct Dev {
   int TG, NG, GG, nchunkG, CHG;  // CHG: lanes used per chunk (balanced)
   int nitems;        // B*NG*nchunkG work items of one sweep
   const double* obs_step;  // NULL or [B*M][d]: per-timestep obstacle displacement (NEXT f3)
+  int dyn_model;           // 1: unicycle relinearised every primal step (NEXT f2)
+  double dt;
   double* obs_vert;  // d = 2: vertices of every obstacle polygon, [obs row][2] (k_vertices2d)
   int* obs_nv;       //        vertex count per obstacle
   double* part_vert; // d = 2: robot-part vertices (body frame), [part row][2]
@@ -866,6 +868,36 @@ __device__ __forceinline__ bool solve_sq(double A[D + 1][D + 2], double x[D + 1]
 }
 
 #ifdef CA_COMMON_KERNELS
+// NEXT f2 (dyn_model 1): the car's unicycle linearised at the current iterate s^k_t,
+// one thread per (scene, t) -- the SQP step of P:272; same operation
+// order as the oracle's unicycle_ltv.  Writes the per-(scene, t) dynamics blocks.
+__global__ void k_relin_unicycle(Dev P) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + t
+  if (q >= (long long)P.B * P.N) return;
+  const int b = (int)(q / P.N), t = (int)(q % P.N);
+  const double* sb = P.s + ((long long)b * (P.N + 1) + t) * 4;
+  const double dt = P.dt, th = sb[2], v = sb[3], cs = cos(th), sn = sin(th);
+  double A[16];
+  for (int a = 0; a < 16; ++a) A[a] = (a % 5 == 0) ? 1.0 : 0.0;
+  A[0 * 4 + 2] += -dt * v * sn;
+  A[0 * 4 + 3] += dt * cs;
+  A[1 * 4 + 2] += dt * v * cs;
+  A[1 * 4 + 3] += dt * sn;
+  double* Ao = const_cast<double*>(P.dynA) + q * 16;
+  double* Bo = const_cast<double*>(P.dynB) + q * 8;
+  double* co = const_cast<double*>(P.dync) + q * 4;
+  for (int a = 0; a < 16; ++a) Ao[a] = A[a];
+  for (int a = 0; a < 8; ++a) Bo[a] = 0.0;
+  Bo[2 * 2 + 1] = dt;
+  Bo[3 * 2 + 0] = dt;
+  const double f[4] = {dt * v * cs, dt * v * sn, 0.0, 0.0};
+  for (int a = 0; a < 4; ++a) {
+    double acc = 0.0;
+    for (int k = 0; k < 4; ++k) acc += A[a * 4 + k] * sb[k];
+    co[a] = sb[a] + f[a] - acc;
+  }
+}
+
 // 2-D polygon vertices from the H-representation (once per load): pairwise facet
 // intersections that satisfy every facet (1e-9 relative), de-duplicated.  rows use
 // the [r][4] = (n_0, n_1, -, offset) layout of part_rows / obs_rows.

@@ -29,9 +29,11 @@ def c4m_short():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["c2", "c4m"])
+@pytest.mark.parametrize("case", ["c2", "c4m", "c2n"])
 def test_closed_loop_gpu_equals_oracle(case):
-    sc, K, speed, steps = (scenes.make_config(2), 40, 3.0, 5) if case == "c2" else (c4m_short(), 30, 20.0, 3)
+    """c2n: the unicycle relinearised at every ADMM iterate inside each MPC solve."""
+    sc, K, speed, steps = {"c2": (scenes.make_config(2), 40, 3.0, 5), "c4m": (c4m_short(), 30, 20.0, 3),
+                           "c2n": (scenes.make_config(7), 40, 3.0, 5)}[case]
     runs = {}
     for backend in ("gpu", "oracle"):
         loop = mpc.RecedingHorizon(sc, K=K, speed=speed, solver=None if backend == "gpu" else OracleSolver())

@@ -70,7 +70,7 @@ def test_t1_dual_sweep(ca, cfg, k0):
     assert np.array_equal(st["zeta"], zeta) and np.array_equal(st["xi"], xi)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7])
 def test_t1_primal_and_multiplier(ca, cfg):
     sc = scene(cfg)
     o = warm(sc, 3)
@@ -78,6 +78,7 @@ def test_t1_primal_and_multiplier(ca, cfg):
     g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
     g.dual_sweep()
     o.dual_sweep()
+    s_lin = o.s.copy()  # dyn_model 1 linearises here
     g.primal_step()
     o.primal_step()
     s, u = g.trajectory()
@@ -92,14 +93,18 @@ def test_t1_primal_and_multiplier(ca, cfg):
     close(r.r_pri, rp.sum(), 1e-8, "r_pri")
     # dynamics hold exactly (Eq. 13b)
     sc0 = sc
+    if sc0.dyn_model == 1:  # the unicycle linearised at the pre-step iterate
+        dA, dB, dc = scenes.unicycle_ltv(s_lin[0, :sc0.horizon], sc0.dt)
     for t in range(sc0.horizon):
-        nt = sc0.horizon if sc0.dyn_per_time else 1
         k = t if sc0.dyn_per_time else 0
-        A, B, c = sc0.dyn_A[k], sc0.dyn_B[k], sc0.dyn_c[k]
+        if sc0.dyn_model == 1:
+            A, B, c = dA[t], dB[t], dc[t]
+        else:
+            A, B, c = sc0.dyn_A[k], sc0.dyn_B[k], sc0.dyn_c[k]
         assert np.abs(s[0, t + 1] - (A @ s[0, t] + B @ u[0, t] + c)).max() <= 1e-12 * (1 + np.abs(s).max())
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7])
 def test_t2_full_iterations(ca, cfg):
     sc = scene(cfg)
     K = sc.iters
