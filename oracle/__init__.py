@@ -51,6 +51,7 @@ def lib():
                                         dp, C.c_double, dp, C.c_double, C.c_double, C.c_int, dp, ip, ip]
         _lib.orc_pair_solve.restype = C.c_int
         _lib.orc_init_iterate.argtypes = [C.c_void_p, C.c_void_p]
+        _lib.orc_reset_box.argtypes = [C.c_void_p, C.c_void_p]
         _lib.orc_dual_sweep.argtypes = [C.c_void_p, C.c_void_p, dp]
         _lib.orc_dual_sweep.restype = C.c_longlong
         _lib.orc_primal_step.argtypes = [C.c_void_p, C.c_void_p]
@@ -91,12 +92,16 @@ class _Problem(C.Structure):
         ("sigma", C.c_double), ("pivot_tol", C.c_double), ("tie_tol", C.c_double),
         ("max_pivot_factor", C.c_int), ("ny", C.c_int), ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
         ("dyn_model", C.c_int), ("dt", C.c_double),
+        ("s_min", C.c_void_p), ("s_max", C.c_void_p), ("u_min", C.c_void_p), ("u_max", C.c_void_p),
+        ("box_rho", C.c_double),
     ]
 
 
 class _Iterate(C.Structure):
     _fields_ = [("s", C.c_void_p), ("u", C.c_void_p), ("y", C.c_void_p), ("zeta", C.c_void_p),
-                ("xi", C.c_void_p), ("pivots", C.c_void_p), ("status", C.c_void_p)]
+                ("xi", C.c_void_p), ("pivots", C.c_void_p), ("status", C.c_void_p),
+                ("ws", C.c_void_p), ("ls", C.c_void_p), ("wu", C.c_void_p), ("lu", C.c_void_p),
+                ("boxres", C.c_void_p)]
 
 
 class Oracle:
@@ -137,6 +142,10 @@ class Oracle:
         step = getattr(sc, "obs_step", None)  # NEXT f3: moving obstacles (None = static)
         P.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
         P.dyn_model, P.dt = int(getattr(sc, "dyn_model", 0)), float(sc.dt)  # NEXT f2: SQP relinearisation
+        for name, n in (("s_min", sc.n_state), ("s_max", sc.n_state), ("u_min", sc.n_ctrl), ("u_max", sc.n_ctrl)):
+            v = getattr(sc, name, None)  # NEXT f1: boxes of Eq. 13c-d (None = unbounded)
+            setattr(P, name, None if v is None else k(name, _f64(v).reshape(n)))
+        P.box_rho = float(getattr(sc, "box_rho", 0.0))
         self.ny = P.ny = sc.n_max if sc.n_obs > 0 else 1
         self.P = P
         B, N, ns, nu, d = sc.n_scenes, sc.horizon, sc.n_state, sc.n_ctrl, sc.dim
@@ -148,10 +157,15 @@ class Oracle:
         self.xi = np.zeros((max(npair, 1), d))
         self.pivots = np.zeros(max(npair, 1), np.int32)
         self.status = np.zeros(max(npair, 1), np.int32)
+        self.ws, self.ls = np.zeros((B, N + 1, ns)), np.zeros((B, N + 1, ns))  # box block (reading #22)
+        self.wu, self.lu = np.zeros((B, N, nu)), np.zeros((B, N, nu))
+        self.boxres = np.zeros(B)
         It = _Iterate()
         It.s, It.u, It.y = self.s.ctypes.data, self.u.ctypes.data, self.y.ctypes.data
         It.zeta, It.xi = self.zeta.ctypes.data, self.xi.ctypes.data
         It.pivots, It.status = self.pivots.ctypes.data, self.status.ctypes.data
+        It.ws, It.ls, It.wu, It.lu = (a.ctypes.data for a in (self.ws, self.ls, self.wu, self.lu))
+        It.boxres = self.boxres.ctypes.data
         self.I = It
         self.init_iterate()
 
@@ -165,6 +179,7 @@ class Oracle:
         for name, val in (("s", s), ("u", u), ("y", y), ("zeta", zeta), ("xi", xi)):
             if val is not None:
                 getattr(self, name)[...] = np.asarray(val, np.float64).reshape(getattr(self, name).shape)
+        lib().orc_reset_box(*self._pp())  # w = Pi_box(s, u), l = 0 (reading #22)
 
     def dual_sweep(self):
         rd = np.zeros(self.sc.n_scenes)

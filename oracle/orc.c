@@ -21,6 +21,9 @@
  *   orc_primal_step    zero-obstacle step == dense KKT LQ solve (numpy);
  *                      GN gradient/Hessian vs finite differences
  *   orc_multiplier_update  identity zeta+ - zeta = T (Eq. 10) recomputed in numpy
+ *   box block (f1)     zero-obstacle fixed point == box-constrained LQ optimum
+ *                      (scipy lsq_linear; KKT certificate with state bounds);
+ *                      infinite bounds == no bounds, bitwise
  *   whole ADMM         translation equivariance, obstacle-permutation invariance
  *   Lemke's choice among non-unique QP minimisers: parity unpinned (only the
  *   rules L1-L7 of DESIGN.md reading #4 define it).
@@ -441,16 +444,61 @@ static int n_pose_coords(const orc_problem* P) {
 
 /* O1 initial iterate (reading #11): s_0 fixed, s_t = s_ref_t, u = 0,
  * lambda = 1/sum(b_i) 1 (so b_i^T lambda = 1), mu = 0, gamma = 0, zeta = xi = 0. */
+/* ---------------------------------------------------------------------------
+ * Box block of IC_0 (Eq. 13c-d; reading #22, NEXT f1).  The boxes are
+ * handled by one more ADMM block: a copy w of every bounded state (t = 1..N) and
+ * control, the consensus constraint x = w with scaled multiplier l and penalty
+ * rho_b.  The primal step (Eq. 16) gains (rho_b/2) ||x - w^k + l^k||^2 and is
+ * followed by  w^{k+1} = Pi_box(x^{k+1} + l^k),  l^{k+1} = l^k + x^{k+1} - w^{k+1}
+ * (the scaled-form ADMM of P:283-320's reference [boyd2011distributed]).
+ * ------------------------------------------------------------------------- */
+static int has_box(const orc_problem* P) { return P->s_min || P->s_max || P->u_min || P->u_max; }
+static double box_lo(const double* v, int a) { return v ? v[a] : -INFINITY; }
+static double box_hi(const double* v, int a) { return v ? v[a] : INFINITY; }
+/* 1 if component a has a finite bound on either side */
+static int box_on(const double* lo, const double* hi, int a) {
+  return box_lo(lo, a) > -INFINITY || box_hi(hi, a) < INFINITY;
+}
+/* projection onto [lo, hi] */
+static double clip(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* w = Pi_box(s, u), l = 0, boxres = 0 (after an initial or user-set iterate) */
+void orc_reset_box(const orc_problem* P, orc_iterate* I) {
+  if (!has_box(P)) return;
+  int B = P->n_scenes, N = P->horizon, ns = P->n_state, nu = P->n_ctrl;
+  for (int b = 0; b < B; ++b) {
+    for (int t = 0; t <= N; ++t)
+      for (int a = 0; a < ns; ++a) {
+        long long k = ((long long)b * (N + 1) + t) * ns + a;
+        I->ws[k] = clip(I->s[k], box_lo(P->s_min, a), box_hi(P->s_max, a));
+        I->ls[k] = 0.0;
+      }
+    for (int t = 0; t < N; ++t)
+      for (int a = 0; a < nu; ++a) {
+        long long k = ((long long)b * N + t) * nu + a;
+        I->wu[k] = clip(I->u[k], box_lo(P->u_min, a), box_hi(P->u_max, a));
+        I->lu[k] = 0.0;
+      }
+    I->boxres[b] = 0.0;
+  }
+}
+
+/* Cold start (reading #11): states from the reference (clipped to the box),
+ * controls zero (clipped), certificates lambda = 1/sum(b_i), mu = gamma = 0, zeta = xi = 0. */
 void orc_init_iterate(const orc_problem* P, orc_iterate* I) {
   int B = P->n_scenes, N = P->horizon, ns = P->n_state, nu = P->n_ctrl, d = P->dim;
   for (int b = 0; b < B; ++b) {
     for (int t = 0; t <= N; ++t)
       for (int a = 0; a < ns; ++a)
         I->s[((long long)b * (N + 1) + t) * ns + a] =
-            (t == 0) ? P->s0[b * ns + a] : P->s_ref[((long long)b * (N + 1) + t) * ns + a];
+            (t == 0) ? P->s0[b * ns + a]
+                     : clip(P->s_ref[((long long)b * (N + 1) + t) * ns + a], box_lo(P->s_min, a),
+                            box_hi(P->s_max, a));
     for (int t = 0; t < N; ++t)
-      for (int a = 0; a < nu; ++a) I->u[((long long)b * N + t) * nu + a] = 0.0;
+      for (int a = 0; a < nu; ++a)
+        I->u[((long long)b * N + t) * nu + a] = clip(0.0, box_lo(P->u_min, a), box_hi(P->u_max, a));
   }
+  orc_reset_box(P, I);
   long long np = n_pairs(P);
   for (long long p = 0; p < np; ++p) {
     int i = (int)((p / P->n_obs) % P->n_parts);
@@ -610,6 +658,8 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
   int N = P->horizon, ns = P->n_state, nu = P->n_ctrl, npc = n_pose_coords(P);
   int m = N * nu;
   double sig = P->sigma;
+  const int box = has_box(P);
+  const double rb = P->box_rho;
   double* S = (double*)malloc(sizeof(double) * N * npc * npc);
   double* g = (double*)malloc(sizeof(double) * N * npc);
   double* F = (double*)malloc(sizeof(double) * ns * m);   /* s_t = F U + f */
@@ -637,6 +687,14 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
     for (int t = 0; t < N; ++t)
       for (int a = 0; a < nu; ++a)
         for (int c = 0; c < nu; ++c) Hc[(t * nu + a) * m + t * nu + c] += 2.0 * P->Qu[a * nu + c];
+    if (box) /* control part of (rho_b/2) ||u - w + l||^2: Hessian rho_b, gradient -rho_b (w - l) */
+      for (int t = 0; t < N; ++t)
+        for (int a = 0; a < nu; ++a)
+          if (box_on(P->u_min, P->u_max, a)) {
+            long long k = ((long long)b * N + t) * nu + a;
+            Hc[(t * nu + a) * m + t * nu + a] += rb;
+            gc[t * nu + a] += -rb * (I->wu[k] - I->lu[k]);
+          }
     memset(F, 0, sizeof(double) * ns * m);
     for (int a = 0; a < ns; ++a) f[a] = P->s0[b * ns + a];
     for (int t = 0; t < N; ++t) {
@@ -678,6 +736,13 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
         }
         h[pidx[a]] += sig * sp;
       }
+      if (box) /* state part of (rho_b/2) ||s_t - w_t + l_t||^2 */
+        for (int a = 0; a < ns; ++a)
+          if (box_on(P->s_min, P->s_max, a)) {
+            long long k = ((long long)b * (N + 1) + tt) * ns + a;
+            H[a * ns + a] += rb;
+            h[a] += -rb * (I->ws[k] - I->ls[k]);
+          }
       /* Hc += F^T H F, gc += F^T (H f + h) */
       for (int a = 0; a < ns; ++a)
         for (int col = 0; col < m; ++col) {
@@ -714,6 +779,30 @@ int orc_primal_step(const orc_problem* P, orc_iterate* I) {
         for (int c = 0; c < nu; ++c) acc += Bt[a * nu + c] * ut[c];
         sb[(t + 1) * ns + a] = acc;
       }
+    }
+    if (box) { /* w^{k+1} = Pi_box(x^{k+1} + l^k), l^{k+1} = l^k + x^{k+1} - w^{k+1} */
+      double res = 0.0;
+      for (int t = 0; t < N; ++t) {
+        for (int a = 0; a < nu; ++a) {
+          if (!box_on(P->u_min, P->u_max, a)) continue;
+          long long k = ((long long)b * N + t) * nu + a;
+          double x = I->u[k];
+          double w = clip(x + I->lu[k], box_lo(P->u_min, a), box_hi(P->u_max, a));
+          I->lu[k] = I->lu[k] + (x - w);
+          I->wu[k] = w;
+          res += (x - w) * (x - w);
+        }
+        for (int a = 0; a < ns; ++a) {
+          if (!box_on(P->s_min, P->s_max, a)) continue;
+          long long k = ((long long)b * (N + 1) + t + 1) * ns + a;
+          double x = I->s[k];
+          double w = clip(x + I->ls[k], box_lo(P->s_min, a), box_hi(P->s_max, a));
+          I->ls[k] = I->ls[k] + (x - w);
+          I->ws[k] = w;
+          res += (x - w) * (x - w);
+        }
+      }
+      I->boxres[b] = res;
     }
   }
 #undef DYN_A
@@ -771,6 +860,9 @@ void orc_multiplier_update(const orc_problem* P, orc_iterate* I, double* rpri) {
     }
     rpri[b] += r2;
   }
+  /* box block (reading #22): its primal residual ||x - w||^2 joins Eq. 18a's sum */
+  if (has_box(P))
+    for (int b = 0; b < P->n_scenes; ++b) rpri[b] += I->boxres[b];
 }
 
 /* ---------------------------------------------------------------------------

@@ -42,6 +42,7 @@ CONFIG_NAMES = {
     5: "C5: 4096 scenes x 200 obstacles x N=50, K=100",
     6: "C4m: C4 with moving traffic (vehicles at 12-18 m/s, NEXT f3), N=60, K=300",
     7: "C2n: C2 with the unicycle relinearised at every ADMM iterate (SQP, NEXT f2), N=50, K=200",
+    8: "C2b: C2 with state/control boxes (|a| <= 0.5, |om| <= 1.5, 2.5 <= v <= 3.5; NEXT f1), N=50, K=200",
 }
 
 
@@ -98,6 +99,13 @@ class Scene:
     # 0: dyn_A/B/c as given; 1: the car's unicycle relinearised at every ADMM iterate
     # (SQP step; NEXT f2) -- dyn_A/B/c then only seed nothing
     dyn_model: int = 0
+    # NEXT f1: state / control boxes of Eq. 13c-d; None = unbounded, else
+    # [n_state] / [n_ctrl] (+-inf entries allowed); box_rho = penalty of the box block
+    s_min: Optional[np.ndarray] = None
+    s_max: Optional[np.ndarray] = None
+    u_min: Optional[np.ndarray] = None
+    u_max: Optional[np.ndarray] = None
+    box_rho: float = 0.0
 
     @property
     def n_parts(self) -> int:
@@ -433,4 +441,9 @@ def make_config(cfg: int, **kw) -> Scene:
         return make_c4(moving=True, **kw)
     if cfg == 7:
         return dataclasses.replace(make_c2(**kw), name="C2n", config=7, dyn_model=1)
+    if cfg == 8:
+        inf = np.inf
+        return dataclasses.replace(make_c2(**kw), name="C2b", config=8, s_min=np.array([-inf, -inf, -1.2, 2.5]),
+                                   s_max=np.array([inf, inf, 1.2, 3.5]), u_min=np.array([-0.5, -1.5]),
+                                   u_max=np.array([0.5, 1.5]), box_rho=3.0)
     return {1: make_c1, 2: make_c2, 3: make_c3, 4: make_c4, 5: make_c5}[cfg](**kw)
