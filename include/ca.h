@@ -118,6 +118,20 @@ typedef struct {
    * are then ignored (may be NULL). */
   int32_t dyn_model;
   double dt;
+  /* NEXT f1: the state / control boxes of Eq. 13c-d, part of IC_0 in the
+   * primal step.  Each nullable HOST array (NULL = unbounded on that side):
+   * s_min/s_max[n_state], u_min/u_max[n_ctrl], shared by every scene and timestep;
+   * +-inf entries leave a component free.  The state box applies to t = 1..N (s_0 is
+   * given).  Handled by an extra ADMM block (reading #7): a copy w of every bounded
+   * component constrained to the box, consensus x = w with scaled multiplier l and
+   * penalty box_rho (> 0 when any bound is finite); r_pri (Eq. 18a) then also sums
+   * ||x - w||^2.  The cold-start iterate is projected into the box;
+   * ca_set_iterate resets w = Pi_box(x), l = 0.  min > max or NaN -> CA_E_INVALID. */
+  const double* s_min;
+  const double* s_max;
+  const double* u_min;
+  const double* u_max;
+  double box_rho;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;
@@ -213,9 +227,15 @@ ca_status ca_get_trajectory(ca_problem* h, double* s, double* u);
 ca_status ca_get_pair_state(ca_problem* h, int64_t p0, int64_t count, double* y, double* zeta,
                             double* xi, int32_t* pivots, int32_t* status, uint32_t* zmask);
 
-/* Overwrite the iterate (any pointer may be NULL = keep).  Layouts as the getters. */
+/* Overwrite the iterate (any pointer may be NULL = keep).  Layouts as the getters.
+ * With boxes (NEXT f1) the box block restarts from w = Pi_box(s, u), l = 0. */
 ca_status ca_set_iterate(ca_problem* h, const double* s, const double* u, const double* y,
                          const double* zeta, const double* xi);
+
+/* Box block state (NEXT f1, reading #7) into HOST arrays (any may be NULL): w_s, l_s
+ * [B][N+1][ns] (t = 0 entries are Pi_box(s_0), 0), w_u, l_u [B][N][nu], res[B] =
+ * sum ||x - w||^2 after the last primal step.  CA_E_INVALID if the problem has no box. */
+ca_status ca_get_box_state(ca_problem* h, double* w_s, double* l_s, double* w_u, double* l_u, double* res);
 
 /* Device milliseconds accumulated per kernel family since the last reset (CUDA
  * events on the handle's stream, only while ca_set_timing(h, 1)): ms[0] pair

@@ -157,7 +157,7 @@ class Oracle:
         self.xi = np.zeros((max(npair, 1), d))
         self.pivots = np.zeros(max(npair, 1), np.int32)
         self.status = np.zeros(max(npair, 1), np.int32)
-        self.ws, self.ls = np.zeros((B, N + 1, ns)), np.zeros((B, N + 1, ns))  # box block (reading #22)
+        self.ws, self.ls = np.zeros((B, N + 1, ns)), np.zeros((B, N + 1, ns))  # box block (reading #7)
         self.wu, self.lu = np.zeros((B, N, nu)), np.zeros((B, N, nu))
         self.boxres = np.zeros(B)
         It = _Iterate()
@@ -179,7 +179,7 @@ class Oracle:
         for name, val in (("s", s), ("u", u), ("y", y), ("zeta", zeta), ("xi", xi)):
             if val is not None:
                 getattr(self, name)[...] = np.asarray(val, np.float64).reshape(getattr(self, name).shape)
-        lib().orc_reset_box(*self._pp())  # w = Pi_box(s, u), l = 0 (reading #22)
+        lib().orc_reset_box(*self._pp())  # w = Pi_box(s, u), l = 0 (reading #7)
 
     def dual_sweep(self):
         rd = np.zeros(self.sc.n_scenes)

@@ -445,7 +445,7 @@ static int n_pose_coords(const orc_problem* P) {
 /* O1 initial iterate (reading #11): s_0 fixed, s_t = s_ref_t, u = 0,
  * lambda = 1/sum(b_i) 1 (so b_i^T lambda = 1), mu = 0, gamma = 0, zeta = xi = 0. */
 /* ---------------------------------------------------------------------------
- * Box block of IC_0 (Eq. 13c-d; reading #22, NEXT f1).  The boxes are
+ * Box block of IC_0 (Eq. 13c-d; reading #7, NEXT f1).  The boxes are
  * handled by one more ADMM block: a copy w of every bounded state (t = 1..N) and
  * control, the consensus constraint x = w with scaled multiplier l and penalty
  * rho_b.  The primal step (Eq. 16) gains (rho_b/2) ||x - w^k + l^k||^2 and is
@@ -860,7 +860,7 @@ void orc_multiplier_update(const orc_problem* P, orc_iterate* I, double* rpri) {
     }
     rpri[b] += r2;
   }
-  /* box block (reading #22): its primal residual ||x - w||^2 joins Eq. 18a's sum */
+  /* box block (reading #7): its primal residual ||x - w||^2 joins Eq. 18a's sum */
   if (has_box(P))
     for (int b = 0; b < P->n_scenes; ++b) rpri[b] += I->boxres[b];
 }

@@ -56,7 +56,7 @@ typedef struct {
   /* State / control boxes of Eq. 13c-d, part of IC_0 -- NEXT f1.
    * NULL = unbounded in that direction; else [n_state] / [n_ctrl], shared by every scene
    * and timestep (s_0 is given, so the state box applies to t = 1..N).  Handled by an
-   * extra ADMM block (reading #22): consensus x = w with w in the box, scaled multiplier
+   * extra ADMM block (reading #7): consensus x = w with w in the box, scaled multiplier
    * l, penalty box_rho > 0. */
   const double* s_min;
   const double* s_max;
@@ -73,7 +73,7 @@ typedef struct {
   double* xi;   /* [P][d]       */
   int* pivots;  /* [P] pivots of the last dual sweep */
   int* status;  /* [P] ORC_* of the last dual sweep */
-  /* box block (reading #22), used only when the problem has a box: */
+  /* box block (reading #7), used only when the problem has a box: */
   double* ws;     /* [B][N+1][ns] w for the states (t = 0 unused) */
   double* ls;     /* [B][N+1][ns] scaled multiplier l for the states */
   double* wu;     /* [B][N][nu]  w for the controls */

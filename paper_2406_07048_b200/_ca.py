@@ -40,6 +40,8 @@ class Desc(C.Structure):
         ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("dyn_model", C.c_int32), ("dt", C.c_double),
+        ("s_min", C.c_void_p), ("s_max", C.c_void_p), ("u_min", C.c_void_p), ("u_max", C.c_void_p),
+        ("box_rho", C.c_double),
     ]
 
 
@@ -88,6 +90,7 @@ def lib():
         L.ca_get_trajectory.argtypes = [vp, vp, vp]
         L.ca_get_pair_state.argtypes = [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp, vp]
         L.ca_set_iterate.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.ca_get_box_state.argtypes = [vp, vp, vp, vp, vp, vp]
         L.ca_kernel_times.argtypes = [vp, dp, i64p, C.c_int32]
         L.ca_set_timing.argtypes = [vp, C.c_int32]
         L.ca_set_record_basis.argtypes = [vp, C.c_int32]
@@ -103,7 +106,8 @@ def lib():
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
                      "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace",
-                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size"):
+                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size",
+                     "ca_get_box_state"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib
@@ -163,6 +167,10 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
     step = getattr(sc, "obs_step", None)
     D.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
     D.dyn_model, D.dt = int(getattr(sc, "dyn_model", 0)), float(sc.dt)
+    for name, n in (("s_min", sc.n_state), ("s_max", sc.n_state), ("u_min", sc.n_ctrl), ("u_max", sc.n_ctrl)):
+        v = getattr(sc, name, None)  # NEXT f1 boxes (None = unbounded)
+        setattr(D, name, None if v is None else k(name, _f64(v).reshape(n)))
+    D.box_rho = float(getattr(sc, "box_rho", 0.0))
     return D
 
 
@@ -295,6 +303,15 @@ class Problem:
         if arrs[2] is not None:
             assert arrs[2].shape == (self.n_pairs, self.ny), arrs[2].shape
         _check(lib().ca_set_iterate(self.h, *[_ptr(a) for a in arrs]))
+
+    def box_state(self):
+        """(w_s, l_s, w_u, l_u, res) of the box block (NEXT f1)."""
+        sc = self.sc
+        ws, ls = np.empty((sc.n_scenes, sc.horizon + 1, sc.n_state)), np.empty((sc.n_scenes, sc.horizon + 1, sc.n_state))
+        wu, lu = np.empty((sc.n_scenes, sc.horizon, sc.n_ctrl)), np.empty((sc.n_scenes, sc.horizon, sc.n_ctrl))
+        res = np.empty(sc.n_scenes)
+        _check(lib().ca_get_box_state(self.h, *[_ptr(a) for a in (ws, ls, wu, lu, res)]))
+        return ws, ls, wu, lu, res
 
     def debug_trace(self, p: int = -1):
         out = np.empty((64, 48))

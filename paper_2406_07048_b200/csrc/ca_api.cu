@@ -230,6 +230,22 @@ ca_status validate(const ca_problem_desc* D) {
     for (long long k = 0; k < (long long)D->n_scenes * D->n_obs * d; ++k)
       if (!std::isfinite(D->obs_step[k])) return fail(CA_E_INVALID, "obs_step must be finite");
   if (!spd(D->Qs, D->n_state) || !spd(D->Qu, D->n_ctrl)) return fail(CA_E_INVALID, "Qs/Qu must be SPD");
+  if (D->s_min || D->s_max || D->u_min || D->u_max) {  // NEXT f1 boxes
+    bool finite = false;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int n = pass ? D->n_ctrl : D->n_state;
+      const double* lo = pass ? D->u_min : D->s_min;
+      const double* hi = pass ? D->u_max : D->s_max;
+      for (int a = 0; a < n; ++a) {
+        const double l = lo ? lo[a] : -INFINITY, u = hi ? hi[a] : INFINITY;
+        if (std::isnan(l) || std::isnan(u) || l > u || l == INFINITY || u == -INFINITY)
+          return fail(CA_E_INVALID, "box bounds must satisfy min <= max (no NaN, no empty side)");
+        finite = finite || std::isfinite(l) || std::isfinite(u);
+      }
+    }
+    if (finite && !(D->box_rho > 0.0 && std::isfinite(D->box_rho)))
+      return fail(CA_E_INVALID, "box_rho must be > 0 with finite bounds");
+  }
   return CA_OK;
 }
 
@@ -237,6 +253,16 @@ template <class T>
 ca_status h2d(ca_problem* h, T* dst, const T* src, size_t count) {
   if (count == 0) return CA_OK;
   CUDA_TRY(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  return CA_OK;
+}
+
+// box block (reading #7): clip_iterate = project s (t >= 1), u into the box first
+ca_status box_reset(ca_problem* h, int clip_iterate) {
+  if (!h->dev.box) return CA_OK;
+  const long long nq = (long long)h->B * (h->N + 1);
+  ca::k_box_reset<<<(unsigned)((nq + 127) / 128), 128, 0, h->stream>>>(h->dev, clip_iterate);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[4]++;
   return CA_OK;
 }
 
@@ -256,7 +282,7 @@ ca_status reset_iterate(ca_problem* h) {
     CUDA_TRY(cudaGetLastError());
     h->launches[4]++;
   }
-  return CA_OK;
+  return box_reset(h, 1);
 }
 
 // upload all per-batch inputs and reset the iterate (reading #11)
@@ -336,6 +362,20 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
     if ((st = h2d(h, const_cast<int*>(v.gperm), perm.data(), perm.size()))) return st;
   }
   if ((st = h2d(h, h->s_start, s0v.data(), s0v.size()))) return st;
+  if (v.box) {  // [s_min | s_max | u_min | u_max], +-inf where unbounded
+    std::vector<double> lim(2 * (size_t)(ns + nu));
+    for (int a = 0; a < ns; ++a) {
+      lim[a] = D->s_min ? D->s_min[a] : -INFINITY;
+      lim[ns + a] = D->s_max ? D->s_max[a] : INFINITY;
+    }
+    for (int a = 0; a < nu; ++a) {
+      lim[2 * ns + a] = D->u_min ? D->u_min[a] : -INFINITY;
+      lim[2 * ns + nu + a] = D->u_max ? D->u_max[a] : INFINITY;
+    }
+    v.box_rho = D->box_rho;
+    if ((st = h2d(h, const_cast<double*>(v.box_lim), lim.data(), lim.size()))) return st;
+    CUDA_TRY(cudaStreamSynchronize(h->stream));  // lim is a stack vector
+  }
   if ((st = reset_iterate(h))) return st;
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return CA_OK;
@@ -493,7 +533,9 @@ ca_status launch_collect(ca_problem* h, double* dst, int mask) {
     CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * 4 * h->B, h->stream));
     return CA_OK;
   }
-  ca::k_collect<<<(h->B + 127) / 128, 128, 0, h->stream>>>(h->dev, dst, mask);
+  // the box residual joins r_pri once (rank 0 of an obstacle-sharded run)
+  const int add_box = ((mask & 2) && (!h->comm || h->rank == 0)) ? 1 : 0;
+  ca::k_collect<<<(h->B + 127) / 128, 128, 0, h->stream>>>(h->dev, dst, mask, add_box);
   CUDA_TRY(cudaGetLastError());
   h->launches[4]++;
   return CA_OK;
@@ -691,6 +733,16 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   AL(v.lam, double, (size_t)h->np * std::max(1, v.nrmax - 1) * (d + 2));
   AL(v.part_e, int, (size_t)h->np);
   AL(v.part_be, double, (size_t)h->np);
+  v.box = (D->s_min || D->s_max || D->u_min || D->u_max) ? 1 : 0;
+  v.box_rho = D->box_rho;
+  if (v.box) {  // NEXT f1 box block
+    AL(v.box_lim, double, 2 * (size_t)(ns + nu));
+    AL(v.box_ws, double, (size_t)B * (N + 1) * ns);
+    AL(v.box_ls, double, (size_t)B * (N + 1) * ns);
+    AL(v.box_wu, double, (size_t)B * N * nu);
+    AL(v.box_lu, double, (size_t)B * N * nu);
+    AL(v.box_res, double, (size_t)B);
+  }
 #undef AL
   // lazily used buffers that also live in the workspace: scale factors, per-iteration
   // statistics for max_iters iterations, moving-obstacle steps
@@ -790,6 +842,8 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
   for (long long o = 0; o < (long long)h->B * h->M; ++o)
     if (D->obs_off[o + 1] - D->obs_off[o] != h->obs_counts[o])
       return fail(CA_E_INVALID, "ca_problem_load: obstacle row counts differ");
+  if ((D->s_min || D->s_max || D->u_min || D->u_max) != (h->dev.box != 0))
+    return fail(CA_E_INVALID, "ca_problem_load: box presence differs from the handle");
   return mark(h, upload(h, D));
 }
 
@@ -1170,6 +1224,21 @@ ca_status ca_set_iterate(ca_problem* h, const double* s, const double* u, const 
       CUDA_TRY(cudaStreamSynchronize(h->stream));
     }
   }
+  if ((st = box_reset(h, 0))) return mark(h, st);
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+ca_status ca_get_box_state(ca_problem* h, double* w_s, double* l_s, double* w_u, double* l_u, double* res) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (!h->dev.box) return fail(CA_E_INVALID, "the problem has no state/control box");
+  const size_t ns_n = (size_t)h->B * (h->N + 1) * h->ns, nu_n = (size_t)h->B * h->N * h->nu;
+  if (w_s) CUDA_TRY(cudaMemcpyAsync(w_s, h->dev.box_ws, sizeof(double) * ns_n, cudaMemcpyDeviceToHost, h->stream));
+  if (l_s) CUDA_TRY(cudaMemcpyAsync(l_s, h->dev.box_ls, sizeof(double) * ns_n, cudaMemcpyDeviceToHost, h->stream));
+  if (w_u) CUDA_TRY(cudaMemcpyAsync(w_u, h->dev.box_wu, sizeof(double) * nu_n, cudaMemcpyDeviceToHost, h->stream));
+  if (l_u) CUDA_TRY(cudaMemcpyAsync(l_u, h->dev.box_lu, sizeof(double) * nu_n, cudaMemcpyDeviceToHost, h->stream));
+  if (res) CUDA_TRY(cudaMemcpyAsync(res, h->dev.box_res, sizeof(double) * h->B, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return CA_OK;
 }

@@ -81,7 +81,28 @@ struct Dev {
   int* part_nv;
   long long dbg_p;   // diagnostics: pair whose pivots are traced into dbg (-1 = off)
   double* dbg;       // [64][12]
+  // box block of IC_0 (Eq. 13c-d; NEXT f1, reading #7): consensus copy w of the
+  // bounded states (t = 1..N) / controls in the box, scaled multiplier l, penalty box_rho
+  int box;                 // 0: no boxes (all below unused)
+  double box_rho;
+  const double* box_lim;   // [ns] s_min | [ns] s_max | [nu] u_min | [nu] u_max (+-inf = none)
+  double *box_ws, *box_ls; // [B][N+1][ns] (t = 0 unused)
+  double *box_wu, *box_lu; // [B][N][nu]
+  double* box_res;         // [B]: sum ||x - w||^2 after the last primal step
 };
+
+// component with a finite bound on either side
+__device__ __forceinline__ bool box_on(double lo, double hi) { return lo > -INFINITY || hi < INFINITY; }
+__device__ __forceinline__ double box_clip(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// w = Pi_box(x + l), l += x - w; returns (x - w)^2
+__device__ __forceinline__ double box_update(double x, double lo, double hi, double* w, double* l) {
+  const double lv = *l;
+  const double wv = box_clip(x + lv, lo, hi);
+  const double r = x - wv;
+  *l = lv + r;
+  *w = wv;
+  return r * r;
+}
 
 __device__ __forceinline__ void pose_of(const Dev& P, const double* st, double* R, double* rho) {
   const int d = P.d;
@@ -231,7 +252,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
 #ifdef CA_COMMON_KERNELS
 // per-scene sums of the record statistics -> dst[b*4 + {rdual, rpri, piv, fail}]
 // (fields with mask bit f clear are left untouched)
-__global__ void k_collect(Dev P, double* dst, int mask) {
+__global__ void k_collect(Dev P, double* dst, int mask, int add_box) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= P.B) return;
   double acc[4] = {0, 0, 0, 0};
@@ -244,6 +265,7 @@ __global__ void k_collect(Dev P, double* dst, int mask) {
     acc[2] += rec[R_PIV];
     acc[3] += rec[R_FAIL];
   }
+  if (P.box && add_box) acc[1] += P.box_res[b];  // box block's ||x - w||^2 (reading #7)
   for (int f = 0; f < 4; ++f)
     if ((mask >> f) & 1) dst[b * 4 + f] = acc[f];
 }
@@ -316,6 +338,14 @@ static __device__ void stage_assemble(const Dev& P, long long q, const double* r
     }
     ho[P.pidx[a]] += sig * spv;
   }
+  if (P.box) {  // (rho_b/2) ||s_t - w_t + l_t||^2 of the box block (reading #7)
+    const long long k0 = ((long long)b * (N + 1) + t) * NS;
+    for (int a = 0; a < NS; ++a)
+      if (box_on(P.box_lim[a], P.box_lim[NS + a])) {
+        out[a * NS + a] += P.box_rho;
+        ho[a] += -P.box_rho * (P.box_ws[k0 + a] - P.box_ls[k0 + a]);
+      }
+  }
   so[0] = rec[R_RDUAL];
   so[1] = rec[R_RPRI];
   so[2] = rec[R_PIV];
@@ -379,6 +409,15 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
   const int N = P.N;
   double Pm[NS][NS], pv[NS];
   double st[4] = {0, 0, 0, 0};
+  // box block (reading #7): control bounds, their penalty on the Quu diagonal
+  double ulo[NU], uhi[NU], urho[NU];
+#pragma unroll
+  for (int a = 0; a < NU; ++a) {
+    ulo[a] = P.box ? P.box_lim[2 * NS + a] : -INFINITY;
+    uhi[a] = P.box ? P.box_lim[2 * NS + NU + a] : INFINITY;
+    urho[a] = (P.box && box_on(ulo[a], uhi[a])) ? P.box_rho : 0.0;
+  }
+  const double box_res_prev = P.box ? P.box_res[b] : 0.0;
   for (int t = 1; t <= N; ++t) {
     const double* so = P.stg_stats + ((long long)b * N + (t - 1)) * 4;
 #pragma unroll
@@ -453,7 +492,7 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
     for (int a = 0; a < NU; ++a) {
 #pragma unroll
       for (int c = 0; c < NU; ++c) {
-        double s = 2.0 * P.Qu[a * NU + c];
+        double s = 2.0 * P.Qu[a * NU + c] + ((a == c) ? urho[a] : 0.0);
 #pragma unroll
         for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PB[k][c], s);
         Quu[a][c] = s;
@@ -465,7 +504,9 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
         for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PA[k][c], s);
         Qux[a][c] = s;
       }
-      double s = 0.0;
+      // control part of the box term: r_t = -rho_b (w_t - l_t)
+      const long long ku = ((long long)b * N + t) * NU + a;
+      double s = (urho[a] != 0.0) ? -urho[a] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;
 #pragma unroll
       for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
       qu[a] = s;
@@ -547,8 +588,9 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
       for (int c = 0; c < NS; ++c) Pm[a][c] = 0.5 * (Pn[a][c] + Pn[c][a]);
     }
   }
-  // forward rollout from s_0 (Eq. 13b holds exactly)
+  // forward rollout from s_0 (Eq. 13b holds exactly), then the box block's w, l update
   double x[NS];
+  double box_res = 0.0;
   double* sb = P.s + (long long)b * (N + 1) * NS;
 #pragma unroll
   for (int a = 0; a < NS; ++a) {
@@ -568,6 +610,14 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
       uu[a] = s;
       P.u[((long long)b * N + t) * NU + a] = s;
     }
+    if (P.box) {  // w = Pi_box(u + l), l += u - w
+#pragma unroll
+      for (int a = 0; a < NU; ++a)
+        if (urho[a] != 0.0) {
+          const long long ku = ((long long)b * N + t) * NU + a;
+          box_res += box_update(uu[a], ulo[a], uhi[a], &P.box_wu[ku], &P.box_lu[ku]);
+        }
+    }
     double xn[NS];
 #pragma unroll
     for (int a = 0; a < NS; ++a) {
@@ -583,13 +633,22 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
       x[a] = xn[a];
       sb[(t + 1) * NS + a] = xn[a];
     }
+    if (P.box) {  // states of t + 1
+      const long long k0 = ((long long)b * (N + 1) + t + 1) * NS;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        const double lo = P.box_lim[a], hi = P.box_lim[NS + a];
+        if (box_on(lo, hi)) box_res += box_update(xn[a], lo, hi, &P.box_ws[k0 + a], &P.box_ls[k0 + a]);
+      }
+    }
   }
+  if (P.box) P.box_res[b] = box_res;
   if (dst_cur) {
     dst_cur[b * 4 + 0] = st[0];
     dst_cur[b * 4 + 2] = st[2];
     dst_cur[b * 4 + 3] = st[3];
   }
-  if (dst_prev) dst_prev[b * 4 + 1] = st[1];
+  if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
 }
 
 // shared-memory footprint of k_riccati (doubles): stage blocks, stats, dynamics, gains
@@ -636,11 +695,20 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
     tri_col[u] = a_ + r;
   }
   static_assert(NS * (NS + 1) / 2 <= 64, "two upper-triangle entries per lane at most");
-  double qu2[NU][NU];  // 2 Qu, kept in registers
+  // box block (reading #7): control bounds and their penalty on the Quu diagonal
+  double ulo[NU], uhi[NU], urho[NU];
+#pragma unroll
+  for (int a_ = 0; a_ < NU; ++a_) {
+    ulo[a_] = P.box ? P.box_lim[2 * NS + a_] : -INFINITY;
+    uhi[a_] = P.box ? P.box_lim[2 * NS + NU + a_] : INFINITY;
+    urho[a_] = (P.box && box_on(ulo[a_], uhi[a_])) ? P.box_rho : 0.0;
+  }
+  const double box_res_prev = (P.box && lane == 0) ? P.box_res[b] : 0.0;
+  double qu2[NU][NU];  // 2 Qu (+ rho_b on bounded controls), kept in registers
 #pragma unroll
   for (int a_ = 0; a_ < NU; ++a_)
 #pragma unroll
-    for (int c = 0; c < NU; ++c) qu2[a_][c] = 2.0 * P.Qu[a_ * NU + c];
+    for (int c = 0; c < NU; ++c) qu2[a_][c] = 2.0 * P.Qu[a_ * NU + c] + ((a_ == c) ? urho[a_] : 0.0);
   // P_N = H_N, p_N = h_N
   for (int k = lane; k < SB; k += 32) {
     const double v = sstg[(long long)(N - 1) * SB + k];
@@ -693,6 +761,10 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
           Qm[a_][cc] = s_;
         }
         double s_ = 0.0;
+        if (c == NS && urho[a_] != 0.0) {  // control part of the box term: -rho_b (w_t - l_t)
+          const long long ku = ((long long)b * N + t) * NU + a_;
+          s_ = -urho[a_] * (P.box_wu[ku] - P.box_lu[ku]);
+        }
 #pragma unroll
         for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], (c < NS) ? PA[q][c] : w[q], s_);
         qx[a_] = s_;
@@ -779,6 +851,7 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   __syncwarp();
   double* xc = xs;
   double* xn = xs2;
+  double box_res = 0.0;  // this lane's part of the box block's ||x - w||^2
   for (int t = 0; t < N; ++t) {
     const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
     const double* Bm = A + NS * NS;
@@ -792,7 +865,11 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
       for (int c = 0; c < NS; ++c) s_ = __fma_rn(kr[c], xc[c], s_);
       uu[a_] = s_;
     }
-    if (lane < NU) P.u[((long long)b * N + t) * NU + lane] = uu[lane];
+    if (lane < NU) {
+      const long long ku = ((long long)b * N + t) * NU + lane;
+      P.u[ku] = uu[lane];
+      if (urho[lane] != 0.0) box_res += box_update(uu[lane], ulo[lane], uhi[lane], &P.box_wu[ku], &P.box_lu[ku]);
+    }
     if (lane < NS) {
       double s_ = cv[lane];
 #pragma unroll
@@ -801,11 +878,21 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
       for (int c = 0; c < NU; ++c) s_ = __fma_rn(Bm[lane * NU + c], uu[c], s_);
       xn[lane] = s_;
       sb[(t + 1) * NS + lane] = s_;
+      if (P.box) {
+        const double lo = P.box_lim[lane], hi = P.box_lim[NS + lane];
+        const long long ks = ((long long)b * (N + 1) + t + 1) * NS + lane;
+        if (box_on(lo, hi)) box_res += box_update(s_, lo, hi, &P.box_ws[ks], &P.box_ls[ks]);
+      }
     }
     __syncwarp();
     double* tmp = xc;
     xc = xn;
     xn = tmp;
+  }
+  if (P.box) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) box_res += __shfl_xor_sync(0xffffffffu, box_res, o);
+    if (lane == 0) P.box_res[b] = box_res;
   }
   if (lane == 0) {
     double st[4] = {0, 0, 0, 0};
@@ -819,7 +906,7 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
       dst_cur[b * 4 + 2] = st[2];
       dst_cur[b * 4 + 3] = st[3];
     }
-    if (dst_prev) dst_prev[b * 4 + 1] = st[1];
+    if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
   }
 }
 
@@ -1208,6 +1295,32 @@ __global__ void k_init_y(Dev P) {
   double sb = 0.0;
   for (int k = 0; k < nr; ++k) sb += P.part_rows[4 * (r0 + k) + 3];
   for (int k = 0; k < P.ny; ++k) P.y[(long long)k * P.P + p] = (k < nr) ? 1.0 / sb : 0.0;
+}
+
+// Box block reset (reading #7), one thread per (scene, t), t = 0..N: with
+// clip_iterate (cold start) the iterate's states (t >= 1) and controls are
+// first projected into the box; then w = Pi_box(x), l = 0, and the residual is 0.
+__global__ void k_box_reset(Dev P, int clip_iterate) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)P.B * (P.N + 1)) return;
+  const int b = (int)(q / (P.N + 1)), t = (int)(q % (P.N + 1));
+  const int NS = P.ns, NU = P.nu;
+  for (int a = 0; a < NS; ++a) {
+    const long long k = q * NS + a;
+    const double lo = P.box_lim[a], hi = P.box_lim[NS + a];
+    if (clip_iterate && t >= 1) P.s[k] = box_clip(P.s[k], lo, hi);
+    P.box_ws[k] = box_clip(P.s[k], lo, hi);
+    P.box_ls[k] = 0.0;
+  }
+  if (t < P.N)
+    for (int a = 0; a < NU; ++a) {
+      const long long k = ((long long)b * P.N + t) * NU + a;
+      const double lo = P.box_lim[2 * NS + a], hi = P.box_lim[2 * NS + NU + a];
+      if (clip_iterate) P.u[k] = box_clip(P.u[k], lo, hi);
+      P.box_wu[k] = box_clip(P.u[k], lo, hi);
+      P.box_lu[k] = 0.0;
+    }
+  if (t == 0) P.box_res[b] = 0.0;
 }
 
 __global__ void k_dfma(double* out, long long iters) {

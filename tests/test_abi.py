@@ -68,6 +68,10 @@ def test_validation_errors_precede_device(ca):
     step[0, 0] = np.nan
     bad = dataclasses.replace(sc, obs_step=step)
     assert _create(ca, bad)[0] == -1  # CA_E_INVALID (moving obstacles: finite steps)
+    c2b = scenes.make_config(8)  # boxes (NEXT f1): min <= max, no NaN, box_rho > 0
+    assert _create(ca, dataclasses.replace(c2b, box_rho=0.0))[0] == -1
+    assert _create(ca, dataclasses.replace(c2b, u_min=np.array([1.0, -1.0])))[0] == -1
+    assert _create(ca, dataclasses.replace(c2b, s_max=np.array([np.nan, 1, 1, 1])))[0] == -1
 
 
 @pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="GPU present")

@@ -70,12 +70,13 @@ def test_t1_dual_sweep(ca, cfg, k0):
     assert np.array_equal(st["zeta"], zeta) and np.array_equal(st["xi"], xi)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8])
 def test_t1_primal_and_multiplier(ca, cfg):
     sc = scene(cfg)
     o = warm(sc, 3)
     g = ca.Problem(sc)
     g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    o.set_iterate()  # both box blocks restart from w = Pi_box(s, u), l = 0 (C2b)
     g.dual_sweep()
     o.dual_sweep()
     s_lin = o.s.copy()  # dyn_model 1 linearises here
@@ -104,7 +105,7 @@ def test_t1_primal_and_multiplier(ca, cfg):
         assert np.abs(s[0, t + 1] - (A @ s[0, t] + B @ u[0, t] + c)).max() <= 1e-12 * (1 + np.abs(s).max())
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8])
 def test_t2_full_iterations(ca, cfg):
     sc = scene(cfg)
     K = sc.iters
@@ -339,3 +340,55 @@ def test_torch_workspace_bitwise(ca, cfg):
     aa, ma = a.scale_detect()
     ab, mb = b.scale_detect()
     assert np.array_equal(aa, ab) and np.array_equal(ma, mb)
+
+
+def test_box_block_parity(ca):
+    """NEXT f1 (reading #7): the box block's w, l and residual after K iterations,
+    then one more primal step from the same (nonzero-l) state, against the oracle."""
+    sc = scenes.make_config(8)
+    g = ca.Problem(sc)
+    o = oracle.Oracle(sc)
+    ws, ls, wu, lu, res = g.box_state()  # cold start: iterate projected into the box
+    s, u = g.trajectory()
+    np.testing.assert_array_equal(s, o.s)
+    np.testing.assert_array_equal(u, o.u)
+    np.testing.assert_array_equal(ws, o.ws)
+    assert not ls.any() and not lu.any() and not res.any()
+    g.admm_iterate(6)
+    o.admm_iterate(6)
+    ws, ls, wu, lu, res = g.box_state()
+    for a, b, what in ((ws, o.ws, "w_s"), (ls, o.ls, "l_s"), (wu, o.wu, "w_u"), (lu, o.lu, "l_u")):
+        close(a[:, 1:] if a.shape == o.ws.shape else a, b[:, 1:] if b.shape == o.ws.shape else b, 1e-8, what)
+    assert np.abs(ls).max() > 1e-3 and np.abs(lu).max() > 1e-3  # the bounds are active
+    close(res, o.boxres, 1e-8, "box residual")
+    # the same state on both sides, then one primal step with l != 0
+    s, u = g.trajectory()
+    st = g.pair_state()
+    o.s[...], o.u[...] = s, u
+    o.y[: g.n_pairs], o.zeta[: g.n_pairs], o.xi[: g.n_pairs] = st["y"], st["zeta"], st["xi"]
+    o.ws[...], o.ls[...], o.wu[...], o.lu[...] = ws, ls, wu, lu
+    g.dual_sweep()
+    o.dual_sweep()
+    g.primal_step()
+    o.primal_step()
+    s, u = g.trajectory()
+    close(s, o.s, 1e-9, "s after primal step (box)")
+    close(u, o.u, 1e-9, "u after primal step (box)")
+    ws, ls, wu, lu, res = g.box_state()
+    close(ls[:, 1:], o.ls[:, 1:], 1e-9, "l_s after primal step")
+    close(lu, o.lu, 1e-9, "l_u after primal step")
+    close(res, o.boxres, 1e-8, "box residual after primal step")
+
+
+def test_box_infinite_bounds_equal_unbounded_bitwise(ca):
+    sc = scenes.make_config(2)
+    inf = np.inf
+    sb = dataclasses.replace(sc, s_min=np.full(4, -inf), s_max=np.full(4, inf), u_min=np.full(2, -inf),
+                             u_max=np.full(2, inf), box_rho=5.0)
+    a, b = ca.Problem(sc), ca.Problem(sb)
+    ha = a.admm_iterate(20)[1]
+    hb = b.admm_iterate(20)[1]
+    sa, ua = a.trajectory()
+    s2, u2 = b.trajectory()
+    assert np.array_equal(sa, s2) and np.array_equal(ua, u2)
+    assert np.array_equal(ha["r_pri"], hb["r_pri"])

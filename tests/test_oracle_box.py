@@ -1,5 +1,5 @@
 """Pins of the oracle's box block (state / control bounds of Eq. 13c-d, P:253-254,
-inside IC_0 of P:289-290; NEXT f1; reading #22).
+inside IC_0 of P:289-290; NEXT f1; reading #7).
 
 The oracle handles the boxes with one more ADMM block (consensus x = w, w in the
 box, scaled multiplier l).  What pins it, independently of the oracle's code:
