@@ -52,6 +52,7 @@ def lib():
         _lib.orc_pair_solve.restype = C.c_int
         _lib.orc_init_iterate.argtypes = [C.c_void_p, C.c_void_p]
         _lib.orc_reset_box.argtypes = [C.c_void_p, C.c_void_p]
+        _lib.orc_sense.argtypes = [C.c_void_p, dp, C.c_void_p]
         _lib.orc_dual_sweep.argtypes = [C.c_void_p, C.c_void_p, dp]
         _lib.orc_dual_sweep.restype = C.c_longlong
         _lib.orc_primal_step.argtypes = [C.c_void_p, C.c_void_p]
@@ -93,7 +94,7 @@ class _Problem(C.Structure):
         ("max_pivot_factor", C.c_int), ("ny", C.c_int), ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
         ("dyn_model", C.c_int), ("dt", C.c_double),
         ("s_min", C.c_void_p), ("s_max", C.c_void_p), ("u_min", C.c_void_p), ("u_max", C.c_void_p),
-        ("box_rho", C.c_double),
+        ("box_rho", C.c_double), ("sensed", C.c_void_p),
     ]
 
 
@@ -146,6 +147,12 @@ class Oracle:
             v = getattr(sc, name, None)  # NEXT f1: boxes of Eq. 13c-d (None = unbounded)
             setattr(P, name, None if v is None else k(name, _f64(v).reshape(n)))
         P.box_rho = float(getattr(sc, "box_rho", 0.0))
+        self.sensed = None  # NEXT f3 sensing: obstacles meeting the box rho(s0) + [-h, h]
+        half = getattr(sc, "sense_half", None)
+        if half is not None and sc.n_obs > 0:
+            self.sensed = np.zeros(sc.n_scenes * sc.n_obs, np.uint8)
+            lib().orc_sense(C.byref(P), _d(_f64(half).reshape(sc.dim)), self.sensed.ctypes.data)
+            P.sensed = self.sensed.ctypes.data
         self.ny = P.ny = sc.n_max if sc.n_obs > 0 else 1
         self.P = P
         B, N, ns, nu, d = sc.n_scenes, sc.horizon, sc.n_state, sc.n_ctrl, sc.dim

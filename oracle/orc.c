@@ -411,6 +411,38 @@ static long long n_pairs(const orc_problem* P) {
   return (long long)P->n_scenes * P->horizon * P->n_parts * P->n_obs;
 }
 
+/* 1 if obstacle (b, j) is in the (i, j, t) table (sensing, NEXT f3) */
+static int sensed(const orc_problem* P, int b, int j) {
+  return !P->sensed || P->sensed[(long long)b * P->n_obs + j];
+}
+
+/* Sensing (NEXT f3): obstacle (b, j) is sensed iff it meets the
+ * axis-aligned box rho(s0_b) + [-half, half] (world frame) -- i.e. iff the scale
+ * factor alpha* (Eq. 3) of that box as a "robot part" against the obstacle is <= 1
+ * (1e-9 slack: touching counts as sensed).  Static obstacle positions (t = 0). */
+void orc_sense(const orc_problem* P, const double* half, unsigned char* out) {
+  int d = P->dim;
+  double A[6 * MAXD], bb[6], R[9], rho[3];
+  for (int a = 0; a < d; ++a) {
+    for (int c = 0; c < d; ++c) {
+      A[(2 * a) * d + c] = (a == c) ? 1.0 : 0.0;
+      A[(2 * a + 1) * d + c] = (a == c) ? -1.0 : 0.0;
+    }
+    bb[2 * a] = half[a];
+    bb[2 * a + 1] = half[a];
+  }
+  for (int b = 0; b < P->n_scenes; ++b) {
+    orc_pose(P->pose_model, P->pose_idx, d, P->s0 + (long long)b * P->n_state, R, rho);
+    for (int a = 0; a < d * d; ++a) R[a] = (a % (d + 1) == 0) ? 1.0 : 0.0; /* world-aligned box */
+    for (int j = 0; j < P->n_obs; ++j) {
+      int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
+      double alpha;
+      int rc = orc_scale_lp(d, 2 * d, A, bb, R, rho, no, P->obs_C + (long long)l0 * d, P->obs_d + l0, &alpha, NULL);
+      out[o] = (rc == 0 && alpha <= 1.0 + 1e-9) ? 1 : 0;
+    }
+  }
+}
+
 static const double* dyn_ptr(const orc_problem* P, const double* base, int b, int t, int blk) {
   long long nt = P->dyn_per_time ? P->horizon : 1;
   long long idx = (P->dyn_per_scene ? (long long)b * nt : 0) + (P->dyn_per_time ? t : 0);
@@ -537,6 +569,11 @@ long long orc_dual_sweep(const orc_problem* P, orc_iterate* I, double* rdual) {
   for (long long p = 0; p < np; ++p) {
     int b, t, i, j;
     decode(P, p, &b, &t, &i, &j);
+    if (!sensed(P, b, j)) {
+      if (I->pivots) I->pivots[p] = 0;
+      if (I->status) I->status[p] = ORC_OK;
+      continue;
+    }
     double R[9], rho[3];
     orc_pose(P->pose_model, P->pose_idx, d, I->s + ((long long)b * (N + 1) + t) * ns, R, rho);
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
@@ -614,6 +651,7 @@ static void scene_aggregates(const orc_problem* P, const orc_iterate* I, int b, 
     for (int i = 0; i < P->n_parts; ++i) {
       int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
       for (int j = 0; j < P->n_obs; ++j) {
+        if (!sensed(P, b, j)) continue;
         long long p = (((long long)b * N + (t - 1)) * P->n_parts + i) * P->n_obs + j;
         int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
         int n = nr + no + 1;
@@ -825,6 +863,7 @@ void orc_multiplier_update(const orc_problem* P, orc_iterate* I, double* rpri) {
   for (long long p = 0; p < np; ++p) {
     int b, t, i, j;
     decode(P, p, &b, &t, &i, &j);
+    if (!sensed(P, b, j)) continue;
     double R[9], rho[3];
     orc_pose(P->pose_model, P->pose_idx, d, I->s + ((long long)b * (N + 1) + t) * ns, R, rho);
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
@@ -897,6 +936,10 @@ long long orc_scale_detect(const orc_problem* P, const double* s, double* alpha)
   for (long long p = 0; p < np; ++p) {
     int b, t, i, j;
     decode(P, p, &b, &t, &i, &j);
+    if (!sensed(P, b, j)) {
+      alpha[p] = INFINITY;
+      continue;
+    }
     double R[9], rho[3];
     orc_pose(P->pose_model, P->pose_idx, d, s + ((long long)b * (N + 1) + t) * ns, R, rho);
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;

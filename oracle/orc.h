@@ -63,6 +63,11 @@ typedef struct {
   const double* u_min;
   const double* u_max;
   double box_rho;
+  /* Sensing ("can only sense the obstacles within 20m x 20m x 6m"; NEXT
+   * f3): NULL = every obstacle, else [n_scenes*n_obs] 0/1 -- pairs of an unsensed
+   * obstacle leave the (i, j, t) table (no dual step, no aggregate, no multiplier
+   * update, alpha = +inf).  orc_sense() fills it from the sensing box. */
+  const unsigned char* sensed;
 } orc_problem;
 
 typedef struct {

@@ -43,6 +43,7 @@ CONFIG_NAMES = {
     6: "C4m: C4 with moving traffic (vehicles at 12-18 m/s, NEXT f3), N=60, K=300",
     7: "C2n: C2 with the unicycle relinearised at every ADMM iterate (SQP, NEXT f2), N=50, K=200",
     8: "C2b: C2 with state/control boxes (|a| <= 0.5, |om| <= 1.5, 2.5 <= v <= 3.5; NEXT f1), N=50, K=200",
+    9: "C4s: C4m sensing only the vehicles within 60 m x 8 m of the ego (P:541; NEXT f3), N=60, K=300",
 }
 
 
@@ -106,6 +107,10 @@ class Scene:
     u_min: Optional[np.ndarray] = None
     u_max: Optional[np.ndarray] = None
     box_rho: float = 0.0
+    # NEXT f3 sensing: None = every obstacle, else [dim] half-extents of the
+    # world-aligned box around the robot's current position; only obstacles meeting it
+    # enter the (i, j, t) table
+    sense_half: Optional[np.ndarray] = None
 
     @property
     def n_parts(self) -> int:
@@ -441,6 +446,8 @@ def make_config(cfg: int, **kw) -> Scene:
         return make_c4(moving=True, **kw)
     if cfg == 7:
         return dataclasses.replace(make_c2(**kw), name="C2n", config=7, dyn_model=1)
+    if cfg == 9:
+        return dataclasses.replace(make_c4(moving=True, **kw), name="C4s", config=9, sense_half=np.array([60.0, 8.0]))
     if cfg == 8:
         inf = np.inf
         return dataclasses.replace(make_c2(**kw), name="C2b", config=8, s_min=np.array([-inf, -inf, -1.2, 2.5]),
