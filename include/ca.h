@@ -132,6 +132,13 @@ typedef struct {
   const double* u_min;
   const double* u_max;
   double box_rho;
+  /* NEXT f3, sensing ("can only sense the obstacles within 20m x 20m x 6m";
+   * S:553).  Nullable HOST [dim] half-extents h > 0: only obstacles meeting the
+   * world-aligned box rho(s0_b) + [-h, h] around each scene's current position enter
+   * the (i, j, t) table (static positions, t = 0); pairs of the others are skipped by
+   * every step (certificates keep their values, alpha = +inf).  Re-evaluated at every
+   * create/load (each MPC step).  NULL = every obstacle. */
+  const double* sense_half;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;

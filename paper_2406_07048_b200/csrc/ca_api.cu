@@ -86,6 +86,7 @@ struct ca_problem {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
   double* obs_step_buf = nullptr;  // moving obstacles (allocated on first use)
+  double* sense_half = nullptr;    // [3] sensing box half-extents (NEXT f3)
   // caller-provided device workspace (bump allocation, 256-B aligned); count_only:
   // ca_workspace_size's planning pass (no device calls)
   char* ws = nullptr;
@@ -246,6 +247,10 @@ ca_status validate(const ca_problem_desc* D) {
     if (finite && !(D->box_rho > 0.0 && std::isfinite(D->box_rho)))
       return fail(CA_E_INVALID, "box_rho must be > 0 with finite bounds");
   }
+  if (D->sense_half)
+    for (int a = 0; a < d; ++a)
+      if (!(D->sense_half[a] > 0.0 && std::isfinite(D->sense_half[a])))
+        return fail(CA_E_INVALID, "sense_half must be finite and > 0");
   return CA_OK;
 }
 
@@ -375,6 +380,14 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
     v.box_rho = D->box_rho;
     if ((st = h2d(h, const_cast<double*>(v.box_lim), lim.data(), lim.size()))) return st;
     CUDA_TRY(cudaStreamSynchronize(h->stream));  // lim is a stack vector
+  }
+  if (v.sensed) {  // which obstacles enter the pair table (NEXT f3)
+    if ((st = h2d(h, h->sense_half, D->sense_half, (size_t)d))) return st;
+    const long long no = (long long)B * h->M;
+    if (d == 2) ca::k_sense<2><<<(unsigned)((no + 127) / 128), 128, 0, h->stream>>>(v, h->sense_half, const_cast<uint8_t*>(v.sensed));
+    else ca::k_sense<3><<<(unsigned)((no + 127) / 128), 128, 0, h->stream>>>(v, h->sense_half, const_cast<uint8_t*>(v.sensed));
+    CUDA_TRY(cudaGetLastError());
+    h->launches[4]++;
   }
   if ((st = reset_iterate(h))) return st;
   CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -735,6 +748,12 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   AL(v.part_be, double, (size_t)h->np);
   v.box = (D->s_min || D->s_max || D->u_min || D->u_max) ? 1 : 0;
   v.box_rho = D->box_rho;
+  if (D->sense_half && h->M > 0) {  // NEXT f3 sensing mask + its box
+    uint8_t* m_ = nullptr;
+    if ((st = h->alloc(&m_, (size_t)B * h->M))) return st;
+    v.sensed = m_;
+    AL(h->sense_half, double, 3);
+  }
   if (v.box) {  // NEXT f1 box block
     AL(v.box_lim, double, 2 * (size_t)(ns + nu));
     AL(v.box_ws, double, (size_t)B * (N + 1) * ns);
@@ -844,6 +863,8 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
       return fail(CA_E_INVALID, "ca_problem_load: obstacle row counts differ");
   if ((D->s_min || D->s_max || D->u_min || D->u_max) != (h->dev.box != 0))
     return fail(CA_E_INVALID, "ca_problem_load: box presence differs from the handle");
+  if ((D->sense_half && h->M > 0) != (h->dev.sensed != nullptr))
+    return fail(CA_E_INVALID, "ca_problem_load: sensing presence differs from the handle");
   return mark(h, upload(h, D));
 }
 

@@ -89,7 +89,13 @@ struct Dev {
   double *box_ws, *box_ls; // [B][N+1][ns] (t = 0 unused)
   double *box_wu, *box_lu; // [B][N][nu]
   double* box_res;         // [B]: sum ||x - w||^2 after the last primal step
+  // sensing (NEXT f3): NULL = every obstacle, else [B*M] 0/1 from
+  // k_sense -- pairs of unsensed obstacles leave the (i, j, t) table
+  const uint8_t* sensed;
 };
+__device__ __forceinline__ bool is_sensed(const Dev& P, int b, int j) {
+  return !P.sensed || P.sensed[(long long)b * P.M + j];
+}
 
 // component with a finite bound on either side
 __device__ __forceinline__ bool box_on(double lo, double hi) { return lo > -INFINITY || hi < INFINITY; }
@@ -136,9 +142,11 @@ __device__ __forceinline__ int sym_idx(int a, int c, int npc) { return a * npc -
 // Record of (scene b, timestep t = 1..N, chunk c) in agg: each sweep work item
 // (b, group, chunk) writes one record per timestep of its group.
 // packed execution-order entry: timestep slot tl (< 8), robot part ip (< 8), obstacle j
+// (bit 31: the obstacle is not sensed -- the slot is skipped)
+constexpr uint32_t PAIR_UNSENSED = 0x80000000u;
 __device__ __forceinline__ uint32_t pack_pair(int tl, int ip, int j) { return (uint32_t)(tl << 19 | ip << 16 | j); }
 __device__ __forceinline__ void unpack_pair(uint32_t u, int& tl, int& ip, int& j) {
-  tl = (int)(u >> 19);
+  tl = (int)((u >> 19) & 0xfffu);
   ip = (int)((u >> 16) & 7u);
   j = (int)(u & 0xffffu);
 }
@@ -198,9 +206,11 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
   double rec[1] = {0.0};
   const int gs = it.chunk * P.CHG + tid;  // slot in the execution order of the group
   int tl = -1;
-  if (tid < P.CHG && gs < it.size) {
+  const uint32_t pk = (tid < P.CHG && gs < it.size) ? P.gperm2[((long long)it.b * P.NG + it.grp) * P.GG + gs]
+                                                    : PAIR_UNSENSED;
+  if (!(pk & PAIR_UNSENSED)) {
     int i, j;
-    unpack_pair(P.gperm2[((long long)it.b * P.NG + it.grp) * P.GG + gs], tl, i, j);
+    unpack_pair(pk, tl, i, j);
     const int g = i * P.M + j, t = it.grp * P.TG + tl + 1;
     const long long bt = (long long)it.b * P.N + t - 1;
     const long long p = bt * P.G + g, PP = P.P;
@@ -1035,6 +1045,10 @@ __global__ void __launch_bounds__(128) k_scale2(Dev P, const double* states, dou
   double R[9], rho[3];
   pose_of(P, states + ((long long)b * (P.N + 1) + t) * P.ns, R, rho);
   const int i = g / P.M, j = g % P.M;
+  if (!is_sensed(P, b, j)) {
+    alpha[q] = INFINITY;
+    return;
+  }
   obstacle_frame<2>(P, b, j, t, rho);
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
   const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
@@ -1076,6 +1090,10 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
   const int g = P.gperm[(long long)b * P.G + gs];
   const long long p = (long long)bt * P.G + g;
   const int i = g / P.M, j = g % P.M;
+  if (!is_sensed(P, b, j)) {
+    alpha[p] = INFINITY;
+    return;
+  }
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
   const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
   const int m = nr + no;
@@ -1213,6 +1231,10 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   auto key_of = [&](int s_, uint32_t& u) {
     const int tl = s_ / G, g = base[s_ % G];
     u = pack_pair(tl, g / P.M, g % P.M);
+    if (!is_sensed(P, b, g % P.M)) {  // unsensed obstacle: skipped slot, sorted last
+      u |= PAIR_UNSENSED;
+      return NB - 1;
+    }
     return min((int)(pst[(long long)tl * G + g] & 0xffffu), NB - 1);
   };
   for (int k = 0; k < NB; ++k) cnt[k][tid] = 0;
@@ -1295,6 +1317,74 @@ __global__ void k_init_y(Dev P) {
   double sb = 0.0;
   for (int k = 0; k < nr; ++k) sb += P.part_rows[4 * (r0 + k) + 3];
   for (int k = 0; k < P.ny; ++k) P.y[(long long)k * P.P + p] = (k < nr) ? 1.0 / sb : 0.0;
+}
+
+// Sensing (NEXT f3), one thread per obstacle (b, j): sensed iff the
+// polytope {C y <= d} meets the world-aligned box rho(s0_b) + [-h, h] -- tested by
+// enumerating the vertices of the intersection (every D-subset of its rows with a
+// nonsingular system; the intersection is bounded, so it is empty iff no vertex is
+// feasible).  Feasibility slack 1e-9 (1 + |rhs|): touching counts as sensed.
+template <int D>
+__global__ void k_sense(Dev P, const double* half, uint8_t* out) {
+  const long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= (long long)P.B * P.M) return;
+  const int b = (int)(o / P.M);
+  double R[9], rho[3];
+  pose_of(P, P.s0 + (long long)b * P.ns, R, rho);
+  const int l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0, m = no + 2 * D;
+  auto row = [&](int r, double* c) -> double {  // row r: c^T y <= rhs
+    if (r < no) {
+      const double* q = P.obs_rows + 4 * ((long long)l0 + r);
+#pragma unroll
+      for (int a = 0; a < D; ++a) c[a] = q[a];
+      return q[3];
+    }
+    const int k = r - no, a0 = k >> 1;
+    const double sg = (k & 1) ? -1.0 : 1.0;  // +y_a <= rho_a + h_a, -y_a <= h_a - rho_a
+#pragma unroll
+    for (int a = 0; a < D; ++a) c[a] = (a == a0) ? sg : 0.0;
+    return sg * rho[a0] + half[a0];
+  };
+  auto feasible = [&](const double* y) {
+    for (int r = 0; r < m; ++r) {
+      double c[D];
+      const double h = row(r, c);
+      double v = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) v += c[a] * y[a];
+      if (v > h + 1e-9 * (1.0 + fabs(h))) return false;
+    }
+    return true;
+  };
+  bool hit = false;
+  double c0[D], c1[D], c2[D];
+  for (int r0 = 0; r0 < m && !hit; ++r0) {
+    const double h0 = row(r0, c0);
+    for (int r1 = r0 + 1; r1 < m && !hit; ++r1) {
+      const double h1 = row(r1, c1);
+      if (D == 2) {
+        const double det = c0[0] * c1[1] - c0[1] * c1[0];
+        if (fabs(det) < 1e-12) continue;
+        const double y[2] = {(h0 * c1[1] - c0[1] * h1) / det, (c0[0] * h1 - h0 * c1[0]) / det};
+        hit = feasible(y);
+      } else {
+        for (int r2 = r1 + 1; r2 < m && !hit; ++r2) {
+          const double h2 = row(r2, c2);
+          // Cramer's rule on [c0; c1; c2] y = (h0, h1, h2)
+          const double k0 = c1[1] * c2[2] - c1[2] * c2[1], k1 = c1[2] * c2[0] - c1[0] * c2[2],
+                       k2 = c1[0] * c2[1] - c1[1] * c2[0];
+          const double det = c0[0] * k0 + c0[1] * k1 + c0[2] * k2;
+          if (fabs(det) < 1e-12) continue;
+          const double y[3] = {
+              (h0 * k0 + c0[1] * (h2 * c1[2] - h1 * c2[2]) + c0[2] * (h1 * c2[1] - h2 * c1[1])) / det,
+              (c0[0] * (h1 * c2[2] - h2 * c1[2]) + h0 * k1 + c0[2] * (h2 * c1[0] - h1 * c2[0])) / det,
+              (c0[0] * (h2 * c1[1] - h1 * c2[1]) + c0[1] * (h1 * c2[0] - h2 * c1[0]) + h0 * k2) / det};
+          hit = feasible(y);
+        }
+      }
+    }
+  }
+  out[o] = hit ? 1 : 0;
 }
 
 // Box block reset (reading #7), one thread per (scene, t), t = 0..N: with

@@ -269,10 +269,12 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   const double* prow = P.part_rows;
   uint32_t zb = 0;
   bool z0b = false, fallback = false;
-  const bool act = tid < P.CHG && gs < it.size;
+  const uint32_t pk = (tid < P.CHG && gs < it.size) ? P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs]
+                                                    : PAIR_UNSENSED;
+  const bool act = !(pk & PAIR_UNSENSED);  // padding lane or unsensed obstacle (NEXT f3): idle
   if (act) {
     int j;
-    unpack_pair(P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs], tl, ip, j);
+    unpack_pair(pk, tl, ip, j);
     const int g = ip * P.M + j;
     const long long bt = (long long)b * P.N + it.grp * P.TG + tl;  // b*N + (t-1)
     po = P.pose + bt * 12;                                        // pose(s_t^k) (k_sortpairs)

@@ -11,7 +11,9 @@ here:
 3. loads the new problem into the SAME device handle (ca_problem_load), warm-starts
    it with the previous iterate shifted by one timestep (s, u, and every pair's
    y, zeta, xi) via ca_set_iterate,
-4. runs K ADMM iterations on the GPU and applies the first control to the plant.
+4. runs K ADMM iterations on the GPU and applies the first control to the plant
+   (saturated to the control box, if the problem has one: the ADMM iterate meets the
+   box only at convergence, reading #7).
 
 Moving obstacles (obs_step) advance with the loop.  Everything numerical in a solve
 runs in libca.so; this module only prepares inputs (host numpy).  The solver is
@@ -124,6 +126,9 @@ class RecedingHorizon:
         self.latency.append(time.perf_counter() - t0)
         self.prev = (np.array(s[0]), np.array(u[0]), np.array(y), np.array(zeta), np.array(xi))
         u0 = np.array(u[0, 0])
+        if self.sc0.u_min is not None or self.sc0.u_max is not None:  # actuator saturation (NEXT f1 boxes)
+            u0 = np.clip(u0, self.sc0.u_min if self.sc0.u_min is not None else -np.inf,
+                         self.sc0.u_max if self.sc0.u_max is not None else np.inf)
         self.s_now = unicycle_step(self.s_now, u0, self.sc0.dt)
         self.k += 1
         return u0

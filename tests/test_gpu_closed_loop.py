@@ -29,11 +29,14 @@ def c4m_short():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["c2", "c4m", "c2n"])
+@pytest.mark.parametrize("case", ["c2", "c4m", "c2n", "c2b", "c4s"])
 def test_closed_loop_gpu_equals_oracle(case):
-    """c2n: the unicycle relinearised at every ADMM iterate inside each MPC solve."""
+    """c2n: the unicycle relinearised at every ADMM iterate inside each MPC solve;
+    c2b: state/control boxes (NEXT f1), the plant saturating the applied control;
+    c4s: sensing (NEXT f3) re-evaluated at every step as the ego advances."""
     sc, K, speed, steps = {"c2": (scenes.make_config(2), 40, 3.0, 5), "c4m": (c4m_short(), 30, 20.0, 3),
-                           "c2n": (scenes.make_config(7), 40, 3.0, 5)}[case]
+                           "c2n": (scenes.make_config(7), 40, 3.0, 5), "c2b": (scenes.make_config(8), 40, 3.0, 5),
+                           "c4s": (dataclasses.replace(c4m_short(), sense_half=np.array([40.0, 8.0])), 30, 20.0, 3)}[case]
     runs = {}
     for backend in ("gpu", "oracle"):
         loop = mpc.RecedingHorizon(sc, K=K, speed=speed, solver=None if backend == "gpu" else OracleSolver())

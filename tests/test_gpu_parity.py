@@ -50,7 +50,7 @@ def close(a, b, rtol, what):
     assert err.max() <= rtol, f"{what}: max rel err {err.max():.3e} at {np.unravel_index(err.argmax(), err.shape)}"
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 9])
 @pytest.mark.parametrize("k0", [0, 3])
 def test_t1_dual_sweep(ca, cfg, k0):
     sc = scene(cfg)
@@ -70,7 +70,7 @@ def test_t1_dual_sweep(ca, cfg, k0):
     assert np.array_equal(st["zeta"], zeta) and np.array_equal(st["xi"], xi)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9])
 def test_t1_primal_and_multiplier(ca, cfg):
     sc = scene(cfg)
     o = warm(sc, 3)
@@ -105,7 +105,7 @@ def test_t1_primal_and_multiplier(ca, cfg):
         assert np.abs(s[0, t + 1] - (A @ s[0, t] + B @ u[0, t] + c)).max() <= 1e-12 * (1 + np.abs(s).max())
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9])
 def test_t2_full_iterations(ca, cfg):
     sc = scene(cfg)
     K = sc.iters
@@ -392,3 +392,33 @@ def test_box_infinite_bounds_equal_unbounded_bitwise(ca):
     s2, u2 = b.trajectory()
     assert np.array_equal(sa, s2) and np.array_equal(ua, u2)
     assert np.array_equal(ha["r_pri"], hb["r_pri"])
+
+
+def sensing_scenes():
+    return {"c4s": scenes.make_config(9),
+            "c5s": dataclasses.replace(scenes.make_c5(scene_ids=[0, 7, 4000]), sense_half=np.array([25.0, 25.0])),
+            "c3s": dataclasses.replace(scenes.make_config(3), sense_half=np.array([4.0, 1.0, 0.6]))}
+
+
+@pytest.mark.parametrize("case", ["c4s", "c5s", "c3s"])
+def test_sensing_mask_and_sweep(ca, case):
+    """NEXT f3 sensing: the GPU's sensed set (k_sense, vertex enumeration) equals the
+    oracle's (scale LP of the sensing box); unsensed pairs report alpha = +inf and are
+    skipped by the dual step; one warm dual sweep matches pair by pair."""
+    sc = sensing_scenes()[case]
+    o = warm(sc, 2)
+    g = ca.Problem(sc)
+    alpha, _ = g.scale_detect(states=o.s)
+    a_o = o.scale_detect()
+    assert 0 < np.isfinite(a_o).sum() < a_o.size
+    assert np.array_equal(np.isinf(alpha[: g.n_pairs]), np.isinf(a_o))
+    fin = np.isfinite(a_o)
+    close(alpha[: g.n_pairs][fin], a_o[fin], 1e-9, "alpha (sensed pairs)")
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    s, zeta, xi = o.s.copy(), o.zeta.copy(), o.xi.copy()
+    rc, r = g.dual_sweep()
+    rd, fails = o.dual_sweep()
+    st = g.pair_state()
+    flips = compare_dual_sweep(sc, s, zeta, xi, st["y"], o.y, st["pivots"], o.pivots, st["status"], o.status)
+    assert r.n_fail == fails
+    assert r.pivots == o.pivots.sum() or flips
