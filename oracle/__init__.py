@@ -94,7 +94,7 @@ class _Problem(C.Structure):
         ("max_pivot_factor", C.c_int), ("ny", C.c_int), ("prox_eps", C.c_double), ("obs_step", C.c_void_p),
         ("dyn_model", C.c_int), ("dt", C.c_double),
         ("s_min", C.c_void_p), ("s_max", C.c_void_p), ("u_min", C.c_void_p), ("u_max", C.c_void_p),
-        ("box_rho", C.c_double), ("sensed", C.c_void_p),
+        ("box_rho", C.c_double), ("sensed", C.c_void_p), ("part_ctr", C.c_void_p),
     ]
 
 
@@ -147,6 +147,8 @@ class Oracle:
             v = getattr(sc, name, None)  # NEXT f1: boxes of Eq. 13c-d (None = unbounded)
             setattr(P, name, None if v is None else k(name, _f64(v).reshape(n)))
         P.box_rho = float(getattr(sc, "box_rho", 0.0))
+        ctr = getattr(sc, "part_ctr", None)  # NEXT f3: per-part scaling centres (None = body origin)
+        P.part_ctr = None if ctr is None else k("part_ctr", _f64(ctr).reshape(-1, sc.dim))
         self.sensed = None  # NEXT f3 sensing: obstacles meeting the box rho(s0) + [-h, h]
         half = getattr(sc, "sense_half", None)
         if half is not None and sc.n_obs > 0:

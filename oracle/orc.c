@@ -416,6 +416,26 @@ static int sensed(const orc_problem* P, int b, int j) {
   return !P->sensed || P->sensed[(long long)b * P->n_obs + j];
 }
 
+/* Part i about its scaling centre o_i (reading #22; NEXT f3): b~ = b - A o_i and the
+ * pair origin rho_i = rho + R o_i.  Without centres b~ = b, rho_i = rho. */
+static void part_frame(const orc_problem* P, int i, const double* R, const double* rho, double* bt,
+                       double* rho_i) {
+  int d = P->dim, r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
+  const double* o = P->part_ctr ? P->part_ctr + (long long)i * d : NULL;
+  for (int k = 0; k < nr; ++k) {
+    double v = P->part_b[r0 + k];
+    if (o)
+      for (int a = 0; a < d; ++a) v -= P->part_A[(long long)(r0 + k) * d + a] * o[a];
+    bt[k] = v;
+  }
+  for (int a = 0; a < d; ++a) {
+    double v = rho[a];
+    if (o)
+      for (int c = 0; c < d; ++c) v += R[a * d + c] * o[c];
+    rho_i[a] = v;
+  }
+}
+
 /* Sensing (NEXT f3): obstacle (b, j) is sensed iff it meets the
  * axis-aligned box rho(s0_b) + [-half, half] (world frame) -- i.e. iff the scale
  * factor alpha* (Eq. 3) of that box as a "robot part" against the obstacle is <= 1
@@ -536,7 +556,9 @@ void orc_init_iterate(const orc_problem* P, orc_iterate* I) {
     int i = (int)((p / P->n_obs) % P->n_parts);
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
     double sb = 0.0;
-    for (int k = 0; k < nr; ++k) sb += P->part_b[r0 + k];
+    double bt[MAXN], R0[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, z0[3] = {0, 0, 0}, r_[3];
+    part_frame(P, i, R0, z0, bt, r_);
+    for (int k = 0; k < nr; ++k) sb += bt[k];
     for (int k = 0; k < P->ny; ++k) I->y[p * P->ny + k] = (k < nr) ? 1.0 / sb : 0.0;
     I->zeta[p] = 0.0;
     for (int a = 0; a < d; ++a) I->xi[p * d + a] = 0.0;
@@ -581,8 +603,10 @@ long long orc_dual_sweep(const orc_problem* P, orc_iterate* I, double* rdual) {
     double ynew[MAXN];
     int piv;
     double rj[3];
-    obstacle_frame(P, b, j, t, rho, rj);
-    int st = orc_pair_solve(d, nr, P->part_A + (long long)r0 * d, P->part_b + r0, no,
+    double bt[MAXN], rhoi[3];
+    part_frame(P, i, R, rho, bt, rhoi);
+    obstacle_frame(P, b, j, t, rhoi, rj);
+    int st = orc_pair_solve(d, nr, P->part_A + (long long)r0 * d, bt, no,
                             P->obs_C + (long long)l0 * d, P->obs_d + l0, R, rj, I->zeta[p],
                             I->xi + p * d, P->prox_eps, I->y + p * P->ny, P->pivot_tol,
                             P->tie_tol, P->max_pivot_factor, ynew, &piv, NULL);
@@ -655,8 +679,9 @@ static void scene_aggregates(const orc_problem* P, const orc_iterate* I, int b, 
         long long p = (((long long)b * N + (t - 1)) * P->n_parts + i) * P->n_obs + j;
         int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
         int n = nr + no + 1;
-        double K[MAXN * (MAXD + 1)], rj[3];
-        obstacle_frame(P, b, j, t, rho, rj);
+        double K[MAXN * (MAXD + 1)], rj[3], bt[MAXN], rhoi[3];
+        part_frame(P, i, R, rho, bt, rhoi);
+        obstacle_frame(P, b, j, t, rhoi, rj);
         orc_build_K(d, nr, P->part_A + (long long)r0 * d, no, P->obs_C + (long long)l0 * d,
                     P->obs_d + l0, R, rj, K);
         const double* y = I->y + p * P->ny;
@@ -686,6 +711,18 @@ static void scene_aggregates(const orc_problem* P, const orc_iterate* I, int b, 
           for (int a = 0; a < d; ++a) { gg2 += gg[a] * gg[a]; ge += gg[a] * eR[a]; }
           St[d * npc + d] += gg2;
           gt[d] += ge;
+          if (P->part_ctr) {
+            /* scaling centre (reading #22): T depends on theta through rho_i = rho + R o_i,
+             * dT/dtheta = tau = -v^T (dR/dtheta) o_i = -w^T G o_i = w_0 o_1 - w_1 o_0 */
+            const double* oc = P->part_ctr + (long long)i * d;
+            double tau = wv[0] * oc[1] - wv[1] * oc[0];
+            for (int a = 0; a < d; ++a) {
+              St[a * npc + d] += -v[a] * tau;
+              St[d * npc + a] += -v[a] * tau;
+            }
+            St[d * npc + d] += tau * tau;
+            gt[d] += tau * eT;
+          }
         }
       }
     }
@@ -872,8 +909,9 @@ void orc_multiplier_update(const orc_problem* P, orc_iterate* I, double* rpri) {
     const double* lam = y;
     const double* mu = y + nr;
     double gam = y[nr + no];
-    double T = 1.0, rj[3];
-    obstacle_frame(P, b, j, t, rho, rj);
+    double T = 1.0, rj[3], bt[MAXN], rhoi[3];
+    part_frame(P, i, R, rho, bt, rhoi);
+    obstacle_frame(P, b, j, t, rhoi, rj);
     for (int l = 0; l < no; ++l) {
       double cr = 0.0;
       for (int a = 0; a < d; ++a) cr += P->obs_C[(long long)(l0 + l) * d + a] * rj[a];
@@ -945,8 +983,10 @@ long long orc_scale_detect(const orc_problem* P, const double* s, double* alpha)
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
     int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
     double rj[3];
-    obstacle_frame(P, b, j, t, rho, rj);
-    if (orc_scale_lp(d, nr, P->part_A + (long long)r0 * d, P->part_b + r0, R, rj, no,
+    double bt[MAXN], rhoi[3];
+    part_frame(P, i, R, rho, bt, rhoi);
+    obstacle_frame(P, b, j, t, rhoi, rj);
+    if (orc_scale_lp(d, nr, P->part_A + (long long)r0 * d, bt, R, rj, no,
                      P->obs_C + (long long)l0 * d, P->obs_d + l0, alpha + p, NULL) != 0) {
       alpha[p] = NAN;
       ++bad;

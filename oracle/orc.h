@@ -68,6 +68,11 @@ typedef struct {
    * obstacle leave the (i, j, t) table (no dual step, no aggregate, no multiplier
    * update, alpha = +inf).  orc_sense() fills it from the sensing box. */
   const unsigned char* sensed;
+  /* Per-part scaling centres (NEXT f3; reading #22): NULL = every part scales about the
+   * body origin, else [n_parts][dim] body-frame points o_i strictly inside their parts.
+   * Part i is then the polytope A_i (x - o_i) <= b~_i, b~_i = b_i - A_i o_i, scaled about
+   * o_i: its pairs use b~_i and the origin rho_i(s) = rho(s) + R(s) o_i. */
+  const double* part_ctr;
 } orc_problem;
 
 typedef struct {

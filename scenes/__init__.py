@@ -44,6 +44,7 @@ CONFIG_NAMES = {
     7: "C2n: C2 with the unicycle relinearised at every ADMM iterate (SQP, NEXT f2), N=50, K=200",
     8: "C2b: C2 with state/control boxes (|a| <= 0.5, |om| <= 1.5, 2.5 <= v <= 3.5; NEXT f1), N=50, K=200",
     9: "C4s: C4m sensing only the vehicles within 60 m x 8 m of the ego (P:541; NEXT f3), N=60, K=300",
+    10: "C2t: C2 with a rigid trailer behind the body origin, scaled about its own centre (NEXT f3), N=50, K=200",
 }
 
 
@@ -111,6 +112,9 @@ class Scene:
     # world-aligned box around the robot's current position; only obstacles meeting it
     # enter the (i, j, t) table
     sense_half: Optional[np.ndarray] = None
+    # NEXT f3: per-part scaling centres [n_parts, d] (body frame, strictly inside each
+    # part); None = every part scales about the body origin (reading #22)
+    part_ctr: Optional[np.ndarray] = None
 
     @property
     def n_parts(self) -> int:
@@ -446,6 +450,11 @@ def make_config(cfg: int, **kw) -> Scene:
         return make_c4(moving=True, **kw)
     if cfg == 7:
         return dataclasses.replace(make_c2(**kw), name="C2n", config=7, dyn_model=1)
+    if cfg == 10:
+        sc = make_c2(**kw)
+        part_off, part_A, part_b = _pack([box_hrep([0.0, 0.0], [2.25, 1.0]), box_hrep([-5.0, 0.0], [2.5, 1.1])])
+        return dataclasses.replace(sc, name="C2t", config=10, part_off=part_off, part_A=part_A, part_b=part_b,
+                                   part_ctr=np.array([[0.0, 0.0], [-5.0, 0.0]]))
     if cfg == 9:
         return dataclasses.replace(make_c4(moving=True, **kw), name="C4s", config=9, sense_half=np.array([60.0, 8.0]))
     if cfg == 8:

@@ -85,6 +85,8 @@ def pair_residual(sc, y, zeta, xi, b, t, i, j, st):
     """r_p(s_t) = (T_p + zeta, R_p + xi) from the geometric definitions."""
     d = sc.dim
     R, rho = pose_of(sc, st)
+    if getattr(sc, "part_ctr", None) is not None:  # part scaled about its centre o_i (NEXT f3)
+        rho = rho + R @ sc.part_ctr[i]
     A = sc.part_A[sc.part_off[i]:sc.part_off[i + 1]]
     o = b * sc.n_obs + j
     Cm = sc.obs_C[sc.obs_off[o]:sc.obs_off[o + 1]]
@@ -96,7 +98,7 @@ def pair_residual(sc, y, zeta, xi, b, t, i, j, st):
     return np.r_[T + zeta, Rr + xi]
 
 
-@pytest.mark.parametrize("cfg", [2, 3])
+@pytest.mark.parametrize("cfg", [2, 3, 10])
 def test_gn_primal_step_vs_fd_least_squares(orc, cfg):
     sc = scenes.make_config(cfg)
     o = orc.Oracle(sc)
