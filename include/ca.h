@@ -36,7 +36,7 @@ enum {
   CA_OK = 0,
   CA_E_INVALID = -1,     /* null pointer, non-positive size, bad parameter */
   CA_E_DIM = -2,         /* d not in {2,3}; n = n_r + n_o + 1 > 32; pose index out of range */
-  CA_E_GEOMETRY = -3,    /* robot part with b_i not > 0 (reading #22) or < d+1 rows */
+  CA_E_GEOMETRY = -3,    /* robot part with b_i (b~_i with part_ctr) not > 0 (reading #22) or < d+1 rows */
   CA_E_UNSUPPORTED = -4, /* unknown pose model, n_state > 8, n_ctrl > 4 */
   CA_E_CUDA = -5,        /* CUDA error / no sm_100 device */
   CA_E_NCCL = -6,
@@ -139,6 +139,12 @@ typedef struct {
    * every step (certificates keep their values, alpha = +inf).  Re-evaluated at every
    * create/load (each MPC step).  NULL = every obstacle. */
   const double* sense_half;
+  /* NEXT f3, per-part scaling centres (reading #22): nullable HOST [n_parts*dim]
+   * body-frame points o_i strictly inside their parts (b~_i = b_i - A_i o_i > 0, else
+   * CA_E_GEOMETRY).  Part i is scaled about o_i instead of the body origin: its pairs
+   * use b~_i and the origin rho(s) + R(s) o_i (Eq. 3-11 unchanged otherwise), so parts
+   * that do not contain the body origin (a trailer) are allowed.  NULL = origin. */
+  const double* part_ctr;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;

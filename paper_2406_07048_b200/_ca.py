@@ -41,7 +41,7 @@ class Desc(C.Structure):
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("dyn_model", C.c_int32), ("dt", C.c_double),
         ("s_min", C.c_void_p), ("s_max", C.c_void_p), ("u_min", C.c_void_p), ("u_max", C.c_void_p),
-        ("box_rho", C.c_double), ("sense_half", C.c_void_p),
+        ("box_rho", C.c_double), ("sense_half", C.c_void_p), ("part_ctr", C.c_void_p),
     ]
 
 
@@ -173,6 +173,8 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
     D.box_rho = float(getattr(sc, "box_rho", 0.0))
     half = getattr(sc, "sense_half", None)  # NEXT f3 sensing box (None = every obstacle)
     D.sense_half = None if half is None else k("sense_half", _f64(half).reshape(sc.dim))
+    ctr = getattr(sc, "part_ctr", None)  # NEXT f3 per-part scaling centres (None = body origin)
+    D.part_ctr = None if ctr is None else k("part_ctr", _f64(ctr).reshape(-1, sc.dim))
     return D
 
 

@@ -217,7 +217,14 @@ ca_status validate(const ca_problem_desc* D) {
     const int r0 = D->part_off[i], nr = D->part_off[i + 1] - r0;
     if (nr < d + 1) return fail(CA_E_GEOMETRY, "robot part with fewer than d+1 faces");
     for (int k = 0; k < nr; ++k)
-      if (!(D->part_b[r0 + k] > 0.0)) return fail(CA_E_GEOMETRY, "robot part b_i must be > 0 (body origin inside)");
+      {
+        double bt = D->part_b[r0 + k];  // b~ = b - A o_i with a scaling centre (NEXT f3)
+        if (D->part_ctr)
+          for (int a = 0; a < d; ++a) bt -= D->part_A[(r0 + k) * d + a] * D->part_ctr[i * d + a];
+        if (!(bt > 0.0))
+          return fail(CA_E_GEOMETRY, D->part_ctr ? "robot part: its scaling centre must lie strictly inside"
+                                                 : "robot part b_i must be > 0 (body origin inside)");
+      }
     nrmax = std::max(nrmax, nr);
   }
   int nomax = 0;
@@ -247,6 +254,9 @@ ca_status validate(const ca_problem_desc* D) {
     if (finite && !(D->box_rho > 0.0 && std::isfinite(D->box_rho)))
       return fail(CA_E_INVALID, "box_rho must be > 0 with finite bounds");
   }
+  if (D->part_ctr)
+    for (int k = 0; k < D->n_parts * d; ++k)
+      if (!std::isfinite(D->part_ctr[k])) return fail(CA_E_INVALID, "part_ctr must be finite");
   if (D->sense_half)
     for (int a = 0; a < d; ++a)
       if (!(D->sense_half[a] > 0.0 && std::isfinite(D->sense_half[a])))
@@ -310,6 +320,15 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
   ca_status st;
   if ((st = h2d(h, const_cast<double*>(v.part_rows), pr.data(), pr.size()))) return st;
   if ((st = h2d(h, const_cast<int*>(v.part_off), D->part_off, (size_t)h->np + 1))) return st;
+  if (v.part_ctr) {  // scaling centres (NEXT f3): b~ = b - A o_i on the device
+    std::vector<double> oc(3 * (size_t)h->np, 0.0);
+    for (int i = 0; i < h->np; ++i)
+      for (int a = 0; a < d; ++a) oc[3 * i + a] = D->part_ctr[i * d + a];
+    if ((st = h2d(h, const_cast<double*>(v.part_ctr), oc.data(), oc.size()))) return st;
+    ca::k_part_centre<<<1, 32, 0, h->stream>>>(v, const_cast<double*>(v.part_rows));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(h->stream));  // oc is a stack vector
+  }
   ca::k_lamtab<<<1, 32, 0, h->stream>>>(v);
   CUDA_TRY(cudaGetLastError());
   if (d == 2) {  // polygon vertices for the separating-axis scale detection
@@ -748,6 +767,7 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   AL(v.part_be, double, (size_t)h->np);
   v.box = (D->s_min || D->s_max || D->u_min || D->u_max) ? 1 : 0;
   v.box_rho = D->box_rho;
+  if (D->part_ctr) AL(v.part_ctr, double, 3 * (size_t)h->np);  // NEXT f3 scaling centres
   if (D->sense_half && h->M > 0) {  // NEXT f3 sensing mask + its box
     uint8_t* m_ = nullptr;
     if ((st = h->alloc(&m_, (size_t)B * h->M))) return st;
@@ -863,6 +883,8 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
       return fail(CA_E_INVALID, "ca_problem_load: obstacle row counts differ");
   if ((D->s_min || D->s_max || D->u_min || D->u_max) != (h->dev.box != 0))
     return fail(CA_E_INVALID, "ca_problem_load: box presence differs from the handle");
+  if ((D->part_ctr != nullptr) != (h->dev.part_ctr != nullptr))
+    return fail(CA_E_INVALID, "ca_problem_load: scaling-centre presence differs from the handle");
   if ((D->sense_half && h->M > 0) != (h->dev.sensed != nullptr))
     return fail(CA_E_INVALID, "ca_problem_load: sensing presence differs from the handle");
   return mark(h, upload(h, D));

@@ -92,7 +92,24 @@ struct Dev {
   // sensing (NEXT f3): NULL = every obstacle, else [B*M] 0/1 from
   // k_sense -- pairs of unsensed obstacles leave the (i, j, t) table
   const uint8_t* sensed;
+  // per-part scaling centres (NEXT f3, reading #22): NULL = body origin, else [np][3]
+  // body-frame o_i; part_rows then hold b~ = b - A o_i (k_part_centre) and the pairs
+  // of part i use the origin rho_i = rho + R o_i
+  const double* part_ctr;
 };
+// rho <- rho + R o_i (part i's scaling centre), R row-major D x D
+template <int DD>
+__device__ __forceinline__ void part_origin(const Dev& P, int i, const double* R, double* rho) {
+  if (!P.part_ctr) return;
+  const double* o = P.part_ctr + 3 * i;
+#pragma unroll
+  for (int a = 0; a < DD; ++a) {
+    double v = rho[a];
+#pragma unroll
+    for (int c = 0; c < DD; ++c) v += R[a * DD + c] * o[c];
+    rho[a] = v;
+  }
+}
 __device__ __forceinline__ bool is_sensed(const Dev& P, int b, int j) {
   return !P.sensed || P.sensed[(long long)b * P.M + j];
 }
@@ -216,6 +233,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
     const long long p = bt * P.G + g, PP = P.P;
     double sR[9], srho[3];  // pose(s_t^{k+1}): the trajectory the last primal step produced
     pose_of(P, P.s + ((long long)it.b * (P.N + 1) + t) * P.ns, sR, srho);
+    part_origin<D>(P, i, sR, srho);
     obstacle_frame<D>(P, it.b, j, t, srho);
     const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
     const int o = it.b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
@@ -1049,6 +1067,7 @@ __global__ void __launch_bounds__(128) k_scale2(Dev P, const double* states, dou
     alpha[q] = INFINITY;
     return;
   }
+  part_origin<2>(P, i, R, rho);
   obstacle_frame<2>(P, b, j, t, rho);
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
   const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
@@ -1097,7 +1116,8 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
   const int r0 = P.part_off[i], nr = P.part_off[i + 1] - r0;
   const int o = b * P.M + j, l0 = P.obs_off[o], no = P.obs_off[o + 1] - l0;
   const int m = nr + no;
-  double rho[3] = {srho[0], srho[1], srho[2]};  // this pair's origin (moving obstacles)
+  double rho[3] = {srho[0], srho[1], srho[2]};  // this pair's origin (centre, moving obstacles)
+  part_origin<D>(P, i, sR, rho);
   obstacle_frame<D>(P, b, j, t, rho);
   double* Gr = smem + tid;  // rows [m][D+2] (g_0..g_D, h), stride CTA
 #define GR(r_, c_) Gr[((r_) * (D + 2) + (c_)) * CTA]
@@ -1188,6 +1208,18 @@ __global__ void __launch_bounds__(CTA) k_scale(Dev P, const double* states, doub
 // deterministic, results are stored at each pair's own index.
 // Eqs. 20-21 for the lambda rows depend on the robot part only (once per load):
 //   e = argmax_k b_k (lowest k on ties), kt_k = b_k / b_e, at_k = a_k - kt_k a_e
+// b~ = b - A o_i for every row of part i (scaling centres, NEXT f3), in place
+__global__ void k_part_centre(Dev P, double* rows) {
+  const int ip = threadIdx.x;
+  if (ip >= P.np || !P.part_ctr) return;
+  const double* o = P.part_ctr + 3 * ip;
+  for (int r = P.part_off[ip]; r < P.part_off[ip + 1]; ++r) {
+    double v = rows[4 * r + 3];
+    for (int a = 0; a < P.d; ++a) v -= rows[4 * r + a] * o[a];
+    rows[4 * r + 3] = v;
+  }
+}
+
 __global__ void k_lamtab(Dev P) {
   const int ip = threadIdx.x;
   if (ip >= P.np) return;

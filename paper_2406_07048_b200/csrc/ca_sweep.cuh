@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     for (int a = 0; a < D * D; ++a) sR[a] = po[a];
 #pragma unroll
     for (int a = 0; a < D; ++a) srho[a] = po[9 + a];
+    part_origin<D>(P, ip, sR, srho);                           // scaling centre (NEXT f3)
     obstacle_frame<D>(P, b, j, it.grp * P.TG + tl + 1, srho);  // moving obstacles (NEXT f3)
 #pragma unroll 1
     for (int lo = 0; lo < no; ++lo) {
@@ -723,6 +724,14 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       const double g0 = vb[1], g1 = -vb[0];
       rec[sym_idx(D, D, L1)] = g0 * g0 + g1 * g1;
       rec[L1 * (L1 + 1) / 2 + D] = g0 * eR[0] + g1 * eR[1];
+      if (P.part_ctr) {  // scaling centre: dT/dtheta = vb_0 o_1 - vb_1 o_0 (reading #22)
+        const double* oc = P.part_ctr + 3 * ip;
+        const double tau = vb[0] * oc[1] - vb[1] * oc[0];
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[sym_idx(a, D, L1)] = -v[a] * tau;
+        rec[sym_idx(D, D, L1)] += tau * tau;
+        rec[L1 * (L1 + 1) / 2 + D] += tau * eT;
+      }
     }
   }
 #undef VAL

@@ -72,6 +72,9 @@ def test_validation_errors_precede_device(ca):
     assert _create(ca, dataclasses.replace(c2b, box_rho=0.0))[0] == -1
     assert _create(ca, dataclasses.replace(c2b, u_min=np.array([1.0, -1.0])))[0] == -1
     assert _create(ca, dataclasses.replace(c2b, s_max=np.array([np.nan, 1, 1, 1])))[0] == -1
+    c2t = scenes.make_config(10)  # scaling centres (NEXT f3): the trailer needs its own
+    assert _create(ca, dataclasses.replace(c2t, part_ctr=None))[0] == -3
+    assert _create(ca, dataclasses.replace(c2t, part_ctr=np.array([[0.0, 0.0], [3.0, 0.0]])))[0] == -3
 
 
 @pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="GPU present")
