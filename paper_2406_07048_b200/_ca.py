@@ -90,7 +90,9 @@ def lib():
         L.ca_get_trajectory.argtypes = [vp, vp, vp]
         L.ca_get_pair_state.argtypes = [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp, vp]
         L.ca_set_iterate.argtypes = [vp, vp, vp, vp, vp, vp]
-        L.ca_get_box_state.argtypes = [vp, vp, vp, vp, vp, vp]
+        if hasattr(L, "ca_get_box_state") or not os.environ.get("CA_LIBRARY"):  # older tuning builds lack it
+            L.ca_get_box_state.argtypes = [vp, vp, vp, vp, vp, vp]
+            L.ca_get_box_state.restype = C.c_int32
         L.ca_kernel_times.argtypes = [vp, dp, i64p, C.c_int32]
         L.ca_set_timing.argtypes = [vp, C.c_int32]
         L.ca_set_record_basis.argtypes = [vp, C.c_int32]
@@ -106,8 +108,7 @@ def lib():
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
                      "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace",
-                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size",
-                     "ca_get_box_state"):
+                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib

@@ -428,12 +428,17 @@ __global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
 }
 #endif  // CA_COMMON_KERNELS
 
-// Large batches: one thread per scene (throughput), stage blocks from k_stage in
-// global memory; the same arithmetic per entry as the warp version below.
+// One scene's Riccati recursion (Eq. 16 as an LQ with the GN stage blocks) and
+// forward rollout, run by ONE thread with every matrix in registers: stage blocks
+// stg[t-1] = (H_t, h_t), dynamics A_t = A0 + t*sA, B_t = B0 + t*sB, c_t = c0 + t*sC
+// (strides 0: time-invariant), statistics stats[t-1][4]; gains go to ric[N][NU][NS+1].  Used by
+// k_riccati_thread (global-memory operands, large batches) and by k_riccati's lane 0
+// (shared-memory operands, small batches) -- one arithmetic, bitwise-equal results.
 template <int NS, int NU>
-__global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= P.B) return;
+__device__ __forceinline__ void riccati_serial(const Dev& P, int b, const double* stg, const double* A0,
+                                               const double* B0, const double* c0, long long sA, long long sB,
+                                               long long sC, const double* stats, double* ric, double* dst_cur,
+                                               double* dst_prev) {
   const int N = P.N;
   double Pm[NS][NS], pv[NS];
   double st[4] = {0, 0, 0, 0};
@@ -447,24 +452,19 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
   }
   const double box_res_prev = P.box ? P.box_res[b] : 0.0;
   for (int t = 1; t <= N; ++t) {
-    const double* so = P.stg_stats + ((long long)b * N + (t - 1)) * 4;
+    const double* so = stats + (long long)(t - 1) * 4;
 #pragma unroll
     for (int f = 0; f < 4; ++f) st[f] += so[f];
   }
   // stage cost of time t (1..N), assembled by k_stage
   auto stage = [&](int t, double H[NS][NS], double h[NS]) {
-    const double* in = P.stg + ((long long)b * N + (t - 1)) * (NS * NS + NS);
+    const double* in = stg + (long long)(t - 1) * (NS * NS + NS);
 #pragma unroll
     for (int a = 0; a < NS; ++a) {
       h[a] = in[NS * NS + a];
 #pragma unroll
       for (int c = 0; c < NS; ++c) H[a][c] = in[a * NS + c];
     }
-  };
-  auto dynp = [&](const double* base, int t, int blk) {
-    const long long nt = P.dyn_pt ? N : 1;
-    const long long idx = (P.dyn_ps ? (long long)b * nt : 0) + (P.dyn_pt ? t : 0);
-    return base + idx * blk;
   };
   {
     double H[NS][NS], h[NS];
@@ -476,11 +476,10 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
       for (int c = 0; c < NS; ++c) Pm[a][c] = H[a][c];
     }
   }
-  double* ric = P.ric + (long long)b * N * NU * (NS + 1);
   for (int t = N - 1; t >= 0; --t) {
-    const double* A = dynp(P.dynA, t, NS * NS);
-    const double* Bm = dynp(P.dynB, t, NS * NU);
-    const double* cv = dynp(P.dync, t, NS);
+    const double* A = A0 + t * sA;
+    const double* Bm = B0 + t * sB;
+    const double* cv = c0 + t * sC;
     double H[NS][NS], h[NS];
     if (t >= 1) {
       stage(t, H, h);
@@ -626,9 +625,9 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
     sb[a] = x[a];
   }
   for (int t = 0; t < N; ++t) {
-    const double* A = dynp(P.dynA, t, NS * NS);
-    const double* Bm = dynp(P.dynB, t, NS * NU);
-    const double* cv = dynp(P.dync, t, NS);
+    const double* A = A0 + t * sA;
+    const double* Bm = B0 + t * sB;
+    const double* cv = c0 + t * sC;
     double uu[NU];
 #pragma unroll
     for (int a = 0; a < NU; ++a) {
@@ -679,6 +678,21 @@ __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
   if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
 }
 
+
+// Large batches: one thread per scene (throughput), stage blocks from k_stage in
+// global memory.
+template <int NS, int NU>
+__global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  const int N = P.N;
+  const long long nt = P.dyn_pt ? N : 1, i0 = P.dyn_ps ? (long long)b * nt : 0;
+  riccati_serial<NS, NU>(P, b, P.stg + (long long)b * N * (NS * NS + NS), P.dynA + i0 * NS * NS,
+                         P.dynB + i0 * NS * NU, P.dync + i0 * NS, P.dyn_pt ? NS * NS : 0, P.dyn_pt ? NS * NU : 0,
+                         P.dyn_pt ? NS : 0, P.stg_stats + (long long)b * N * 4,
+                         P.ric + (long long)b * N * NU * (NS + 1), dst_cur, dst_prev);
+}
+
 // shared-memory footprint of k_riccati (doubles): stage blocks, stats, dynamics, gains
 __host__ __device__ inline long long riccati_smem_doubles(int N, int NS, int NU, bool dyn_pt) {
   return (long long)N * (NS * NS + NS) + 4LL * N + (dyn_pt ? N : 1) * (NS * NS + NS * NU + NS) +
@@ -713,6 +727,18 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
     for (int k = lane; k < nd * NS; k += 32) sdyn[(k / NS) * DB + NS * NS + NS * NU + k % NS] = P.dync[idx0 * NS + k];
   }
   __syncwarp();
+  // The recursion is a chain of small dependent products.  For n_s <= 4 one thread
+  // with every matrix in registers and its operands in shared memory is fastest
+  // (C4: 126 vs 135 us per ADMM iteration); larger states would spill, so they split
+  // each step over the lanes in three phases (C3: 229 vs 480 us).
+  if constexpr (NS <= 4) {
+    if (lane == 0) {
+      const long long ds = P.dyn_pt ? DB : 0;
+      riccati_serial<NS, NU>(P, b, sstg, sdyn, sdyn + NS * NS, sdyn + NS * NS + NS * NU, ds, ds, ds, sst, ric,
+                             dst_cur, dst_prev);
+    }
+    return;
+  }
   // 2 Qu of this lane's phase-2 entry (kept in a register)
   // this lane's upper-triangle entries (row-major order), decoded once
   int tri_row[2] = {0, 0}, tri_col[2] = {0, 0};

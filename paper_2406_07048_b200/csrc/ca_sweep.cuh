@@ -17,7 +17,8 @@
 // shared-memory slot / local memory.  Rare cases (multi-way ties, an ineligible
 // provisional minimum, failures, unverified answers) leave the pivot loop for the
 // warp-cooperative dense Lemke, so the loop's instruction footprint and register
-// pressure stay small; the pivot trace is a separate kernel variant (TRACE).
+// pressure stay small; the pivot trace and the scaling-centre terms are a separate
+// kernel variant (TRACE).
 #pragma once
 #include "ca_kernels.cuh"
 #include "ca_lemke.cuh"
@@ -271,7 +272,11 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   bool z0b = false, fallback = false;
   const uint32_t pk = (tid < P.CHG && gs < it.size) ? P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs]
                                                     : PAIR_UNSENSED;
+#ifndef CA_EXP_NO_SENSE
   const bool act = !(pk & PAIR_UNSENSED);  // padding lane or unsensed obstacle (NEXT f3): idle
+#else
+  const bool act = tid < P.CHG && gs < it.size;
+#endif
   if (act) {
     int j;
     unpack_pair(pk, tl, ip, j);
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     for (int a = 0; a < D * D; ++a) sR[a] = po[a];
 #pragma unroll
     for (int a = 0; a < D; ++a) srho[a] = po[9 + a];
-    part_origin<D>(P, ip, sR, srho);                           // scaling centre (NEXT f3)
+    if constexpr (TRACE) part_origin<D>(P, ip, sR, srho);      // scaling centre (NEXT f3)
     obstacle_frame<D>(P, b, j, it.grp * P.TG + tl + 1, srho);  // moving obstacles (NEXT f3)
 #pragma unroll 1
     for (int lo = 0; lo < no; ++lo) {
@@ -724,7 +729,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       const double g0 = vb[1], g1 = -vb[0];
       rec[sym_idx(D, D, L1)] = g0 * g0 + g1 * g1;
       rec[L1 * (L1 + 1) / 2 + D] = g0 * eR[0] + g1 * eR[1];
-      if (P.part_ctr) {  // scaling centre: dT/dtheta = vb_0 o_1 - vb_1 o_0 (reading #22)
+      if (TRACE && P.part_ctr) {  // scaling centre: dT/dtheta = vb_0 o_1 - vb_1 o_0 (reading #22)
         const double* oc = P.part_ctr + 3 * ip;
         const double tau = vb[0] * oc[1] - vb[1] * oc[0];
 #pragma unroll
@@ -746,9 +751,10 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
 }
 
 // host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build).
-// The pivot-trace variant (TRACE) is a separate kernel, launched only while a
-// ca_debug_trace request is armed, so the production pivot loop carries no
-// diagnostic code.
+// The extended variant (TRACE) is a separate kernel, launched only while a
+// ca_debug_trace request is armed or the problem has per-part scaling centres, so
+// the production kernel carries neither the diagnostic code nor the centre terms
+// (2 % of the C5 sweep when compiled in).
 template <int D, int NM, bool F, bool T>
 cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 #ifndef CA_EXP_SMEM_PAD
@@ -784,8 +790,8 @@ cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 
 template <int D, int NM, bool F>
 cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
-  return (P.dbg_p >= 0) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
-                        : sweep_launch_v<D, NM, F, false>(P, grid, stream);
+  return (P.dbg_p >= 0 || P.part_ctr) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
+                                      : sweep_launch_v<D, NM, F, false>(P, grid, stream);
 }
 
 #define CA_SWEEP_NMAX_LIST(X, D, F) X(D, 9, F) X(D, 11, F) X(D, 13, F) X(D, 15, F) X(D, 20, F) X(D, 32, F)
