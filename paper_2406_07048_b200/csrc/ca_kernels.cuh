@@ -717,14 +717,50 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   double* ric = sdyn + (long long)nd * DB;  // [N][NU][NS+1]: feedback K_t | k_t
   // recursion work area (static): value function, products, gains
   __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Qux[NU][NS + 1], xs[NS], xs2[NS];
-  for (int t = lane; t < N; t += 32)
-    stage_block(P, recs, nchunk, (long long)b * N + t, sstg + (long long)t * SB, sst + 4LL * t);
+  // stage blocks: each lane sums the records of two timesteps (all loads in flight
+  // before either block is assembled), same chunk order as stage_block
+  for (int t0 = lane; t0 < N; t0 += 64) {
+    const int t1 = t0 + 32;
+    double ra[REC], rb[REC];
+#pragma unroll
+    for (int f = 0; f < REC; ++f) ra[f] = rb[f] = 0.0;
+    const long long q0 = (long long)b * N + t0, q1 = q0 + 32;
+    for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
+      const double* r0 = recs + (nchunk ? rec_index(P, b, t0 + 1, c) : q0) * REC;
+      const double* r1 = recs + (nchunk ? rec_index(P, b, min(t1, N - 1) + 1, c) : min(q1, q0 - t0 + N - 1)) * REC;
+#pragma unroll
+      for (int f = 0; f < REC; ++f) {
+        ra[f] += __ldg(r0 + f);
+        rb[f] += __ldg(r1 + f);
+      }
+    }
+    stage_assemble(P, q0, ra, sstg + (long long)t0 * SB, sst + 4LL * t0);
+    if (t1 < N) stage_assemble(P, q1, rb, sstg + (long long)t1 * SB, sst + 4LL * t1);
+  }
   {
+    // dynamics blocks, 8 coalesced loads in flight per lane before their stores (a
+    // load-store loop would serialise one global round trip per element)
     const long long idx0 = P.dyn_ps ? (long long)b * nd : 0;
-    for (int k = lane; k < nd * NS * NS; k += 32) sdyn[(k / (NS * NS)) * DB + k % (NS * NS)] = P.dynA[idx0 * NS * NS + k];
-    for (int k = lane; k < nd * NS * NU; k += 32)
-      sdyn[(k / (NS * NU)) * DB + NS * NS + k % (NS * NU)] = P.dynB[idx0 * NS * NU + k];
-    for (int k = lane; k < nd * NS; k += 32) sdyn[(k / NS) * DB + NS * NS + NS * NU + k % NS] = P.dync[idx0 * NS + k];
+    auto stage_dyn = [&](const double* __restrict__ src, int blk, int off) {
+      constexpr int U = 8;
+      const int tot = nd * blk;
+      for (int k0 = lane; k0 < tot; k0 += 32 * U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + 32 * u;
+          v[u] = (k < tot) ? __ldg(src + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + 32 * u;
+          if (k < tot) sdyn[(k / blk) * DB + off + k % blk] = v[u];
+        }
+      }
+    };
+    stage_dyn(P.dynA + idx0 * NS * NS, NS * NS, 0);
+    stage_dyn(P.dynB + idx0 * NS * NU, NS * NU, NS * NS);
+    stage_dyn(P.dync + idx0 * NS, NS, NS * NS + NS * NU);
   }
   __syncwarp();
   // The recursion is a chain of small dependent products.  For n_s <= 4 one thread
