@@ -257,7 +257,7 @@ def test_c5_full_size_stepwise(ca):
     print("C5 validated Lemke flips:", total_flips)
 
 
-@pytest.mark.parametrize("cfg", [2, 4, 6])
+@pytest.mark.parametrize("cfg", [2, 4, 6, 8, 9, 10])
 def test_obstacle_sharded_world1_nccl(ca, cfg):
     """The obstacle-sharded path (record reduction + ncclAllReduce + replicated Riccati)
     at world size 1 matches the unsharded solve (summation order differs)."""
@@ -422,3 +422,22 @@ def test_sensing_mask_and_sweep(ca, case):
     flips = compare_dual_sweep(sc, s, zeta, xi, st["y"], o.y, st["pivots"], o.pivots, st["status"], o.status)
     assert r.n_fail == fails
     assert r.pivots == o.pivots.sum() or flips
+
+
+def test_load_keeps_feature_presence(ca):
+    """ca_problem_load refuses a problem whose optional features (boxes, sensing,
+    scaling centres) differ from the handle's (their buffers are sized at create),
+    and reloading the same kind of problem re-evaluates them (sensing from the new s0)."""
+    sc = scenes.make_config(9)
+    g = ca.Problem(sc)
+    for bad in (dataclasses.replace(sc, sense_half=None),
+                dataclasses.replace(sc, u_min=np.array([-1.0, -1.0]), u_max=np.array([1.0, 1.0]), box_rho=1.0)):
+        with pytest.raises(ca.CAError):
+            g.load(bad)
+    moved = dataclasses.replace(sc, s0=sc.s0 + np.array([[150.0, 0.0, 0.0, 0.0]]))
+    g.load(moved)
+    alpha, _ = g.scale_detect()
+    o = oracle.Oracle(moved)
+    a_o = o.scale_detect()
+    assert np.array_equal(np.isinf(alpha[: g.n_pairs]), np.isinf(a_o))
+    assert not np.array_equal(np.isinf(a_o), np.isinf(oracle.Oracle(sc).scale_detect()))
