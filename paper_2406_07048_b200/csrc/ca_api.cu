@@ -312,11 +312,6 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
     pr[4 * r + 3] = D->part_b[r];
   }
   const long long orow = (h->M > 0) ? D->obs_off[(long long)B * h->M] : 0;
-  std::vector<double> orr(4 * (size_t)std::max<long long>(orow, 1), 0.0);
-  for (long long r = 0; r < orow; ++r) {
-    for (int a = 0; a < d; ++a) orr[4 * r + a] = D->obs_C[r * d + a];
-    orr[4 * r + 3] = D->obs_d[r];
-  }
   ca_status st;
   if ((st = h2d(h, const_cast<double*>(v.part_rows), pr.data(), pr.size()))) return st;
   if ((st = h2d(h, const_cast<int*>(v.part_off), D->part_off, (size_t)h->np + 1))) return st;
@@ -336,7 +331,14 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
     CUDA_TRY(cudaGetLastError());
   }
   if (h->M > 0) {
-    if ((st = h2d(h, const_cast<double*>(v.obs_rows), orr.data(), 4 * (size_t)orow))) return st;
+    // obstacle rows: C and d straight from the caller's arrays into a staging area
+    // (the certificate array y, rewritten by reset_iterate below), interleaved into
+    // (c_0, c_1, c_2, d) rows on the device
+    double* stg = h->dev.y;
+    if ((st = h2d(h, stg, D->obs_C, (size_t)orow * d))) return st;
+    if ((st = h2d(h, stg + (size_t)orow * d, D->obs_d, (size_t)orow))) return st;
+    ca::k_pack_obs<<<(unsigned)((orow + 255) / 256), 256, 0, h->stream>>>(stg, orow, d, const_cast<double*>(v.obs_rows));
+    CUDA_TRY(cudaGetLastError());
     if ((st = h2d(h, const_cast<int*>(v.obs_off), D->obs_off, (size_t)B * h->M + 1))) return st;
     if (D->obs_step) {  // moving obstacles (NEXT f3)
       if (!h->obs_step_buf && (st = h->alloc(&h->obs_step_buf, (size_t)B * h->M * d))) return st;
@@ -360,32 +362,18 @@ ca_status upload(ca_problem* h, const ca_problem_desc* D) {
   if ((st = h2d(h, const_cast<double*>(v.Qu), D->Qu, (size_t)nu * nu))) return st;
   if ((st = h2d(h, const_cast<double*>(v.s0), D->s0, (size_t)B * ns))) return st;
   if ((st = h2d(h, const_cast<double*>(v.sref), D->s_ref, (size_t)B * (N + 1) * ns))) return st;
-  // iterate: s = s_init (default s_ref) with s_0 = s0; u = 0; lambda = 1/sum(b) 1; rest 0
-  std::vector<double> s0v((size_t)B * (N + 1) * ns);
-  const double* si = D->s_init ? D->s_init : D->s_ref;
-  for (int b = 0; b < B; ++b)
-    for (int t = 0; t <= N; ++t)
-      for (int a = 0; a < ns; ++a)
-        s0v[((size_t)b * (N + 1) + t) * ns + a] = (t == 0) ? D->s0[b * ns + a] : si[((size_t)b * (N + 1) + t) * ns + a];
+  // iterate: s = s_init (default s_ref) with s_0 = s0 (set on the device); u = 0;
+  // lambda = 1/sum(b) 1; rest 0
+  if ((st = h2d(h, h->s_start, D->s_init ? D->s_init : D->s_ref, (size_t)B * (N + 1) * ns))) return st;
+  ca::k_set_s0<<<(unsigned)((B * ns + 127) / 128), 128, 0, h->stream>>>(v, h->s_start);
+  CUDA_TRY(cudaGetLastError());
   // execution order of each (b, t) group: pairs stably sorted by LCP size n so that a
   // warp's 32 threads mostly run the same-size Lemke (pure scheduling; results are
-  // stored at the pair's own index p)
+  // stored at the pair's own index p) -- one thread per scene on the device
   if (h->P > 0) {
-    const int G = h->np * h->M;
-    std::vector<int> perm((size_t)B * G);
-    std::vector<int> key(G);
-    for (int b = 0; b < B; ++b) {
-      int* pb = perm.data() + (size_t)b * G;
-      for (int g = 0; g < G; ++g) {
-        const int i = g / h->M, j = g % h->M;
-        key[g] = (D->part_off[i + 1] - D->part_off[i]) + (D->obs_off[(long long)b * h->M + j + 1] - D->obs_off[(long long)b * h->M + j]);
-        pb[g] = g;
-      }
-      std::stable_sort(pb, pb + G, [&](int a, int c) { return key[a] < key[c]; });
-    }
-    if ((st = h2d(h, const_cast<int*>(v.gperm), perm.data(), perm.size()))) return st;
+    ca::k_gperm<<<(unsigned)((B + 63) / 64), 64, 0, h->stream>>>(v, const_cast<int*>(v.gperm));
+    CUDA_TRY(cudaGetLastError());
   }
-  if ((st = h2d(h, h->s_start, s0v.data(), s0v.size()))) return st;
   if (v.box) {  // [s_min | s_max | u_min | u_max], +-inf where unbounded
     std::vector<double> lim(2 * (size_t)(ns + nu));
     for (int a = 0; a < ns; ++a) {

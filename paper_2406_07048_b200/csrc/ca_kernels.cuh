@@ -1481,6 +1481,44 @@ __global__ void k_sense(Dev P, const double* half, uint8_t* out) {
   out[o] = hit ? 1 : 0;
 }
 
+// Problem upload helpers (pure data movement / scheduling, no method arithmetic):
+// obstacle rows (c_0, c_1, c_2, d) from the staged C [rows][d] and d [rows]
+__global__ void k_pack_obs(const double* stg, long long rows, int d, double* out) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double4 o;
+  o.x = stg[r * d];
+  o.y = stg[r * d + 1];
+  o.z = (d == 3) ? stg[r * d + 2] : 0.0;
+  o.w = stg[rows * d + r];
+  reinterpret_cast<double4*>(out)[r] = o;
+}
+// s_start[b][0] = s0[b]
+__global__ void k_set_s0(Dev P, double* s_start) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.B * P.ns) return;
+  const int b = k / P.ns, a = k % P.ns;
+  s_start[(long long)b * (P.N + 1) * P.ns + a] = P.s0[k];
+}
+// per scene: the G = np*M pair slots of a (b, t) group stably ordered by LCP size
+// n = n_r(i) + n_o(b, j) + 1 (counting sort, n <= 32)
+__global__ void k_gperm(Dev P, int* gperm) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  int cnt[34];
+  for (int k = 0; k < 34; ++k) cnt[k] = 0;
+  const int G = P.G, M = P.M;
+  auto key = [&](int g) {
+    const int i = g / M, j = g % M;
+    const long long o = (long long)b * M + j;
+    return (P.part_off[i + 1] - P.part_off[i]) + (P.obs_off[o + 1] - P.obs_off[o]) + 1;
+  };
+  for (int g = 0; g < G; ++g) cnt[key(g) + 1]++;
+  for (int k = 1; k < 34; ++k) cnt[k] += cnt[k - 1];
+  int* out = gperm + (long long)b * G;
+  for (int g = 0; g < G; ++g) out[cnt[key(g)]++] = g;
+}
+
 // Box block reset (reading #7), one thread per (scene, t), t = 0..N: with
 // clip_iterate (cold start) the iterate's states (t >= 1) and controls are
 // first projected into the box; then w = Pi_box(x), l = 0, and the residual is 0.
