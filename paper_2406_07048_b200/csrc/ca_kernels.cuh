@@ -428,6 +428,175 @@ __global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
 }
 #endif  // CA_COMMON_KERNELS
 
+// Quu^{-1} applied to a column, shared by every Riccati path so their gains agree
+// bitwise.  n_u <= 3: adjugate and one reciprocal of the determinant (Quu is SPD; a
+// short dependency chain: the per-step latency of the small-batch recursion is
+// dominated by this solve); n_u = 4: Cholesky with reciprocal diagonal.
+template <int NU>
+struct QuuSolve {
+  double m[NU][NU];  // adjugate (n_u <= 3) or Cholesky factor (n_u = 4)
+  double inv[NU];    // 1/det in inv[0] (n_u <= 3) or 1/L_jj
+  __device__ __forceinline__ void factor(const double Q[NU][NU]) {
+    if constexpr (NU == 1) {
+      m[0][0] = 1.0;
+      inv[0] = 1.0 / Q[0][0];
+    } else if constexpr (NU == 2) {
+      m[0][0] = Q[1][1];
+      m[0][1] = -Q[0][1];
+      m[1][0] = -Q[1][0];
+      m[1][1] = Q[0][0];
+      inv[0] = 1.0 / (Q[0][0] * Q[1][1] - Q[0][1] * Q[1][0]);
+    } else if constexpr (NU == 3) {
+      m[0][0] = Q[1][1] * Q[2][2] - Q[1][2] * Q[2][1];
+      m[0][1] = Q[0][2] * Q[2][1] - Q[0][1] * Q[2][2];
+      m[0][2] = Q[0][1] * Q[1][2] - Q[0][2] * Q[1][1];
+      m[1][0] = Q[1][2] * Q[2][0] - Q[1][0] * Q[2][2];
+      m[1][1] = Q[0][0] * Q[2][2] - Q[0][2] * Q[2][0];
+      m[1][2] = Q[0][2] * Q[1][0] - Q[0][0] * Q[1][2];
+      m[2][0] = Q[1][0] * Q[2][1] - Q[1][1] * Q[2][0];
+      m[2][1] = Q[0][1] * Q[2][0] - Q[0][0] * Q[2][1];
+      m[2][2] = Q[0][0] * Q[1][1] - Q[0][1] * Q[1][0];
+      inv[0] = 1.0 / (Q[0][0] * m[0][0] + Q[0][1] * m[1][0] + Q[0][2] * m[2][0]);
+    } else {
+#pragma unroll
+      for (int a = 0; a < NU; ++a)
+#pragma unroll
+        for (int c = 0; c < NU; ++c) m[a][c] = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NU; ++jj) {
+        double s = Q[jj][jj];
+#pragma unroll
+        for (int k = 0; k < jj; ++k) s -= m[jj][k] * m[jj][k];
+        const double ljj = sqrt(s);
+        m[jj][jj] = ljj;
+        inv[jj] = 1.0 / ljj;
+#pragma unroll
+        for (int ii = jj + 1; ii < NU; ++ii) {
+          double a = Q[ii][jj];
+#pragma unroll
+          for (int k = 0; k < jj; ++k) a -= m[ii][k] * m[jj][k];
+          m[ii][jj] = a * inv[jj];
+        }
+      }
+    }
+  }
+  // r <- Quu^{-1} r
+  __device__ __forceinline__ void apply(double r[NU]) const {
+    if constexpr (NU <= 3) {
+      double x[NU];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NU; ++c) s = __fma_rn(m[a][c], r[c], s);
+        x[a] = s * inv[0];
+      }
+#pragma unroll
+      for (int a = 0; a < NU; ++a) r[a] = x[a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < NU; ++a) {
+        double s = r[a];
+#pragma unroll
+        for (int k = 0; k < a; ++k) s -= m[a][k] * r[k];
+        r[a] = s * inv[a];
+      }
+#pragma unroll
+      for (int a = NU - 1; a >= 0; --a) {
+        double s = r[a];
+#pragma unroll
+        for (int k = a + 1; k < NU; ++k) s -= m[k][a] * r[k];
+        r[a] = s * inv[a];
+      }
+    }
+  }
+};
+
+// Forward rollout of one scene from s_0 with the gains ric (Eq. 13b holds exactly),
+// the box block's w, l update, and the per-scene statistics -> dst (one thread).
+template <int NS, int NU>
+__device__ __forceinline__ void riccati_forward(const Dev& P, int b, const double* A0, const double* B0,
+                                                const double* c0, long long sA, long long sB, long long sC,
+                                                const double* stats, const double* ric, double* dst_cur,
+                                                double* dst_prev) {
+  const int N = P.N;
+  double st[4] = {0, 0, 0, 0};
+  for (int t = 1; t <= N; ++t) {
+    const double* so = stats + (long long)(t - 1) * 4;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) st[f] += so[f];
+  }
+  double ulo[NU], uhi[NU], urho[NU];
+#pragma unroll
+  for (int a = 0; a < NU; ++a) {
+    ulo[a] = P.box ? P.box_lim[2 * NS + a] : -INFINITY;
+    uhi[a] = P.box ? P.box_lim[2 * NS + NU + a] : INFINITY;
+    urho[a] = (P.box && box_on(ulo[a], uhi[a])) ? P.box_rho : 0.0;
+  }
+  const double box_res_prev = P.box ? P.box_res[b] : 0.0;
+  // forward rollout from s_0 (Eq. 13b holds exactly), then the box block's w, l update
+  double x[NS];
+  double box_res = 0.0;
+  double* sb = P.s + (long long)b * (N + 1) * NS;
+#pragma unroll
+  for (int a = 0; a < NS; ++a) {
+    x[a] = P.s0[b * NS + a];
+    sb[a] = x[a];
+  }
+  for (int t = 0; t < N; ++t) {
+    const double* A = A0 + t * sA;
+    const double* Bm = B0 + t * sB;
+    const double* cv = c0 + t * sC;
+    double uu[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], x[c], s);
+      uu[a] = s;
+      P.u[((long long)b * N + t) * NU + a] = s;
+    }
+    if (P.box) {  // w = Pi_box(u + l), l += u - w
+#pragma unroll
+      for (int a = 0; a < NU; ++a)
+        if (urho[a] != 0.0) {
+          const long long ku = ((long long)b * N + t) * NU + a;
+          box_res += box_update(uu[a], ulo[a], uhi[a], &P.box_wu[ku], &P.box_lu[ku]);
+        }
+    }
+    double xn[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double s = cv[a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(A[a * NS + c], x[c], s);
+#pragma unroll
+      for (int c = 0; c < NU; ++c) s = __fma_rn(Bm[a * NU + c], uu[c], s);
+      xn[a] = s;
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      x[a] = xn[a];
+      sb[(t + 1) * NS + a] = xn[a];
+    }
+    if (P.box) {  // states of t + 1
+      const long long k0 = ((long long)b * (N + 1) + t + 1) * NS;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        const double lo = P.box_lim[a], hi = P.box_lim[NS + a];
+        if (box_on(lo, hi)) box_res += box_update(xn[a], lo, hi, &P.box_ws[k0 + a], &P.box_ls[k0 + a]);
+      }
+    }
+  }
+  if (P.box) P.box_res[b] = box_res;
+  if (dst_cur) {
+    dst_cur[b * 4 + 0] = st[0];
+    dst_cur[b * 4 + 2] = st[2];
+    dst_cur[b * 4 + 3] = st[3];
+  }
+  if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
+}
+
 // One scene's Riccati recursion (Eq. 16 as an LQ with the GN stage blocks) and
 // forward rollout, run by ONE thread with every matrix in registers: stage blocks
 // stg[t-1] = (H_t, h_t), dynamics A_t = A0 + t*sA, B_t = B0 + t*sB, c_t = c0 + t*sC
@@ -441,7 +610,6 @@ __device__ __forceinline__ void riccati_serial(const Dev& P, int b, const double
                                                double* dst_prev) {
   const int N = P.N;
   double Pm[NS][NS], pv[NS];
-  double st[4] = {0, 0, 0, 0};
   // box block (reading #7): control bounds, their penalty on the Quu diagonal
   double ulo[NU], uhi[NU], urho[NU];
 #pragma unroll
@@ -449,12 +617,6 @@ __device__ __forceinline__ void riccati_serial(const Dev& P, int b, const double
     ulo[a] = P.box ? P.box_lim[2 * NS + a] : -INFINITY;
     uhi[a] = P.box ? P.box_lim[2 * NS + NU + a] : INFINITY;
     urho[a] = (P.box && box_on(ulo[a], uhi[a])) ? P.box_rho : 0.0;
-  }
-  const double box_res_prev = P.box ? P.box_res[b] : 0.0;
-  for (int t = 1; t <= N; ++t) {
-    const double* so = stats + (long long)(t - 1) * 4;
-#pragma unroll
-    for (int f = 0; f < 4; ++f) st[f] += so[f];
   }
   // stage cost of time t (1..N), assembled by k_stage
   auto stage = [&](int t, double H[NS][NS], double h[NS]) {
@@ -538,49 +700,16 @@ __device__ __forceinline__ void riccati_serial(const Dev& P, int b, const double
       for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
       qu[a] = s;
     }
-    // Cholesky Quu = L L^T
-    double Lc[NU][NU], Li[NU];
-#pragma unroll
-    for (int a = 0; a < NU; ++a)
-#pragma unroll
-      for (int c = 0; c < NU; ++c) Lc[a][c] = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < NU; ++jj) {
-      double s = Quu[jj][jj];
-#pragma unroll
-      for (int k = 0; k < jj; ++k) s -= Lc[jj][k] * Lc[jj][k];
-      const double ljj = sqrt(s);
-      Lc[jj][jj] = ljj;
-      Li[jj] = 1.0 / ljj;
-#pragma unroll
-      for (int ii = jj + 1; ii < NU; ++ii) {
-        double a = Quu[ii][jj];
-#pragma unroll
-        for (int k = 0; k < jj; ++k) a -= Lc[ii][k] * Lc[jj][k];
-        Lc[ii][jj] = a * Li[jj];
-      }
-    }
-    // K = -Quu^{-1} Qux, k = -Quu^{-1} qu (columns solved with the factor)
+    // K = -Quu^{-1} Qux, k = -Quu^{-1} qu (column by column, QuuSolve)
+    QuuSolve<NU> qs;
+    qs.factor(Quu);
     double Kg[NU][NS + 1];
 #pragma unroll
     for (int c = 0; c <= NS; ++c) {
       double rhs[NU];
 #pragma unroll
       for (int a = 0; a < NU; ++a) rhs[a] = (c < NS) ? Qux[a][c] : qu[a];
-#pragma unroll
-      for (int a = 0; a < NU; ++a) {
-        double s = rhs[a];
-#pragma unroll
-        for (int k = 0; k < a; ++k) s -= Lc[a][k] * rhs[k];
-        rhs[a] = s * Li[a];
-      }
-#pragma unroll
-      for (int a = NU - 1; a >= 0; --a) {
-        double s = rhs[a];
-#pragma unroll
-        for (int k = a + 1; k < NU; ++k) s -= Lc[k][a] * rhs[k];
-        rhs[a] = s * Li[a];
-      }
+      qs.apply(rhs);
 #pragma unroll
       for (int a = 0; a < NU; ++a) Kg[a][c] = -rhs[a];
     }
@@ -615,69 +744,119 @@ __device__ __forceinline__ void riccati_serial(const Dev& P, int b, const double
       for (int c = 0; c < NS; ++c) Pm[a][c] = 0.5 * (Pn[a][c] + Pn[c][a]);
     }
   }
-  // forward rollout from s_0 (Eq. 13b holds exactly), then the box block's w, l update
-  double x[NS];
-  double box_res = 0.0;
-  double* sb = P.s + (long long)b * (N + 1) * NS;
-#pragma unroll
-  for (int a = 0; a < NS; ++a) {
-    x[a] = P.s0[b * NS + a];
-    sb[a] = x[a];
-  }
-  for (int t = 0; t < N; ++t) {
-    const double* A = A0 + t * sA;
-    const double* Bm = B0 + t * sB;
-    const double* cv = c0 + t * sC;
-    double uu[NU];
-#pragma unroll
-    for (int a = 0; a < NU; ++a) {
-      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], x[c], s);
-      uu[a] = s;
-      P.u[((long long)b * N + t) * NU + a] = s;
-    }
-    if (P.box) {  // w = Pi_box(u + l), l += u - w
-#pragma unroll
-      for (int a = 0; a < NU; ++a)
-        if (urho[a] != 0.0) {
-          const long long ku = ((long long)b * N + t) * NU + a;
-          box_res += box_update(uu[a], ulo[a], uhi[a], &P.box_wu[ku], &P.box_lu[ku]);
-        }
-    }
-    double xn[NS];
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      double s = cv[a];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) s = __fma_rn(A[a * NS + c], x[c], s);
-#pragma unroll
-      for (int c = 0; c < NU; ++c) s = __fma_rn(Bm[a * NU + c], uu[c], s);
-      xn[a] = s;
-    }
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      x[a] = xn[a];
-      sb[(t + 1) * NS + a] = xn[a];
-    }
-    if (P.box) {  // states of t + 1
-      const long long k0 = ((long long)b * (N + 1) + t + 1) * NS;
-#pragma unroll
-      for (int a = 0; a < NS; ++a) {
-        const double lo = P.box_lim[a], hi = P.box_lim[NS + a];
-        if (box_on(lo, hi)) box_res += box_update(xn[a], lo, hi, &P.box_ws[k0 + a], &P.box_ls[k0 + a]);
-      }
-    }
-  }
-  if (P.box) P.box_res[b] = box_res;
-  if (dst_cur) {
-    dst_cur[b * 4 + 0] = st[0];
-    dst_cur[b * 4 + 2] = st[2];
-    dst_cur[b * 4 + 3] = st[3];
-  }
-  if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
+  riccati_forward<NS, NU>(P, b, A0, B0, c0, sA, sB, sC, stats, ric, dst_cur, dst_prev);
 }
 
+
+// Backward Riccati recursion of one scene split over the lanes of a warp, for
+// NS^2 + NS NU + NS <= 32.  Per step: X = [P A | P B | P c + p], one entry per lane;
+// [Qux | qu | Quu] = B^T X (+ 2 Qu, box terms), one entry per lane; gains column c
+// (c <= NS) on lane c, every one of those lanes factoring Quu itself; then P and p,
+// one entry per lane.  Operands move by shuffles (no shared-memory round trips, no
+// barriers); every entry keeps the summation order of riccati_serial, so the gains
+// are bitwise those of the one-thread recursion.
+template <int NS, int NU>
+__device__ __forceinline__ void riccati_lanes(const Dev& P, int b, int lane, const double* stg, const double* A0,
+                                              const double* B0, const double* c0, long long ds, double* ric) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int XA = NS * NS, XB = XA + NS * NU, XW = XB + NS;  // X lanes: PA | PB | w
+  constexpr int QX = NU * NS, QQ = QX + NU;                     // Q lanes: Qux | qu | Quu
+  static_assert(XW <= 32 && QQ + NU * NU <= 32, "one entry per lane");
+  const int N = P.N;
+  constexpr int SB = NS * NS + NS;
+  // X-phase role: row xr of P times column xc of A (kind 0) / B (kind 1) / c (kind 2)
+  const int xk = (lane < XA) ? 0 : (lane < XB) ? 1 : 2;
+  const int xr = (lane < XA) ? lane / NS : (lane < XB) ? (lane - XA) / NU : min(lane - XB, NS - 1);
+  const int xc = (lane < XA) ? lane % NS : (lane < XB) ? (lane - XA) % NU : 0;
+  // Q-phase role: Qux[qi][qc] (kind 0), qu[qi] (kind 1), Quu[qi][qc] (kind 2)
+  const int qk = (lane < QX) ? 0 : (lane < QQ) ? 1 : 2;
+  const int qi = (lane < QX) ? lane / NS : (lane < QQ) ? lane - QX : min((lane - QQ) / NU, NU - 1);
+  const int qc = (lane < QX) ? lane % NS : (lane < QQ) ? 0 : (lane - QQ) % NU;
+  // P-phase role: P[pa][pc] on lanes < XA, p[pa] on lanes XB + pa (column NS)
+  const bool isP = lane < XA, isp = lane >= XB && lane < XW;
+  const int pa = isP ? lane / NS : (isp ? lane - XB : 0);
+  const int pc = isP ? lane % NS : NS;
+  double qinit2 = 0.0;  // Quu lanes: 2 Qu (+ rho_b on a bounded control's diagonal)
+  if (qk == 2) {
+    const double lo = P.box ? P.box_lim[2 * NS + qi] : -INFINITY, hi = P.box ? P.box_lim[2 * NS + NU + qi] : INFINITY;
+    const double ur = (P.box && box_on(lo, hi)) ? P.box_rho : 0.0;
+    qinit2 = 2.0 * P.Qu[qi * NU + qc] + ((qi == qc) ? ur : 0.0);
+  }
+  double urho_u = 0.0;  // qu lanes: box penalty of control qi
+  if (qk == 1 && P.box) {
+    const double lo = P.box_lim[2 * NS + qi], hi = P.box_lim[2 * NS + NU + qi];
+    urho_u = box_on(lo, hi) ? P.box_rho : 0.0;
+  }
+  // P_N = H_N, p_N = h_N
+  double pm = 0.0, pval = 0.0;
+  {
+    const double* in = stg + (long long)(N - 1) * SB;
+    if (isP) pm = in[pa * NS + pc];
+    if (isp) pval = in[NS * NS + pa];
+  }
+  for (int t = N - 1; t >= 0; --t) {
+    const double* A = A0 + t * ds;
+    const double* Bm = B0 + t * ds;
+    const double* cv = c0 + t * ds;
+    // X = [P A | P B | P c + p]  (every lane executes every shuffle: no divergent shfl)
+    const double pw = __shfl_sync(FULL, pval, XB + xr);
+    double xv = (xk == 2) ? pw : 0.0;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const double pq = __shfl_sync(FULL, pm, xr * NS + q);
+      const double op = (xk == 0) ? A[q * NS + xc] : (xk == 1) ? Bm[q * NU + xc] : cv[q];
+      xv = __fma_rn(pq, op, xv);
+    }
+    // Qux = B^T PA, qu = r_t + B^T w, Quu = 2 Qu (+ rho_b) + B^T PB
+    double qv = (qk == 2) ? qinit2 : 0.0;
+    if (qk == 1 && urho_u != 0.0) {
+      const long long ku = ((long long)b * N + t) * NU + qi;
+      qv = -urho_u * (P.box_wu[ku] - P.box_lu[ku]);
+    }
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const int src = (qk == 0) ? q * NS + qc : (qk == 1) ? XB + q : XA + q * NU + qc;
+      qv = __fma_rn(Bm[q * NU + qi], __shfl_sync(FULL, xv, src), qv);
+    }
+    // gains: lane c <= NS solves column c of -Quu^{-1} [Qux | qu]
+    double Qm[NU][NU], rhs[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+#pragma unroll
+      for (int j = 0; j < NU; ++j) Qm[i][j] = __shfl_sync(FULL, qv, QQ + i * NU + j);
+      rhs[i] = __shfl_sync(FULL, qv, (lane < NS) ? i * NS + lane : QX + i);
+    }
+    QuuSolve<NU> qs;
+    qs.factor(Qm);
+    qs.apply(rhs);
+    double kg[NU];  // this lane's gains column (lanes c <= NS)
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+      kg[a] = -rhs[a];
+      if (lane <= NS) ric[((long long)t * NU + a) * (NS + 1) + lane] = kg[a];
+    }
+    // P <- sym(H + A^T P A + Qux^T K), p <- h + A^T w + Qux^T k
+    double v = 0.0;
+    if (t >= 1) {
+      const double* in = stg + (long long)(t - 1) * SB;
+      v = isP ? in[pa * NS + pc] : (isp ? in[NS * NS + pa] : 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const double xq = __shfl_sync(FULL, xv, isP ? q * NS + pc : XB + q);
+      v = __fma_rn(A[q * NS + pa], xq, v);
+    }
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const double qka = __shfl_sync(FULL, qv, k * NS + pa);
+      const double kk = __shfl_sync(FULL, kg[k], pc);
+      v = __fma_rn(qka, kk, v);
+    }
+    const double vt = __shfl_sync(FULL, v, isP ? pc * NS + pa : lane);
+    if (isP) pm = 0.5 * (v + vt);
+    if (isp) pval = v;
+  }
+}
 
 // Large batches: one thread per scene (throughput), stage blocks from k_stage in
 // global memory.
@@ -767,12 +946,13 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   // with every matrix in registers and its operands in shared memory is fastest
   // (C4: 126 vs 135 us per ADMM iteration); larger states would spill, so they split
   // each step over the lanes in three phases (C3: 229 vs 480 us).
-  if constexpr (NS <= 4) {
-    if (lane == 0) {
-      const long long ds = P.dyn_pt ? DB : 0;
-      riccati_serial<NS, NU>(P, b, sstg, sdyn, sdyn + NS * NS, sdyn + NS * NS + NS * NU, ds, ds, ds, sst, ric,
-                             dst_cur, dst_prev);
-    }
+  if constexpr (NS * NS + NS * NU + NS <= 32) {
+    const long long ds = P.dyn_pt ? DB : 0;
+    riccati_lanes<NS, NU>(P, b, lane, sstg, sdyn, sdyn + NS * NS, sdyn + NS * NS + NS * NU, ds, ric);
+    __syncwarp();
+    if (lane == 0)
+      riccati_forward<NS, NU>(P, b, sdyn, sdyn + NS * NS, sdyn + NS * NS + NS * NU, ds, ds, ds, sst, ric, dst_cur,
+                              dst_prev);
     return;
   }
   // 2 Qu of this lane's phase-2 entry (kept in a register)
@@ -860,41 +1040,9 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
         qx[a_] = s_;
         Qux[a_][c] = s_;
       }
-      double Lc[NU][NU], Li[NU];  // factor and reciprocal diagonal
-#pragma unroll
-      for (int a_ = 0; a_ < NU; ++a_)
-#pragma unroll
-        for (int cc = 0; cc < NU; ++cc) Lc[a_][cc] = 0.0;
-#pragma unroll
-      for (int jj = 0; jj < NU; ++jj) {
-        double s_ = Qm[jj][jj];
-#pragma unroll
-        for (int q = 0; q < jj; ++q) s_ -= Lc[jj][q] * Lc[jj][q];
-        const double ljj = sqrt(s_);
-        Lc[jj][jj] = ljj;
-        Li[jj] = 1.0 / ljj;
-#pragma unroll
-        for (int ii = jj + 1; ii < NU; ++ii) {
-          double a2 = Qm[ii][jj];
-#pragma unroll
-          for (int q = 0; q < jj; ++q) a2 -= Lc[ii][q] * Lc[jj][q];
-          Lc[ii][jj] = a2 * Li[jj];
-        }
-      }
-#pragma unroll
-      for (int a_ = 0; a_ < NU; ++a_) {
-        double s_ = qx[a_];
-#pragma unroll
-        for (int q = 0; q < a_; ++q) s_ -= Lc[a_][q] * qx[q];
-        qx[a_] = s_ * Li[a_];
-      }
-#pragma unroll
-      for (int a_ = NU - 1; a_ >= 0; --a_) {
-        double s_ = qx[a_];
-#pragma unroll
-        for (int q = a_ + 1; q < NU; ++q) s_ -= Lc[q][a_] * qx[q];
-        qx[a_] = s_ * Li[a_];
-      }
+      QuuSolve<NU> qs;
+      qs.factor(Qm);
+      qs.apply(qx);
 #pragma unroll
       for (int a_ = 0; a_ < NU; ++a_) ric[((long long)t * NU + a_) * (NS + 1) + c] = -qx[a_];
     }
