@@ -72,6 +72,8 @@ struct Dev {
   // one sort pool of up to GG = TG*G pairs, cut into nchunkG warp items of 32
   int TG, NG, GG, nchunkG, CHG;  // CHG: lanes used per chunk (balanced)
   int nitems;        // B*NG*nchunkG work items of one sweep
+  int dense;         // latency mode (small problems): CHG <= 4 pairs per warp, each solved by
+                     // the whole warp with the dense-tableau Lemke (lemke_warp)
   const double* obs_step;  // NULL or [B*M][d]: per-timestep obstacle displacement (NEXT f3)
   int dyn_model;           // 1: unicycle relinearised every primal step (NEXT f2)
   double dt;
@@ -904,6 +906,7 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
 #pragma unroll
     for (int f = 0; f < REC; ++f) ra[f] = rb[f] = 0.0;
     const long long q0 = (long long)b * N + t0, q1 = q0 + 32;
+#pragma unroll 4
     for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
       const double* r0 = recs + (nchunk ? rec_index(P, b, t0 + 1, c) : q0) * REC;
       const double* r1 = recs + (nchunk ? rec_index(P, b, min(t1, N - 1) + 1, c) : min(q1, q0 - t0 + N - 1)) * REC;

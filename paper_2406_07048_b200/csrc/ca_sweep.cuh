@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     pivots = 0;
     status = ST_OK;
     rowb.init(n);
-    if (qmin < 0.0) {  // L1: otherwise z = 0
+    if (qmin < 0.0 && !P.dense) {  // L1: otherwise z = 0 (latency mode: dense re-solve below)
       // L2: z0 enters at row argmin q (ties -> largest index); its column is -1
       const double tl = qmin + tau * fmax(1.0, fabs(qmin));
       int r = 0;
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     // The revised path never forms the tableau, so check its answer against the
     // LCP itself: w = M z + q (O(n d) with the low-rank M), w_i = value of basic
     // w_i or 0, w >= 0, z >= 0.  Failure or RAY / ITER_LIMIT -> dense fallback.
-    fallback = (status != ST_OK);
+    fallback = (status != ST_OK) || P.dense;
     if (!fallback && qmin < 0.0) {
       double uz[D + 1], zl = 0.0, skz = 0.0, zsc = 0.0;
 #pragma unroll

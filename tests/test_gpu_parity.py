@@ -441,3 +441,24 @@ def test_load_keeps_feature_presence(ca):
     a_o = o.scale_detect()
     assert np.array_equal(np.isinf(alpha[: g.n_pairs]), np.isinf(a_o))
     assert not np.array_equal(np.isinf(a_o), np.isinf(oracle.Oracle(sc).scale_detect()))
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 10])
+def test_dense_latency_mode_forced(ca, cfg, monkeypatch):
+    """The latency mode (one pair per warp, warp-cooperative dense Lemke for every
+    pair; chosen automatically for small single-part 2-D problems) forced on other
+    shapes: 3-D pairs, two robot parts, scaling centres -- against the oracle."""
+    monkeypatch.setenv("CA_SWEEP_DENSE", "1")
+    sc = scene(cfg)
+    K = 30
+    g = ca.Problem(sc)
+    rc, hist = g.admm_iterate(K)
+    o = oracle.Oracle(sc)
+    hp, hd, fails = o.admm_iterate(K)
+    s, u = g.trajectory()
+    close(s, o.s, 1e-6, "s")
+    close(u, o.u, 1e-6, "u")
+    assert np.abs(hist["r_pri"] - hp.sum(1)).max() <= 1e-6 * max(1, hp.max())
+    assert hist["n_fail"].sum() == fails == 0
+    st = g.pair_state()
+    assert np.array_equal(st["pivots"], o.pivots[: g.n_pairs])  # the oracle's dense rules, pair by pair
