@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     pivots = 0;
     status = ST_OK;
     rowb.init(n);
-    if (qmin < 0.0 && !P.dense) {  // L1: otherwise z = 0 (latency mode: dense re-solve below)
+    if (qmin < 0.0 && !(TRACE && P.dense)) {  // L1: otherwise z = 0 (latency mode: dense solve below)
       // L2: z0 enters at row argmin q (ties -> largest index); its column is -1
       const double tl = qmin + tau * fmax(1.0, fabs(qmin));
       int r = 0;
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     // The revised path never forms the tableau, so check its answer against the
     // LCP itself: w = M z + q (O(n d) with the low-rank M), w_i = value of basic
     // w_i or 0, w >= 0, z >= 0.  Failure or RAY / ITER_LIMIT -> dense fallback.
-    fallback = (status != ST_OK) || P.dense;
+    fallback = (status != ST_OK) || (TRACE && P.dense);
     if (!fallback && qmin < 0.0) {
       double uz[D + 1], zl = 0.0, skz = 0.0, zsc = 0.0;
 #pragma unroll
@@ -752,9 +752,10 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
 
 // host-side launcher; explicitly instantiated in ca_sweep_*.cu (parallel build).
 // The extended variant (TRACE) is a separate kernel, launched only while a
-// ca_debug_trace request is armed or the problem has per-part scaling centres, so
-// the production kernel carries neither the diagnostic code nor the centre terms
-// (2 % of the C5 sweep when compiled in).
+// ca_debug_trace request is armed, the problem has per-part scaling centres or runs
+// in the small-problem latency mode, so the production kernel carries none of the
+// diagnostic code, the centre terms (2 % of the C5 sweep when compiled in) or the
+// latency-mode switch.
 template <int D, int NM, bool F, bool T>
 cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 #ifndef CA_EXP_SMEM_PAD
@@ -790,8 +791,8 @@ cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 
 template <int D, int NM, bool F>
 cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
-  return (P.dbg_p >= 0 || P.part_ctr) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
-                                      : sweep_launch_v<D, NM, F, false>(P, grid, stream);
+  return (P.dbg_p >= 0 || P.part_ctr || P.dense) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
+                                                 : sweep_launch_v<D, NM, F, false>(P, grid, stream);
 }
 
 #define CA_SWEEP_NMAX_LIST(X, D, F) X(D, 9, F) X(D, 11, F) X(D, 13, F) X(D, 15, F) X(D, 20, F) X(D, 32, F)
