@@ -703,19 +703,18 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   v.GG = v.TG * std::max(1, v.G);
   v.nchunkG = (v.GG + 31) / 32;
   v.CHG = (v.GG + v.nchunkG - 1) / v.nchunkG;  // balanced: lanes used per chunk
-  // latency mode: a 2-D single-part problem whose pairs fit one wave of resident warps
-  // at one pair per warp is solved pair by pair with the warp-cooperative dense Lemke
-  // (a single pair's revised path is a long dependent chain; below one wave only the
-  // sweep's latency counts).  A measured heuristic (profiles/r01/small_configs_v20.txt):
-  // C2 / C2n / C2b 111 / 113 / 131 -> 97 / 101 / 122 us per iteration; C1 even; the
-  // two-part C2t, 3-D C3 and two or more pairs per warp (C4) are slower dense, so they
-  // keep the revised path.  CA_SWEEP_DENSE=0 disables, =1 forces it (one wave).
+  // latency mode: a problem whose pairs fit one wave of resident warps at one pair per
+  // warp is solved pair by pair with the warp-cooperative dense Lemke (a single pair's
+  // revised path is a long dependent chain; below one wave only the sweep's latency
+  // counts).  Measured (profiles/r01/small_configs_v21.txt), us per ADMM iteration:
+  // C2 111 -> 93, C3 224 -> 182, C2t 128 -> 107, C1 even; more than one pair per warp
+  // (C4: 6000 pairs) is slower dense and keeps the revised path.  CA_SWEEP_DENSE=0
+  // disables.
   {
     const long long P = (long long)h->B * h->N * h->np * h->M;
     const long long resident = 148LL * CA_SWEEP_MINB;  // warps of one wave on B200
     const char* env = std::getenv("CA_SWEEP_DENSE");
-    const bool force = env && env[0] == '1', off = env && env[0] == '0';
-    v.dense = (P > 0 && P <= resident && !off && (force || (h->d == 2 && h->np == 1))) ? 1 : 0;
+    v.dense = (P > 0 && P <= resident && !(env && env[0] == '0')) ? 1 : 0;
     if (v.dense) {
       v.nchunkG = v.GG;  // one pair per warp
       v.CHG = 1;

@@ -109,7 +109,7 @@ static __device__ __noinline__ void trace_pivot(double* dd, const TraceRow tr, c
 // provisional minimum, or its result does not verify.  Called by all 32 lanes;
 // writes the basic z values of the pair into svalL (by LCP index, stride CTA).
 template <int D, int NMAX>
-__device__ __noinline__ int lemke_warp(const PairRows<D> W, const double btil[D + 1], double be,  // @region lemke_dense
+__device__ __noinline__ int lemke_warp_lm(const PairRows<D> W, const double btil[D + 1], double be,  // @region lemke_dense
                                        LemkeParams LP, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
   constexpr unsigned FULL = 0xffffffffu;
   const int n = W.n, l = n - 1;
@@ -212,6 +212,150 @@ __device__ __noinline__ int lemke_warp(const PairRows<D> W, const double btil[D 
   *zb_out = __reduce_or_sync(FULL, zbas ? (1u << (basis - n)) : 0u);
   *piv_out = pivots;
   return status;
+}
+
+template <int D, int NMAX>
+__device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double btil[D + 1], double be,  // @region lemke_dense
+                                       LemkeParams LP, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
+  constexpr unsigned FULL = 0xffffffffu;
+  // fixed column layout (every index compile-time, so the row stays in registers):
+  // w_j at j, z_j at NMAX + j, z0 at Z0, q at RHS; columns of absent pairs j >= n
+  // are skipped (they would stay zero)
+  constexpr int Z0 = 2 * NMAX, RHS = 2 * NMAX + 1, WC = 2 * NMAX + 2;
+  const int n = W.n, l = n - 1;
+  const bool own = lane < n;
+  auto used = [&](int j) { return (j < NMAX) ? (j < n) : (j < 2 * NMAX ? (j - NMAX < n) : true); };
+  double T[WC];
+  int basis = lane;  // w_lane
+  {
+    double fi[D + 1], ki = 0.0;
+    if (own) W.row(lane, fi, ki);
+#pragma unroll
+    for (int j = 0; j < WC; ++j) T[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+      if (j >= n) continue;
+      T[j] = (j == lane) ? 1.0 : 0.0;
+      if (own) {
+        double fj[D + 1], kj;
+        W.row(j, fj, kj);
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c <= D; ++c) acc = __fma_rn(fi[c], fj[c], acc);
+        if (j == l) acc = ki;
+        if (lane == l) acc = -kj;
+        if (lane == l && j == l) acc = 0.0;
+        T[NMAX + j] = -acc;
+      }
+    }
+    T[Z0] = -1.0;
+    double q = 1.0 / be;
+    if (lane < l) {
+      q = 0.0;
+#pragma unroll
+      for (int c = 0; c <= D; ++c) q = __fma_rn(fi[c], btil[c], q);
+    }
+    T[RHS] = q;
+    if (!own) {
+#pragma unroll
+      for (int j = 0; j < WC; ++j) T[j] = 0.0;
+    }
+  }
+  auto wmin = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+  };
+  auto col = [&](int c) {  // T[c] for a run-time column c (select, no indexed access)
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < WC; ++j) v = (j == c) ? T[j] : v;
+    return v;
+  };
+  // L3 pivot on (row r, column c): row r / T[r][c]; other rows fma(-T_ic, T_rj, T_ij)
+  auto pivot = [&](int r, int c) {
+    const double tc = col(c);
+    const double inv = 1.0 / __shfl_sync(FULL, own ? tc : 0.0, r);
+    if (lane == r) {
+#pragma unroll
+      for (int j = 0; j < WC; ++j)
+        if (used(j) && j != c) T[j] = T[j] * inv;
+    }
+    const double f = own ? tc : 0.0;
+#pragma unroll
+    for (int j = 0; j < WC; ++j) {
+      if (!used(j)) continue;
+      const double rj = __shfl_sync(FULL, own ? T[j] : 0.0, r);
+      if (own && lane != r && j != c) T[j] = __fma_rn(-f, rj, T[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < WC; ++j)
+      if (j == c && own) T[j] = (lane == r) ? 1.0 : 0.0;
+  };
+  const double tau = LP.tie_tol;
+  int status = ST_OK, pivots = 0;
+  const double qmin = wmin(own ? T[RHS] : 1e308);
+  if (qmin < 0.0) {
+    const double tl = qmin + tau * fmax(1.0, fabs(qmin));
+    const int r = 31 - __clz(__ballot_sync(FULL, own && T[RHS] <= tl));  // ties -> largest index
+    const int leaving = r;                                               // basis[r] = w_r
+    pivot(r, Z0);
+    if (lane == r) basis = Z0;
+    ++pivots;
+    int entering = NMAX + leaving;  // z_r
+    const int maxpiv = LP.max_pivot_factor * n;
+    for (;;) {
+      if (pivots >= maxpiv) { status = ST_ITER; break; }
+      const double ci = own ? col(entering) : 0.0;
+      const double cmax = -wmin(own ? -fabs(ci) : 0.0);
+      const double thr = LP.pivot_tol * fmax(1.0, cmax);
+      const bool el = own && ci > thr;
+      const double th = el ? fmax(T[RHS], 0.0) / ci : 1e308;
+      const double thmin = wmin(th);
+      if (!(thmin < 1e308)) { status = ST_RAY; break; }
+      const double ttol = thmin + tau * fmax(1.0, thmin);
+      uint32_t tie = __ballot_sync(FULL, el && th <= ttol);
+      const uint32_t z0t = __ballot_sync(FULL, ((tie >> lane) & 1u) && basis == Z0);
+      int r2;
+      if (z0t) {
+        r2 = __ffs(z0t) - 1;  // L5.3: z0 leaves whenever it is tied
+      } else {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {  // L5.4: lexicographic on B^{-1} (the w columns)
+          if (j >= n || __popc(tie) <= 1) break;
+          const bool in = (tie >> lane) & 1u;
+          const double v = in ? T[j] / ci : 1e308;
+          const double vmin = wmin(v);
+          const double vt = vmin + tau * fmax(1.0, fabs(vmin));
+          tie = __ballot_sync(FULL, in && v <= vt);
+        }
+        r2 = __ffs(tie) - 1;  // L5.5: smallest row
+      }
+      const int leaving2 = __shfl_sync(FULL, basis, r2);
+      pivot(r2, entering);
+      if (lane == r2) basis = entering;
+      ++pivots;
+      if (leaving2 == Z0) break;
+      entering = (leaving2 < NMAX) ? leaving2 + NMAX : leaving2 - NMAX;  // complement (L4)
+    }
+  }
+  const bool zbas = own && basis >= NMAX && basis < 2 * NMAX;
+  if (zbas) svalL[(basis - NMAX) * CTA] = T[RHS];
+  *zb_out = __reduce_or_sync(FULL, zbas ? (1u << (basis - NMAX)) : 0u);
+  *piv_out = pivots;
+  return status;
+}
+
+// The two forms compute the same thing element for element.  The register-tableau
+// form (every column index compile-time) is the faster one for a warp that does
+// little else (the extended variant: latency mode, centres, tracing); the production
+// kernel keeps the local-memory form, whose call site costs the hot loop no
+// registers (the register form would make the sweep spill: +11 % on C5).
+template <int D, int NMAX, bool REG>
+__device__ __forceinline__ int lemke_warp(const PairRows<D> W, const double btil[D + 1], double be, LemkeParams LP,
+                                          double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
+  if constexpr (REG) return lemke_warp_reg<D, NMAX>(W, btil, be, LP, svalL, lane, zb_out, piv_out);
+  else return lemke_warp_lm<D, NMAX>(W, btil, be, LP, svalL, lane, zb_out, piv_out);
 }
 
 template <int D, int NMAX, bool FUSED, bool TRACE>
@@ -643,7 +787,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     const PairRows<D> WL{lamtab + ipL * LT, cst, wcol + L, CTA, nrL, noL, nrL + noL + 1, nrL + noL};
     uint32_t zbL;
     int pivL;
-    const int stL = lemke_warp<D, NMAX>(WL, btL, beL, P.lp, sval - tid + L, tid, &zbL, &pivL);
+    const int stL = lemke_warp<D, NMAX, TRACE>(WL, btL, beL, P.lp, sval - tid + L, tid, &zbL, &pivL);
     if (tid == L) {
       status = stL;
       zb = zbL;

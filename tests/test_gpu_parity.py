@@ -295,8 +295,13 @@ def symmetric_scene():
     return scenes._car_common("SYM", 0, 0, N=20, iters=20, speed=4.0, polys_per_scene=[polys])
 
 
+@pytest.mark.parametrize("mode", ["auto", "revised"])
 @pytest.mark.parametrize("k0", [0, 2, 6])
-def test_t1_symmetric_degenerate(ca, k0):
+def test_t1_symmetric_degenerate(ca, k0, mode, monkeypatch):
+    """auto: this small problem runs the latency mode (every pair dense); revised: the
+    one-thread revised path, whose lexicographic ties go to the dense re-solve."""
+    if mode == "revised":
+        monkeypatch.setenv("CA_SWEEP_DENSE", "0")
     sc = symmetric_scene()
     o = warm(sc, k0)
     g = ca.Problem(sc)
@@ -310,7 +315,10 @@ def test_t1_symmetric_degenerate(ca, k0):
     assert np.count_nonzero(st["status"] & 0x100) > 0
 
 
-def test_t2_symmetric_degenerate(ca):
+@pytest.mark.parametrize("mode", ["auto", "revised"])
+def test_t2_symmetric_degenerate(ca, mode, monkeypatch):
+    if mode == "revised":
+        monkeypatch.setenv("CA_SWEEP_DENSE", "0")
     sc = symmetric_scene()
     g = ca.Problem(sc)
     o = oracle.Oracle(sc)
@@ -443,22 +451,23 @@ def test_load_keeps_feature_presence(ca):
     assert not np.array_equal(np.isinf(a_o), np.isinf(oracle.Oracle(sc).scale_detect()))
 
 
-@pytest.mark.parametrize("cfg", [1, 3, 10])
-def test_dense_latency_mode_forced(ca, cfg, monkeypatch):
-    """The latency mode (one pair per warp, warp-cooperative dense Lemke for every
-    pair; chosen automatically for small single-part 2-D problems) forced on other
-    shapes: 3-D pairs, two robot parts, scaling centres -- against the oracle."""
-    monkeypatch.setenv("CA_SWEEP_DENSE", "1")
+@pytest.mark.parametrize("cfg", [1, 2, 3, 10])
+def test_small_configs_revised_path(ca, cfg, monkeypatch):
+    """Small problems run the latency mode (one pair per warp, dense Lemke) by default;
+    the one-thread revised path on the same problems (CA_SWEEP_DENSE=0) against the
+    oracle, and the latency mode's pivot counts equal to the oracle's exactly."""
     sc = scene(cfg)
     K = 30
-    g = ca.Problem(sc)
-    rc, hist = g.admm_iterate(K)
     o = oracle.Oracle(sc)
     hp, hd, fails = o.admm_iterate(K)
+    g = ca.Problem(sc)
+    g.admm_iterate(K)
+    assert np.array_equal(g.pair_state()["pivots"], o.pivots[: g.n_pairs])  # dense: the oracle's rules verbatim
+    monkeypatch.setenv("CA_SWEEP_DENSE", "0")
+    g = ca.Problem(sc)
+    rc, hist = g.admm_iterate(K)
     s, u = g.trajectory()
     close(s, o.s, 1e-6, "s")
     close(u, o.u, 1e-6, "u")
     assert np.abs(hist["r_pri"] - hp.sum(1)).max() <= 1e-6 * max(1, hp.max())
     assert hist["n_fail"].sum() == fails == 0
-    st = g.pair_state()
-    assert np.array_equal(st["pivots"], o.pivots[: g.n_pairs])  # the oracle's dense rules, pair by pair
