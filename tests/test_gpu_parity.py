@@ -471,3 +471,25 @@ def test_small_configs_revised_path(ca, cfg, monkeypatch):
     close(u, o.u, 1e-6, "u")
     assert np.abs(hist["r_pri"] - hp.sum(1)).max() <= 1e-6 * max(1, hp.max())
     assert hist["n_fail"].sum() == fails == 0
+
+
+@pytest.mark.parametrize("cfg", [8, 10])
+def test_large_batch_paths_with_features(ca, cfg):
+    """Large batches (> 1024 scenes) take the thread-per-scene Riccati and the pooled
+    revised sweep: with boxes (C2b) and scaling centres (C2t) every scene of a
+    replicated batch must match the single-scene oracle."""
+    sc1 = scenes.make_config(cfg)
+    big = sc1.subset([0] * 1025)
+    K = 10
+    g = ca.Problem(big)
+    g.admm_iterate(K)
+    s, u = g.trajectory()
+    o = oracle.Oracle(sc1)
+    o.admm_iterate(K)
+    for b in (0, 511, 1024):
+        close(s[b], o.s[0], 1e-8, f"s scene {b}")
+        close(u[b], o.u[0], 1e-8, f"u scene {b}")
+    if cfg == 8:
+        ws, ls, wu, lu, res = g.box_state()
+        close(lu[1024], o.lu[0], 1e-8, "l_u")
+        close(res[1024:], o.boxres, 1e-8, "box residual")
