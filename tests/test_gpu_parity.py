@@ -493,3 +493,20 @@ def test_large_batch_paths_with_features(ca, cfg):
         ws, ls, wu, lu, res = g.box_state()
         close(lu[1024], o.lu[0], 1e-8, "l_u")
         close(res[1024:], o.boxres, 1e-8, "box residual")
+
+
+def test_sensing_pooled_sweep(ca):
+    """Sensing through the pooled sweep (800-pair sort pools over 4 timesteps, 256
+    scenes): sampled scenes against the single-scene oracle after K iterations."""
+    big = dataclasses.replace(scenes.make_c5(n_scenes=256), sense_half=np.array([20.0, 20.0]))
+    K = 3
+    g = ca.Problem(big)
+    g.admm_iterate(K)
+    s, u = g.trajectory()
+    for b in (0, 97, 255):
+        one = big.subset([b])
+        o = oracle.Oracle(one)
+        assert 0 < o.sensed.sum() < o.sensed.size
+        o.admm_iterate(K)
+        close(s[b], o.s[0], 1e-8, f"s scene {b}")
+        close(u[b], o.u[0], 1e-8, f"u scene {b}")
