@@ -195,7 +195,7 @@ ca_status validate(const ca_problem_desc* D) {
     return fail(CA_E_INVALID, "dyn_model 1 (unicycle): n_state 4, n_ctrl 2, SE2 pose (0, 1, 2), dt > 0");
   if (D->n_obs > 0 && (!D->obs_off || !D->obs_C || !D->obs_d)) return fail(CA_E_INVALID, "NULL obstacle array");
   if (!(D->sigma > 0.0)) return fail(CA_E_INVALID, "sigma must be > 0");
-  if (D->prox_eps != 0.0) return fail(CA_E_UNSUPPORTED, "prox_eps > 0 (reading #2) is oracle-only in this build");
+  if (!(D->prox_eps >= 0.0 && std::isfinite(D->prox_eps))) return fail(CA_E_INVALID, "prox_eps must be finite and >= 0");
   const int d = D->dim;
   const int pm = D->pose_model;
   if (pm < 0 || pm > 2) return fail(CA_E_UNSUPPORTED, "unknown pose model");
@@ -714,9 +714,15 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
     const long long P = (long long)h->B * h->N * h->np * h->M;
     const long long resident = 148LL * CA_SWEEP_MINB;  // warps of one wave on B200
     const char* env = std::getenv("CA_SWEEP_DENSE");
-    v.dense = (P > 0 && P <= resident && !(env && env[0] == '0')) ? 1 : 0;
-    if (v.dense) {
-      v.nchunkG = v.GG;  // one pair per warp
+    // prox_eps > 0 (reading #2) breaks the low-rank structure the revised path relies
+    // on (M + eps (I + kt kt^T)): such problems always take the dense path
+    v.prox_eps = D->prox_eps;
+    v.dense = (P > 0 && (D->prox_eps > 0.0 || (P <= resident && !(env && env[0] == '0')))) ? 1 : 0;
+    if (v.dense) {  // one pair per warp, one timestep per pool (one record per pair)
+      v.TG = 1;
+      v.NG = h->N;
+      v.GG = std::max(1, v.G);
+      v.nchunkG = v.GG;
       v.CHG = 1;
     }
   }

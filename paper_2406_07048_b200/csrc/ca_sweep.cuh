@@ -108,9 +108,19 @@ static __device__ __noinline__ void trace_pivot(double* dd, const TraceRow tr, c
 // path fails, meets a multi-way tie (lexicographic rule) or an ineligible
 // provisional minimum, or its result does not verify.  Called by all 32 lanes;
 // writes the basic z values of the pair into svalL (by LCP index, stride CTA).
+// Proximal term of reading #2 (prox_eps > 0): (eps/2)||y - y^k||^2 added to Eq. 19a,
+// through Eqs. 20-25: M_UU += eps (I + kt kt^T), q_U -= eps (y^k_U + kt (etatil - y^k_e)).
+// y^k of the pair: y[k * PP + p], eliminated index e.
+struct Prox {
+  double eps;  // 0: off (paper-exact)
+  const double* y;
+  long long PP, p;
+  int e;
+};
+
 template <int D, int NMAX>
 __device__ __noinline__ int lemke_warp_lm(const PairRows<D> W, const double btil[D + 1], double be,  // @region lemke_dense
-                                       LemkeParams LP, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
+                                       LemkeParams LP, Prox X, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
   constexpr unsigned FULL = 0xffffffffu;
   const int n = W.n, l = n - 1;
   const int Wd = 2 * n + 2, Z0 = 2 * n, RHS = 2 * n + 1;
@@ -132,6 +142,7 @@ __device__ __noinline__ int lemke_warp_lm(const PairRows<D> W, const double btil
       if (j == l) acc = ki;
       if (i == l) acc = -kj;
       if (i == l && j == l) acc = 0.0;
+      if (X.eps > 0.0 && i < l && j < l) acc = __fma_rn(X.eps, __fma_rn(ki, kj, (i == j) ? 1.0 : 0.0), acc);
       T[n + j] = -acc;
     }
     T[Z0] = -1.0;
@@ -140,6 +151,10 @@ __device__ __noinline__ int lemke_warp_lm(const PairRows<D> W, const double btil
       q = 0.0;
 #pragma unroll
       for (int c = 0; c <= D; ++c) q = __fma_rn(fi[c], btil[c], q);
+      if (X.eps > 0.0) {
+        const double ye = X.y[(long long)X.e * X.PP + X.p], yu = X.y[(long long)(i + (i >= X.e)) * X.PP + X.p];
+        q = __fma_rn(-X.eps, __fma_rn(ki, 1.0 / be - ye, yu), q);
+      }
     }
     T[RHS] = q;
   }
@@ -216,7 +231,7 @@ __device__ __noinline__ int lemke_warp_lm(const PairRows<D> W, const double btil
 
 template <int D, int NMAX>
 __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double btil[D + 1], double be,  // @region lemke_dense
-                                       LemkeParams LP, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
+                                       LemkeParams LP, Prox X, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
   constexpr unsigned FULL = 0xffffffffu;
   // fixed column layout (every index compile-time, so the row stays in registers):
   // w_j at j, z_j at NMAX + j, z0 at Z0, q at RHS; columns of absent pairs j >= n
@@ -245,6 +260,7 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
         if (j == l) acc = ki;
         if (lane == l) acc = -kj;
         if (lane == l && j == l) acc = 0.0;
+        if (X.eps > 0.0 && lane < l && j < l) acc = __fma_rn(X.eps, __fma_rn(ki, kj, (lane == j) ? 1.0 : 0.0), acc);
         T[NMAX + j] = -acc;
       }
     }
@@ -254,6 +270,10 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
       q = 0.0;
 #pragma unroll
       for (int c = 0; c <= D; ++c) q = __fma_rn(fi[c], btil[c], q);
+      if (X.eps > 0.0) {
+        const double ye = X.y[(long long)X.e * X.PP + X.p], yu = X.y[(long long)(lane + (lane >= X.e)) * X.PP + X.p];
+        q = __fma_rn(-X.eps, __fma_rn(ki, 1.0 / be - ye, yu), q);
+      }
     }
     T[RHS] = q;
     if (!own) {
@@ -353,9 +373,9 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
 // registers (the register form would make the sweep spill: +11 % on C5).
 template <int D, int NMAX, bool REG>
 __device__ __forceinline__ int lemke_warp(const PairRows<D> W, const double btil[D + 1], double be, LemkeParams LP,
-                                          double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
-  if constexpr (REG) return lemke_warp_reg<D, NMAX>(W, btil, be, LP, svalL, lane, zb_out, piv_out);
-  else return lemke_warp_lm<D, NMAX>(W, btil, be, LP, svalL, lane, zb_out, piv_out);
+                                          Prox X, double* svalL, int lane, uint32_t* zb_out, int* piv_out) {
+  if constexpr (REG) return lemke_warp_reg<D, NMAX>(W, btil, be, LP, X, svalL, lane, zb_out, piv_out);
+  else return lemke_warp_lm<D, NMAX>(W, btil, be, LP, X, svalL, lane, zb_out, piv_out);
 }
 
 template <int D, int NMAX, bool FUSED, bool TRACE>
@@ -787,7 +807,10 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     const PairRows<D> WL{lamtab + ipL * LT, cst, wcol + L, CTA, nrL, noL, nrL + noL + 1, nrL + noL};
     uint32_t zbL;
     int pivL;
-    const int stL = lemke_warp<D, NMAX, TRACE>(WL, btL, beL, P.lp, sval - tid + L, tid, &zbL, &pivL);
+    Prox XL{0.0, nullptr, 0, 0, 0};
+    if (TRACE && P.prox_eps > 0.0)  // reading #2 (the latency-mode kernel only)
+      XL = Prox{P.prox_eps, P.y, PP, __shfl_sync(0xffffffffu, p, L), P.part_e[ipL]};
+    const int stL = lemke_warp<D, NMAX, TRACE>(WL, btL, beL, P.lp, XL, sval - tid + L, tid, &zbL, &pivL);
     if (tid == L) {
       status = stL;
       zb = zbL;

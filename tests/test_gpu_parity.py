@@ -510,3 +510,29 @@ def test_sensing_pooled_sweep(ca):
         o.admm_iterate(K)
         close(s[b], o.s[0], 1e-8, f"s scene {b}")
         close(u[b], o.u[0], 1e-8, f"u scene {b}")
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_prox_regularised_parity(ca, cfg):
+    """prox_eps > 0 (reading #2): (eps/2)||y - y^k||^2 makes every pair QP strictly
+    convex; the GPU solves it with the dense Lemke on M + eps (I + kt kt^T).  One warm
+    dual sweep pair by pair (y and pivot counts) and K full iterations vs the oracle."""
+    eps = 1e-2
+    sc = scene(cfg)
+    o = oracle.Oracle(sc, prox_eps=eps)
+    o.admm_iterate(3)
+    g = ca.Problem(sc, prox_eps=eps)
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    rc, r = g.dual_sweep()
+    o.dual_sweep()
+    st = g.pair_state()
+    close(st["y"], o.y[: g.n_pairs], 1e-9, "y (prox)")
+    assert np.array_equal(st["pivots"], o.pivots[: g.n_pairs])
+    K = 20
+    g = ca.Problem(sc, prox_eps=eps)
+    g.admm_iterate(K)
+    o = oracle.Oracle(sc, prox_eps=eps)
+    hp, hd, fails = o.admm_iterate(K)
+    s, u = g.trajectory()
+    close(s, o.s, 1e-6, "s (prox)")
+    close(u, o.u, 1e-6, "u (prox)")
