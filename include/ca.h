@@ -72,7 +72,10 @@ typedef struct ca_problem ca_problem;
  *                (<= 0: default 1e-3 * pairs per scene); max_iters for ca_admm_solve.
  *  Lemke         (reading #4): pivot_tol (1e-11), tie_tol (1e-9), max pivots
  *                = lemke_max_pivot_factor * n (50).  <= 0 selects the default.
- *  prox_eps      (reading #2): 0 = paper-exact Eq. 19; > 0 adds eps/2 ||y - y^k||^2.
+ *  prox_eps      (reading #2): 0 = paper-exact Eq. 19; > 0 adds eps/2 ||y - y^k||^2
+ *                (strictly convex pair QPs: solved by the dense Lemke, one pair per
+ *                warp -- far slower than the paper-exact revised path); < 0 or NaN ->
+ *                CA_E_INVALID.
  */
 typedef struct {
   int32_t dim, n_scenes, horizon, n_state, n_ctrl;
