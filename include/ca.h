@@ -73,9 +73,8 @@ typedef struct ca_problem ca_problem;
  *  Lemke         (reading #4): pivot_tol (1e-11), tie_tol (1e-9), max pivots
  *                = lemke_max_pivot_factor * n (50).  <= 0 selects the default.
  *  prox_eps      (reading #2): 0 = paper-exact Eq. 19; > 0 adds eps/2 ||y - y^k||^2
- *                (strictly convex pair QPs: solved by the dense Lemke, one pair per
- *                warp -- far slower than the paper-exact revised path); < 0 or NaN ->
- *                CA_E_INVALID.
+ *                (strictly convex pair QPs with a unique minimiser, solved as
+ *                prox_solver selects); < 0 or NaN -> CA_E_INVALID.
  */
 typedef struct {
   int32_t dim, n_scenes, horizon, n_state, n_ctrl;
@@ -148,6 +147,13 @@ typedef struct {
    * use b~_i and the origin rho(s) + R(s) o_i (Eq. 3-11 unchanged otherwise), so parts
    * that do not contain the body origin (a trailer) are allowed.  NULL = origin. */
   const double* part_ctr;
+  /* NEXT f4, used only when prox_eps > 0: the solver of the strictly
+   * convex pair QP (reading #2).  0 = the dual semismooth Newton method on the
+   * (d+1)-dimensional dual of Eq. 19 + prox (one pair per thread; a pair that does not
+   * converge is re-solved by the dense Lemke); 1 = the dense Lemke on every pair (one
+   * pair per warp).  Both return the unique minimiser (to rounding).  Other values ->
+   * CA_E_INVALID. */
+  int32_t prox_solver;
 } ca_problem_desc;
 
 /* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;

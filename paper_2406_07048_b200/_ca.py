@@ -42,6 +42,7 @@ class Desc(C.Structure):
         ("dyn_model", C.c_int32), ("dt", C.c_double),
         ("s_min", C.c_void_p), ("s_max", C.c_void_p), ("u_min", C.c_void_p), ("u_max", C.c_void_p),
         ("box_rho", C.c_double), ("sense_half", C.c_void_p), ("part_ctr", C.c_void_p),
+        ("prox_solver", C.c_int32),
     ]
 
 
@@ -133,7 +134,7 @@ def _i32(a):
 
 
 def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot_factor=0, eps_pri=0.0,
-              eps_dual=0.0, max_iters=0, prox_eps=0.0, sigma=None) -> Desc:
+              eps_dual=0.0, max_iters=0, prox_eps=0.0, sigma=None, prox_solver=0) -> Desc:
     """Marshal a problem (any object with the attributes of scenes.Scene) into ca_problem_desc."""
     def k(name, arr):
         keep[name] = arr
@@ -165,6 +166,7 @@ def make_desc(sc, keep: dict, s_init=None, pivot_tol=0.0, tie_tol=0.0, max_pivot
     D.eps_pri, D.eps_dual, D.max_iters = eps_pri, eps_dual, max_iters
     D.lemke_pivot_tol, D.lemke_tie_tol, D.lemke_max_pivot_factor = pivot_tol, tie_tol, max_pivot_factor
     D.prox_eps = prox_eps
+    D.prox_solver = prox_solver  # NEXT f4: 0 dual Newton, 1 dense Lemke (prox_eps > 0 only)
     step = getattr(sc, "obs_step", None)
     D.obs_step = None if step is None else k("obs_step", _f64(step).reshape(-1, sc.dim))
     D.dyn_model, D.dt = int(getattr(sc, "dyn_model", 0)), float(sc.dt)

@@ -196,6 +196,7 @@ ca_status validate(const ca_problem_desc* D) {
   if (D->n_obs > 0 && (!D->obs_off || !D->obs_C || !D->obs_d)) return fail(CA_E_INVALID, "NULL obstacle array");
   if (!(D->sigma > 0.0)) return fail(CA_E_INVALID, "sigma must be > 0");
   if (!(D->prox_eps >= 0.0 && std::isfinite(D->prox_eps))) return fail(CA_E_INVALID, "prox_eps must be finite and >= 0");
+  if (D->prox_solver != 0 && D->prox_solver != 1) return fail(CA_E_INVALID, "prox_solver must be 0 (dual Newton) or 1 (dense Lemke)");
   const int d = D->dim;
   const int pm = D->pose_model;
   if (pm < 0 || pm > 2) return fail(CA_E_UNSUPPORTED, "unknown pose model");
@@ -715,9 +716,11 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
     const long long resident = 148LL * CA_SWEEP_MINB;  // warps of one wave on B200
     const char* env = std::getenv("CA_SWEEP_DENSE");
     // prox_eps > 0 (reading #2) breaks the low-rank structure the revised path relies
-    // on (M + eps (I + kt kt^T)): such problems always take the dense path
+    // on (M + eps (I + kt kt^T)): such problems take the dual Newton solver (NEXT f4,
+    // one pair per thread, normal work items) or, with prox_solver 1, the dense path
     v.prox_eps = D->prox_eps;
-    v.dense = (P > 0 && (D->prox_eps > 0.0 || (P <= resident && !(env && env[0] == '0')))) ? 1 : 0;
+    v.prox_newton = (D->prox_eps > 0.0 && D->prox_solver == 0) ? 1 : 0;
+    v.dense = (P > 0 && !v.prox_newton && (D->prox_eps > 0.0 || (P <= resident && !(env && env[0] == '0')))) ? 1 : 0;
     if (v.dense) {  // one pair per warp, one timestep per pool (one record per pair)
       v.TG = 1;
       v.NG = h->N;

@@ -72,9 +72,10 @@ struct Dev {
   // one sort pool of up to GG = TG*G pairs, cut into nchunkG warp items of 32
   int TG, NG, GG, nchunkG, CHG;  // CHG: lanes used per chunk (balanced)
   int nitems;        // B*NG*nchunkG work items of one sweep
-  int dense;         // latency mode (small problems; every problem with prox_eps > 0): one pair
+  int dense;         // latency mode (small problems; prox_eps > 0 with prox_solver 1): one pair
                      // per warp, solved by the whole warp with the dense-tableau Lemke (lemke_warp)
   double prox_eps;   // reading #2: 0 = paper-exact Eq. 19; > 0 adds eps/2 ||y - y^k||^2
+  int prox_newton;   // NEXT f4: prox_eps > 0 solved by the dual semismooth Newton (prox_newton_pair)
   const double* obs_step;  // NULL or [B*M][d]: per-timestep obstacle displacement (NEXT f3)
   int dyn_model;           // 1: unicycle relinearised every primal step (NEXT f2)
   double dt;

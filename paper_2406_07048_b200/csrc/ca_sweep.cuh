@@ -378,6 +378,248 @@ __device__ __forceinline__ int lemke_warp(const PairRows<D> W, const double btil
   else return lemke_warp_lm<D, NMAX>(W, btil, be, LP, X, svalL, lane, zb_out, piv_out);
 }
 
+// ---------------------------------------------------------------------------
+// NEXT f4: the prox-regularised pair QP of reading #2,
+//   min_y 1/2 ||K^T y + bvec||^2 + eps/2 ||y - y^k||^2   s.t. y >= 0, kappa^T y = 1
+// (Eq. 19 with kappa = (b_i, 0, 0), eta = 1, plus the proximal term), solved
+// through its dual in R^{d+1}.  With u = K^T y + bvec and 1/2||u||^2 = max_w w.u - 1/2||w||^2,
+//   g(w) = w.bvec - 1/2||w||^2 + min_{y in Y} [(K w).y + eps/2 ||y - y^k||^2]
+// is concave with gradient u(w) - w, where y(w) = Pi_Y(y^k - K w / eps) is a Euclidean
+// projection onto Y = {y >= 0, kappa^T y = 1}: mu and gamma entries are clipped at 0,
+// the lambda entries are y_k = max(0, c_k - tau b_k) with tau fixed by b^T y_lambda = 1
+// (variable fixing: drop the entries that go non-positive, recompute tau, until
+// stable).  The minimiser is y(w*) at the unique fixed point w* = u(w*) (= u*).
+// Semismooth Newton on u(w) - w = 0: the projection's Jacobian on the current support
+// S gives H = I + (1/eps) [sum_{k in S} K_k K_k^T - s s^T / (b_F . b_F)], s = sum_{k in F}
+// b_k K_k (F = lambda support), a (d+1) x (d+1) SPD system; backtracking (Armijo) on g
+// makes it global.  A full step that keeps the support lands on the affine piece's
+// root, which ends the iteration (finite termination).  Warm start: w = u(y^k).
+// The oracle solves the same strictly convex QP with the dense Lemke (orc_pair_solve
+// with prox_eps), so the two agree to rounding only (no shared algorithm).
+// Rows: lambda_k (0, a_k), b_k = prow[4k+3]; mu_l the per-lane smem rows (stride CTA);
+// gamma (1, 0).  y^k in ykc (stride CTA); y(w) written to yout (stride CTA) by index k.
+template <int D>
+struct ProxNt {
+  double g, u[D + 1], H[(D + 1) * (D + 2) / 2];
+  uint32_t sup;  // support of y(w) (bit k: y_k > 0)
+};
+
+template <int D>
+__device__ __forceinline__ void prox_row(int k, int nr, int no, const double* prow, const double* mu,
+                                         double f[D + 1]) {
+  if (k < nr) {
+    f[0] = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) f[1 + a] = prow[4 * k + a];
+  } else if (k < nr + no) {
+    const double* m = mu + (k - nr) * (D + 1) * CTA;
+#pragma unroll
+    for (int c = 0; c <= D; ++c) f[c] = m[c * CTA];
+  } else {
+    f[0] = 1.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) f[1 + a] = 0.0;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void prox_eval(const double* prow, const double* mu, int nr, int no, const double bv[D + 1],
+                                       double eps, const double* ykc, const double w[D + 1], double* yout,
+                                       ProxNt<D>& E) {
+  constexpr int L1 = D + 1;
+  const int n = nr + no + 1;
+  const double ie = 1.0 / eps;
+  // lambda block: variable fixing for tau (b^T y_lambda = 1)
+  uint32_t F = (nr >= 32) ? 0xffffffffu : ((1u << nr) - 1u);
+  double tau = 0.0, sbb = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass <= nr; ++pass) {
+    double sb = 0.0;
+    sbb = 0.0;
+#pragma unroll 1
+    for (uint32_t bb = F; bb; bb &= bb - 1) {
+      const int k = __ffs(bb) - 1;
+      double kw = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) kw = __fma_rn(prow[4 * k + a], w[1 + a], kw);
+      const double c = __fma_rn(-ie, kw, ykc[k * CTA]), bk = prow[4 * k + 3];
+      sb = __fma_rn(bk, c, sb);
+      sbb = __fma_rn(bk, bk, sbb);
+    }
+    tau = (sb - 1.0) / sbb;
+    uint32_t F2 = 0;
+#pragma unroll 1
+    for (uint32_t bb = F; bb; bb &= bb - 1) {
+      const int k = __ffs(bb) - 1;
+      double kw = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) kw = __fma_rn(prow[4 * k + a], w[1 + a], kw);
+      const double c = __fma_rn(-ie, kw, ykc[k * CTA]);
+      if (__fma_rn(-tau, prow[4 * k + 3], c) > 0.0) F2 |= 1u << k;
+    }
+    if (F2 == F || F2 == 0u) break;
+    F = F2;
+  }
+  // one pass over every row: y(w), u = K^T y + bvec, g, the Newton matrix
+  double u[L1], Hs[L1 * (L1 + 1) / 2], s[L1], gs = 0.0;
+#pragma unroll
+  for (int c = 0; c < L1; ++c) { u[c] = bv[c]; s[c] = 0.0; }
+#pragma unroll
+  for (int c = 0; c < L1 * (L1 + 1) / 2; ++c) Hs[c] = 0.0;
+  uint32_t sup = 0;
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    double f[L1];
+    prox_row<D>(k, nr, no, prow, mu, f);
+    double kw = 0.0;
+#pragma unroll
+    for (int c = 0; c < L1; ++c) kw = __fma_rn(f[c], w[c], kw);
+    const double yk = ykc[k * CTA], c0 = __fma_rn(-ie, kw, yk);
+    double y = 0.0;
+    if (k < nr) {
+      if ((F >> k) & 1u) y = fmax(__fma_rn(-tau, prow[4 * k + 3], c0), 0.0);
+    } else {
+      y = fmax(c0, 0.0);
+    }
+    yout[k * CTA] = y;
+    const double dy = y - yk;
+    gs = __fma_rn(kw, y, gs);
+    gs = __fma_rn(0.5 * eps, dy * dy, gs);
+    if (y > 0.0) {
+      sup |= 1u << k;
+      int h = 0;
+#pragma unroll
+      for (int a = 0; a < L1; ++a) {
+        u[a] = __fma_rn(y, f[a], u[a]);
+#pragma unroll
+        for (int c = a; c < L1; ++c, ++h) Hs[h] = __fma_rn(f[a], f[c], Hs[h]);
+      }
+      if (k < nr) {
+        const double bk = prow[4 * k + 3];
+#pragma unroll
+        for (int a = 0; a < L1; ++a) s[a] = __fma_rn(bk, f[a], s[a]);
+      }
+    }
+  }
+  double sbF = 0.0;  // b_F . b_F over the final lambda support
+#pragma unroll 1
+  for (uint32_t bb = sup & ((nr >= 32) ? 0xffffffffu : ((1u << nr) - 1u)); bb; bb &= bb - 1) {
+    const double bk = prow[4 * (__ffs(bb) - 1) + 3];
+    sbF = __fma_rn(bk, bk, sbF);
+  }
+  const double isb = sbF > 0.0 ? 1.0 / sbF : 0.0;
+  double gw = 0.0;
+  int h = 0;
+#pragma unroll
+  for (int a = 0; a < L1; ++a) {
+    gw = __fma_rn(w[a], bv[a] - 0.5 * w[a], gw);
+    E.u[a] = u[a];
+#pragma unroll
+    for (int c = a; c < L1; ++c, ++h) {
+      const double t = __fma_rn(-s[a] * isb, s[c], Hs[h]);
+      E.H[h] = __fma_rn(ie, t, a == c ? 1.0 : 0.0);
+    }
+  }
+  E.g = gw + gs;
+  E.sup = sup;
+}
+
+// Returns the Newton iteration count (>= 1) on success, -1 when the iteration did not
+// converge (the caller re-solves the pair with the dense Lemke).  y in yout by index k.
+template <int D>
+__device__ __noinline__ int prox_newton_pair(const double* prow, const double* mu, int nr, int no,
+                                             const double bv[D + 1], double eps, const double* ykc, double* yout) {
+  constexpr int L1 = D + 1;
+  const int n = nr + no + 1;
+  double w[L1];
+#pragma unroll
+  for (int c = 0; c < L1; ++c) w[c] = bv[c];
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {  // warm start w = u(y^k)
+    double f[L1];
+    prox_row<D>(k, nr, no, prow, mu, f);
+    const double yk = ykc[k * CTA];
+#pragma unroll
+    for (int c = 0; c < L1; ++c) w[c] = __fma_rn(yk, f[c], w[c]);
+  }
+  ProxNt<D> E, E2;
+  prox_eval<D>(prow, mu, nr, no, bv, eps, ykc, w, yout, E);
+#pragma unroll 1
+  for (int it = 1; it <= 64; ++it) {
+    double r[L1], rn = 0.0, sc = 1.0;
+#pragma unroll
+    for (int c = 0; c < L1; ++c) {
+      r[c] = E.u[c] - w[c];
+      rn = fmax(rn, fabs(r[c]));
+      sc = fmax(sc, fabs(w[c]));
+    }
+    if (rn <= 1e-15 * sc) return it;
+    // Cholesky of the packed SPD H, then H dx = r
+    double Lm[L1][L1], dx[L1];
+    {
+      int h = 0;
+#pragma unroll
+      for (int a = 0; a < L1; ++a)
+#pragma unroll
+        for (int c = a; c < L1; ++c, ++h) Lm[c][a] = E.H[h];
+#pragma unroll
+      for (int j = 0; j < L1; ++j) {
+        double dj = Lm[j][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) dj = __fma_rn(-Lm[j][k], Lm[j][k], dj);
+        dj = sqrt(dj);
+        const double idj = 1.0 / dj;
+        Lm[j][j] = dj;
+#pragma unroll
+        for (int i = j + 1; i < L1; ++i) {
+          double v = Lm[i][j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) v = __fma_rn(-Lm[i][k], Lm[j][k], v);
+          Lm[i][j] = v * idj;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < L1; ++i) {
+        double v = r[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v = __fma_rn(-Lm[i][k], dx[k], v);
+        dx[i] = v / Lm[i][i];
+      }
+#pragma unroll
+      for (int i = L1 - 1; i >= 0; --i) {
+        double v = dx[i];
+#pragma unroll
+        for (int k = i + 1; k < L1; ++k) v = __fma_rn(-Lm[k][i], dx[k], v);
+        dx[i] = v / Lm[i][i];
+      }
+    }
+    double slope = 0.0;
+#pragma unroll
+    for (int c = 0; c < L1; ++c) slope = __fma_rn(r[c], dx[c], slope);
+    double t = 1.0, wt[L1];
+    int ls = 0;
+#pragma unroll 1
+    for (;; ++ls) {
+#pragma unroll
+      for (int c = 0; c < L1; ++c) wt[c] = __fma_rn(t, dx[c], w[c]);
+      prox_eval<D>(prow, mu, nr, no, bv, eps, ykc, wt, yout, E2);
+      if (E2.g >= E.g + 1e-4 * t * slope - 1e-14 * (1.0 + fabs(E.g)) || ls >= 40) break;
+      t *= 0.5;
+    }
+    const bool same = (ls == 0 && E2.sup == E.sup);
+#pragma unroll
+    for (int c = 0; c < L1; ++c) w[c] = wt[c];
+    E = E2;
+    if (same) {  // full step inside one affine piece: the root (verify the residual)
+      double rn2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < L1; ++c) rn2 = fmax(rn2, fabs(E.u[c] - w[c]));
+      return (rn2 <= 1e-9 * sc) ? it : -1;
+    }
+  }
+  return -1;
+}
+
 template <int D, int NMAX, bool FUSED, bool TRACE>
 __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P) {  // @region cta_setup
   using SM = SweepSmem<D, NMAX>;
@@ -548,7 +790,27 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     pivots = 0;
     status = ST_OK;
     rowb.init(n);
-    if (qmin < 0.0 && !(TRACE && P.dense)) {  // L1: otherwise z = 0 (latency mode: dense solve below)
+    bool nwt_fail = false;
+    if (TRACE && P.prox_newton) {  // NEXT f4: prox_eps > 0 by the dual Newton method, one pair per lane
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) CBV(k) = YK(k);
+      double bv[D + 1];
+      bv[0] = 1.0 + zeta;
+#pragma unroll
+      for (int a = 0; a < D; ++a) bv[1 + a] = xi[a];
+      const int its = prox_newton_pair<D>(prow, mu, nr, no, bv, P.prox_eps, &CBV(0), &VAL(0));
+      nwt_fail = its < 0;
+      pivots = its < 0 ? 0 : its;
+      // y by index k -> the recovery's LCP layout (index u = k - (k > e), support bits)
+#pragma unroll 1
+      for (int k = 0; k < n; ++k) {
+        if (k == e) continue;
+        const int u = k - (k > e);
+        const double yv = VAL(k);
+        VAL(u) = yv;
+        if (yv > 0.0) zb |= 1u << u;
+      }
+    } else if (qmin < 0.0 && !(TRACE && P.dense)) {  // L1: otherwise z = 0 (latency mode: dense solve below)
       // L2: z0 enters at row argmin q (ties -> largest index); its column is -1
       const double tl = qmin + tau * fmax(1.0, fabs(qmin));
       int r = 0;
@@ -754,8 +1016,8 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     // The revised path never forms the tableau, so check its answer against the
     // LCP itself: w = M z + q (O(n d) with the low-rank M), w_i = value of basic
     // w_i or 0, w >= 0, z >= 0.  Failure or RAY / ITER_LIMIT -> dense fallback.
-    fallback = (status != ST_OK) || (TRACE && P.dense);
-    if (!fallback && qmin < 0.0) {
+    fallback = (status != ST_OK) || (TRACE && (P.dense || nwt_fail));
+    if (!fallback && qmin < 0.0 && !(TRACE && P.prox_newton)) {
       double uz[D + 1], zl = 0.0, skz = 0.0, zsc = 0.0;
 #pragma unroll
       for (int c = 0; c <= D; ++c) uz[c] = 0.0;
@@ -958,7 +1220,7 @@ cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 
 template <int D, int NM, bool F>
 cudaError_t sweep_launch(const Dev& P, unsigned grid, cudaStream_t stream) {
-  return (P.dbg_p >= 0 || P.part_ctr || P.dense) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
+  return (P.dbg_p >= 0 || P.part_ctr || P.dense || P.prox_newton) ? sweep_launch_v<D, NM, F, true>(P, grid, stream)
                                                  : sweep_launch_v<D, NM, F, false>(P, grid, stream);
 }
 

@@ -62,6 +62,7 @@ def test_validation_errors_precede_device(ca):
     bad = dataclasses.replace(sc, dim=4)
     assert _create(ca, bad)[0] == -2  # CA_E_DIM
     assert _create(ca, sc, prox_eps=-1e-3)[0] == -1  # CA_E_INVALID (prox_eps >= 0, reading #2)
+    assert _create(ca, sc, prox_eps=1e-2, prox_solver=2)[0] == -1  # CA_E_INVALID (NEXT f4: 0 or 1)
     assert _create(ca, dataclasses.replace(sc, pose_model=7))[0] == -4  # CA_E_UNSUPPORTED
     bad = dataclasses.replace(sc, Qs=-sc.Qs)
     assert _create(ca, bad)[0] == -1  # CA_E_INVALID (not SPD)

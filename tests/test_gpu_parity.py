@@ -521,7 +521,7 @@ def test_prox_regularised_parity(ca, cfg):
     sc = scene(cfg)
     o = oracle.Oracle(sc, prox_eps=eps)
     o.admm_iterate(3)
-    g = ca.Problem(sc, prox_eps=eps)
+    g = ca.Problem(sc, prox_eps=eps, prox_solver=1)
     g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
     rc, r = g.dual_sweep()
     o.dual_sweep()
@@ -529,10 +529,73 @@ def test_prox_regularised_parity(ca, cfg):
     close(st["y"], o.y[: g.n_pairs], 1e-9, "y (prox)")
     assert np.array_equal(st["pivots"], o.pivots[: g.n_pairs])
     K = 20
-    g = ca.Problem(sc, prox_eps=eps)
+    g = ca.Problem(sc, prox_eps=eps, prox_solver=1)
     g.admm_iterate(K)
     o = oracle.Oracle(sc, prox_eps=eps)
     hp, hd, fails = o.admm_iterate(K)
     s, u = g.trajectory()
     close(s, o.s, 1e-6, "s (prox)")
     close(u, o.u, 1e-6, "u (prox)")
+
+
+def prox_rtol(sc, eps):
+    """Tolerance for two different exact solvers of the prox pair QP: 4 ulp x the
+    condition number 1 + ||K||^2 / eps of its Hessian in y, with the unit-row bound
+    ||K_k|| <= 1 + |d_l| + |rho - t step| (Eq. 19b rows), floored at T1's 1e-9."""
+    d = sc.dim
+    pos = np.abs(sc.s_ref[..., [int(i) for i in sc.pose_idx[:d]]]).max()
+    step = getattr(sc, "obs_step", None)
+    if step is not None:
+        pos += sc.horizon * np.abs(step).max()
+    kmax = 1.0 + np.abs(sc.obs_d).max() + pos
+    return max(1e-9, 4e-16 * (1.0 + kmax * kmax / eps))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 10])
+@pytest.mark.parametrize("eps", [1e-3, 1e-1])
+def test_prox_newton_parity(ca, cfg, eps):
+    """NEXT f4: the dual semismooth Newton solver (prox_solver 0, one pair per thread)
+    returns the unique minimiser of the prox-regularised pair QP (reading #2), which the
+    oracle computes with the dense Lemke.  Different algorithms, so agreement is to the
+    rounding of the QP's conditioning: y to prox_rtol (the Hessian in y has condition
+    <= 1 + ||K||^2 / eps), whole ADMM runs (s, u after K iterations) to 1e-6 as T2."""
+    sc = scene(cfg)
+    o = oracle.Oracle(sc, prox_eps=eps)
+    o.admm_iterate(3)
+    g = ca.Problem(sc, prox_eps=eps)
+    g.set_iterate(o.s, o.u, o.y, o.zeta, o.xi)
+    g.dual_sweep()
+    o.dual_sweep()
+    st = g.pair_state()
+    close(st["y"], o.y[: g.n_pairs], prox_rtol(sc, eps), "y (prox, Newton)")
+    assert np.all(st["status"] == 0)
+    K = 20
+    g = ca.Problem(sc, prox_eps=eps)
+    g.admm_iterate(K)
+    o = oracle.Oracle(sc, prox_eps=eps)
+    o.admm_iterate(K)
+    s, u = g.trajectory()
+    close(s, o.s, 1e-6, "s (prox, Newton)")
+    close(u, o.u, 1e-6, "u (prox, Newton)")
+
+
+def test_prox_newton_c5_sample(ca):
+    """NEXT f4 at batch scale: 64 C5 scenes through the Newton solver; sampled scenes
+    against the single-scene oracle after K iterations, and against the dense-Lemke
+    GPU path on the whole batch."""
+    eps = 1e-2
+    big = scenes.make_c5(n_scenes=64)
+    K = 3
+    g = ca.Problem(big, prox_eps=eps)
+    g.admm_iterate(K)
+    s, u = g.trajectory()
+    h = ca.Problem(big, prox_eps=eps, prox_solver=1)
+    h.admm_iterate(K)
+    s1, u1 = h.trajectory()
+    close(s, s1, 1e-7, "s Newton vs dense Lemke")
+    close(u, u1, 1e-7, "u Newton vs dense Lemke")
+    for b in (0, 41):
+        o = oracle.Oracle(big.subset([b]), prox_eps=eps)
+        o.admm_iterate(K)
+        close(s[b], o.s[0], 1e-7, f"s scene {b}")
+        close(u[b], o.u[0], 1e-7, f"u scene {b}")
