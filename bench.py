@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--prox-eps", type=float, default=0.0,
+                    help="reading #2 proximal term (0 = paper-exact Eq. 19); > 0 runs the NEXT f4 dual Newton")
     return ap.parse_args()
 
 
@@ -100,10 +102,12 @@ def slice_obstacles(sc, j0, j1):
                                obs_d=np.concatenate(ds) if ds else np.zeros(0), obs_step=step)
 
 
-def workload_name(cfg, n_scenes, iters):
+def workload_name(cfg, n_scenes, iters, prox_eps=0.0):
+    # prox_eps > 0: the proximal variant of reading #2 (NEXT f4 dual Newton), not the paper's Eq. 19
+    px = f", prox_eps={prox_eps:g} (NEXT f4)" if prox_eps > 0 else ""
     if cfg == 5:
-        return f"C5: {n_scenes} scenes x 200 obstacles x N=50 per GPU, K={iters} ADMM iterations"
-    return scenes.CONFIG_NAMES[cfg].split(",")[0] + f", K={iters}"
+        return f"C5: {n_scenes} scenes x 200 obstacles x N=50 per GPU, K={iters} ADMM iterations" + px
+    return scenes.CONFIG_NAMES[cfg].split(",")[0] + f", K={iters}" + px
 
 
 # ----------------------------------------------------------------------------
@@ -220,12 +224,12 @@ def h2d_bytes(sc):
 # the reference arm: the CPU oracle (test infrastructure), bounded sample
 # ----------------------------------------------------------------------------
 
-def oracle_sample(cfg, iters):
+def oracle_sample(cfg, iters, prox_eps=0.0):
     """Time the oracle as it stands on one scene of the workload (single thread)."""
     import oracle
 
     sc = make_scene(cfg, 0, 1) if cfg == 5 else make_scene(cfg, 0, 1)
-    o = oracle.Oracle(sc)
+    o = oracle.Oracle(sc, prox_eps=prox_eps)
     t0 = time.perf_counter()
     o.scale_detect()
     o.admm_iterate(iters)
@@ -251,11 +255,11 @@ def run_reference(args, rank, world):
     iters_full = args.iters or (100 if cfg == 5 else scenes.make_config(cfg).iters)
     sample_iters = min(iters_full, 20)
     for _ in range(args.warmup):
-        oracle_sample(cfg, max(1, sample_iters // 4))
+        oracle_sample(cfg, max(1, sample_iters // 4), args.prox_eps)
     vals, ts = [], []
     sc = None
     for _ in range(args.steps):
-        v, dt, sc = oracle_sample(cfg, sample_iters)
+        v, dt, sc = oracle_sample(cfg, sample_iters, args.prox_eps)
         vals.append(v)
         ts.append(dt)
     value = float(np.median(vals))
@@ -267,7 +271,7 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(np.mean(ts) * 1e3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes/ generators)",
-        "config": {"workload": workload_name(cfg, args.scenes if cfg == 5 else 1, iters_full),
+        "config": {"workload": workload_name(cfg, args.scenes if cfg == 5 else 1, iters_full, args.prox_eps),
                    "sample": "bounded CPU sample (see cpu_baseline.sample)"},
         "cpu_baseline": {"value": value, "unit": "pair-QP/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "pair-QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -303,11 +307,12 @@ def run_ours(args, rank, world, local):
             box = [nid]
             dist.broadcast_object_list(box, src=0)
             nid = box[0]
-        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid), workspace="torch")
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid), workspace="torch",
+                       prox_eps=args.prox_eps)
         sc_local = slice_obstacles(sc, g.j0, g.j1)
     else:
         sc = make_scene(cfg, rank, args.scenes)
-        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, workspace="torch")
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, workspace="torch", prox_eps=args.prox_eps)
         sc_local = sc
     iters = args.iters or sc.iters
     fp64 = ca.fp64_peak(local, 300.0) if rank == 0 else None
@@ -416,13 +421,16 @@ def run_ours(args, rank, world, local):
         roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64, "unit": "TFLOP/s", "frac": frac_fp,
                 "traffic": traffic, "peak_source": "measured FP64 DFMA loop (ca_fp64_peak)"}
     roof.update({"kernel": "k_sweep (ADMM step 1 + fused step 3)", "launch_ms": avg_sweep_ms,
+                 "pair_solver": ("dual semismooth Newton (NEXT f4; 'pivots' = Newton iterations, the flop "
+                                 "model is the revised Lemke's, indicative only)") if args.prox_eps > 0
+                                else "revised Lemke (paper-exact Eq. 19)",
                  "algorithmic_bytes_per_launch": nbytes, "algorithmic_flops_per_launch": flops,
                  "hbm_frac": frac_hbm, "fp64_frac": frac_fp, "fp64_peak_tflops": fp64,
                  "pivots_per_pair": piv_per_sweep / max(1, sc_local.n_pairs),
                  "share_of_step": sweep_ms / ms if ms else None})
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, dt, ssc = oracle_sample(cfg, min(iters, 100))
+        v, dt, ssc = oracle_sample(cfg, min(iters, 100), args.prox_eps)
         cpu = {"value": v, "unit": "pair-QP/s", "cores": 1, "kind": "oracle",
                "sample": f"scene 0 alone ({ssc.n_pairs} pair-QPs/iter) x {min(iters, 100)} ADMM iterations "
                          f"+ 2 scale detections, {dt:.1f} s single-threaded on {cpu_model()}"}
@@ -431,7 +439,7 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if obstacle_shard else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes/ generators)",
-        "config": {"workload": workload_name(cfg, sc.n_scenes, iters), "scenes_per_gpu": sc.n_scenes,
+        "config": {"workload": workload_name(cfg, sc.n_scenes, iters, args.prox_eps), "scenes_per_gpu": sc.n_scenes,
                    "admm_iters": iters, "pair_qps_per_iter_per_gpu": sc.n_pairs,
                    "parallelism": (f"obstacle-sharded x{world}, one ncclAllReduce of per-(scene,t) aggregates "
                                    f"per iteration" if obstacle_shard else

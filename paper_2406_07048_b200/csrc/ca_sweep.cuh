@@ -391,9 +391,10 @@ __device__ __forceinline__ int lemke_warp(const PairRows<D> W, const double btil
 // stable).  The minimiser is y(w*) at the unique fixed point w* = u(w*) (= u*).
 // Semismooth Newton on u(w) - w = 0: the projection's Jacobian on the current support
 // S gives H = I + (1/eps) [sum_{k in S} K_k K_k^T - s s^T / (b_F . b_F)], s = sum_{k in F}
-// b_k K_k (F = lambda support), a (d+1) x (d+1) SPD system; backtracking (Armijo) on g
-// makes it global.  A full step that keeps the support lands on the affine piece's
-// root, which ends the iteration (finite termination).  Warm start: w = u(y^k).
+// b_k K_k (F = lambda support), a (d+1) x (d+1) SPD system; an Armijo line search on g
+// (quadratic-interpolation backtracking) makes it global.  A full step that keeps the
+// support lands on the affine piece's root, which ends the iteration (finite
+// termination).  Warm start: w = u(y^k).
 // The oracle solves the same strictly convex QP with the dense Lemke (orc_pair_solve
 // with prox_eps), so the two agree to rounding only (no shared algorithm).
 // Rows: lambda_k (0, a_k), b_k = prow[4k+3]; mu_l the per-lane smem rows (stride CTA);
@@ -604,7 +605,10 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
       for (int c = 0; c < L1; ++c) wt[c] = __fma_rn(t, dx[c], w[c]);
       prox_eval<D>(prow, mu, nr, no, bv, eps, ykc, wt, yout, E2);
       if (E2.g >= E.g + 1e-4 * t * slope - 1e-14 * (1.0 + fabs(E.g)) || ls >= 40) break;
-      t *= 0.5;
+      // backtrack to the maximiser of the quadratic through g(0), g'(0), g(t), in [t/10, t/2]
+      const double den = 2.0 * (slope * t - (E2.g - E.g));
+      const double tq = den > 0.0 ? slope * t * t / den : 0.5 * t;
+      t = fmin(fmax(tq, 0.1 * t), 0.5 * t);
     }
     const bool same = (ls == 0 && E2.sup == E.sup);
 #pragma unroll

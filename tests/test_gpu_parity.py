@@ -568,7 +568,7 @@ def test_prox_newton_parity(ca, cfg, eps):
     o.dual_sweep()
     st = g.pair_state()
     close(st["y"], o.y[: g.n_pairs], prox_rtol(sc, eps), "y (prox, Newton)")
-    assert np.all(st["status"] == 0)
+    assert np.all(st["status"] & 15 == 0)  # solved (a Newton non-convergence -> dense re-solve, bit 4)
     K = 20
     g = ca.Problem(sc, prox_eps=eps)
     g.admm_iterate(K)
