@@ -551,7 +551,7 @@ def prox_rtol(sc, eps):
     return max(1e-9, 4e-16 * (1.0 + kmax * kmax / eps))
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 10])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9, 10])
 @pytest.mark.parametrize("eps", [1e-3, 1e-1])
 def test_prox_newton_parity(ca, cfg, eps):
     """NEXT f4: the dual semismooth Newton solver (prox_solver 0, one pair per thread)
