@@ -399,6 +399,10 @@ __device__ __forceinline__ int lemke_warp(const PairRows<D> W, const double btil
 // with prox_eps), so the two agree to rounding only (no shared algorithm).
 // Rows: lambda_k (0, a_k), b_k = prow[4k+3]; mu_l the per-lane smem rows (stride CTA);
 // gamma (1, 0).  y^k in ykc (stride CTA); y(w) written to yout (stride CTA) by index k.
+#ifndef CA_PROX_MAXIT
+#define CA_PROX_MAXIT 64  // Newton iterations before the dense-Lemke re-solve (20: no gain, profiles)
+#endif
+
 template <int D>
 struct ProxNt {
   double g, u[D + 1], H[(D + 1) * (D + 2) / 2];
@@ -546,7 +550,7 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
   ProxNt<D> E, E2;
   prox_eval<D>(prow, mu, nr, no, bv, eps, ykc, w, yout, E);
 #pragma unroll 1
-  for (int it = 1; it <= 64; ++it) {
+  for (int it = 1; it <= CA_PROX_MAXIT; ++it) {
     double r[L1], rn = 0.0, sc = 1.0;
 #pragma unroll
     for (int c = 0; c < L1; ++c) {
