@@ -429,11 +429,10 @@ __device__ __forceinline__ void prox_row(int k, int nr, int no, const double* pr
 
 template <int D>
 __device__ __forceinline__ void prox_eval(const double* prow, const double* mu, int nr, int no, const double bv[D + 1],
-                                       double eps, const double* ykc, const double w[D + 1], double* yout,
-                                       ProxNt<D>& E) {
+                                       double eps, double ie, const double* ykc, const double w[D + 1],
+                                       double* yout, ProxNt<D>& E) {
   constexpr int L1 = D + 1;
-  const int n = nr + no + 1;
-  const double ie = 1.0 / eps;
+  const int n = nr + no + 1;  // ie = 1 / eps (hoisted by the caller)
   // lambda block: variable fixing for tau (b^T y_lambda = 1)
   uint32_t F = (nr >= 32) ? 0xffffffffu : ((1u << nr) - 1u);
   double tau = 0.0, sbb = 0.0;
@@ -536,6 +535,7 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
                                              const double bv[D + 1], double eps, const double* ykc, double* yout) {
   constexpr int L1 = D + 1;
   const int n = nr + no + 1;
+  const double ie = 1.0 / eps;
   double w[L1];
 #pragma unroll
   for (int c = 0; c < L1; ++c) w[c] = bv[c];
@@ -548,7 +548,7 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
     for (int c = 0; c < L1; ++c) w[c] = __fma_rn(yk, f[c], w[c]);
   }
   ProxNt<D> E, E2;
-  prox_eval<D>(prow, mu, nr, no, bv, eps, ykc, w, yout, E);
+  prox_eval<D>(prow, mu, nr, no, bv, eps, ie, ykc, w, yout, E);
 #pragma unroll 1
   for (int it = 1; it <= CA_PROX_MAXIT; ++it) {
     double r[L1], rn = 0.0, sc = 1.0;
@@ -560,7 +560,7 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
     }
     if (rn <= 1e-15 * sc) return it;
     // Cholesky of the packed SPD H, then H dx = r
-    double Lm[L1][L1], dx[L1];
+    double Lm[L1][L1], dx[L1], idg[L1];
     {
       int h = 0;
 #pragma unroll
@@ -575,6 +575,7 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
         dj = sqrt(dj);
         const double idj = 1.0 / dj;
         Lm[j][j] = dj;
+        idg[j] = idj;
 #pragma unroll
         for (int i = j + 1; i < L1; ++i) {
           double v = Lm[i][j];
@@ -588,14 +589,14 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
         double v = r[i];
 #pragma unroll
         for (int k = 0; k < i; ++k) v = __fma_rn(-Lm[i][k], dx[k], v);
-        dx[i] = v / Lm[i][i];
+        dx[i] = v * idg[i];
       }
 #pragma unroll
       for (int i = L1 - 1; i >= 0; --i) {
         double v = dx[i];
 #pragma unroll
         for (int k = i + 1; k < L1; ++k) v = __fma_rn(-Lm[k][i], dx[k], v);
-        dx[i] = v / Lm[i][i];
+        dx[i] = v * idg[i];
       }
     }
     double slope = 0.0;
@@ -607,7 +608,7 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
     for (;; ++ls) {
 #pragma unroll
       for (int c = 0; c < L1; ++c) wt[c] = __fma_rn(t, dx[c], w[c]);
-      prox_eval<D>(prow, mu, nr, no, bv, eps, ykc, wt, yout, E2);
+      prox_eval<D>(prow, mu, nr, no, bv, eps, ie, ykc, wt, yout, E2);
       if (E2.g >= E.g + 1e-4 * t * slope - 1e-14 * (1.0 + fabs(E.g)) || ls >= 40) break;
       // backtrack to the maximiser of the quadratic through g(0), g'(0), g(t), in [t/10, t/2]
       const double den = 2.0 * (slope * t - (E2.g - E.g));
