@@ -528,8 +528,53 @@ __device__ __forceinline__ void prox_eval(const double* prow, const double* mu, 
   E.sup = sup;
 }
 
+// x = A^{-1} r for the packed (upper, row by row) SPD (d+1) x (d+1) matrix A: Cholesky
+// with reciprocal diagonal, forward and back substitution.
+template <int L1>
+__device__ __forceinline__ void prox_chol_solve(const double* Ap, const double r[L1], double x[L1]) {
+  double Lm[L1][L1], idg[L1];
+  int h = 0;
+#pragma unroll
+  for (int a = 0; a < L1; ++a)
+#pragma unroll
+    for (int c = a; c < L1; ++c, ++h) Lm[c][a] = Ap[h];
+#pragma unroll
+  for (int j = 0; j < L1; ++j) {
+    double dj = Lm[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) dj = __fma_rn(-Lm[j][k], Lm[j][k], dj);
+    dj = sqrt(dj);
+    const double idj = 1.0 / dj;
+    idg[j] = idj;
+#pragma unroll
+    for (int i = j + 1; i < L1; ++i) {
+      double v = Lm[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v = __fma_rn(-Lm[i][k], Lm[j][k], v);
+      Lm[i][j] = v * idj;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < L1; ++i) {
+    double v = r[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v = __fma_rn(-Lm[i][k], x[k], v);
+    x[i] = v * idg[i];
+  }
+#pragma unroll
+  for (int i = L1 - 1; i >= 0; --i) {
+    double v = x[i];
+#pragma unroll
+    for (int k = i + 1; k < L1; ++k) v = __fma_rn(-Lm[k][i], x[k], v);
+    x[i] = v * idg[i];
+  }
+}
+
 // Returns the Newton iteration count (>= 1) on success, -1 when the iteration did not
 // converge (the caller re-solves the pair with the dense Lemke).  y in yout by index k.
+// Warm start across ADMM iterations: the root of the affine piece of y^k's support S0,
+// (I + K^T J_S0 K / eps) w = u(y^k) - s (b_F.y^k_F - 1) / (b_F.b_F) -- exact when the
+// support has not changed since the previous iteration (then one evaluation confirms).
 template <int D>
 __device__ __noinline__ int prox_newton_pair(const double* prow, const double* mu, int nr, int no,
                                              const double bv[D + 1], double eps, const double* ykc, double* yout) {
@@ -539,13 +584,49 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
   double w[L1];
 #pragma unroll
   for (int c = 0; c < L1; ++c) w[c] = bv[c];
-#pragma unroll 1
-  for (int k = 0; k < n; ++k) {  // warm start w = u(y^k)
-    double f[L1];
-    prox_row<D>(k, nr, no, prow, mu, f);
-    const double yk = ykc[k * CTA];
+  {
+    double Hs[L1 * (L1 + 1) / 2], s[L1], sbF = 0.0, bdy = 0.0;
 #pragma unroll
-    for (int c = 0; c < L1; ++c) w[c] = __fma_rn(yk, f[c], w[c]);
+    for (int c = 0; c < L1; ++c) s[c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < L1 * (L1 + 1) / 2; ++c) Hs[c] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {  // u(y^k) and the support's Newton matrix
+      const double yk = ykc[k * CTA];
+      if (yk > 0.0) {
+        double f[L1];
+        prox_row<D>(k, nr, no, prow, mu, f);
+        int h = 0;
+#pragma unroll
+        for (int a = 0; a < L1; ++a) {
+          w[a] = __fma_rn(yk, f[a], w[a]);
+#pragma unroll
+          for (int c = a; c < L1; ++c, ++h) Hs[h] = __fma_rn(f[a], f[c], Hs[h]);
+        }
+        if (k < nr) {
+          const double bk = prow[4 * k + 3];
+#pragma unroll
+          for (int a = 0; a < L1; ++a) s[a] = __fma_rn(bk, f[a], s[a]);
+          sbF = __fma_rn(bk, bk, sbF);
+          bdy = __fma_rn(bk, yk, bdy);
+        }
+      }
+    }
+    if (sbF > 0.0) {
+      const double isb = 1.0 / sbF, cr = (bdy - 1.0) * isb;
+      double A[L1 * (L1 + 1) / 2], rhs[L1];
+      int h = 0;
+#pragma unroll
+      for (int a = 0; a < L1; ++a) {
+        rhs[a] = __fma_rn(-cr, s[a], w[a]);
+#pragma unroll
+        for (int c = a; c < L1; ++c, ++h) {
+          const double t = __fma_rn(-s[a] * isb, s[c], Hs[h]);
+          A[h] = __fma_rn(ie, t, a == c ? 1.0 : 0.0);
+        }
+      }
+      prox_chol_solve<L1>(A, rhs, w);
+    }
   }
   ProxNt<D> E, E2;
   prox_eval<D>(prow, mu, nr, no, bv, eps, ie, ykc, w, yout, E);
@@ -559,46 +640,8 @@ __device__ __noinline__ int prox_newton_pair(const double* prow, const double* m
       sc = fmax(sc, fabs(w[c]));
     }
     if (rn <= 1e-15 * sc) return it;
-    // Cholesky of the packed SPD H, then H dx = r
-    double Lm[L1][L1], dx[L1], idg[L1];
-    {
-      int h = 0;
-#pragma unroll
-      for (int a = 0; a < L1; ++a)
-#pragma unroll
-        for (int c = a; c < L1; ++c, ++h) Lm[c][a] = E.H[h];
-#pragma unroll
-      for (int j = 0; j < L1; ++j) {
-        double dj = Lm[j][j];
-#pragma unroll
-        for (int k = 0; k < j; ++k) dj = __fma_rn(-Lm[j][k], Lm[j][k], dj);
-        dj = sqrt(dj);
-        const double idj = 1.0 / dj;
-        Lm[j][j] = dj;
-        idg[j] = idj;
-#pragma unroll
-        for (int i = j + 1; i < L1; ++i) {
-          double v = Lm[i][j];
-#pragma unroll
-          for (int k = 0; k < j; ++k) v = __fma_rn(-Lm[i][k], Lm[j][k], v);
-          Lm[i][j] = v * idj;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < L1; ++i) {
-        double v = r[i];
-#pragma unroll
-        for (int k = 0; k < i; ++k) v = __fma_rn(-Lm[i][k], dx[k], v);
-        dx[i] = v * idg[i];
-      }
-#pragma unroll
-      for (int i = L1 - 1; i >= 0; --i) {
-        double v = dx[i];
-#pragma unroll
-        for (int k = i + 1; k < L1; ++k) v = __fma_rn(-Lm[k][i], dx[k], v);
-        dx[i] = v * idg[i];
-      }
-    }
+    double dx[L1];
+    prox_chol_solve<L1>(E.H, r, dx);
     double slope = 0.0;
 #pragma unroll
     for (int c = 0; c < L1; ++c) slope = __fma_rn(r[c], dx[c], slope);
