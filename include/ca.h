@@ -149,10 +149,12 @@ typedef struct {
   const double* part_ctr;
   /* NEXT f4, used only when prox_eps > 0: the solver of the strictly
    * convex pair QP (reading #2).  0 = the dual semismooth Newton method on the
-   * (d+1)-dimensional dual of Eq. 19 + prox (one pair per thread; a pair that does not
-   * converge is re-solved by the dense Lemke); 1 = the dense Lemke on every pair (one
-   * pair per warp).  Both return the unique minimiser (to rounding).  Other values ->
-   * CA_E_INVALID. */
+   * (d+1)-dimensional dual of Eq. 19 + prox (one pair per thread, warm-started at the
+   * root of the affine piece of y^k's support; a pair that does not converge in 64
+   * iterations is re-solved by the dense Lemke); 1 = the dense Lemke on every pair (one
+   * pair per warp).  Both return the unique minimiser (to rounding), so results agree
+   * to the QP's conditioning, not bitwise; pivot counts report Newton iterations for 0.
+   * Other values -> CA_E_INVALID. */
   int32_t prox_solver;
 } ca_problem_desc;
 
