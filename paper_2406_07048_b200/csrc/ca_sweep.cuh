@@ -844,8 +844,10 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     rowb.init(n);
     bool nwt_fail = false;
     if (TRACE && P.prox_newton) {  // NEXT f4: prox_eps > 0 by the dual Newton method, one pair per lane
+      if (!FUSED) {  // y^k staged in the cbar scratch (the fused multiplier step already did)
 #pragma unroll 4
-      for (int k = 0; k < n; ++k) CBV(k) = YK(k);
+        for (int k = 0; k < n; ++k) CBV(k) = YK(k);
+      }
       double bv[D + 1];
       bv[0] = 1.0 + zeta;
 #pragma unroll
@@ -1150,9 +1152,12 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     if (st == ST_OK && ye < -1e-6) st = ST_NEGYE;
     const bool solved = (st == ST_OK);
     // y used by the aggregates: y^{k+1}, or y^k for a failed pair;
-    // y^k re-staged in the cbar scratch (free again) with batched loads
+    // y^k re-staged in the cbar scratch (free again) with batched loads; the Newton
+    // path (NEXT f4) only reads it, so it is still there
+    if (!(TRACE && P.prox_newton && !fallback)) {
 #pragma unroll 4
-    for (int k = 0; k < n; ++k) CBV(k) = YK(k);
+      for (int k = 0; k < n; ++k) CBV(k) = YK(k);
+    }
     double rd = 0.0;
     double eT = 1.0 + zeta, eR[D], vb[D];  // vb = R^T v = sum_l mu_l R^T c_l (body frame)
 #pragma unroll
