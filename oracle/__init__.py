@@ -24,7 +24,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(src), os.path.getmtime(os.path.join(HERE, "orc.h"))
     ):
         subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread",
              "-o", LIB, src, "-lm"]
         )
     return LIB
@@ -62,6 +62,12 @@ def lib():
         _lib.orc_admm_iterate.restype = C.c_longlong
         _lib.orc_scale_detect.argtypes = [C.c_void_p, dp, dp]
         _lib.orc_scale_detect.restype = C.c_longlong
+        _lib.orc_check_stopping.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double]
+        _lib.orc_check_stopping.restype = C.c_int
+        _lib.orc_admm_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int, ip, ip, dp, dp]
+        _lib.orc_admm_solve.restype = C.c_longlong
+        _lib.orc_admm_iterate_mt.argtypes = [C.c_void_p, C.c_void_p, C.c_int, dp, dp, C.c_int]
+        _lib.orc_admm_iterate_mt.restype = C.c_longlong
     return _lib
 
 
@@ -214,6 +220,32 @@ class Oracle:
             raise RuntimeError("oracle primal step failed")
         return hp, hd, fails
 
+    def admm_iterate_mt(self, K, nthreads):
+        """The same K iterations fanned out over nthreads POSIX threads (timing of the
+        all-core CPU baseline): over scenes when there are >= nthreads of them (bitwise
+        = admm_iterate), else over the pairs of each dual step."""
+        B = self.sc.n_scenes
+        hp = np.zeros((K, B))
+        hd = np.zeros((K, B))
+        fails = lib().orc_admm_iterate_mt(*self._pp(), K, _d(hp), _d(hd), int(nthreads))
+        if fails < 0:
+            raise RuntimeError("oracle primal step failed")
+        return hp, hd, fails
+
+    def admm_solve(self, eps_pri, eps_dual, max_iters):
+        """ADMM until Eq. 18 per scene, or max_iters: (iters[B], converged[B],
+        r_pri[B], r_dual[B], failed pair solves)."""
+        B = self.sc.n_scenes
+        it = np.zeros(B, np.int32)
+        cv = np.zeros(B, np.int32)
+        rp = np.zeros(B)
+        rd = np.zeros(B)
+        fails = lib().orc_admm_solve(*self._pp(), float(eps_pri), float(eps_dual), int(max_iters), _i(it), _i(cv),
+                                     _d(rp), _d(rd))
+        if fails < 0:
+            raise RuntimeError("oracle primal step failed")
+        return it, cv.astype(bool), rp, rd, fails
+
     def scale_detect(self, s=None):
         s = self.s if s is None else _f64(s)
         alpha = np.zeros(max(self.sc.n_pairs, 1))
@@ -224,6 +256,11 @@ class Oracle:
 # --------------------------------------------------------------------------
 # single-pair entry points (used by the pins)
 # --------------------------------------------------------------------------
+
+def check_stopping(r_pri, r_dual, eps_pri, eps_dual) -> bool:
+    """Eq. 18 (P:324-327): r_pri <= eps_pri and r_dual <= eps_dual."""
+    return bool(lib().orc_check_stopping(float(r_pri), float(r_dual), float(eps_pri), float(eps_dual)))
+
 
 def pose(model, idx, d, s):
     R = np.zeros(d * d)

@@ -21,6 +21,13 @@
  *   orc_primal_step    zero-obstacle step == dense KKT LQ solve (numpy);
  *                      GN gradient/Hessian vs finite differences
  *   orc_multiplier_update  identity zeta+ - zeta = T (Eq. 10) recomputed in numpy
+ *   r_pri / r_dual     Eq. 18's sums recomputed in numpy from consecutive iterates
+ *                      (sum ||zeta+ - zeta||^2 + ||xi+ - xi||^2, sum ||lambda+ - lambda||^2
+ *                      + ||mu+ - mu||^2, gamma excluded), tests/test_oracle_stop.py
+ *   orc_check_stopping SPEC S:526-528 examples ('<=' boundary), monotone in eps
+ *   orc_admm_solve     = the first k of the fixed-K history meeting Eq. 18, per scene;
+ *                      a frozen scene's iterate = the K-iteration run stopped there
+ *   orc_admm_iterate_mt  bitwise = orc_admm_iterate (scene fan-out)
  *   box block (f1)     zero-obstacle fixed point == box-constrained LQ optimum
  *                      (scipy lsq_linear; KKT certificate with state bounds);
  *                      infinite bounds == no bounds, bitwise
@@ -29,6 +36,7 @@
  *   rules L1-L7 of DESIGN.md reading #4 define it).
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -584,11 +592,12 @@ static void decode(const orc_problem* P, long long p, int* b, int* t, int* i, in
  * rdual[b] = sum ||lambda^{k+1}-lambda^k||^2 + ||mu^{k+1}-mu^k||^2 (Eq. 18b, P:326;
  * gamma excluded, reading #19).  Returns the number of failed pairs.
  * ------------------------------------------------------------------------- */
-long long orc_dual_sweep(const orc_problem* P, orc_iterate* I, double* rdual) {
+/* pairs [p0, p1) only, rdual[b] += their terms (the whole sweep: p0 = 0, p1 = #pairs,
+ * rdual zeroed first; orc_dual_sweep).  Also the unit of the threaded fan-out. */
+static long long dual_sweep_range(const orc_problem* P, orc_iterate* I, long long p0, long long p1, double* rdual) {
   int d = P->dim, N = P->horizon, ns = P->n_state;
-  long long np = n_pairs(P), fails = 0;
-  for (int b = 0; b < P->n_scenes; ++b) rdual[b] = 0.0;
-  for (long long p = 0; p < np; ++p) {
+  long long fails = 0;
+  for (long long p = p0; p < p1; ++p) {
     int b, t, i, j;
     decode(P, p, &b, &t, &i, &j);
     if (!sensed(P, b, j)) {
@@ -621,6 +630,11 @@ long long orc_dual_sweep(const orc_problem* P, orc_iterate* I, double* rdual) {
     for (int k = 0; k < nr + no + 1; ++k) y[k] = ynew[k];
   }
   return fails;
+}
+
+long long orc_dual_sweep(const orc_problem* P, orc_iterate* I, double* rdual) {
+  for (int b = 0; b < P->n_scenes; ++b) rdual[b] = 0.0;
+  return dual_sweep_range(P, I, 0, n_pairs(P), rdual);
 }
 
 /* ---------------------------------------------------------------------------
@@ -993,4 +1007,180 @@ long long orc_scale_detect(const orc_problem* P, const double* s, double* alpha)
     }
   }
   return bad;
+}
+
+/* ---------------------------------------------------------------------------
+ * Eq. 18: the stopping criteria,
+ *   r_pri  = sum_ijt ||zeta^{k+1} - zeta^k||^2 + ||xi^{k+1} - xi^k||^2  <= eps_pri   (18a)
+ *   r_dual = sum_ijt ||lambda^{k+1} - lambda^k||^2 + ||mu^{k+1} - mu^k||^2 <= eps_dual (18b)
+ * with '<=' as printed ("sum exactly eps -> true").  r_pri is what
+ * orc_multiplier_update returns (zeta^{k+1} - zeta^k = T, Eq. 17; plus the box block's
+ * ||x - w||^2, reading #7), r_dual what orc_dual_sweep returns (gamma excluded,
+ * reading #19).
+ * ------------------------------------------------------------------------- */
+int orc_check_stopping(double r_pri, double r_dual, double eps_pri, double eps_dual) {
+  return (r_pri <= eps_pri) && (r_dual <= eps_dual);
+}
+
+/* The problem and iterate of scene b alone (n_scenes = 1): every per-scene array is
+ * offset to scene b; obs_off keeps absolute row indices into obs_C / obs_d, so the
+ * view's obs_off = P->obs_off + b*M needs no rebasing.  Scenes share nothing in the
+ * method (one robot, its own obstacles), so iterating the view = iterating
+ * scene b of the batch. */
+static void scene_view(const orc_problem* P, const orc_iterate* I, int b, orc_problem* Pb, orc_iterate* Ib) {
+  const int N = P->horizon, ns = P->n_state, nu = P->n_ctrl, M = P->n_obs, d = P->dim;
+  const long long pps = (long long)N * P->n_parts * M; /* pairs per scene */
+  *Pb = *P;
+  Pb->n_scenes = 1;
+  Pb->obs_off = P->obs_off + (long long)b * M;
+  if (P->dyn_per_scene) {
+    const long long nt = P->dyn_per_time ? N : 1;
+    Pb->dyn_A = P->dyn_A + (long long)b * nt * ns * ns;
+    Pb->dyn_B = P->dyn_B + (long long)b * nt * ns * nu;
+    Pb->dyn_c = P->dyn_c + (long long)b * nt * ns;
+  }
+  Pb->s0 = P->s0 + (long long)b * ns;
+  Pb->s_ref = P->s_ref + (long long)b * (N + 1) * ns;
+  if (P->obs_step) Pb->obs_step = P->obs_step + (long long)b * M * d;
+  if (P->sensed) Pb->sensed = P->sensed + (long long)b * M;
+  *Ib = *I;
+  Ib->s = I->s + (long long)b * (N + 1) * ns;
+  Ib->u = I->u + (long long)b * N * nu;
+  Ib->y = I->y + b * pps * P->ny;
+  Ib->zeta = I->zeta + b * pps;
+  Ib->xi = I->xi + b * pps * d;
+  if (I->pivots) Ib->pivots = I->pivots + b * pps;
+  if (I->status) Ib->status = I->status + b * pps;
+  if (I->ws) {
+    Ib->ws = I->ws + (long long)b * (N + 1) * ns;
+    Ib->ls = I->ls + (long long)b * (N + 1) * ns;
+    Ib->wu = I->wu + (long long)b * N * nu;
+    Ib->lu = I->lu + (long long)b * N * nu;
+    Ib->boxres = I->boxres + b;
+  }
+}
+
+/* ADMM until Eq. 18: every scene of the batch is its own MPC problem and
+ * stops at the first iteration k whose residuals meet Eq. 18 (orc_check_stopping),
+ * its iterate left there; or after max_iters.  Per scene: iters[b] (iterations run),
+ * conv[b] (0/1), rpri[b], rdual[b] (residuals of its last iteration).  Returns the
+ * total number of failed pair solves, or -1 if a primal solve failed. */
+long long orc_admm_solve(const orc_problem* P, orc_iterate* I, double eps_pri, double eps_dual, int max_iters,
+                         int* iters, int* conv, double* rpri, double* rdual) {
+  long long fails = 0;
+  for (int b = 0; b < P->n_scenes; ++b) {
+    orc_problem Pb;
+    orc_iterate Ib;
+    scene_view(P, I, b, &Pb, &Ib);
+    double rp = 0.0, rd = 0.0;
+    iters[b] = 0;
+    conv[b] = 0;
+    for (int k = 0; k < max_iters; ++k) {
+      fails += orc_dual_sweep(&Pb, &Ib, &rd);        /* Eq. 15 */
+      if (orc_primal_step(&Pb, &Ib) != 0) return -1; /* Eq. 16 */
+      orc_multiplier_update(&Pb, &Ib, &rp);          /* Eq. 17 */
+      iters[b] = k + 1;
+      if (orc_check_stopping(rp, rd, eps_pri, eps_dual)) { /* Eq. 18 */
+        conv[b] = 1;
+        break;
+      }
+    }
+    rpri[b] = rp;
+    rdual[b] = rd;
+  }
+  return fails;
+}
+
+/* ---------------------------------------------------------------------------
+ * Timing helper for the all-core CPU baseline: the same K fixed
+ * iterations as orc_admm_iterate, fanned out over nthreads POSIX threads.
+ *  - n_scenes >= nthreads: scenes are distributed over the threads, each scene iterated
+ *    alone (scene_view) -- bitwise the sequential result (per-scene order unchanged).
+ *  - fewer scenes: per iteration the pairs of the dual step (Eq. 15) are split into
+ *    nthreads contiguous ranges, each with its own residual partial summed in range
+ *    order (rounding-level differences in r_dual only); the primal step and the
+ *    multiplier update stay sequential.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const orc_problem* P;
+  orc_iterate* I;
+  int K, b0, b1, B;
+  long long p0, p1;
+  double *hist_rpri, *hist_rdual, *rd;
+  long long fails;
+  int rc;
+} mt_job;
+
+static void* mt_scenes(void* arg) {
+  mt_job* J = (mt_job*)arg;
+  for (int b = J->b0; b < J->b1; ++b) {
+    orc_problem Pb;
+    orc_iterate Ib;
+    scene_view(J->P, J->I, b, &Pb, &Ib);
+    for (int k = 0; k < J->K; ++k) {
+      double rd = 0.0, rp = 0.0;
+      J->fails += orc_dual_sweep(&Pb, &Ib, &rd);
+      if (orc_primal_step(&Pb, &Ib) != 0) { J->rc = -1; return NULL; }
+      orc_multiplier_update(&Pb, &Ib, &rp);
+      if (J->hist_rpri) J->hist_rpri[(long long)k * J->B + b] = rp;
+      if (J->hist_rdual) J->hist_rdual[(long long)k * J->B + b] = rd;
+    }
+  }
+  return NULL;
+}
+
+static void* mt_pairs(void* arg) {
+  mt_job* J = (mt_job*)arg;
+  J->fails += dual_sweep_range(J->P, J->I, J->p0, J->p1, J->rd);
+  return NULL;
+}
+
+long long orc_admm_iterate_mt(const orc_problem* P, orc_iterate* I, int K, double* hist_rpri, double* hist_rdual,
+                              int nthreads) {
+  const int B = P->n_scenes;
+  if (nthreads < 1) nthreads = 1;
+  mt_job* J = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  long long fails = 0;
+  if (B >= nthreads) {
+    for (int t = 0; t < nthreads; ++t) {
+      J[t] = (mt_job){P, I, K, (int)((long long)B * t / nthreads), (int)((long long)B * (t + 1) / nthreads), B,
+                      0, 0, hist_rpri, hist_rdual, NULL, 0, 0};
+      pthread_create(&th[t], NULL, mt_scenes, &J[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) {
+      pthread_join(th[t], NULL);
+      fails += J[t].fails;
+      if (J[t].rc) fails = -1;
+    }
+  } else {
+    const long long np = n_pairs(P);
+    double* rd = (double*)calloc((size_t)nthreads * B, sizeof(double));
+    double* rp = (double*)calloc((size_t)B, sizeof(double));
+    for (int k = 0; k < K && fails >= 0; ++k) {
+      for (int t = 0; t < nthreads; ++t) {
+        for (int b = 0; b < B; ++b) rd[(long long)t * B + b] = 0.0;
+        J[t] = (mt_job){P, I, K, 0, 0, B, np * t / nthreads, np * (t + 1) / nthreads, NULL, NULL,
+                        rd + (long long)t * B, 0, 0};
+        pthread_create(&th[t], NULL, mt_pairs, &J[t]);
+      }
+      for (int t = 0; t < nthreads; ++t) {
+        pthread_join(th[t], NULL);
+        fails += J[t].fails;
+      }
+      if (orc_primal_step(P, I) != 0) { fails = -1; break; }
+      orc_multiplier_update(P, I, rp);
+      for (int b = 0; b < B; ++b) {
+        double s = 0.0;
+        for (int t = 0; t < nthreads; ++t) s += rd[(long long)t * B + b];
+        if (hist_rpri) hist_rpri[(long long)k * B + b] = rp[b];
+        if (hist_rdual) hist_rdual[(long long)k * B + b] = s;
+      }
+    }
+    free(rd);
+    free(rp);
+  }
+  free(J);
+  free(th);
+  return fails;
 }

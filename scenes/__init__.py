@@ -45,6 +45,8 @@ CONFIG_NAMES = {
     8: "C2b: C2 with state/control boxes (|a| <= 0.5, |om| <= 1.5, 2.5 <= v <= 3.5; NEXT f1), N=50, K=200",
     9: "C4s: C4m sensing only the vehicles within 60 m x 8 m of the ego (P:541; NEXT f3), N=60, K=300",
     10: "C2t: C2 with a rigid trailer behind the body origin, scaled about its own centre (NEXT f3), N=50, K=200",
+    11: "C2p: C2's obstacles, point-mass (double-integrator) car of fixed heading, TRANSLATION pose, N=50, K=200",
+    12: "C3p: C3's wall and quadrotor with the TRANSLATION pose (yaw not part of the pose), N=40, K=100",
 }
 
 
@@ -445,7 +447,36 @@ def make_c5(n_scenes: int | None = None, scene_ids: Sequence[int] | None = None)
     return sc
 
 
+def double_integrator_lti(dt: float = DT):
+    """s = (x, y, vx, vy), u = (ax, ay): x' = x + dt v, v' = v + dt a (exact, time-invariant)."""
+    A = np.eye(4)
+    A[0, 2] = A[1, 3] = dt
+    B = np.zeros((4, 2))
+    B[2, 0] = B[3, 1] = dt
+    return A[None], B[None], np.zeros((1, 4))
+
+
+def make_c2p(seed: int = 2) -> Scene:
+    """Config 11: C2's corridor with a translating rectangle (TRANSLATION pose: R = I,
+    rho = (x, y); P:197-200 with a robot that does not rotate) driven as a double
+    integrator along the same 3 m/s reference."""
+    sc = make_c2(seed)
+    N = sc.horizon
+    t = np.arange(N + 1) * DT
+    ref = np.stack([3.0 * t, np.zeros(N + 1), np.full(N + 1, 3.0), np.zeros(N + 1)], 1)
+    A, Bm, c = double_integrator_lti()
+    return dataclasses.replace(sc, name="C2p", config=11, pose_model=POSE_TRANSLATION,
+                               pose_idx=np.array([0, 1, 0, 0], np.int32), dyn_per_time=0,
+                               dyn_A=A, dyn_B=Bm, dyn_c=c, Qs=np.diag([1.0, 1.0, 0.1, 0.1]),
+                               s0=ref[0][None].copy(), s_ref=ref[None].copy())
+
+
 def make_config(cfg: int, **kw) -> Scene:
+    if cfg == 11:
+        return make_c2p(**kw)
+    if cfg == 12:  # C3 with the TRANSLATION pose: rho = (x, y, z), R = I (yaw left out of the pose)
+        return dataclasses.replace(make_c3(**kw), name="C3p", config=12, pose_model=POSE_TRANSLATION,
+                                   pose_idx=np.array([0, 1, 2, 0], np.int32))
     if cfg == 6:
         return make_c4(moving=True, **kw)
     if cfg == 7:

@@ -53,7 +53,7 @@ def dense_kkt_lq(sc, b=0):
     return sol[:N * ns].reshape(N, ns), sol[N * ns:nx].reshape(N, nu)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 11, 12])
 def test_zero_obstacles_is_dense_lq(orc, cfg):
     sc = strip_obstacles(scenes.make_config(cfg))
     o = orc.Oracle(sc)
@@ -98,7 +98,7 @@ def pair_residual(sc, y, zeta, xi, b, t, i, j, st):
     return np.r_[T + zeta, Rr + xi]
 
 
-@pytest.mark.parametrize("cfg", [2, 3, 10])
+@pytest.mark.parametrize("cfg", [2, 3, 10, 11, 12])
 def test_gn_primal_step_vs_fd_least_squares(orc, cfg):
     sc = scenes.make_config(cfg)
     o = orc.Oracle(sc)
@@ -220,8 +220,9 @@ def translate_scene(sc, delta):
                                dyn_c=c), ds
 
 
-def test_translation_equivariance(orc):
-    sc = scenes.make_config(2)
+@pytest.mark.parametrize("cfg", [2, 11])
+def test_translation_equivariance(orc, cfg):
+    sc = scenes.make_config(cfg)
     a = orc.Oracle(sc)
     a.admm_iterate(sc.iters)
     sc2, ds = translate_scene(sc, np.array([3.7, -1.2]))
