@@ -158,13 +158,32 @@ typedef struct {
   int32_t prox_solver;
 } ca_problem_desc;
 
-/* Residuals of one ADMM iteration, summed over the handle's scenes (Eq. 18, P:324-327;
- * r_dual excludes gamma, reading #19).  pivots = total Lemke pivots of the sweep. */
+/* Residuals and statistics of one ADMM iteration (or one step), summed over the
+ * handle's scenes -- over ALL scenes of a scene-sharded run in ca_admm_iterate's history
+ * and ca_admm_solve's report (Eq. 18; r_dual excludes gamma, reading #19;
+ * raw sums, reading #20).
+ *   n_pairs      pair QPs of the handle (rank-local)
+ *   n_fail       pairs that kept their previous certificate =
+ *                n_ray + n_iterlimit + n_neg_ye:
+ *   n_ray        Lemke ray termination
+ *   n_iterlimit  more than lemke_max_pivot_factor * n pivots
+ *   n_neg_ye     recovered y_e < -1e-6
+ *   pivots       total Lemke pivots (Newton iterations for prox_solver 0);
+ *   max_pivots   the largest pivot count of one pair
+ *   ms_*         device milliseconds of the pair sweep, NCCL collectives, primal step
+ *                (Riccati) and standalone multiplier update of that iteration / step --
+ *                CUDA events on the handle's stream, only while ca_set_timing(h, 1), else 0. */
 typedef struct {
   double r_pri, r_dual;
   int64_t n_pairs, n_fail, pivots;
+  int64_t n_ray, n_iterlimit, n_neg_ye;
+  int32_t max_pivots, reserved_;
+  float ms_sweep, ms_comm, ms_riccati, ms_mult;
 } ca_residuals;
 
+/* ca_admm_solve's report: iterations = the most iterations any scene ran, converged = 1
+ * iff every scene met Eq. 18; last = the statistics of each scene's final iteration,
+ * combined over scenes (per scene: ca_get_scene_residuals, ca_get_solve_scenes). */
 typedef struct {
   int32_t iterations, converged;
   ca_residuals last;
@@ -182,17 +201,28 @@ ca_status ca_workspace_size(const ca_problem_desc* desc, const struct ca_dist_de
 ca_status ca_problem_create(const ca_problem_desc* desc, int device, void* stream, ca_problem** out);
 void ca_problem_destroy(ca_problem* h);
 
-/* ---- multi-GPU: obstacle sharding (one process per GPU, NCCL over NVLink) ----
- * Rank r of W owns obstacles [j0, j1) of every scene (a contiguous block balanced by
- * total face count, ca_obstacle_partition) and solves only those pairs; every rank
- * holds the full trajectory.  Per iteration the per-(scene, t) aggregates of step 2
- * and the residual partials are summed by ONE ncclAllReduce on
- * the handle's stream; the primal step then runs replicated on identical bytes.
- * Pair indices of the getters are rank-local (j counted from j0).
- * Scene sharding needs no collective: give each rank its own scenes instead. */
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink / NVSwitch) ----
+ * The ranks form a scene_shards x obstacle_shards grid (world_size = product; rank r
+ * has scene shard r / obstacle_shards and obstacle shard r % obstacle_shards; 0, 0 =
+ * 1 x world_size, obstacle sharding only).
+ *  - Scene shard s holds scenes [B s / Ws, B (s+1) / Ws) of the full problem (scenes are
+ *    independent MPC problems).  Per iteration ONE ncclAllReduce over all ranks carries
+ *    every scene's statistics (NSTAT doubles per scene: Eq. 18's r_pri, r_dual, pivot and
+ *    failure counts), so every rank sees the global residuals: ca_admm_solve's stop
+ *    decision (Eq. 18 per scene, until every scene of every rank has stopped) and
+ *    ca_admm_iterate's history are global and identical on every rank.
+ *  - Obstacle shard o owns obstacles [j0, j1) of its scenes (a contiguous block balanced
+ *    by total face count, ca_obstacle_partition) and solves only those pairs; every rank
+ *    of the group holds the full trajectory of its scenes.  Per iteration the per-(scene,
+ *    t) aggregates of step 2 and the residual partials are summed by ONE
+ *    ncclAllReduce over the group (ncclCommSplit of the world); the primal step then runs
+ *    replicated on identical bytes.
+ * Getters are rank-local: scenes counted from the shard's first scene, pair indices with
+ * j counted from j0. */
 typedef struct ca_dist_desc_s {
   int32_t world_size, rank;
   const uint8_t* nccl_id; /* 128 bytes from ca_nccl_unique_id on one rank, broadcast */
+  int32_t scene_shards, obstacle_shards; /* grid; 0, 0 = 1 x world_size */
 } ca_dist_desc;
 
 ca_status ca_nccl_unique_id(uint8_t* out128);
@@ -201,8 +231,11 @@ ca_status ca_nccl_unique_id(uint8_t* out128);
 ca_status ca_obstacle_partition(int32_t n_scenes, int32_t n_obs, const int32_t* obs_off, int32_t world_size,
                                 int32_t rank, int32_t* j0, int32_t* j1);
 
-/* ca_problem_create for rank dist->rank of an obstacle-sharded problem (desc is the
- * FULL problem; the rank keeps its block).  world_size == 1 is allowed. */
+/* ca_problem_create for rank dist->rank of a sharded problem (desc is the FULL problem;
+ * the rank keeps its scene and obstacle block).  world_size == 1 is allowed (the NCCL
+ * path on one rank).  CA_E_INVALID if scene_shards * obstacle_shards != world_size or
+ * scene_shards > n_scenes.  A rank whose obstacle block is empty still takes part in
+ * every collective. */
 ca_status ca_problem_create_dist(const ca_problem_desc* desc, const ca_dist_desc* dist, int device, void* stream,
                                  ca_problem** out);
 
@@ -228,9 +261,18 @@ ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, do
  * early stop.  hist: HOST [iters] per-iteration residuals or NULL. */
 ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist);
 
-/* Iterate until every scene meets Eq. 18 (r_pri <= eps_pri and r_dual <= eps_dual,
- * '<=' per P:325-326) or max_iters; CA_W_NOT_CONVERGED if the cap was hit. */
+/* ADMM until Eq. 18: every scene is its own MPC problem and stops at the
+ * first iteration with r_pri <= eps_pri and r_dual <= eps_dual ('<=' as printed; SPEC
+ * S:528) -- its iterate stays there while the other scenes continue -- or after
+ * max_iters.  eps <= 0 at create: 1e-3 * pairs per scene of the FULL problem (SPEC
+ * S:551).  Scene-sharded: the loop ends when every scene of every rank has stopped (the
+ * per-iteration allreduce makes that decision identical on every rank).  Each call
+ * starts from the current iterate.  CA_W_NOT_CONVERGED if a scene hit max_iters. */
 ca_status ca_admm_solve(ca_problem* h, ca_solve_report* out);
+
+/* After ca_admm_solve: per local scene, the iterations it ran and whether it met Eq. 18
+ * (HOST [n_scenes] int32 each, nullable).  CA_E_INVALID before any solve. */
+ca_status ca_get_solve_scenes(ca_problem* h, int32_t* iterations, int32_t* converged);
 
 /* The three ADMM steps one at a time (frozen-input parity): step 1 (Eq. 15),
  * step 2 (Eq. 16), step 3 (Eq. 17).  out may be NULL. */
@@ -238,7 +280,19 @@ ca_status ca_dual_sweep(ca_problem* h, ca_residuals* out);
 ca_status ca_primal_step(ca_problem* h);
 ca_status ca_multiplier_update(ca_problem* h, ca_residuals* out);
 
-/* Per-scene residuals of the last completed step: HOST [n_scenes] each (nullable). */
+/* The obstacle-sharded exchange made observable on one GPU: the
+ * per-(scene, t) records of the last dual sweep, each the fixed-order sum over this
+ * handle's pairs of that (scene, t) -- exactly what an obstacle-sharded rank
+ * contributes to the per-iteration ncclAllReduce -- into HOST rec[B*N][R] (R = 17 for
+ * dim 2, 22 for dim 3: (d+1)(d+2)/2 + (d+1) Gauss-Newton terms, then r_dual, r_pri,
+ * pivots, failures, rays, iteration limits, negative y_e, max pivots).
+ * ca_primal_step_records runs Eq. 16 (the replicated Riccati step of the sharded path)
+ * on given HOST records of the same layout (e.g. the sum of two obstacle halves). */
+ca_status ca_get_stage_records(ca_problem* h, double* rec);
+ca_status ca_primal_step_records(ca_problem* h, const double* rec);
+
+/* Per-scene residuals of the last completed step (after ca_admm_solve: of each scene's
+ * final iteration): HOST [n_scenes] each (nullable). */
 ca_status ca_get_scene_residuals(ca_problem* h, double* r_pri, double* r_dual);
 
 /* HOST s[B*(N+1)*ns], u[B*N*nu] (either may be NULL). */
@@ -261,12 +315,12 @@ ca_status ca_set_iterate(ca_problem* h, const double* s, const double* u, const 
  * sum ||x - w||^2 after the last primal step.  CA_E_INVALID if the problem has no box. */
 ca_status ca_get_box_state(ca_problem* h, double* w_s, double* l_s, double* w_u, double* l_u, double* res);
 
-/* Device milliseconds accumulated per kernel family since the last reset (CUDA
- * events on the handle's stream, only while ca_set_timing(h, 1)): ms[0] pair
- * sweep, [1] primal, [2] multiplier, [3] scale detect (+ per-scene min), [4] other
- * small kernels (init, collect, history; not timed, ms[4] = 0); launches[0..4] the
- * matching kernel-launch counts (always counted).  Arrays have 5 entries; reset != 0
- * zeroes. */
+/* Device milliseconds accumulated per family since the last reset (CUDA events on
+ * the handle's stream, only while ca_set_timing(h, 1)): ms[0] pair sweep, [1] primal,
+ * [2] multiplier, [3] scale detect (+ per-scene min), [4] other small kernels (init,
+ * collect, history; not timed, ms[4] = 0), [5] NCCL collectives; launches[0..4] the
+ * matching counts of this library's kernel launches, launches[5] the collectives
+ * (always counted).  Arrays have 6 entries; reset != 0 zeroes. */
 ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t reset);
 
 /* Enable (1) / disable (0) per-launch event timing (default off). */

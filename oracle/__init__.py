@@ -108,7 +108,7 @@ class _Iterate(C.Structure):
     _fields_ = [("s", C.c_void_p), ("u", C.c_void_p), ("y", C.c_void_p), ("zeta", C.c_void_p),
                 ("xi", C.c_void_p), ("pivots", C.c_void_p), ("status", C.c_void_p),
                 ("ws", C.c_void_p), ("ls", C.c_void_p), ("wu", C.c_void_p), ("lu", C.c_void_p),
-                ("boxres", C.c_void_p)]
+                ("boxres", C.c_void_p), ("zmask", C.c_void_p)]
 
 
 class Oracle:
@@ -175,12 +175,14 @@ class Oracle:
         self.ws, self.ls = np.zeros((B, N + 1, ns)), np.zeros((B, N + 1, ns))  # box block (reading #7)
         self.wu, self.lu = np.zeros((B, N, nu)), np.zeros((B, N, nu))
         self.boxres = np.zeros(B)
+        self.zmask = np.zeros(max(npair, 1), np.uint32)  # final Lemke basis per pair (last dual sweep)
         It = _Iterate()
         It.s, It.u, It.y = self.s.ctypes.data, self.u.ctypes.data, self.y.ctypes.data
         It.zeta, It.xi = self.zeta.ctypes.data, self.xi.ctypes.data
         It.pivots, It.status = self.pivots.ctypes.data, self.status.ctypes.data
         It.ws, It.ls, It.wu, It.lu = (a.ctypes.data for a in (self.ws, self.ls, self.wu, self.lu))
         It.boxres = self.boxres.ctypes.data
+        It.zmask = self.zmask.ctypes.data
         self.I = It
         self.init_iterate()
 

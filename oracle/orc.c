@@ -610,7 +610,7 @@ static long long dual_sweep_range(const orc_problem* P, orc_iterate* I, long lon
     int r0 = P->part_off[i], nr = P->part_off[i + 1] - r0;
     int o = b * P->n_obs + j, l0 = P->obs_off[o], no = P->obs_off[o + 1] - l0;
     double ynew[MAXN];
-    int piv;
+    int piv, basis[MAXN];
     double rj[3];
     double bt[MAXN], rhoi[3];
     part_frame(P, i, R, rho, bt, rhoi);
@@ -618,7 +618,16 @@ static long long dual_sweep_range(const orc_problem* P, orc_iterate* I, long lon
     int st = orc_pair_solve(d, nr, P->part_A + (long long)r0 * d, bt, no,
                             P->obs_C + (long long)l0 * d, P->obs_d + l0, R, rj, I->zeta[p],
                             I->xi + p * d, P->prox_eps, I->y + p * P->ny, P->pivot_tol,
-                            P->tie_tol, P->max_pivot_factor, ynew, &piv, NULL);
+                            P->tie_tol, P->max_pivot_factor, ynew, &piv, basis);
+    if (I->zmask) { /* basis labels: w_i = i, z_j = n + j, z0 = 2n */
+      const int n = nr + no + 1;
+      unsigned zm = 0;
+      for (int r = 0; r < n; ++r) {
+        if (basis[r] >= n && basis[r] < 2 * n) zm |= 1u << (basis[r] - n);
+        if (basis[r] == 2 * n) zm |= 0x80000000u;
+      }
+      I->zmask[p] = zm;
+    }
     if (I->pivots) I->pivots[p] = piv;
     if (I->status) I->status[p] = st;
     if (st != ORC_OK) { ++fails; continue; }
@@ -1051,6 +1060,7 @@ static void scene_view(const orc_problem* P, const orc_iterate* I, int b, orc_pr
   Ib->xi = I->xi + b * pps * d;
   if (I->pivots) Ib->pivots = I->pivots + b * pps;
   if (I->status) Ib->status = I->status + b * pps;
+  if (I->zmask) Ib->zmask = I->zmask + b * pps;
   if (I->ws) {
     Ib->ws = I->ws + (long long)b * (N + 1) * ns;
     Ib->ls = I->ls + (long long)b * (N + 1) * ns;

@@ -89,6 +89,9 @@ typedef struct {
   double* wu;     /* [B][N][nu]  w for the controls */
   double* lu;     /* [B][N][nu]  l for the controls */
   double* boxres; /* [B] sum ||x - w||^2 after the last primal step */
+  /* nullable: [P] final Lemke basis of the last dual sweep, bit j = z_j basic (LCP
+   * index j), bit 31 = z0 basic (ITER_LIMIT); 0 for q >= 0 (L1) */
+  unsigned* zmask;
 } orc_iterate;
 
 #endif

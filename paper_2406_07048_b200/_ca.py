@@ -47,12 +47,22 @@ class Desc(C.Structure):
 
 
 class DistDesc(C.Structure):
-    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p)]
+    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p),
+                ("scene_shards", C.c_int32), ("obstacle_shards", C.c_int32)]
+
+
+RES_FIELDS = ("r_pri", "r_dual", "n_pairs", "n_fail", "pivots", "n_ray", "n_iterlimit", "n_neg_ye", "max_pivots",
+              "ms_sweep", "ms_comm", "ms_riccati", "ms_mult")
 
 
 class Residuals(C.Structure):
     _fields_ = [("r_pri", C.c_double), ("r_dual", C.c_double), ("n_pairs", C.c_int64),
-                ("n_fail", C.c_int64), ("pivots", C.c_int64)]
+                ("n_fail", C.c_int64), ("pivots", C.c_int64), ("n_ray", C.c_int64), ("n_iterlimit", C.c_int64),
+                ("n_neg_ye", C.c_int64), ("max_pivots", C.c_int32), ("reserved_", C.c_int32),
+                ("ms_sweep", C.c_float), ("ms_comm", C.c_float), ("ms_riccati", C.c_float), ("ms_mult", C.c_float)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f in RES_FIELDS}
 
 
 class SolveReport(C.Structure):
@@ -84,6 +94,9 @@ def lib():
         L.ca_scale_detect.argtypes = [vp, vp, vp, vp]
         L.ca_admm_iterate.argtypes = [vp, C.c_int32, vp]
         L.ca_admm_solve.argtypes = [vp, C.POINTER(SolveReport)]
+        L.ca_get_solve_scenes.argtypes = [vp, vp, vp]
+        L.ca_get_stage_records.argtypes = [vp, vp]
+        L.ca_primal_step_records.argtypes = [vp, vp]
         L.ca_dual_sweep.argtypes = [vp, C.POINTER(Residuals)]
         L.ca_primal_step.argtypes = [vp]
         L.ca_multiplier_update.argtypes = [vp, C.POINTER(Residuals)]
@@ -109,7 +122,8 @@ def lib():
                      "ca_multiplier_update", "ca_get_scene_residuals", "ca_get_trajectory",
                      "ca_get_pair_state", "ca_set_iterate", "ca_kernel_times", "ca_set_timing",
                      "ca_set_record_basis", "ca_fp64_peak", "ca_reset_iterate", "ca_debug_trace",
-                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size"):
+                     "ca_nccl_unique_id", "ca_obstacle_partition", "ca_problem_create_dist", "ca_workspace_size",
+                     "ca_get_solve_scenes", "ca_get_stage_records", "ca_primal_step_records"):
             getattr(L, name).restype = C.c_int32
         _lib = L
     return _lib
@@ -186,8 +200,9 @@ class Problem:
 
     def __init__(self, sc, device: int = 0, stream: int | None = None, dist=None, workspace: str | None = None,
                  **params):
-        """dist = (world_size, rank, nccl_id bytes): obstacle-sharded rank of the full
-        problem `sc` (include/ca.h ca_problem_create_dist); None = single GPU.
+        """dist = (world_size, rank, nccl_id bytes[, scene_shards, obstacle_shards]): rank of
+        the sharded full problem `sc` (include/ca.h ca_problem_create_dist; grid 0, 0 =
+        obstacle sharding only); None = single GPU.
         workspace = "torch": every device buffer is carved out of one torch uint8 tensor
         of ca_workspace_size bytes (device memory owned by PyTorch's allocator)."""
         self.sc = sc
@@ -197,9 +212,10 @@ class Problem:
         h = C.c_void_p()
         self.dist = dist
         if dist is not None:
-            world, rank, nid = dist
+            world, rank, nid = dist[:3]
+            ws, wo = (tuple(dist[3:5]) + (0, 0))[:2]
             self._nid = C.create_string_buffer(bytes(nid), 128)
-            dd = DistDesc(world, rank, C.cast(self._nid, C.c_void_p))
+            dd = DistDesc(world, rank, C.cast(self._nid, C.c_void_p), ws, wo)
         if workspace == "torch":
             import torch
 
@@ -215,7 +231,11 @@ class Problem:
             self.j0, self.j1 = 0, sc.n_obs
         else:
             _check(lib().ca_problem_create_dist(C.byref(desc), C.byref(dd), device, stream, C.byref(h)), ok=(CA_OK,))
-            self.j0, self.j1 = obstacle_partition(sc, world, rank)
+            self.grid = grid_position(sc.n_scenes, world, rank, ws, wo)
+            b0, b1 = self.grid["scenes"]
+            self.j0, self.j1 = obstacle_partition(sc.subset(range(b0, b1)) if (b0, b1) != (0, sc.n_scenes) else sc,
+                                                  self.grid["Wo"], self.grid["ro"])
+            self.sc = sc.subset(range(b0, b1)) if (b0, b1) != (0, sc.n_scenes) else sc  # the rank's scenes
         self.h = h
         n, ny, nb = C.c_int64(), C.c_int32(), C.c_int64()
         _check(lib().ca_problem_info(h, C.byref(n), C.byref(ny), C.byref(nb)))
@@ -248,12 +268,19 @@ class Problem:
         rc = _check(lib().ca_admm_iterate(self.h, iters, H))
         if not hist:
             return rc
-        return rc, {f: np.array([getattr(r, f) for r in H]) for f in ("r_pri", "r_dual", "n_fail", "pivots")}
+        return rc, {f: np.array([getattr(r, f) for r in H]) for f in RES_FIELDS}
 
     def admm_solve(self):
+        """ADMM until Eq. 18 per scene (include/ca.h ca_admm_solve): (rc, report dict,
+        per-scene iterations, per-scene converged flags)."""
         rep = SolveReport()
         rc = _check(lib().ca_admm_solve(self.h, C.byref(rep)))
-        return rc, rep
+        B = self.sc.n_scenes
+        it = np.empty(B, np.int32)
+        cv = np.empty(B, np.int32)
+        _check(lib().ca_get_solve_scenes(self.h, _ptr(it), _ptr(cv)))
+        out = {"iterations": rep.iterations, "converged": bool(rep.converged), **rep.last.as_dict()}
+        return rc, out, it, cv.astype(bool)
 
     def dual_sweep(self):
         r = Residuals()
@@ -262,6 +289,18 @@ class Problem:
 
     def primal_step(self):
         _check(lib().ca_primal_step(self.h))
+
+    def stage_records(self):
+        """[B, N, R] per-(scene, t) records of the last dual sweep (include/ca.h)."""
+        sc = self.sc
+        R = rec_len(sc.dim)
+        out = np.empty((sc.n_scenes, sc.horizon, R))
+        _check(lib().ca_get_stage_records(self.h, _ptr(out)))
+        return out
+
+    def primal_step_records(self, rec):
+        rec = _f64(rec)
+        _check(lib().ca_primal_step_records(self.h, _ptr(rec)))
 
     def multiplier_update(self):
         r = Residuals()
@@ -289,20 +328,17 @@ class Problem:
         _check(lib().ca_get_scene_residuals(self.h, _ptr(rp), _ptr(rd)))
         return rp, rd
 
-    def pair_state(self, p0: int = 0, count: int | None = None, zmask: bool = False):
+    def pair_state(self, p0: int = 0, count: int | None = None, zmask: bool = False, fields=None):
+        """Pair state of pairs [p0, p0 + count): y, zeta, xi, pivots, status (and zmask);
+        `fields` restricts the copies (e.g. ("status",) for a cheap failure scan)."""
         count = self.n_pairs - p0 if count is None else count
         d = self.sc.dim
-        y = np.empty((count, self.ny))
-        zeta = np.empty(count)
-        xi = np.empty((count, d))
-        piv = np.empty(count, np.int32)
-        st = np.empty(count, np.int32)
-        zm = np.empty(count, np.uint32) if zmask else None
-        _check(lib().ca_get_pair_state(self.h, p0, count, _ptr(y), _ptr(zeta), _ptr(xi), _ptr(piv), _ptr(st),
-                                       _ptr(zm)))
-        out = {"y": y, "zeta": zeta, "xi": xi, "pivots": piv, "status": st}
-        if zmask:
-            out["zmask"] = zm
+        want = set(fields) if fields is not None else {"y", "zeta", "xi", "pivots", "status"} | ({"zmask"} if zmask else set())
+        shapes = {"y": ((count, self.ny), np.float64), "zeta": ((count,), np.float64), "xi": ((count, d), np.float64),
+                  "pivots": ((count,), np.int32), "status": ((count,), np.int32), "zmask": ((count,), np.uint32)}
+        out = {k: np.empty(*shapes[k]) for k in want}
+        _check(lib().ca_get_pair_state(self.h, p0, count, *[_ptr(out.get(k)) for k in
+                                                              ("y", "zeta", "xi", "pivots", "status", "zmask")]))
         return out
 
     def set_iterate(self, s=None, u=None, y=None, zeta=None, xi=None):
@@ -332,10 +368,11 @@ class Problem:
         _check(lib().ca_set_record_basis(self.h, int(on)))
 
     def kernel_times(self, reset: bool = False):
-        ms = (C.c_double * 5)()
-        ln = (C.c_int64 * 5)()
+        """{family: (device ms, count)}: the library's kernel families and 'comm' (NCCL)."""
+        ms = (C.c_double * 6)()
+        ln = (C.c_int64 * 6)()
         _check(lib().ca_kernel_times(self.h, ms, ln, int(reset)))
-        names = ("sweep", "primal", "multiplier", "scale", "other")
+        names = ("sweep", "primal", "multiplier", "scale", "other", "comm")
         return {n: (ms[i], ln[i]) for i, n in enumerate(names)}
 
 
@@ -343,6 +380,26 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().ca_nccl_unique_id(buf))
     return buf.raw
+
+
+def rec_len(d: int) -> int:
+    """doubles per record: (d+1)(d+2)/2 + (d+1) Gauss-Newton terms + 8 statistics"""
+    return (d + 1) * (d + 2) // 2 + (d + 1) + 8
+
+
+def grid_position(n_scenes: int, world: int, rank: int, scene_shards: int = 0, obstacle_shards: int = 0):
+    """The rank's place in the scene x obstacle grid (include/ca.h ca_dist_desc; the
+    library computes the same on its side): shard indices and the scene block."""
+    ws, wo = scene_shards, obstacle_shards
+    if ws <= 0 and wo <= 0:
+        ws, wo = 1, world
+    elif ws <= 0:
+        ws = world // wo
+    elif wo <= 0:
+        wo = world // ws
+    rs, ro = rank // wo, rank % wo
+    return {"Ws": ws, "Wo": wo, "rs": rs, "ro": ro,
+            "scenes": (n_scenes * rs // ws, n_scenes * (rs + 1) // ws)}
 
 
 def obstacle_partition(sc, world: int, rank: int):

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -57,34 +58,57 @@ constexpr int NMAX_SET[] = {9, 11, 13, 15, 20, 32};
 
 }  // namespace
 
+constexpr int NST = ca::NSTAT;  // per-scene statistics per slot (ca::S_* order)
+constexpr int NFAM = 6;          // timing families: sweep, primal, multiplier, scale, other, comm
+
 struct ca_problem {
   int device = 0;
   cudaStream_t stream = nullptr;
   ca::Dev dev{};
   int d = 0, B = 0, N = 0, ns = 0, nu = 0, np = 0, M = 0, nmax = 0, nmax_t = 0, rows_max = 0;
   long long P = 0;
+  int M_full = 0;  // obstacles per scene of the FULL problem (default Eq. 18 thresholds)
   std::vector<int> obs_counts;  // per obstacle row counts (shape check on load)
   std::vector<int> part_off;
   std::vector<void*> allocs;
   double* alpha = nullptr;
   double* slots = nullptr;
   int slots_cap = 0;
-  double* scene_res = nullptr;  // [B*4] (rdual, rpri, piv, fail) of the last step
+  double* scene_res = nullptr;  // [B][NST] statistics of the last step (ca::S_* order)
   double* hist_dev = nullptr;
   int hist_cap = 0;
   double eps_pri = 0, eps_dual = 0;
   int max_iters = 100;
   bool timing = false;
-  double ms[5] = {0, 0, 0, 0, 0};
-  long long launches[5] = {0, 0, 0, 0, 0};
+  double ms[NFAM] = {0, 0, 0, 0, 0, 0};
+  long long launches[NFAM] = {0, 0, 0, 0, 0, 0};
   double* s_start = nullptr;  // initial state trajectory (reset point)
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  struct Pending {
+    int fam, iter;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  int cur_iter = -1;  // iteration index of the launches being enqueued (timing per iteration)
   std::vector<cudaEvent_t> event_pool;
   bool sticky = false;
   long long bytes = 0;
-  // obstacle sharding
-  ncclComm_t comm = nullptr;
+  // multi-GPU (include/ca.h ca_dist_desc): a scene_shards x obstacle_shards grid.
+  // comm = the obstacle group of this rank (ranks holding the same scenes; NULL when
+  // obstacle_shards == 1), comm_all = every rank (NULL when scene_shards == 1: comm is
+  // then the world).  j0/j1: obstacle block; b0: first global scene; B_total: all scenes.
+  ncclComm_t comm = nullptr, comm_all = nullptr;
   int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
+  int Ws = 1, Wo = 1, rs = 0, ro = 0, b0 = 0, B_total = 0;
+  double* glob = nullptr;  // scene-sharded: [slots_cap][B_total][NST] allreduced statistics
+  double* pmx = nullptr;   // [max(B*N, B)] S_PMAX column for the max-allreduce
+  // ca_admm_solve (Eq. 18 per scene)
+  uint8_t* active = nullptr;
+  int* s_iters = nullptr;
+  int* d_remaining = nullptr;
+  double* s_fin = nullptr;    // [B][NST] statistics of each scene's last iteration
+  double* states_buf = nullptr;  // ca_scale_detect(states != NULL) staging
+  bool dist_mode = false;        // created by ca_problem_create_dist
+  bool solved = false;           // ca_admm_solve has run (ca_get_solve_scenes)
   double* obs_step_buf = nullptr;  // moving obstacles (allocated on first use)
   double* sense_half = nullptr;    // [3] sensing box half-extents (NEXT f3)
   // caller-provided device workspace (bump allocation, 256-B aligned); count_only:
@@ -96,25 +120,27 @@ struct ca_problem {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream to capture on (the handle's may be legacy)
   int g_iters = 0;
-  long long g_launches[5] = {0, 0, 0, 0, 0};
+  long long g_launches[NFAM] = {0, 0, 0, 0, 0, 0};
   bool use_graphs = std::getenv("CA_NO_GRAPHS") == nullptr;  // diagnostics: CA_NO_GRAPHS=1 disables
   void drop_graph() {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
     g_iters = 0;
   }
-  double* rb = nullptr;     // [B*N][REC] reduced records (allreduced)
-  double* tmpB4 = nullptr;  // [B][4]
+  double* rb = nullptr;    // [B*N][rec] reduced records (allreduced)
+  size_t agg_n = 0;        // doubles of dev.agg
+  double* tmpB = nullptr;  // [B][NST]
 
   ~ca_problem() {
     drop_graph();
     if (cap_stream) cudaStreamDestroy(cap_stream);
-    if (comm) ncclCommDestroy(comm);
+    if (comm && comm != comm_all) ncclCommDestroy(comm);
+    if (comm_all) ncclCommDestroy(comm_all);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : event_pool) cudaEventDestroy(e);
     for (auto& pe : pending) {
-      cudaEventDestroy(pe.second.first);
-      cudaEventDestroy(pe.second.second);
+      cudaEventDestroy(pe.a);
+      cudaEventDestroy(pe.b);
     }
   }
   template <class T>
@@ -289,6 +315,8 @@ ca_status reset_iterate(ca_problem* h) {
   CUDA_TRY(cudaMemcpyAsync(v.s, h->s_start, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns,
                            cudaMemcpyDeviceToDevice, h->stream));
   CUDA_TRY(cudaMemsetAsync(v.u, 0, sizeof(double) * (size_t)h->B * h->N * h->nu, h->stream));
+  if (h->P == 0)  // no pair ever writes a record: the primal step then reads zero aggregates
+    CUDA_TRY(cudaMemsetAsync(v.agg, 0, sizeof(double) * h->agg_n, h->stream));
   if (h->P > 0) {
     CUDA_TRY(cudaMemsetAsync(v.zeta, 0, sizeof(double) * (size_t)h->P, h->stream));
     CUDA_TRY(cudaMemsetAsync(v.xi, 0, sizeof(double) * (size_t)h->d * h->P, h->stream));
@@ -414,17 +442,20 @@ void t_end(ca_problem* h, int fam, cudaEvent_t e0) {
   if (h->timing) {
     cudaEvent_t e1 = h->ev();
     cudaEventRecord(e1, h->stream);
-    h->pending.push_back({fam, {e0, e1}});
+    h->pending.push_back({fam, h->cur_iter, e0, e1});
   }
 }
-ca_status flush_timing(ca_problem* h) {
+// Accumulate the recorded launch times into h->ms; with per_iter (HOST [n_iter][NFAM])
+// also per iteration of the enqueue that recorded them.
+ca_status flush_timing(ca_problem* h, double* per_iter = nullptr, int n_iter = 0) {
   for (auto& pe : h->pending) {
     float ms = 0.f;
-    CUDA_TRY(cudaEventSynchronize(pe.second.second));
-    CUDA_TRY(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
-    h->ms[pe.first] += ms;
-    h->event_pool.push_back(pe.second.first);
-    h->event_pool.push_back(pe.second.second);
+    CUDA_TRY(cudaEventSynchronize(pe.b));
+    CUDA_TRY(cudaEventElapsedTime(&ms, pe.a, pe.b));
+    h->ms[pe.fam] += ms;
+    if (per_iter && pe.iter >= 0 && pe.iter < n_iter) per_iter[pe.iter * NFAM + pe.fam] += ms;
+    h->event_pool.push_back(pe.a);
+    h->event_pool.push_back(pe.b);
   }
   h->pending.clear();
   return CA_OK;
@@ -491,17 +522,22 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
     return CA_OK;
   }
   const size_t sm = sizeof(double) * (size_t)ca::riccati_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
-  static size_t configured = 48 * 1024;
-  if (sm > configured) {
-    CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    configured = sm;
+  if (sm > 48 * 1024) {  // the attribute is per device: cached per device ordinal under a lock
+    static std::mutex mu;
+    static size_t configured[CA_MAX_DEVICES] = {};
+    if (h->device >= CA_MAX_DEVICES) return fail(CA_E_CUDA, "device ordinal too large");
+    std::lock_guard<std::mutex> lk(mu);
+    if (sm > configured[h->device]) {
+      CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      configured[h->device] = sm;
+    }
   }
   ca::k_riccati<NS, NU><<<(unsigned)h->B, 32, sm, h->stream>>>(h->dev, recs, nchunk, cur, prev);
   CUDA_TRY(cudaGetLastError());
   return CA_OK;
 }
 
-ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
+ca_status launch_riccati(ca_problem* h, double* cur, double* prev, const double* given_recs = nullptr) {
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
   ca_status st;
@@ -513,13 +549,26 @@ ca_status launch_riccati(ca_problem* h, double* cur, double* prev) {
   }
   const double* recs = h->dev.agg;
   int nchunk = h->dev.nchunkG;
-  if (h->comm) {
-    // a5: one allreduce of the per-(scene, t) aggregates + residual partials
+  if (given_recs) {  // ca_primal_step_records: one record per (scene, t) given
+    recs = given_recs;
+    nchunk = 0;
+  } else if (h->comm) {
+    // a5: one allreduce of the per-(scene, t) aggregates + residual partials (the S_PMAX
+    // column max-reduced in the same NCCL group: one fused collective)
     const long long nq = (long long)h->B * h->N;
     const unsigned gq = (unsigned)((nq + 127) / 128);
-    ca::k_reduce_records<<<gq, 128, 0, h->stream>>>(h->dev, h->rb);
+    ca::k_reduce_records<<<gq, 128, 0, h->stream>>>(h->dev, h->rb, h->pmx);
     CUDA_TRY(cudaGetLastError());
-    NCCL_TRY(ncclAllReduce(h->rb, h->rb, (size_t)nq * ca::REC, ncclDouble, ncclSum, h->comm, h->stream));
+    h->launches[1]++;
+    cudaEvent_t c0 = nullptr;
+    t_begin(h, &c0);
+    NCCL_TRY(ncclGroupStart());
+    NCCL_TRY(ncclAllReduce(h->rb, h->rb, (size_t)nq * h->dev.rec, ncclDouble, ncclSum, h->comm, h->stream));
+    NCCL_TRY(ncclAllReduce(h->pmx, h->pmx, (size_t)nq, ncclDouble, ncclMax, h->comm, h->stream));
+    NCCL_TRY(ncclGroupEnd());
+    t_end(h, 5, c0);
+    ca::k_pmax_back<<<gq, 128, 0, h->stream>>>(h->dev, h->rb, h->pmx);
+    CUDA_TRY(cudaGetLastError());
     h->launches[1]++;
     recs = h->rb;
     nchunk = 0;  // one reduced record per (scene, t)
@@ -551,7 +600,7 @@ ca_status launch_mult(ca_problem* h) {
 
 ca_status launch_collect(ca_problem* h, double* dst, int mask) {
   if (h->P == 0) {
-    CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * 4 * h->B, h->stream));
+    CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * NST * h->B, h->stream));
     return CA_OK;
   }
   // the box residual joins r_pri once (rank 0 of an obstacle-sharded run)
@@ -562,33 +611,68 @@ ca_status launch_collect(ca_problem* h, double* dst, int mask) {
   return CA_OK;
 }
 
+// [n][NST] statistics summed over the ranks of `comm` (S_PMAX: max), one NCCL group
+ca_status allreduce_stats(ca_problem* h, double* buf, int n, ncclComm_t comm) {
+  const unsigned g = (unsigned)((n + 127) / 128);
+  ca::k_stat_split<<<g, 128, 0, h->stream>>>(buf, h->pmx, n);
+  CUDA_TRY(cudaGetLastError());
+  cudaEvent_t c0 = nullptr;
+  t_begin(h, &c0);
+  NCCL_TRY(ncclGroupStart());
+  NCCL_TRY(ncclAllReduce(buf, buf, (size_t)n * NST, ncclDouble, ncclSum, comm, h->stream));
+  NCCL_TRY(ncclAllReduce(h->pmx, h->pmx, (size_t)n, ncclDouble, ncclMax, comm, h->stream));
+  NCCL_TRY(ncclGroupEnd());
+  t_end(h, 5, c0);
+  ca::k_stat_join<<<g, 128, 0, h->stream>>>(buf, h->pmx, n);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[4] += 2;
+  return CA_OK;
+}
+
 // per-scene statistics of the local pairs -> fields `mask` of dst; in obstacle-sharded
-// runs summed over ranks (one small allreduce).  Other fields are left untouched.
+// runs combined over the obstacle group (one small allreduce).  Other fields are left
+// untouched.
 ca_status collect_global(ca_problem* h, double* dst, int mask) {
   if (!h->comm) return launch_collect(h, dst, mask);
-  CUDA_TRY(cudaMemsetAsync(h->tmpB4, 0, sizeof(double) * 4 * h->B, h->stream));
-  ca_status st = launch_collect(h, h->tmpB4, mask);
+  CUDA_TRY(cudaMemsetAsync(h->tmpB, 0, sizeof(double) * NST * h->B, h->stream));
+  ca_status st = launch_collect(h, h->tmpB, mask);
   if (st) return st;
-  NCCL_TRY(ncclAllReduce(h->tmpB4, h->tmpB4, (size_t)4 * h->B, ncclDouble, ncclSum, h->comm, h->stream));
-  for (int f = 0; f < 4; ++f)
+  if ((st = allreduce_stats(h, h->tmpB, h->B, h->comm))) return st;
+  for (int f = 0; f < NST; ++f)
     if ((mask >> f) & 1)
-      CUDA_TRY(cudaMemcpy2DAsync(dst + f, 4 * sizeof(double), h->tmpB4 + f, 4 * sizeof(double), sizeof(double),
+      CUDA_TRY(cudaMemcpy2DAsync(dst + f, NST * sizeof(double), h->tmpB + f, NST * sizeof(double), sizeof(double),
                                  h->B, cudaMemcpyDeviceToDevice, h->stream));
   return CA_OK;
 }
 
-// the rank-local slice [j0, j1) of every scene's obstacles
+// scene-sharded runs (a5 of the scene grid): the completed per-scene statistics of one
+// iteration (slot, [B][NST]) into the global table glob_k ([B_total][NST]) and one
+// ncclAllReduce over every rank -- the global Eq. 18 residuals of every scene on every
+// rank (the stop decision of ca_admm_solve, the global history of ca_admm_iterate).
+ca_status scene_exchange(ca_problem* h, const double* slot, double* glob_k) {
+  if (!h->comm_all) return CA_OK;
+  const int n = h->B * NST;
+  ca::k_scatter_slot<<<(unsigned)((n + 127) / 128), 128, 0, h->stream>>>(glob_k, slot, h->B, h->b0, h->ro == 0);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[4]++;
+  cudaEvent_t c0 = nullptr;
+  t_begin(h, &c0);
+  NCCL_TRY(ncclAllReduce(glob_k, glob_k, (size_t)h->B_total * NST, ncclDouble, ncclSum, h->comm_all, h->stream));
+  t_end(h, 5, c0);
+  return CA_OK;
+}
+
+// The rank-local view of the full problem: scenes [b0, b1), obstacles [j0, j1) of each
+// (pure data movement; the caller's arrays are only read).
 struct LocalObs {
   std::vector<int> off;
-  std::vector<double> C, d, step;
+  std::vector<double> C, d, step, s0, sref, sinit, dA, dB, dc;
 };
-void slice_obstacles(const ca_problem_desc* D, int j0, int j1, LocalObs& L, ca_problem_desc& out) {
-  const int M = D->n_obs, dim = D->dim, Ml = j1 - j0;
+void slice_problem(const ca_problem_desc* D, int b0, int b1, int j0, int j1, LocalObs& L, ca_problem_desc& out) {
+  const int M = D->n_obs, dim = D->dim, Ml = j1 - j0, ns = D->n_state, nu = D->n_ctrl, N = D->horizon;
+  L = LocalObs{};
   L.off.assign(1, 0);
-  L.C.clear();
-  L.d.clear();
-  L.step.clear();
-  for (int b = 0; b < D->n_scenes; ++b)
+  for (int b = b0; b < b1; ++b)
     for (int j = j0; j < j1; ++j) {
       if (D->obs_step)
         for (int a = 0; a < dim; ++a) L.step.push_back(D->obs_step[((long long)b * M + j) * dim + a]);
@@ -605,31 +689,112 @@ void slice_obstacles(const ca_problem_desc* D, int j0, int j1, LocalObs& L, ca_p
   out.obs_C = L.C.empty() ? nullptr : L.C.data();
   out.obs_d = L.d.empty() ? nullptr : L.d.data();
   out.obs_step = (D->obs_step && !L.step.empty()) ? L.step.data() : nullptr;
+  if (b0 == 0 && b1 == D->n_scenes) return;
+  // scene slice of the per-scene arrays
+  out.n_scenes = b1 - b0;
+  L.s0.assign(D->s0 + (long long)b0 * ns, D->s0 + (long long)b1 * ns);
+  L.sref.assign(D->s_ref + (long long)b0 * (N + 1) * ns, D->s_ref + (long long)b1 * (N + 1) * ns);
+  out.s0 = L.s0.data();
+  out.s_ref = L.sref.data();
+  if (D->s_init) {
+    L.sinit.assign(D->s_init + (long long)b0 * (N + 1) * ns, D->s_init + (long long)b1 * (N + 1) * ns);
+    out.s_init = L.sinit.data();
+  }
+  if (D->dyn_per_scene && D->dyn_model == 0) {
+    const long long nt = D->dyn_per_time ? N : 1;
+    L.dA.assign(D->dyn_A + b0 * nt * ns * ns, D->dyn_A + b1 * nt * ns * ns);
+    L.dB.assign(D->dyn_B + b0 * nt * ns * nu, D->dyn_B + b1 * nt * ns * nu);
+    L.dc.assign(D->dyn_c + b0 * nt * ns, D->dyn_c + b1 * nt * ns);
+    out.dyn_A = L.dA.data();
+    out.dyn_B = L.dB.data();
+    out.dyn_c = L.dc.data();
+  }
+}
+
+// The grid position of dist->rank (include/ca.h ca_dist_desc) and its local problem.
+struct GridPos {
+  int world = 1, rank = 0, Ws = 1, Wo = 1, rs = 0, ro = 0, b0 = 0, b1 = 0, j0 = 0, j1 = 0, B_total = 0, M_full = 0;
+};
+ca_status grid_position(const ca_problem_desc* D, const ca_dist_desc* dist, GridPos& g, LocalObs& L,
+                        ca_problem_desc& Dl) {
+  if (!dist->nccl_id || dist->world_size < 1 || dist->rank < 0 || dist->rank >= dist->world_size)
+    return fail(CA_E_INVALID, "bad ca_dist_desc");
+  g.world = dist->world_size;
+  g.rank = dist->rank;
+  int Ws = dist->scene_shards, Wo = dist->obstacle_shards;
+  if (Ws <= 0 && Wo <= 0) {
+    Ws = 1;
+    Wo = g.world;
+  } else if (Ws <= 0) {
+    Ws = g.world / std::max(1, Wo);
+  } else if (Wo <= 0) {
+    Wo = g.world / std::max(1, Ws);
+  }
+  if (Ws * Wo != g.world) return fail(CA_E_INVALID, "scene_shards * obstacle_shards != world_size");
+  if (Ws > D->n_scenes) return fail(CA_E_INVALID, "more scene shards than scenes");
+  g.Ws = Ws;
+  g.Wo = Wo;
+  g.rs = g.rank / Wo;
+  g.ro = g.rank % Wo;
+  g.B_total = D->n_scenes;
+  g.M_full = D->n_obs;
+  g.b0 = (int)((long long)D->n_scenes * g.rs / Ws);
+  g.b1 = (int)((long long)D->n_scenes * (g.rs + 1) / Ws);
+  // the obstacle partition of this scene shard (balanced by its face counts)
+  ca_status st;
+  if ((st = ca_obstacle_partition(g.b1 - g.b0, D->n_obs, D->n_obs > 0 ? D->obs_off + (long long)g.b0 * D->n_obs : nullptr,
+                                  Wo, g.ro, &g.j0, &g.j1)))
+    return st;
+  slice_problem(D, g.b0, g.b1, g.j0, g.j1, L, Dl);
+  return CA_OK;
 }
 
 ca_status ensure_slots(ca_problem* h, int n) {
   if (n <= h->slots_cap) return CA_OK;
   ca_status st;
-  if ((st = h->alloc(&h->slots, (size_t)n * h->B * 4))) return st;
-  if ((st = h->alloc(&h->hist_dev, (size_t)n * 4))) return st;
+  if ((st = h->alloc(&h->slots, (size_t)n * h->B * NST))) return st;
+  if ((st = h->alloc(&h->hist_dev, (size_t)n * NST))) return st;
+  if (h->Ws > 1 && (st = h->alloc(&h->glob, (size_t)n * h->B_total * NST))) return st;
   h->slots_cap = n;
   return CA_OK;
 }
 
-ca_status sums(ca_problem* h, const double* dst_dev, ca_residuals* out) {
-  std::vector<double> v((size_t)h->B * 4);
+// combined statistics [NST] (ca::S_* order) -> ca_residuals
+void fill_res(const double* c, long long n_pairs, ca_residuals* r) {
+  *r = ca_residuals{};
+  r->r_dual = c[ca::S_RDUAL];
+  r->r_pri = c[ca::S_RPRI];
+  r->pivots = (int64_t)c[ca::S_PIV];
+  r->n_fail = (int64_t)c[ca::S_FAIL];
+  r->n_ray = (int64_t)c[ca::S_RAY];
+  r->n_iterlimit = (int64_t)c[ca::S_ITER];
+  r->n_neg_ye = (int64_t)c[ca::S_NEGYE];
+  r->max_pivots = (int32_t)c[ca::S_PMAX];
+  r->n_pairs = n_pairs;
+}
+
+// per-scene statistics [nb][NST] on the device -> their combination over scenes (sum;
+// max for S_PMAX), in scene order
+ca_status sums(ca_problem* h, const double* dst_dev, ca_residuals* out, int nb = -1) {
+  if (nb < 0) nb = h->B;
+  std::vector<double> v((size_t)nb * NST);
   CUDA_TRY(cudaMemcpyAsync(v.data(), dst_dev, sizeof(double) * v.size(), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
-  ca_residuals r{};
-  for (int b = 0; b < h->B; ++b) {
-    r.r_dual += v[b * 4 + 0];
-    r.r_pri += v[b * 4 + 1];
-    r.pivots += (int64_t)v[b * 4 + 2];
-    r.n_fail += (int64_t)v[b * 4 + 3];
-  }
-  r.n_pairs = h->P;
+  double c[NST] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < nb; ++b)
+    for (int f = 0; f < NST; ++f) c[f] = ca::stat_comb(f, c[f], v[(size_t)b * NST + f]);
+  ca_residuals r;
+  fill_res(c, h->P, &r);
   if (out) *out = r;
   return CA_OK;
+}
+
+// the timed device milliseconds (families of flush_timing) into a ca_residuals
+void fill_ms(const double* fam_ms, ca_residuals* r) {
+  r->ms_sweep = (float)fam_ms[0];
+  r->ms_riccati = (float)fam_ms[1];
+  r->ms_mult = (float)fam_ms[2];
+  r->ms_comm = (float)fam_ms[5];
 }
 
 ca_status check_handle(ca_problem* h) {
@@ -649,6 +814,24 @@ ca_status mark(ca_problem* h, ca_status st) {
 extern "C" {
 
 const char* ca_last_error(void) { return g_err.c_str(); }
+
+// the grid position of a sharded handle (NULL: single GPU)
+void set_grid(ca_problem* h, const GridPos* g) {
+  if (!g) return;
+  h->dist_mode = true;
+  h->world = g->world;
+  h->rank = g->rank;
+  h->Ws = g->Ws;
+  h->Wo = g->Wo;
+  h->rs = g->rs;
+  h->ro = g->ro;
+  h->b0 = g->b0;
+  h->B_total = g->B_total;
+  h->j0 = g->j0;
+  h->j1 = g->j1;
+  h->n_obs_full = g->M_full;
+  h->M_full = g->M_full;
+}
 
 // Host-side setup of a handle: shapes, work decomposition and every device buffer
 // (through h->alloc, so a planning pass can size the caller's workspace).
@@ -678,6 +861,10 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   v.d = h->d; v.B = h->B; v.N = h->N; v.ns = h->ns; v.nu = h->nu; v.np = h->np; v.M = h->M;
   v.pose_model = D->pose_model;
   v.npc = (D->pose_model == CA_POSE_TRANSLATION) ? h->d : h->d + 1;
+  v.nagg = ca::rec_nagg(h->d);
+  v.rec = ca::rec_n(h->d);
+  v.active = nullptr;
+  if (!h->M_full) h->M_full = D->n_obs;
   for (int a = 0; a < 4; ++a) v.pidx[a] = D->pose_idx[a];
   v.dyn_ps = (D->dyn_per_scene || D->dyn_model) ? 1 : 0;  // relinearised: one block per (scene, t)
   v.dyn_pt = (D->dyn_per_time || D->dyn_model) ? 1 : 0;
@@ -761,8 +948,9 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   AL(v.zeta, double, std::max<long long>(h->P, 1));
   AL(v.xi, double, (size_t)d * std::max<long long>(h->P, 1));
   AL(v.pst, uint32_t, std::max<long long>(h->P, 1));
-  AL(v.agg, double, (size_t)B * v.NG * v.nchunkG * v.TG * ca::REC);
-  AL(h->scene_res, double, (size_t)B * 4);
+  h->agg_n = (size_t)B * v.NG * v.nchunkG * v.TG * v.rec;
+  AL(v.agg, double, h->agg_n);
+  AL(h->scene_res, double, (size_t)B * NST);
   AL(h->s_start, double, (size_t)B * (N + 1) * ns);
   AL(v.gperm, int, (size_t)B * std::max(1, v.G));
   AL(v.gperm2, uint32_t, (size_t)B * v.NG * v.GG);
@@ -774,7 +962,7 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   AL(v.part_nv, int, (size_t)h->np);
   AL(v.ric, double, (size_t)B * N * nu * (ns + 1));
   AL(v.stg, double, (size_t)B * N * (ns * ns + ns));
-  AL(v.stg_stats, double, (size_t)B * N * 4);
+  AL(v.stg_stats, double, (size_t)B * N * NST);
   v.nitems = (int)std::min<long long>((long long)B * v.NG * v.nchunkG, 0x7fffffff);
   AL(v.lam, double, (size_t)h->np * std::max(1, v.nrmax - 1) * (d + 2));
   AL(v.part_e, int, (size_t)h->np);
@@ -802,14 +990,21 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
   if ((st = h->alloc(&h->alpha, (size_t)h->P + h->B))) return st;
   if ((st = ensure_slots(h, h->max_iters))) return st;
   if (D->obs_step && (st = h->alloc(&h->obs_step_buf, (size_t)B * h->M * d))) return st;
+  // ca_admm_solve (per-scene Eq. 18) and ca_scale_detect(states) staging
+  if ((st = h->alloc(&h->active, (size_t)B)) || (st = h->alloc(&h->s_iters, (size_t)B)) ||
+      (st = h->alloc(&h->s_fin, (size_t)B * NST)) || (st = h->alloc(&h->d_remaining, 1)) ||
+      (st = h->alloc(&h->states_buf, (size_t)B * (N + 1) * ns)))
+    return st;
+  if (h->dist_mode) {  // sharded: reduced records, statistics staging, S_PMAX column
+    if ((st = h->alloc(&h->rb, (size_t)B * N * v.rec)) || (st = h->alloc(&h->tmpB, (size_t)B * NST)) ||
+        (st = h->alloc(&h->pmx, (size_t)std::max(B * N, B))))
+      return st;
+  }
   return CA_OK;
 }
 
-ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, ca_problem** out) {
-  if (!out) return fail(CA_E_INVALID, "out is NULL");
-  *out = nullptr;
-  ca_status st = validate(D);
-  if (st) return st;
+// create a handle for the (rank-local) problem D; g = its grid position (NULL: one GPU)
+ca_status create_impl(const ca_problem_desc* D, int device, void* stream, const GridPos* g, ca_problem** out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
     return fail(CA_E_CUDA, "no CUDA device (this library has no CPU fallback)");
@@ -824,6 +1019,8 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
     h->ws = static_cast<char*>(D->workspace);
     h->ws_size = D->workspace_bytes;
   }
+  set_grid(h, g);
+  ca_status st;
   if ((st = setup_handle(h, D))) {
     delete h;
     return st;
@@ -840,6 +1037,14 @@ ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, 
   return CA_OK;
 }
 
+ca_status ca_problem_create(const ca_problem_desc* D, int device, void* stream, ca_problem** out) {
+  if (!out) return fail(CA_E_INVALID, "out is NULL");
+  *out = nullptr;
+  ca_status st = validate(D);
+  if (st) return st;
+  return create_impl(D, device, stream, nullptr, out);
+}
+
 ca_status ca_workspace_size(const ca_problem_desc* D, const ca_dist_desc* dist, size_t* bytes) {
   if (!bytes) return fail(CA_E_INVALID, "bytes is NULL");
   *bytes = 0;
@@ -847,20 +1052,17 @@ ca_status ca_workspace_size(const ca_problem_desc* D, const ca_dist_desc* dist, 
   if (st) return st;
   LocalObs lobs;
   ca_problem_desc Dl;
+  GridPos g;
   const ca_problem_desc* Du = D;
-  long long extra = 0;
-  if (dist && dist->world_size > 1) {
-    int j0 = 0, j1 = 0;
-    if ((st = ca_obstacle_partition(D->n_scenes, D->n_obs, D->obs_off, dist->world_size, dist->rank, &j0, &j1)))
-      return st;
-    slice_obstacles(D, j0, j1, lobs, Dl);
+  if (dist) {
+    if ((st = grid_position(D, dist, g, lobs, Dl))) return st;
     Du = &Dl;
   }
-  if (dist) extra = (((long long)D->n_scenes * D->horizon * ca::REC * 8 + 255) / 256 + ((long long)D->n_scenes * 32 + 255) / 256) * 256;
   ca_problem h;
   h.count_only = true;
+  set_grid(&h, dist ? &g : nullptr);
   if ((st = setup_handle(&h, Du))) return st;
-  *bytes = h.ws_used + (size_t)extra;
+  *bytes = h.ws_used;
   return CA_OK;
 }
 
@@ -879,9 +1081,10 @@ ca_status ca_problem_load(ca_problem* h, const ca_problem_desc* Dfull) {
   LocalObs lobs;
   ca_problem_desc Dl;
   const ca_problem_desc* D = Dfull;
-  if (h->comm) {
-    if (Dfull->n_obs != h->n_obs_full) return fail(CA_E_INVALID, "ca_problem_load: obstacle count differs");
-    slice_obstacles(Dfull, h->j0, h->j1, lobs, Dl);
+  if (h->dist_mode) {  // the FULL problem: keep this rank's scene and obstacle block
+    if (Dfull->n_obs != h->n_obs_full || Dfull->n_scenes != h->B_total)
+      return fail(CA_E_INVALID, "ca_problem_load: scene / obstacle count differs");
+    slice_problem(Dfull, h->b0, h->b0 + h->B, h->j0, h->j1, lobs, Dl);
     D = &Dl;
   }
   if (D->dim != h->d || D->n_scenes != h->B || D->horizon != h->N || D->n_state != h->ns ||
@@ -962,32 +1165,33 @@ ca_status ca_problem_create_dist(const ca_problem_desc* D, const ca_dist_desc* d
   *out = nullptr;
   ca_status st = validate(D);
   if (st) return st;
-  if (!dist->nccl_id || dist->world_size < 1 || dist->rank < 0 || dist->rank >= dist->world_size)
-    return fail(CA_E_INVALID, "bad ca_dist_desc");
-  int j0 = 0, j1 = 0;
-  if ((st = ca_obstacle_partition(D->n_scenes, D->n_obs, D->obs_off, dist->world_size, dist->rank, &j0, &j1)))
-    return st;
   LocalObs lobs;
   ca_problem_desc Dl;
-  slice_obstacles(D, j0, j1, lobs, Dl);
+  GridPos g;
+  if ((st = grid_position(D, dist, g, lobs, Dl))) return st;
   ca_problem* h = nullptr;
-  if ((st = ca_problem_create(&Dl, device, stream, &h))) return st;
-  h->world = dist->world_size;
-  h->rank = dist->rank;
-  h->j0 = j0;
-  h->j1 = j1;
-  h->n_obs_full = D->n_obs;
-  if ((st = h->alloc(&h->rb, (size_t)h->B * h->N * ca::REC)) || (st = h->alloc(&h->tmpB4, (size_t)h->B * 4))) {
-    delete h;
-    return st;
-  }
+  if ((st = create_impl(&Dl, device, stream, &g, &h))) return st;
+  // the world communicator; the obstacle group by ncclCommSplit (color = scene shard)
   ncclUniqueId id;
   std::memcpy(&id, dist->nccl_id, sizeof(id));
-  ncclResult_t r = ncclCommInitRank(&h->comm, dist->world_size, id, dist->rank);
+  ncclComm_t world = nullptr;
+  ncclResult_t r = ncclCommInitRank(&world, g.world, id, g.rank);
   if (r != ncclSuccess) {
-    h->comm = nullptr;
     delete h;
     return fail(CA_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  if (g.Ws == 1) {
+    h->comm = world;  // one scene shard: the world is the obstacle group
+  } else {
+    h->comm_all = world;
+    if (g.Wo > 1) {
+      r = ncclCommSplit(world, g.rs, g.ro, &h->comm, nullptr);
+      if (r != ncclSuccess) {
+        h->comm = nullptr;
+        delete h;
+        return fail(CA_E_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+      }
+    }
   }
   *out = h;
   return CA_OK;
@@ -1017,7 +1221,7 @@ ca_status ca_kernel_times(ca_problem* h, double* ms, int64_t* launches, int32_t 
   ca_status st = check_handle(h);
   if (st) return st;
   if ((st = flush_timing(h))) return mark(h, st);
-  for (int f = 0; f < 5; ++f) {
+  for (int f = 0; f < NFAM; ++f) {
     if (ms) ms[f] = h->ms[f];
     if (launches) launches[f] = h->launches[f];
     if (reset) {
@@ -1043,14 +1247,29 @@ ca_status ca_set_record_basis(ca_problem* h, int32_t enable) {
   return CA_OK;
 }
 
+// the device milliseconds per family of the launches recorded since `mark` (timing on)
+ca_status step_ms(ca_problem* h, ca_residuals* r) {
+  if (!h->timing) return CA_OK;
+  double fam[NFAM] = {0, 0, 0, 0, 0, 0};
+  const int it = h->cur_iter;
+  for (auto& pe : h->pending) pe.iter = 0;
+  ca_status st = flush_timing(h, fam, 1);
+  h->cur_iter = it;
+  if (st) return st;
+  fill_ms(fam, r);
+  return CA_OK;
+}
+
 ca_status ca_dual_sweep(ca_problem* h, ca_residuals* out) {
   ca_status st = check_handle(h);
   if (st) return st;
+  if ((st = flush_timing(h))) return mark(h, st);
   if ((st = launch_sweep(h, false))) return mark(h, st);
-  CUDA_TRY(cudaMemsetAsync(h->scene_res, 0, sizeof(double) * 4 * h->B, h->stream));
-  if ((st = collect_global(h, h->scene_res, 1 | 4 | 8))) return mark(h, st);
+  CUDA_TRY(cudaMemsetAsync(h->scene_res, 0, sizeof(double) * NST * h->B, h->stream));
+  if ((st = collect_global(h, h->scene_res, 0xff & ~(1 << ca::S_RPRI)))) return mark(h, st);
   ca_residuals r{};
   if ((st = sums(h, h->scene_res, &r))) return mark(h, st);
+  if ((st = step_ms(h, &r))) return mark(h, st);
   r.r_pri = 0.0;
   if (out) *out = r;
   return r.n_fail ? CA_W_PAIR_FAILURES : CA_OK;
@@ -1064,38 +1283,87 @@ ca_status ca_primal_step(ca_problem* h) {
   return CA_OK;
 }
 
+// the dist-path buffers (reduced records, S_PMAX column) on a single-GPU handle
+ca_status ensure_rb(ca_problem* h) {
+  ca_status st;
+  if (!h->rb && (st = h->alloc(&h->rb, (size_t)h->B * h->N * h->dev.rec))) return st;
+  if (!h->pmx && (st = h->alloc(&h->pmx, (size_t)std::max(h->B * h->N, h->B)))) return st;
+  return CA_OK;
+}
+
+ca_status ca_get_stage_records(ca_problem* h, double* rec) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (!rec) return fail(CA_E_INVALID, "rec is NULL");
+  if ((st = ensure_rb(h))) return mark(h, st);
+  const long long nq = (long long)h->B * h->N;
+  const unsigned gq = (unsigned)((nq + 127) / 128);
+  ca::k_reduce_records<<<gq, 128, 0, h->stream>>>(h->dev, h->rb, h->pmx);
+  CUDA_TRY(cudaGetLastError());
+  ca::k_pmax_back<<<gq, 128, 0, h->stream>>>(h->dev, h->rb, h->pmx);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[4] += 2;
+  CUDA_TRY(cudaMemcpyAsync(rec, h->rb, sizeof(double) * nq * h->dev.rec, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
+ca_status ca_primal_step_records(ca_problem* h, const double* rec) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (!rec) return fail(CA_E_INVALID, "rec is NULL");
+  if ((st = ensure_rb(h))) return mark(h, st);
+  const long long nq = (long long)h->B * h->N;
+  CUDA_TRY(cudaMemcpyAsync(h->rb, rec, sizeof(double) * nq * h->dev.rec, cudaMemcpyHostToDevice, h->stream));
+  if ((st = launch_riccati(h, nullptr, nullptr, h->rb))) return mark(h, st);
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CA_OK;
+}
+
 ca_status ca_multiplier_update(ca_problem* h, ca_residuals* out) {
   ca_status st = check_handle(h);
   if (st) return st;
+  if ((st = flush_timing(h))) return mark(h, st);
   if ((st = launch_mult(h))) return mark(h, st);
-  if ((st = collect_global(h, h->scene_res, 2))) return mark(h, st);
+  if ((st = collect_global(h, h->scene_res, 1 << ca::S_RPRI))) return mark(h, st);
   ca_residuals r{};
   if ((st = sums(h, h->scene_res, &r))) return mark(h, st);
-  if (out) {
-    out->r_pri = r.r_pri;
-    out->n_pairs = h->P;
-  }
+  ca_residuals o{};
+  if ((st = step_ms(h, &o))) return mark(h, st);
+  o.r_pri = r.r_pri;
+  o.n_pairs = h->P;
+  if (out) *out = o;
   return CA_OK;
 }
 
 // The device work of one ca_admm_iterate(iters): K sweeps + primal steps, the final
-// multiplier update, residual collection and the per-iteration history.
+// multiplier update, residual collection and the per-iteration history.  Scene-sharded
+// runs add one allreduce of every scene's statistics per iteration (scene_exchange) and
+// take the history from that global table.
 ca_status enqueue_iterations(ca_problem* h, int iters) {
   ca_status st;
-  CUDA_TRY(cudaMemsetAsync(h->slots, 0, sizeof(double) * (size_t)iters * h->B * 4, h->stream));
+  const size_t SL = (size_t)h->B * NST, GL = (size_t)h->B_total * NST;
+  CUDA_TRY(cudaMemsetAsync(h->slots, 0, sizeof(double) * (size_t)iters * SL, h->stream));
+  if (h->comm_all) CUDA_TRY(cudaMemsetAsync(h->glob, 0, sizeof(double) * (size_t)iters * GL, h->stream));
   for (int it = 0; it < iters; ++it) {
+    h->cur_iter = it;
     if ((st = launch_sweep(h, it > 0))) return st;
-    double* cur = h->slots + (size_t)it * h->B * 4;
-    double* prev = it > 0 ? h->slots + (size_t)(it - 1) * h->B * 4 : nullptr;
+    double* cur = h->slots + (size_t)it * SL;
+    double* prev = it > 0 ? h->slots + (size_t)(it - 1) * SL : nullptr;
     if ((st = launch_riccati(h, cur, prev))) return st;
+    if (prev && (st = scene_exchange(h, prev, h->glob + (size_t)(it - 1) * GL))) return st;  // slot it-1 complete
   }
+  h->cur_iter = iters - 1;
   if ((st = launch_mult(h))) return st;
-  double* last = h->slots + (size_t)(iters - 1) * h->B * 4;
-  if ((st = collect_global(h, last, 2))) return st;
-  CUDA_TRY(cudaMemcpyAsync(h->scene_res, last, sizeof(double) * h->B * 4, cudaMemcpyDeviceToDevice, h->stream));
-  ca::k_hist<<<iters, 256, 0, h->stream>>>(h->slots, h->B, iters, h->hist_dev);
+  double* last = h->slots + (size_t)(iters - 1) * SL;
+  if ((st = collect_global(h, last, 1 << ca::S_RPRI))) return st;
+  if ((st = scene_exchange(h, last, h->glob + (size_t)(iters - 1) * GL))) return st;
+  CUDA_TRY(cudaMemcpyAsync(h->scene_res, last, sizeof(double) * SL, cudaMemcpyDeviceToDevice, h->stream));
+  if (h->comm_all) ca::k_hist<<<iters, 256, 0, h->stream>>>(h->glob, h->B_total, iters, h->hist_dev);
+  else ca::k_hist<<<iters, 256, 0, h->stream>>>(h->slots, h->B, iters, h->hist_dev);
   CUDA_TRY(cudaGetLastError());
   h->launches[4]++;
+  h->cur_iter = -1;
   return CA_OK;
 }
 
@@ -1105,8 +1373,8 @@ ca_status enqueue_iterations(ca_problem* h, int iters) {
 ca_status launch_iterations_graph(ca_problem* h, int iters) {
   if (!h->gexec || h->g_iters != iters) {
     h->drop_graph();
-    long long before[5];
-    for (int f = 0; f < 5; ++f) before[f] = h->launches[f];
+    long long before[NFAM];
+    for (int f = 0; f < NFAM; ++f) before[f] = h->launches[f];
     if (!h->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     const cudaStream_t user = h->stream;
     h->stream = h->cap_stream;  // the launch helpers enqueue on h->stream
@@ -1131,13 +1399,40 @@ ca_status launch_iterations_graph(ca_problem* h, int iters) {
       return fail(CA_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
     }
     h->g_iters = iters;
-    for (int f = 0; f < 5; ++f) {
+    for (int f = 0; f < NFAM; ++f) {
       h->g_launches[f] = h->launches[f] - before[f];
       h->launches[f] = before[f];
     }
   }
   CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
-  for (int f = 0; f < 5; ++f) h->launches[f] += h->g_launches[f];
+  for (int f = 0; f < NFAM; ++f) h->launches[f] += h->g_launches[f];
+  return CA_OK;
+}
+
+// K iterations; hist (HOST [iters], nullable) gets each iteration's statistics (global
+// in scene-sharded runs) and, with timing on, its device milliseconds per family.
+ca_status iterate_impl(ca_problem* h, int32_t iters, ca_residuals* hist) {
+  ca_status st;
+  if (iters > h->slots_cap) h->drop_graph();  // slot buffers are reallocated
+  if ((st = ensure_slots(h, iters))) return st;
+  if ((st = flush_timing(h))) return st;
+  const bool graph = h->use_graphs && !h->timing && !h->comm && !h->comm_all && h->dev.dbg_p < 0 && !h->dev.active;
+  if ((st = graph ? launch_iterations_graph(h, iters) : enqueue_iterations(h, iters))) return st;
+  if (!hist) {
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return CA_OK;
+  }
+  std::vector<double> hv((size_t)iters * NST), fam;
+  CUDA_TRY(cudaMemcpyAsync(hv.data(), h->hist_dev, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (h->timing) {
+    fam.assign((size_t)iters * NFAM, 0.0);
+    if ((st = flush_timing(h, fam.data(), iters))) return st;
+  }
+  for (int k = 0; k < iters; ++k) {
+    fill_res(&hv[(size_t)k * NST], h->P, &hist[k]);
+    if (h->timing) fill_ms(&fam[(size_t)k * NFAM], &hist[k]);
+  }
   return CA_OK;
 }
 
@@ -1145,64 +1440,115 @@ ca_status ca_admm_iterate(ca_problem* h, int32_t iters, ca_residuals* hist) {
   ca_status st = check_handle(h);
   if (st) return st;
   if (iters <= 0) return fail(CA_E_INVALID, "iters must be > 0");
-  if (iters > h->slots_cap) h->drop_graph();  // slot buffers are reallocated
-  if ((st = ensure_slots(h, iters))) return mark(h, st);
-  const bool graph = h->use_graphs && !h->timing && !h->comm && h->dev.dbg_p < 0;
-  if ((st = graph ? launch_iterations_graph(h, iters) : enqueue_iterations(h, iters))) return mark(h, st);
-  int64_t fails = 0;
-  if (hist) {
-    std::vector<double> hv((size_t)iters * 4);
-    CUDA_TRY(cudaMemcpyAsync(hv.data(), h->hist_dev, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
-    for (int k = 0; k < iters; ++k) {
-      hist[k].r_dual = hv[k * 4 + 0];
-      hist[k].r_pri = hv[k * 4 + 1];
-      hist[k].pivots = (int64_t)hv[k * 4 + 2];
-      hist[k].n_fail = (int64_t)hv[k * 4 + 3];
-      hist[k].n_pairs = h->P;
-      fails += hist[k].n_fail;
-    }
-  } else {
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  std::vector<ca_residuals> own;
+  if (!hist) {  // the failure count decides the warning
+    own.resize((size_t)iters);
+    hist = own.data();
   }
+  if ((st = iterate_impl(h, iters, hist))) return mark(h, st);
+  int64_t fails = 0;
+  for (int k = 0; k < iters; ++k) fails += hist[k].n_fail;
   return fails ? CA_W_PAIR_FAILURES : CA_OK;
 }
 
-ca_status ca_admm_solve(ca_problem* h, ca_solve_report* out) {
-  ca_status st = check_handle(h);
-  if (st) return st;
-  const double pairs_per_scene = (double)h->N * h->np * h->M;
+// ADMM until Eq. 18 per scene: one iteration at a time; after each, k_stop
+// freezes the scenes that meet Eq. 18 (the kernels skip them from the next iteration on,
+// so their iterate stays where they stopped) and counts the scenes still running (in a
+// scene-sharded run summed over every rank: the same count, hence the same loop, on
+// every rank -- no rank can leave a collective the others still enter).
+ca_status solve_impl(ca_problem* h, ca_solve_report* out) {
+  ca_status st;
+  const double pairs_per_scene = (double)h->N * h->np * h->M_full;  // the FULL problem's
   const double ep = h->eps_pri > 0 ? h->eps_pri : 1e-3 * std::max(1.0, pairs_per_scene);
   const double ed = h->eps_dual > 0 ? h->eps_dual : 1e-3 * std::max(1.0, pairs_per_scene);
-  ca_solve_report rep{};
-  std::vector<double> v((size_t)h->B * 4);
+  CUDA_TRY(cudaMemsetAsync(h->active, 1, (size_t)h->B, h->stream));
+  CUDA_TRY(cudaMemsetAsync(h->s_iters, 0, sizeof(int) * h->B, h->stream));
+  CUDA_TRY(cudaMemsetAsync(h->s_fin, 0, sizeof(double) * NST * h->B, h->stream));
+  h->drop_graph();
+  h->dev.active = h->active;
+  h->solved = true;
+  int done_iters = 0;
   for (int k = 0; k < h->max_iters; ++k) {
-    ca_residuals r{};
-    st = ca_admm_iterate(h, 1, &r);
-    if (st < 0) return st;
-    rep.iterations = k + 1;
-    rep.last = r;
-    CUDA_TRY(cudaMemcpy(v.data(), h->scene_res, sizeof(double) * v.size(), cudaMemcpyDeviceToHost));
-    bool all = true;
-    for (int b = 0; b < h->B && all; ++b) all = (v[b * 4 + 1] <= ep) && (v[b * 4 + 0] <= ed);  // Eq. 18 '<='
-    if (all) {
-      rep.converged = 1;
-      break;
+    if ((st = iterate_impl(h, 1, nullptr))) return st;
+    CUDA_TRY(cudaMemsetAsync(h->d_remaining, 0, sizeof(int), h->stream));
+    ca::k_stop<<<(h->B + 127) / 128, 128, 0, h->stream>>>(h->scene_res, h->active, h->s_iters, h->s_fin, h->B, ep, ed,
+                                                         k, h->d_remaining);
+    CUDA_TRY(cudaGetLastError());
+    h->launches[4]++;
+    if (h->comm_all) {
+      cudaEvent_t c0 = nullptr;
+      t_begin(h, &c0);
+      NCCL_TRY(ncclAllReduce(h->d_remaining, h->d_remaining, 1, ncclInt32, ncclSum, h->comm_all, h->stream));
+      t_end(h, 5, c0);
     }
+    int remaining = 0;
+    CUDA_TRY(cudaMemcpyAsync(&remaining, h->d_remaining, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    done_iters = k + 1;
+    if (remaining == 0) break;
+  }
+  // every scene's statistics at its own last iteration become the scene residuals
+  CUDA_TRY(cudaMemcpyAsync(h->scene_res, h->s_fin, sizeof(double) * NST * h->B, cudaMemcpyDeviceToDevice, h->stream));
+  std::vector<int> it((size_t)h->B);
+  std::vector<uint8_t> act((size_t)h->B);
+  CUDA_TRY(cudaMemcpyAsync(it.data(), h->s_iters, sizeof(int) * h->B, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(act.data(), h->active, (size_t)h->B, cudaMemcpyDeviceToHost, h->stream));
+  ca_solve_report rep{};
+  if ((st = sums(h, h->s_fin, &rep.last))) return st;
+  int conv = 1, mx = 0;
+  for (int b = 0; b < h->B; ++b) {
+    conv &= act[b] ? 0 : 1;
+    mx = std::max(mx, it[b]);
+  }
+  rep.iterations = h->comm_all ? done_iters : mx;
+  rep.converged = conv;
+  if (h->comm_all) {  // global: every scene of every rank
+    int c = conv;
+    int* dc = h->d_remaining;
+    CUDA_TRY(cudaMemcpyAsync(dc, &c, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    NCCL_TRY(ncclAllReduce(dc, dc, 1, ncclInt32, ncclMin, h->comm_all, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(&c, dc, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    rep.converged = c;
   }
   if (out) *out = rep;
   return rep.converged ? CA_OK : CA_W_NOT_CONVERGED;
 }
 
+ca_status ca_admm_solve(ca_problem* h, ca_solve_report* out) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  st = solve_impl(h, out);
+  h->dev.active = nullptr;  // later ca_admm_iterate calls run every scene again
+  h->drop_graph();
+  return (st < 0) ? mark(h, st) : st;
+}
+
+ca_status ca_get_solve_scenes(ca_problem* h, int32_t* iterations, int32_t* converged) {
+  ca_status st = check_handle(h);
+  if (st) return st;
+  if (!h->solved) return fail(CA_E_INVALID, "no ca_admm_solve has run on this handle");
+  std::vector<int> it((size_t)h->B);
+  std::vector<uint8_t> act((size_t)h->B);
+  CUDA_TRY(cudaMemcpyAsync(it.data(), h->s_iters, sizeof(int) * h->B, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(act.data(), h->active, (size_t)h->B, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (int b = 0; b < h->B; ++b) {
+    if (iterations) iterations[b] = it[b];
+    if (converged) converged[b] = act[b] ? 0 : 1;
+  }
+  return CA_OK;
+}
+
 ca_status ca_get_scene_residuals(ca_problem* h, double* r_pri, double* r_dual) {
   ca_status st = check_handle(h);
   if (st) return st;
-  std::vector<double> v((size_t)h->B * 4);
+  std::vector<double> v((size_t)h->B * NST);
   CUDA_TRY(cudaMemcpyAsync(v.data(), h->scene_res, sizeof(double) * v.size(), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   for (int b = 0; b < h->B; ++b) {
-    if (r_pri) r_pri[b] = v[b * 4 + 1];
-    if (r_dual) r_dual[b] = v[b * 4 + 0];
+    if (r_pri) r_pri[b] = v[(size_t)b * NST + ca::S_RPRI];
+    if (r_dual) r_dual[b] = v[(size_t)b * NST + ca::S_RDUAL];
   }
   return CA_OK;
 }
@@ -1303,20 +1649,19 @@ ca_status ca_get_box_state(ca_problem* h, double* w_s, double* l_s, double* w_u,
 ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, double* min_alpha) {
   ca_status st = check_handle(h);
   if (st) return st;
-  if (h->P == 0) {
-    if (min_alpha)
-      for (int b = 0; b < h->B; ++b) min_alpha[b] = INFINITY;
+  if (h->P == 0) {  // no local pairs: +inf minima -- but still join the group's min-allreduce
+    std::vector<double> inf((size_t)h->B, INFINITY);
+    CUDA_TRY(cudaMemcpyAsync(h->alpha, inf.data(), sizeof(double) * h->B, cudaMemcpyHostToDevice, h->stream));
+    if (h->comm) NCCL_TRY(ncclAllReduce(h->alpha, h->alpha, h->B, ncclDouble, ncclMin, h->comm, h->stream));
+    if (min_alpha) CUDA_TRY(cudaMemcpyAsync(min_alpha, h->alpha, sizeof(double) * h->B, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
     return CA_OK;
   }
-  if (!h->alpha) {
-    if ((st = h->alloc(&h->alpha, (size_t)h->P + h->B))) return st;
-  }
   const double* sd = h->dev.s;
-  double* tmp_states = nullptr;
-  if (states) {
-    if ((st = h->alloc(&tmp_states, (size_t)h->B * (h->N + 1) * h->ns))) return st;
-    CUDA_TRY(cudaMemcpyAsync(tmp_states, states, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns, cudaMemcpyHostToDevice, h->stream));
-    sd = tmp_states;
+  if (states) {  // the handle's own staging buffer (allocated at create)
+    CUDA_TRY(cudaMemcpyAsync(h->states_buf, states, sizeof(double) * (size_t)h->B * (h->N + 1) * h->ns,
+                             cudaMemcpyHostToDevice, h->stream));
+    sd = h->states_buf;
   }
   cudaEvent_t e0 = nullptr;
   t_begin(h, &e0);
@@ -1332,16 +1677,12 @@ ca_status ca_scale_detect(ca_problem* h, const double* states, double* alpha, do
   ca::k_scene_min<<<h->B, 256, 0, h->stream>>>(h->alpha, h->P / h->B, h->alpha + h->P);
   CUDA_TRY(cudaGetLastError());
   h->launches[3]++;  // k_scene_min (k_scale is counted by t_end)
-  if (h->comm)
+  if (h->comm)  // obstacle group: the per-scene minimum over every rank's obstacles
     NCCL_TRY(ncclAllReduce(h->alpha + h->P, h->alpha + h->P, h->B, ncclDouble, ncclMin, h->comm, h->stream));
   t_end(h, 3, e0);
   if (alpha) CUDA_TRY(cudaMemcpyAsync(alpha, h->alpha, sizeof(double) * h->P, cudaMemcpyDeviceToHost, h->stream));
   if (min_alpha) CUDA_TRY(cudaMemcpyAsync(min_alpha, h->alpha + h->P, sizeof(double) * h->B, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
-  if (tmp_states) {
-    cudaFree(tmp_states);
-    h->allocs.erase(std::remove(h->allocs.begin(), h->allocs.end(), (void*)tmp_states), h->allocs.end());
-  }
   return CA_OK;
 }
 

@@ -28,8 +28,20 @@
 
 namespace ca {
 
-constexpr int REC = 20;  // per (scene, t, chunk) record
-constexpr int R_RDUAL = 16, R_RPRI = 17, R_PIV = 18, R_FAIL = 19;
+// Record of one (work item, timestep) of the sweep = [Gauss-Newton aggregates (nagg) |
+// statistics (NSTAT)], nagg = (d+1)(d+2)/2 + (d+1) (the SE2 / yaw pose block's S, g).
+// The statistics are in the order of the per-scene slots: dual residual (Eq. 18b),
+// primal residual (Eq. 18a), pivots, failed pairs and their kinds (RAY, ITER_LIMIT,
+// y_e < -1e-6: SPEC S:243), the largest pivot count.  Every field is summed
+// over pairs, except S_PMAX (max).  d = 2: 17 doubles, d = 3: 22.
+constexpr int NSTAT = 8;
+enum { S_RDUAL = 0, S_RPRI = 1, S_PIV = 2, S_FAIL = 3, S_RAY = 4, S_ITER = 5, S_NEGYE = 6, S_PMAX = 7 };
+__host__ __device__ constexpr int rec_nagg(int d) { return (d + 1) * (d + 2) / 2 + (d + 1); }
+__host__ __device__ constexpr int rec_n(int d) { return rec_nagg(d) + NSTAT; }
+constexpr int RECMAX = rec_n(3);
+__host__ __device__ __forceinline__ double stat_comb(int f, double a, double b) {
+  return f == S_PMAX ? (a > b ? a : b) : a + b;
+}
 constexpr int CTA = 32;  // threads per CTA of the per-pair kernels: one warp (no cross-warp barriers)
 
 struct LemkeParams {
@@ -39,6 +51,10 @@ struct LemkeParams {
 
 struct Dev {
   int d, B, N, ns, nu, np, M, pose_model, npc;
+  int nagg, rec;  // record layout: rec_nagg(d), rec_n(d)
+  // ca_admm_solve (Eq. 18 per scene): NULL = every scene iterates; else [B] 0/1 and the
+  // scenes with 0 (stopped) are skipped by every kernel of an iteration (frozen iterate)
+  const uint8_t* active;
   int nrmax;  // largest robot-part face count
   int nomax;  // largest obstacle face count
   int pidx[4];
@@ -114,6 +130,7 @@ __device__ __forceinline__ void part_origin(const Dev& P, int i, const double* R
     rho[a] = v;
   }
 }
+__device__ __forceinline__ bool scene_on(const Dev& P, int b) { return !P.active || P.active[b]; }
 __device__ __forceinline__ bool is_sensed(const Dev& P, int b, int j) {
   return !P.sensed || P.sensed[(long long)b * P.M + j];
 }
@@ -192,12 +209,13 @@ __device__ __forceinline__ Item item_of(const Dev& P, int item) {
   return it;
 }
 
-// Deterministic grouped record reduction of one warp: lane l holds rec[REC] for its
+// Deterministic grouped record reduction of one warp: lane l holds rec[NFIELD] for its
 // pair's timestep slot tl (-1: no pair), staged in its smem column red[f*32];
-// out[tt*REC + f] = sum over lanes l = 0..31 with tl(l) == tt, in lane order.
+// out[tt*stride + f0 + f] = sum over lanes l = 0..31 with tl(l) == tt, in lane order
+// (field fmx, if any: the max, for S_PMAX).
 template <int NFIELD>
-__device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int TG, double* out, const double* rec,
-                                             int f0) {
+__device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int TG, double* out, int stride,
+                                             const double* rec, int f0, int fmx) {
   __syncwarp();  // every lane is done with its columns (stl below crosses columns)
   double* red = col0 + lane;
 #pragma unroll
@@ -208,9 +226,14 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
   for (int o = lane; o < TG * NFIELD; o += 32) {
     const int tt = o / NFIELD, f = o % NFIELD;
     double acc = 0.0;
+    if (f == fmx) {
 #pragma unroll 8
-    for (int l = 0; l < 32; ++l) acc += (stl[l] == tt) ? col0[f * 32 + l] : 0.0;
-    out[tt * REC + f0 + f] = acc;
+      for (int l = 0; l < 32; ++l) acc = fmax(acc, (stl[l] == tt) ? col0[f * 32 + l] : 0.0);
+    } else {
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) acc += (stl[l] == tt) ? col0[f * 32 + l] : 0.0;
+    }
+    out[tt * stride + f0 + f] = acc;
   }
   __syncwarp();
 }
@@ -224,6 +247,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
   __shared__ double sred[2 * CTA];
   const int tid = threadIdx.x;
   const Item it = item_of(P, blockIdx.x);
+  if (!scene_on(P, it.b)) return;  // stopped scene (ca_admm_solve): frozen
   double rec[1] = {0.0};
   const int gs = it.chunk * P.CHG + tid;  // slot in the execution order of the group
   int tl = -1;
@@ -278,28 +302,29 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
     }
     rec[0] = r2;
   }
-  group_reduce<1>(sred, tid, tl, P.TG, P.agg + (long long)blockIdx.x * P.TG * REC, rec, R_RPRI);
+  group_reduce<1>(sred, tid, tl, P.TG, P.agg + (long long)blockIdx.x * P.TG * P.rec, P.rec, rec, P.nagg + S_RPRI, -1);
 }
 
 #ifdef CA_COMMON_KERNELS
-// per-scene sums of the record statistics -> dst[b*4 + {rdual, rpri, piv, fail}]
-// (fields with mask bit f clear are left untouched)
+// per-scene statistics of the records -> dst[b*NSTAT + S_*] (fields with mask bit f
+// clear are left untouched; stopped scenes of ca_admm_solve keep theirs)
 __global__ void k_collect(Dev P, double* dst, int mask, int add_box) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= P.B) return;
-  double acc[4] = {0, 0, 0, 0};
+  if (b >= P.B || !scene_on(P, b)) return;
+  double acc[NSTAT];
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f) acc[f] = 0.0;
   const long long per = (long long)P.NG * P.nchunkG * P.TG;  // records of one scene (contiguous)
   const long long base = (long long)b * per;
   for (long long r = 0; r < per; ++r) {
-    const double* rec = P.agg + (base + r) * REC;
-    acc[0] += rec[R_RDUAL];
-    acc[1] += rec[R_RPRI];
-    acc[2] += rec[R_PIV];
-    acc[3] += rec[R_FAIL];
+    const double* rec = P.agg + (base + r) * P.rec + P.nagg;
+#pragma unroll
+    for (int f = 0; f < NSTAT; ++f) acc[f] = stat_comb(f, acc[f], rec[f]);
   }
-  if (P.box && add_box) acc[1] += P.box_res[b];  // box block's ||x - w||^2 (reading #7)
-  for (int f = 0; f < 4; ++f)
-    if ((mask >> f) & 1) dst[b * 4 + f] = acc[f];
+  if (P.box && add_box) acc[S_RPRI] += P.box_res[b];  // box block's ||x - w||^2 (reading #7)
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f)
+    if ((mask >> f) & 1) dst[b * NSTAT + f] = acc[f];
 }
 #endif
 
@@ -314,20 +339,54 @@ __global__ void k_collect(Dev P, double* dst, int mask, int add_box) {
 #ifdef CA_COMMON_KERNELS
 // Obstacle-sharded runs: per (scene, t), sum the rank-local chunk records in fixed
 // order into one record (the buffer that is then ncclAllReduce'd across ranks).
-__global__ void k_reduce_records(Dev P, double* out) {
+__global__ void k_reduce_records(Dev P, double* out, double* pmax) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= (long long)P.B * P.N) return;
-  double acc[REC];
+  double acc[RECMAX];
 #pragma unroll
-  for (int f = 0; f < REC; ++f) acc[f] = 0.0;
+  for (int f = 0; f < RECMAX; ++f) acc[f] = 0.0;
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
-  for (int c = 0; c < P.nchunkG; ++c) {
-    const double* rec = P.agg + rec_index(P, b, t, c) * REC;
+  const int fm = P.nagg + S_PMAX;
+  if (P.M > 0)  // (no local pairs: the sweep wrote no records; contribute zeros)
+    for (int c = 0; c < P.nchunkG; ++c) {
+      const double* rec = P.agg + rec_index(P, b, t, c) * P.rec;
 #pragma unroll
-    for (int f = 0; f < REC; ++f) acc[f] += rec[f];
-  }
+      for (int f = 0; f < RECMAX; ++f)
+        if (f < P.rec) acc[f] = (f == fm) ? fmax(acc[f], rec[f]) : acc[f] + rec[f];
+    }
+  // the sum-allreduce carries every field but S_PMAX, which goes to pmax[q] (max-allreduce)
 #pragma unroll
-  for (int f = 0; f < REC; ++f) out[q * REC + f] = acc[f];
+  for (int f = 0; f < RECMAX; ++f)
+    if (f < P.rec) out[q * P.rec + f] = (f == fm) ? 0.0 : acc[f];
+  pmax[q] = acc[fm];
+}
+// statistics [n][NSTAT] around a sum-allreduce: S_PMAX moves to pm[n] (max-allreduced
+// alongside) and back
+__global__ void k_stat_split(double* st, double* pm, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  pm[b] = st[(long long)b * NSTAT + S_PMAX];
+  st[(long long)b * NSTAT + S_PMAX] = 0.0;
+}
+__global__ void k_stat_join(double* st, const double* pm, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  st[(long long)b * NSTAT + S_PMAX] = pm[b];
+}
+// scene-sharded runs: this rank's per-scene statistics into the global table (scenes
+// [b0, b0 + B) of every rank's copy; the other entries stay 0 for the sum-allreduce).
+// Within an obstacle group every rank holds the same (allreduced) statistics: only the
+// group's first rank contributes.
+__global__ void k_scatter_slot(double* glob, const double* slot, int B, int b0, int contribute) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= B * NSTAT) return;
+  glob[(long long)b0 * NSTAT + k] = contribute ? slot[k] : 0.0;
+}
+// after the allreduce: the max-reduced S_PMAX back into the records
+__global__ void k_pmax_back(Dev P, double* out, const double* pmax) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)P.B * P.N) return;
+  out[q * P.rec + P.nagg + S_PMAX] = pmax[q];
 }
 
 #endif  // CA_COMMON_KERNELS
@@ -378,10 +437,8 @@ static __device__ void stage_assemble(const Dev& P, long long q, const double* r
         ho[a] += -P.box_rho * (P.box_ws[k0 + a] - P.box_ls[k0 + a]);
       }
   }
-  so[0] = rec[R_RDUAL];
-  so[1] = rec[R_RPRI];
-  so[2] = rec[R_PIV];
-  so[3] = rec[R_FAIL];
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f) so[f] = rec[P.nagg + f];
 }
 
 // Stage assembly of one (scene, t): sum its chunk records in fixed chunk order
@@ -389,13 +446,15 @@ static __device__ void stage_assemble(const Dev& P, long long q, const double* r
 static __device__ void stage_block(const Dev& P, const double* recs, int nchunk, long long q, double* out,
                                    double* so) {
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
-  double rec[REC];
+  double rec[RECMAX];
 #pragma unroll
-  for (int f = 0; f < REC; ++f) rec[f] = 0.0;
+  for (int f = 0; f < RECMAX; ++f) rec[f] = 0.0;
+  const int fm = P.nagg + S_PMAX;
   for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
-    const double* r = recs + (nchunk ? rec_index(P, b, t, c) : q) * REC;
+    const double* r = recs + (nchunk ? rec_index(P, b, t, c) : q) * P.rec;
 #pragma unroll
-    for (int f = 0; f < REC; ++f) rec[f] += r[f];
+    for (int f = 0; f < RECMAX; ++f)
+      if (f < P.rec) rec[f] = (f == fm) ? fmax(rec[f], r[f]) : rec[f] + r[f];
   }
   stage_assemble(P, q, rec, out, so);
 }
@@ -405,29 +464,35 @@ static __device__ void stage_block(const Dev& P, const double* recs, int nchunk,
 // Stage assembly for the thread-per-scene Riccati: one thread per (scene, t).
 __global__ void k_stage(Dev P, const double* recs, int nchunk) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + (t-1)
-  if (q >= (long long)P.B * P.N) return;
-  stage_block(P, recs, nchunk, q, P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * 4);
+  if (q >= (long long)P.B * P.N || !scene_on(P, (int)(q / P.N))) return;
+  stage_block(P, recs, nchunk, q, P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * NSTAT);
 }
 
 // Same from the sweep's grouped records, one warp per (scene, timestep group): the
 // group's records are contiguous, so lane o sums output (timestep o / REC, field
 // o % REC) over the chunks with coalesced loads (same chunk order as stage_block).
 __global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
-  __shared__ double sums[4][8 * REC];
+  __shared__ double sums[4][8 * RECMAX];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long bg = (long long)blockIdx.x * 4 + w;
   if (bg >= (long long)P.B * P.NG) return;
   const int b = (int)(bg / P.NG), grp = (int)(bg % P.NG), nt = min(P.TG, P.N - grp * P.TG);
-  const double* base = P.agg + bg * P.nchunkG * P.TG * REC;
-  for (int o = lane; o < nt * REC; o += 32) {
+  if (!scene_on(P, b)) return;
+  const int RC = P.rec, fm = P.nagg + S_PMAX;
+  const double* base = P.agg + bg * P.nchunkG * P.TG * RC;
+  for (int o = lane; o < nt * RC; o += 32) {
     double acc = 0.0;
-    for (int c = 0; c < P.nchunkG; ++c) acc += base[(long long)c * P.TG * REC + o];
+    const bool mx = (o % RC) == fm;
+    for (int c = 0; c < P.nchunkG; ++c) {
+      const double v = base[(long long)c * P.TG * RC + o];
+      acc = mx ? fmax(acc, v) : acc + v;
+    }
     sums[w][o] = acc;
   }
   __syncwarp();
   if (lane < nt) {
     const long long q = (long long)b * P.N + grp * P.TG + lane;
-    stage_assemble(P, q, &sums[w][lane * REC], P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * 4);
+    stage_assemble(P, q, &sums[w][lane * RC], P.stg + q * (P.ns * P.ns + P.ns), P.stg_stats + q * NSTAT);
   }
 }
 #endif  // CA_COMMON_KERNELS
@@ -524,11 +589,13 @@ __device__ __forceinline__ void riccati_forward(const Dev& P, int b, const doubl
                                                 const double* stats, const double* ric, double* dst_cur,
                                                 double* dst_prev) {
   const int N = P.N;
-  double st[4] = {0, 0, 0, 0};
-  for (int t = 1; t <= N; ++t) {
-    const double* so = stats + (long long)(t - 1) * 4;
+  double st[NSTAT];
 #pragma unroll
-    for (int f = 0; f < 4; ++f) st[f] += so[f];
+  for (int f = 0; f < NSTAT; ++f) st[f] = 0.0;
+  for (int t = 1; t <= N; ++t) {
+    const double* so = stats + (long long)(t - 1) * NSTAT;
+#pragma unroll
+    for (int f = 0; f < NSTAT; ++f) st[f] = stat_comb(f, st[f], so[f]);
   }
   double ulo[NU], uhi[NU], urho[NU];
 #pragma unroll
@@ -593,12 +660,11 @@ __device__ __forceinline__ void riccati_forward(const Dev& P, int b, const doubl
     }
   }
   if (P.box) P.box_res[b] = box_res;
-  if (dst_cur) {
-    dst_cur[b * 4 + 0] = st[0];
-    dst_cur[b * 4 + 2] = st[2];
-    dst_cur[b * 4 + 3] = st[3];
-  }
-  if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
+  if (dst_cur)
+#pragma unroll
+    for (int f = 0; f < NSTAT; ++f)
+      if (f != S_RPRI) dst_cur[b * NSTAT + f] = st[f];
+  if (dst_prev) dst_prev[b * NSTAT + S_RPRI] = st[S_RPRI] + box_res_prev;
 }
 
 // One scene's Riccati recursion (Eq. 16 as an LQ with the GN stage blocks) and
@@ -867,18 +933,18 @@ __device__ __forceinline__ void riccati_lanes(const Dev& P, int b, int lane, con
 template <int NS, int NU>
 __global__ void k_riccati_thread(Dev P, double* dst_cur, double* dst_prev) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= P.B) return;
+  if (b >= P.B || !scene_on(P, b)) return;
   const int N = P.N;
   const long long nt = P.dyn_pt ? N : 1, i0 = P.dyn_ps ? (long long)b * nt : 0;
   riccati_serial<NS, NU>(P, b, P.stg + (long long)b * N * (NS * NS + NS), P.dynA + i0 * NS * NS,
                          P.dynB + i0 * NS * NU, P.dync + i0 * NS, P.dyn_pt ? NS * NS : 0, P.dyn_pt ? NS * NU : 0,
-                         P.dyn_pt ? NS : 0, P.stg_stats + (long long)b * N * 4,
+                         P.dyn_pt ? NS : 0, P.stg_stats + (long long)b * N * NSTAT,
                          P.ric + (long long)b * N * NU * (NS + 1), dst_cur, dst_prev);
 }
 
 // shared-memory footprint of k_riccati (doubles): stage blocks, stats, dynamics, gains
 __host__ __device__ inline long long riccati_smem_doubles(int N, int NS, int NU, bool dyn_pt) {
-  return (long long)N * (NS * NS + NS) + 4LL * N + (dyn_pt ? N : 1) * (NS * NS + NS * NU + NS) +
+  return (long long)N * (NS * NS + NS) + (long long)NSTAT * N + (dyn_pt ? N : 1) * (NS * NS + NS * NU + NS) +
          (long long)N * NU * (NS + 1);
 }
 
@@ -891,11 +957,12 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
                                                double* dst_prev) {
   extern __shared__ double rsm[];
   const int b = blockIdx.x, lane = threadIdx.x;
+  if (!scene_on(P, b)) return;  // stopped scene (ca_admm_solve)
   const int N = P.N;
   constexpr int SB = NS * NS + NS, DB = NS * NS + NS * NU + NS;
   double* sstg = rsm;                      // [N][SB]: H_t, h_t
-  double* sst = sstg + (long long)N * SB;  // [N][4]
-  double* sdyn = sst + 4LL * N;            // [nd][DB]: A, B, c
+  double* sst = sstg + (long long)N * SB;  // [N][NSTAT]
+  double* sdyn = sst + (long long)NSTAT * N;  // [nd][DB]: A, B, c
   const int nd = P.dyn_pt ? N : 1;
   double* ric = sdyn + (long long)nd * DB;  // [N][NU][NS+1]: feedback K_t | k_t
   // recursion work area (static): value function, products, gains
@@ -904,22 +971,25 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   // before either block is assembled), same chunk order as stage_block
   for (int t0 = lane; t0 < N; t0 += 64) {
     const int t1 = t0 + 32;
-    double ra[REC], rb[REC];
+    double ra[RECMAX], rb[RECMAX];
 #pragma unroll
-    for (int f = 0; f < REC; ++f) ra[f] = rb[f] = 0.0;
+    for (int f = 0; f < RECMAX; ++f) ra[f] = rb[f] = 0.0;
     const long long q0 = (long long)b * N + t0, q1 = q0 + 32;
+    const int RC = P.rec, fm = P.nagg + S_PMAX;
 #pragma unroll 4
     for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
-      const double* r0 = recs + (nchunk ? rec_index(P, b, t0 + 1, c) : q0) * REC;
-      const double* r1 = recs + (nchunk ? rec_index(P, b, min(t1, N - 1) + 1, c) : min(q1, q0 - t0 + N - 1)) * REC;
+      const double* r0 = recs + (nchunk ? rec_index(P, b, t0 + 1, c) : q0) * RC;
+      const double* r1 = recs + (nchunk ? rec_index(P, b, min(t1, N - 1) + 1, c) : min(q1, q0 - t0 + N - 1)) * RC;
 #pragma unroll
-      for (int f = 0; f < REC; ++f) {
-        ra[f] += __ldg(r0 + f);
-        rb[f] += __ldg(r1 + f);
+      for (int f = 0; f < RECMAX; ++f) {
+        if (f >= RC) continue;
+        const double v0 = __ldg(r0 + f), v1 = __ldg(r1 + f);
+        ra[f] = (f == fm) ? fmax(ra[f], v0) : ra[f] + v0;
+        rb[f] = (f == fm) ? fmax(rb[f], v1) : rb[f] + v1;
       }
     }
-    stage_assemble(P, q0, ra, sstg + (long long)t0 * SB, sst + 4LL * t0);
-    if (t1 < N) stage_assemble(P, q1, rb, sstg + (long long)t1 * SB, sst + 4LL * t1);
+    stage_assemble(P, q0, ra, sstg + (long long)t0 * SB, sst + (long long)NSTAT * t0);
+    if (t1 < N) stage_assemble(P, q1, rb, sstg + (long long)t1 * SB, sst + (long long)NSTAT * t1);
   }
   {
     // dynamics blocks, 8 coalesced loads in flight per lane before their stores (a
@@ -1138,18 +1208,19 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
     if (lane == 0) P.box_res[b] = box_res;
   }
   if (lane == 0) {
-    double st[4] = {0, 0, 0, 0};
-    for (int t = 1; t <= N; ++t) {
-      const double* so = sst + 4LL * (t - 1);
+    double st[NSTAT];
 #pragma unroll
-      for (int f = 0; f < 4; ++f) st[f] += so[f];
+    for (int f = 0; f < NSTAT; ++f) st[f] = 0.0;
+    for (int t = 1; t <= N; ++t) {
+      const double* so = sst + (long long)NSTAT * (t - 1);
+#pragma unroll
+      for (int f = 0; f < NSTAT; ++f) st[f] = stat_comb(f, st[f], so[f]);
     }
-    if (dst_cur) {
-      dst_cur[b * 4 + 0] = st[0];
-      dst_cur[b * 4 + 2] = st[2];
-      dst_cur[b * 4 + 3] = st[3];
-    }
-    if (dst_prev) dst_prev[b * 4 + 1] = st[1] + box_res_prev;
+    if (dst_cur)
+#pragma unroll
+      for (int f = 0; f < NSTAT; ++f)
+        if (f != S_RPRI) dst_cur[b * NSTAT + f] = st[f];
+    if (dst_prev) dst_prev[b * NSTAT + S_RPRI] = st[S_RPRI] + box_res_prev;
   }
 }
 
@@ -1205,6 +1276,7 @@ __global__ void k_relin_unicycle(Dev P) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // b*N + t
   if (q >= (long long)P.B * P.N) return;
   const int b = (int)(q / P.N), t = (int)(q % P.N);
+  if (!scene_on(P, b)) return;
   const double* sb = P.s + ((long long)b * (P.N + 1) + t) * 4;
   const double dt = P.dt, th = sb[2], v = sb[3], cs = cos(th), sn = sin(th);
   double A[16];
@@ -1464,6 +1536,7 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   const int bg = blockIdx.x, b = bg / P.NG, grp = bg % P.NG, tid = threadIdx.x;
   const int t0 = grp * P.TG + 1, nt = min(P.TG, P.N - grp * P.TG);
   if (bg == 0 && tid == 0 && P.work) *P.work = 0;  // persistent-sweep work counter
+  if (!scene_on(P, b)) return;  // stopped scene: its items are skipped by the sweep
   for (int tl = tid; tl < nt; tl += 32) {  // pose(s_t^k) of the group's timesteps
     const long long bt = (long long)b * P.N + t0 - 1 + tl;
     double* po = P.pose + bt * 12;
@@ -1532,27 +1605,48 @@ __global__ void k_scene_min(const double* alpha, long long per_scene, double* ou
   }
 }
 
-// sum per-scene stats of `nslot` iteration slots: hist[k*4 + f] = sum_b slots[(k*B + b)*4 + f]
+// per-scene stats of `nslot` iteration slots combined over scenes (sum; max for S_PMAX):
+// hist[k*NSTAT + f] = comb_b slots[(k*B + b)*NSTAT + f]
 __global__ void k_hist(const double* slots, int B, int nslot, double* hist) {
   const int k = blockIdx.x;
   if (k >= nslot) return;
-  __shared__ double red[4][32];
-  double acc[4] = {0, 0, 0, 0};
+  __shared__ double red[NSTAT][32];
+  double acc[NSTAT];
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f) acc[f] = 0.0;
   for (int b = threadIdx.x; b < B; b += blockDim.x)
-    for (int f = 0; f < 4; ++f) acc[f] += slots[((long long)k * B + b) * 4 + f];
-  for (int f = 0; f < 4; ++f) {
+#pragma unroll
+    for (int f = 0; f < NSTAT; ++f) acc[f] = stat_comb(f, acc[f], slots[((long long)k * B + b) * NSTAT + f]);
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f) {
     double v = acc[f];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v = stat_comb(f, v, __shfl_xor_sync(0xffffffffu, v, o));
     if ((threadIdx.x & 31) == 0) red[f][threadIdx.x >> 5] = v;
   }
   __syncthreads();
   if (threadIdx.x == 0)
-    for (int f = 0; f < 4; ++f) {
+    for (int f = 0; f < NSTAT; ++f) {
       double r = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red[f][w];
-      hist[k * 4 + f] = r;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = stat_comb(f, r, red[f][w]);
+      hist[k * NSTAT + f] = r;
     }
+}
+
+// ca_admm_solve, after each iteration (Eq. 18 per scene, '<=' as printed):
+// a running scene records its residuals; it stops when r_pri <= eps_pri and
+// r_dual <= eps_dual (its iterate then stays frozen: the kernels skip it).  *remaining
+// = number of scenes still running (deterministic: integer atomics only).
+__global__ void k_stop(const double* res, uint8_t* active, int* iters, double* fin, int B, double ep, double ed,
+                       int k, int* remaining) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  const double* r = res + (long long)b * NSTAT;
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f) fin[(long long)b * NSTAT + f] = r[f];
+  iters[b] = k + 1;
+  if (r[S_RPRI] <= ep && r[S_RDUAL] <= ed) active[b] = 0;
+  else atomicAdd(remaining, 1);
 }
 
 // O1 initial dual iterate (reading #11): lambda = 1/sum(b_i) 1, mu = gamma = 0

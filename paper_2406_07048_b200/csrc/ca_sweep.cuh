@@ -20,8 +20,14 @@
 // pressure stay small; the pivot trace and the scaling-centre terms are a separate
 // kernel variant (TRACE).
 #pragma once
+#include <mutex>
+
 #include "ca_kernels.cuh"
 #include "ca_lemke.cuh"
+
+#ifndef CA_MAX_DEVICES
+#define CA_MAX_DEVICES 64
+#endif
 
 #ifndef CA_EXP_MU_UNROLL
 #define CA_EXP_MU_UNROLL 1
@@ -76,7 +82,7 @@ template <int D, int NMAX>
 struct SweepSmem {
   static constexpr int VAL = NMAX, CB = NMAX;
   static constexpr int ROWB = (NMAX <= 15) ? 0 : (NMAX + 1 + 7) / 8;  // label bytes, in doubles
-  static_assert(VAL + CB + (D + 1) * (D + 1) >= REC + 1, "the record reduction reuses the per-thread columns");
+  static_assert(VAL + CB + (D + 1) * (D + 1) >= rec_n(D) + 1, "the record reduction reuses the per-thread columns");
   static __host__ __device__ int mu(int nomax) { return nomax * (D + 1); }
   static __host__ __device__ int rowb_off(int nomax) { return mu(nomax) + VAL + CB; }
   static __host__ __device__ int per_thread(int nomax) { return mu(nomax) + VAL + CB + ROWB; }
@@ -676,6 +682,7 @@ template <int D, int NMAX, bool FUSED, bool TRACE>
 __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P) {  // @region cta_setup
   using SM = SweepSmem<D, NMAX>;
   constexpr int L1 = D + 1;
+  constexpr int RECD = rec_n(D), NAGG = rec_nagg(D);  // record: aggregates | statistics
   extern __shared__ double smem[];
   const int tid = threadIdx.x & 31, warp = threadIdx.x >> 5;  // lane; warps are independent
   const int PT = SM::per_thread(P.nomax);
@@ -713,9 +720,10 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   // item = (scene b, group of TG timesteps, chunk of 32 slots of its sort pool)
   const Item it = item_of(P, item);
   const int b = it.b;
-  double rec[REC];
+  if (!scene_on(P, b)) continue;  // stopped scene (ca_admm_solve): frozen, no record
+  double rec[RECD];
 #pragma unroll
-  for (int f = 0; f < REC; ++f) rec[f] = 0.0;
+  for (int f = 0; f < RECD; ++f) rec[f] = 0.0;
   const int gs = it.chunk * P.CHG + tid;  // slot in the group's execution order
   int tl = -1;                            // this lane's timestep within the group
   // pair state shared by the two halves of the pair's work (around the warp's
@@ -810,7 +818,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         xi[a] += Rv[a];
         r2 = __fma_rn(Rv[a], Rv[a], r2);
       }
-      rec[R_RPRI] = r2;
+      rec[NAGG + S_RPRI] = r2;
       P.zeta[p] = zeta;
 #pragma unroll
       for (int a = 0; a < D; ++a) P.xi[(long long)a * PP + p] = xi[a];
@@ -1199,9 +1207,14 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       for (int a = 0; a < D; ++a) acc = __fma_rn(po[c * D + a], vb[a], acc);
       v[c] = acc;
     }
-    if (solved) rec[R_RDUAL] = rd;
-    else rec[R_FAIL] = 1.0;
-    rec[R_PIV] = (double)pivots;
+    if (solved) rec[NAGG + S_RDUAL] = rd;
+    else rec[NAGG + S_FAIL] = 1.0;
+    // failure kinds: RAY, ITER_LIMIT, y_e < -1e-6
+    rec[NAGG + S_RAY] = (st == ST_RAY) ? 1.0 : 0.0;
+    rec[NAGG + S_ITER] = (st == ST_ITER) ? 1.0 : 0.0;
+    rec[NAGG + S_NEGYE] = (st == ST_NEGYE) ? 1.0 : 0.0;
+    rec[NAGG + S_PIV] = (double)pivots;
+    rec[NAGG + S_PMAX] = (double)pivots;
     P.pst[p] = (uint32_t)min(pivots, 65535) | ((uint32_t)st << 16) | (fallback ? (1u << 20) : 0u);
     if (P.zmask) P.zmask[p] = zb | (z0b ? 0x80000000u : 0u);
 #pragma unroll
@@ -1231,7 +1244,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   {  // @region cta_reduce
     // deterministic grouped reduction: one record per timestep of the group, lanes
     // summed in lane order, staged through the (now free) per-thread columns
-    group_reduce<REC>(wcol, tid, tl, P.TG, P.agg + (long long)item * P.TG * REC, rec, 0);
+    group_reduce<RECD>(wcol, tid, tl, P.TG, P.agg + (long long)item * P.TG * RECD, RECD, rec, 0, NAGG + S_PMAX);
   }
   }  // work item
 }
@@ -1248,26 +1261,39 @@ cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
 #define CA_EXP_SMEM_PAD 0
 #endif
   const size_t sm = SweepSmem<D, NM>::bytes(P.np, P.nrmax, P.nomax) + CA_EXP_SMEM_PAD;
-  static size_t configured = 0;
-  static int resident = 0;
-  if (configured < sm) {
-    resident = 0;
-    cudaError_t e = cudaFuncSetAttribute(k_sweep<D, NM, F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    // all of the unified L1/shared array as shared memory: residency is smem-bound
-    e = cudaFuncSetAttribute(k_sweep<D, NM, F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    configured = sm;
+  // the dynamic-smem attribute and the residency are per device (and per instantiation):
+  // cached per device ordinal under a lock (handles may live on several devices / threads)
+  static std::mutex mu;
+  static size_t configured[CA_MAX_DEVICES] = {};
+  static int resident[CA_MAX_DEVICES] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= CA_MAX_DEVICES) return cudaErrorInvalidDevice;
+  int res_dev = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (configured[dev] < sm) {
+      resident[dev] = 0;
+      e = cudaFuncSetAttribute(k_sweep<D, NM, F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      // all of the unified L1/shared array as shared memory: residency is smem-bound
+      e = cudaFuncSetAttribute(k_sweep<D, NM, F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      configured[dev] = sm;
+    }
+#if CA_SWEEP_PERSIST
+    if (!resident[dev]) {
+      int nsm = 0, per = 0;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F, T>, CTA * WPC, sm);
+      resident[dev] = nsm * (per > 0 ? per : 1) * WPC;  // in warps
+    }
+#endif
+    res_dev = resident[dev];
   }
 #if CA_SWEEP_PERSIST
-  if (!resident) {
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<D, NM, F, T>, CTA * WPC, sm);
-    resident = nsm * (per > 0 ? per : 1) * WPC;  // in warps
-  }
-  unsigned warps = (unsigned)resident < grid ? (unsigned)resident : grid;
+  unsigned warps = (unsigned)res_dev < grid ? (unsigned)res_dev : grid;
 #else
   unsigned warps = grid;
 #endif

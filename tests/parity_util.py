@@ -45,9 +45,10 @@ def validate_pair_choice(sc, s, zeta, xi, p, y_gpu, y_orc, tol=1e-9):
 
 
 def compare_dual_sweep(sc, s, zeta, xi, y_gpu, y_orc, piv_gpu, piv_orc, st_gpu, st_orc, rtol=1e-9,
-                       max_flip_frac=1e-3):
+                       max_flip_frac=2e-5):
     """T1 contract: per pair ||y_gpu - y_orc||_inf <= rtol max(1, ||y_orc||_inf) and equal
-    pivot counts/status, except rare near-tie Lemke path flips, each validated."""
+    pivot counts/status, except rare near-tie Lemke path flips -- at most max(1, 2e-5 P)
+    per sweep (the rate measured on C5, reading #2), each validated."""
     st_gpu = np.asarray(st_gpu) & 0xff  # 0x100 = re-solved by the dense fallback
     assert np.array_equal(st_gpu, st_orc), np.nonzero(st_gpu != st_orc)[0][:10]
     sc_y = np.maximum(1.0, np.abs(y_orc).max(1))

@@ -50,7 +50,7 @@ def close(a, b, rtol, what):
     assert err.max() <= rtol, f"{what}: max rel err {err.max():.3e} at {np.unravel_index(err.argmax(), err.shape)}"
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 9, 10])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 9, 10, 11, 12])
 @pytest.mark.parametrize("k0", [0, 3])
 def test_t1_dual_sweep(ca, cfg, k0):
     sc = scene(cfg)
@@ -70,7 +70,7 @@ def test_t1_dual_sweep(ca, cfg, k0):
     assert np.array_equal(st["zeta"], zeta) and np.array_equal(st["xi"], xi)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12])
 def test_t1_primal_and_multiplier(ca, cfg):
     sc = scene(cfg)
     o = warm(sc, 3)
@@ -105,7 +105,7 @@ def test_t1_primal_and_multiplier(ca, cfg):
         assert np.abs(s[0, t + 1] - (A @ s[0, t] + B @ u[0, t] + c)).max() <= 1e-12 * (1 + np.abs(s).max())
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12])
 def test_t2_full_iterations(ca, cfg):
     sc = scene(cfg)
     K = sc.iters
@@ -116,8 +116,9 @@ def test_t2_full_iterations(ca, cfg):
     s, u = g.trajectory()
     close(s, o.s, 1e-6, "s")
     close(u, o.u, 1e-6, "u")
-    assert np.abs(hist["r_pri"] - hp.sum(1)).max() <= 1e-6 * max(1, hp.max())
-    assert np.abs(hist["r_dual"] - hd.sum(1)).max() <= 1e-6 * max(1, hd.max())
+    # per entry of the residual histories, 1e-6 max(1, |r_orc|)
+    close(hist["r_pri"], hp.sum(1), 1e-6, "r_pri history")
+    close(hist["r_dual"], hd.sum(1), 1e-6, "r_dual history")
     assert hist["n_fail"].sum() == fails == 0
     st = g.pair_state()
     scale = 1.0 + np.abs(o.zeta).max()
@@ -152,7 +153,7 @@ def test_run_to_run_bitwise(ca):
     assert np.array_equal(p1["y"], p2["y"]) and np.array_equal(h1["r_pri"], h2["r_pri"])
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 10])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 10, 11, 12])
 def test_scale_detect(ca, cfg):
     sc = scene(cfg)
     o = warm(sc, 5)
@@ -469,7 +470,8 @@ def test_small_configs_revised_path(ca, cfg, monkeypatch):
     s, u = g.trajectory()
     close(s, o.s, 1e-6, "s")
     close(u, o.u, 1e-6, "u")
-    assert np.abs(hist["r_pri"] - hp.sum(1)).max() <= 1e-6 * max(1, hp.max())
+    close(hist["r_pri"], hp.sum(1), 1e-6, "r_pri history")
+    close(hist["r_dual"], hd.sum(1), 1e-6, "r_dual history")
     assert hist["n_fail"].sum() == fails == 0
 
 
