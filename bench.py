@@ -8,15 +8,20 @@ multiplier update, Riccati primal step), final multiplier update, and scale
 detection at the final trajectory.
 
 Workload (default): BASELINE.json configs[4] = C5, 4096 independent scenes x 200
-obstacles x N = 50, K = 100 per GPU (weak scaling: rank r solves scenes
-[4096 r, 4096 (r+1)); scenes are independent, so there is no data-path
-collective -- torch.distributed is used for the barrier and the max-over-ranks
-timer only).  Inputs (5.6 GB of resident iterate) exceed the 126 MB L2.
+obstacles x N = 50, K = 100.  On N GPUs the SAME 4096 scenes are split over the ranks
+(strong scaling, the scene grid of include/ca.h ca_dist_desc: rank r solves scenes
+[4096 r / N, 4096 (r+1) / N)) with ONE ncclAllReduce per ADMM iteration of every
+scene's Eq. 18 statistics (global residuals on every rank, BASELINE config 5).
+--shard weak: 4096 scenes PER rank, no data-path collective (weak scaling);
+--shard obstacles: one problem split by obstacle blocks (ncclAllReduce of the
+per-(scene, t) aggregates per iteration).  Inputs (>= 5 GB of resident iterate at
+N = 1) exceed the 126 MB L2.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py --gpus 8        # spawns 8 ranks itself (torch.distributed.run)
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
-    python bench.py --config 4 --shard obstacles   # one problem split across GPUs by
-                                                   # obstacle blocks (ncclAllReduce/iter)
+    python bench.py --config 4 --shard obstacles
+    python bench.py --config 2      # C1-C4: one scene, full K, oracle at full K
 
 Prints ONE JSON line (rank 0).
 """
@@ -56,10 +61,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
-    ap.add_argument("--shard", default="scenes", choices=["scenes", "obstacles"],
-                    help="multi-GPU split: independent scenes per rank (no collective, weak scaling) or the "
-                         "obstacles of one problem (one ncclAllReduce per iteration, strong scaling)")
-    ap.add_argument("--scenes", type=int, default=scenes.C5_SCENES, help="C5 scenes per rank")
+    ap.add_argument("--shard", default="scenes", choices=["scenes", "weak", "obstacles"],
+                    help="multi-GPU split: the batch's scenes over the ranks with a per-iteration allreduce of "
+                         "per-scene statistics (strong scaling, default), independent scene batches per rank "
+                         "(weak scaling, no collective), or the obstacles of one problem (strong scaling, one "
+                         "ncclAllReduce of the aggregates per iteration)")
+    ap.add_argument("--scenes", type=int, default=scenes.C5_SCENES,
+                    help="C5 scenes: of the whole job (scenes / obstacles sharding), per rank (weak)")
     ap.add_argument("--iters", type=int, default=0, help="ADMM iterations per solve (0 = config default)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
@@ -77,6 +85,8 @@ def dist_env():
 
 
 def make_scene(cfg, rank, n_scenes):
+    """C5: scenes [rank n, (rank+1) n) (a weak-scaling rank's own batch; rank 0 = the
+    first n scenes); other configs: the single-scene problem."""
     if cfg == 5:
         return scenes.make_c5(scene_ids=range(rank * n_scenes, (rank + 1) * n_scenes))
     return scenes.make_config(cfg)
@@ -102,11 +112,12 @@ def slice_obstacles(sc, j0, j1):
                                obs_d=np.concatenate(ds) if ds else np.zeros(0), obs_step=step)
 
 
-def workload_name(cfg, n_scenes, iters, prox_eps=0.0):
+def workload_name(cfg, n_scenes, iters, prox_eps=0.0, per_gpu=False):
     # prox_eps > 0: the proximal variant of reading #2 (NEXT f4 dual Newton), not the paper's Eq. 19
     px = f", prox_eps={prox_eps:g} (NEXT f4)" if prox_eps > 0 else ""
     if cfg == 5:
-        return f"C5: {n_scenes} scenes x 200 obstacles x N=50 per GPU, K={iters} ADMM iterations" + px
+        return (f"C5: {n_scenes} scenes x 200 obstacles x N=50{' per GPU' if per_gpu else ''}, "
+                f"K={iters} ADMM iterations" + px)
     return scenes.CONFIG_NAMES[cfg].split(",")[0] + f", K={iters}" + px
 
 
@@ -224,20 +235,6 @@ def h2d_bytes(sc):
 # the reference arm: the CPU oracle (test infrastructure), bounded sample
 # ----------------------------------------------------------------------------
 
-def oracle_sample(cfg, iters, prox_eps=0.0):
-    """Time the oracle as it stands on one scene of the workload (single thread)."""
-    import oracle
-
-    sc = make_scene(cfg, 0, 1) if cfg == 5 else make_scene(cfg, 0, 1)
-    o = oracle.Oracle(sc, prox_eps=prox_eps)
-    t0 = time.perf_counter()
-    o.scale_detect()
-    o.admm_iterate(iters)
-    o.scale_detect()
-    dt = time.perf_counter() - t0
-    return sc.n_pairs * iters / dt, dt, sc
-
-
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -248,32 +245,89 @@ def cpu_model():
     return "unknown"
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_rates(cfg, iters, prox_eps=0.0, budget_s=20.0):
+    """The CPU oracle as it stands (test infrastructure, oracle/liborc.so), timed on this
+    box's host cores on a bounded sample of the workload:
+      one core:  C5 -- one scene, C1-C4 -- the whole problem; at up to `iters` iterations
+      all cores: C5 -- one scene per core fanned out over scenes (POSIX threads,
+                 orc_admm_iterate_mt: bitwise the sequential run), C1-C4 -- the pairs of
+                 each dual step fanned out over the cores.
+    Both include the two scale detections of a step.  Returns a cpu_baseline dict."""
+    import oracle
+
+    ncores = host_cores()
+
+    def timed(sc, k, threads):
+        o = oracle.Oracle(sc, prox_eps=prox_eps)
+        t0 = time.perf_counter()
+        o.scale_detect()
+        if threads > 1:
+            o.admm_iterate_mt(k, threads)
+        else:
+            o.admm_iterate(k)
+        o.scale_detect()
+        return time.perf_counter() - t0
+
+    if cfg == 5:
+        one = make_scene(5, 0, 1)
+        k1 = min(iters, 20)
+        t1 = timed(one, k1, 1)
+        v1 = one.n_pairs * k1 / t1
+        many = make_scene(5, 0, ncores)
+        # enough iterations for ~budget/2 seconds of all-core work (the rate per core is v1)
+        km = int(max(2, min(iters, 0.5 * budget_s * v1 / many.n_pairs * ncores)))
+        tm = timed(many, km, ncores)
+        vm = many.n_pairs * km / tm
+        s1 = f"scene 0 alone ({one.n_pairs} pair-QPs/iter) x {k1} ADMM iterations + 2 scale detections, {t1:.2f} s"
+        sm = (f"scenes 0..{ncores - 1} ({many.n_pairs} pair-QPs/iter) x {km} iterations + 2 scale detections, "
+              f"{ncores} threads over scenes, {tm:.2f} s")
+    else:
+        sc = make_scene(cfg, 0, 1)
+        t1 = timed(sc, iters, 1)
+        v1 = sc.n_pairs * iters / t1
+        tm = timed(sc, iters, ncores)
+        vm = sc.n_pairs * iters / tm
+        s1 = f"the whole problem ({sc.n_pairs} pair-QPs/iter) x K={iters} (full K) + 2 scale detections, {t1:.2f} s"
+        sm = f"the same, {ncores} threads over the pairs of each dual step, {tm:.2f} s"
+    return {"value": vm, "unit": "pair-QP/s", "cores": ncores, "kind": "oracle",
+            "sample": f"all cores: {sm}; one core: {s1}; {cpu_model()}, hardware_concurrency {os.cpu_count()}",
+            "single_core": {"value": v1, "unit": "pair-QP/s", "cores": 1, "sample": s1},
+            "cpu_model": cpu_model(), "hardware_concurrency": os.cpu_count()}
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, all host cores, each step a bounded
+    sample of this config's workload (the reference arm of this tier); rank 0 only."""
     if rank != 0:
         return
     cfg = args.config
     iters_full = args.iters or (100 if cfg == 5 else scenes.make_config(cfg).iters)
-    sample_iters = min(iters_full, 20)
     for _ in range(args.warmup):
-        oracle_sample(cfg, max(1, sample_iters // 4), args.prox_eps)
-    vals, ts = [], []
-    sc = None
+        oracle_rates(cfg, max(1, min(iters_full, 20) // 4), args.prox_eps, budget_s=2.0)
+    vals, ts, cb = [], [], None
     for _ in range(args.steps):
-        v, dt, sc = oracle_sample(cfg, sample_iters, args.prox_eps)
-        vals.append(v)
-        ts.append(dt)
+        t0 = time.perf_counter()
+        cb = oracle_rates(cfg, iters_full if cfg != 5 else 100, args.prox_eps, budget_s=6.0)
+        ts.append(time.perf_counter() - t0)
+        vals.append(cb["value"])
     value = float(np.median(vals))
-    sample = (f"1 scene ({sc.n_pairs // max(1, sc.horizon)} pairs/timestep x N={sc.horizon}, "
-              f"{sc.n_pairs} pair-QPs/iter) x {sample_iters} ADMM iterations + 2 scale detections per step; "
-              f"oracle/liborc.so single-threaded on {cpu_model()}")
+    cb = dict(cb, value=value)
     line = {
         "impl": "reference", "metric": "pair-QPs/sec", "value": value, "unit": "pair-QP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.mean(ts) * 1e3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": float(np.mean(ts) * 1e3), "higher_is_better": True,
+        "scaling": "strong" if cfg != 5 or args.shard != "weak" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes/ generators)",
         "config": {"workload": workload_name(cfg, args.scenes if cfg == 5 else 1, iters_full, args.prox_eps),
                    "sample": "bounded CPU sample (see cpu_baseline.sample)"},
-        "cpu_baseline": {"value": value, "unit": "pair-QP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "pair-QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -298,19 +352,23 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     cfg = args.config
-    obstacle_shard = args.shard == "obstacles"
-    if obstacle_shard:
-        # every rank holds the same problem and solves its obstacle block
+    mode = args.shard if world > 1 else "single"
+    if cfg != 5 and mode == "scenes":
+        mode = "obstacles"  # one scene: its obstacles are what can be split
+    if mode in ("scenes", "obstacles"):
+        # every rank holds the FULL problem; the library keeps this rank's block of the
+        # scene x obstacle grid (include/ca.h ca_dist_desc) and exchanges one allreduce
+        # per ADMM iteration over NCCL
         sc = make_scene(cfg, 0, args.scenes)
         nid = ca.nccl_unique_id() if rank == 0 else None
-        if dist:
-            box = [nid]
-            dist.broadcast_object_list(box, src=0)
-            nid = box[0]
-        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid), workspace="torch",
-                       prox_eps=args.prox_eps)
-        sc_local = slice_obstacles(sc, g.j0, g.j1)
-    else:
+        box = [nid]
+        dist.broadcast_object_list(box, src=0)
+        nid = box[0]
+        grid = (world, 1) if mode == "scenes" else (1, world)
+        g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid, *grid),
+                       workspace="torch", prox_eps=args.prox_eps)
+        sc_local = slice_obstacles(g.sc, g.j0, g.j1) if mode == "obstacles" else g.sc
+    else:  # one GPU, or weak scaling: this rank's own independent batch
         sc = make_scene(cfg, rank, args.scenes)
         g = ca.Problem(sc, device=local, stream=stream.cuda_stream, workspace="torch", prox_eps=args.prox_eps)
         sc_local = sc
@@ -352,16 +410,20 @@ def run_ours(args, rank, world, local):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    units = 1 if obstacle_shard else world  # obstacle sharding splits ONE problem
+    units = world if mode == "weak" else 1  # weak: every rank its own batch; else ONE batch split
     pairs_total = sc.n_pairs * iters * args.steps * units
     value = pairs_total / (ms * 1e-3)
     solves = sc.n_scenes * args.steps * units / (ms * 1e-3)
-    launches = int(sum(v[1] for v in kt.values()))
+    launches = int(sum(v[1] for k, v in kt.items() if k != "comm"))  # this library's kernels (NCCL apart)
     # pivots of the last solve (for the algorithmic flop count; rank-local pairs)
     g.reset_iterate()
     rc, hist = g.admm_iterate(iters, hist=True)
     piv_per_sweep = float(hist["pivots"].mean())
+    if mode == "scenes":  # the history is global there: this rank's share of the pivots
+        piv_per_sweep *= sc_local.n_pairs / sc.n_pairs
     fails = int(hist["n_fail"].sum())
+    fail_kinds = {k: int(hist[k].sum()) for k in ("n_ray", "n_iterlimit", "n_neg_ye")}
+    max_piv = int(hist["max_pivots"].max())
 
     # e2e through the public API with host buffers: load (H2D) + solve + D2H
     e2e = None
@@ -389,7 +451,7 @@ def run_ours(args, rank, world, local):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": sc.n_pairs * iters * args.e2e_steps * units / dt, "unit": "pair-QP/s",
-               "h2d_bytes_per_step": h2d_bytes(sc),
+               "h2d_bytes_per_step": h2d_bytes(sc) * units,
                "d2h_bytes_per_step": int(8 * (sc.n_scenes * (sc.horizon + 1) * sc.n_state
                                               + sc.n_scenes * sc.horizon * sc.n_ctrl + 2 * sc.n_scenes)),
                "steps": args.e2e_steps,
@@ -408,7 +470,7 @@ def run_ours(args, rank, world, local):
     traffic = None
     try:
         prof = json.load(open(PROFILE_SUMMARY))
-        if prof.get("workload_key") == f"C{cfg}-{sc.n_scenes}" and not obstacle_shard:
+        if prof.get("workload_key") == f"C{cfg}-{sc_local.n_scenes}" and mode != "obstacles":
             traffic = prof.get("sweep_dram_bytes_per_launch")
     except Exception:
         pass
@@ -430,36 +492,56 @@ def run_ours(args, rank, world, local):
                  "share_of_step": sweep_ms / ms if ms else None})
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, dt, ssc = oracle_sample(cfg, min(iters, 100), args.prox_eps)
-        cpu = {"value": v, "unit": "pair-QP/s", "cores": 1, "kind": "oracle",
-               "sample": f"scene 0 alone ({ssc.n_pairs} pair-QPs/iter) x {min(iters, 100)} ADMM iterations "
-                         f"+ 2 scale detections, {dt:.1f} s single-threaded on {cpu_model()}"}
+        cpu = oracle_rates(cfg, iters, args.prox_eps)
+    par = {"single": "one GPU",
+           "scenes": f"scene-sharded x{world} (one batch split by scenes), one ncclAllReduce of every scene's "
+                     f"Eq. 18 statistics per iteration",
+           "weak": f"weak x{world} (every rank its own {sc.n_scenes}-scene batch), no data-path collective",
+           "obstacles": f"obstacle-sharded x{world}, one ncclAllReduce of per-(scene,t) aggregates per iteration"}[mode]
     line = {
         "metric": "pair-QPs/sec", "value": value, "unit": "pair-QP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if obstacle_shard else "weak",
+        "scaling": "weak" if mode == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes/ generators)",
-        "config": {"workload": workload_name(cfg, sc.n_scenes, iters, args.prox_eps), "scenes_per_gpu": sc.n_scenes,
-                   "admm_iters": iters, "pair_qps_per_iter_per_gpu": sc.n_pairs,
-                   "parallelism": (f"obstacle-sharded x{world}, one ncclAllReduce of per-(scene,t) aggregates "
-                                   f"per iteration" if obstacle_shard else
-                                   f"scene-sharded x{world}, no data-path collective"),
-                   "l2": "inputs larger than L2 (resident iterate %.1f GB)" % (g.device_bytes / 1e9)},
+        "config": {"workload": workload_name(cfg, sc.n_scenes, iters, args.prox_eps, per_gpu=mode == "weak"),
+                   "scenes_total": sc.n_scenes * units, "scenes_per_gpu": sc_local.n_scenes,
+                   "admm_iters": iters, "pair_qps_per_iter_per_gpu": sc_local.n_pairs, "parallelism": par,
+                   "l2": "inputs larger than L2 (resident iterate %.1f GB per GPU)" % (g.device_bytes / 1e9)},
         "admm_solves_per_sec": solves,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
-        "lemke_failures": fails, "min_alpha_final": float(np.min(amin)),
+        "nccl_collectives": int(kt["comm"][1]),
+        "lemke_failures": fails, "lemke_failure_kinds": fail_kinds, "max_pivots": max_piv,
+        "min_alpha_final": float(np.min(amin)),
     }
     emit(line)
 
 
+def spawn_ranks(args):
+    """--gpus N > 1 without a torchrun environment: launch the N ranks ourselves (one
+    process per GPU, torch.distributed.run, rendezvous on 127.0.0.1); rank 0's JSON line
+    comes through our stdout."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     global _JSON_OUT
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     sys.stdout.flush()
     os.dup2(2, 1)
-    args = parse()
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

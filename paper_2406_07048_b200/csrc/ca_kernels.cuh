@@ -238,6 +238,30 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
   __syncwarp();
 }
 
+// The integer statistics of a warp's pairs per timestep slot tt (exact, order-free
+// warp reductions): out[tt*stride + S_PIV, S_FAIL, S_RAY, S_ITER, S_NEGYE] = sums of
+// ist[0..4] over the lanes with tl == tt, out[.. + S_PMAX] = max of ist[0].
+__device__ __forceinline__ void group_reduce_int(int lane, int tl, int TG, double* out, int stride, const int ist[5]) {
+  constexpr unsigned FULL = 0xffffffffu;
+  for (int tt = 0; tt < TG; ++tt) {
+    const bool mine = tl == tt;
+    const int piv = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[0] : 0u);
+    const int fl = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[1] : 0u);
+    const int ry = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[2] : 0u);
+    const int it = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[3] : 0u);
+    const int ng = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[4] : 0u);
+    const int pm = (int)__reduce_max_sync(FULL, mine ? (unsigned)ist[0] : 0u);
+    if (lane == tt) {
+      double* o = out + (long long)tt * stride;
+      o[S_PIV] = piv;
+      o[S_FAIL] = fl;
+      o[S_RAY] = ry;
+      o[S_ITER] = it;
+      o[S_NEGYE] = ng;
+      o[S_PMAX] = pm;
+    }
+  }
+}
 
 // ----------------------------------------------------------------------------
 // ADMM step 3 standalone (Eq. 17 with Eqs. 10-11 at s^{k+1}, y^{k+1})

@@ -721,9 +721,14 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   const Item it = item_of(P, item);
   const int b = it.b;
   if (!scene_on(P, b)) continue;  // stopped scene (ca_admm_solve): frozen, no record
-  double rec[RECD];
+  // this pair's record: the double fields (aggregates, r_dual, r_pri) staged for the
+  // lane-ordered reduction; the integer statistics (pivots, failure kinds) reduced
+  // exactly by warp integer reductions
+  constexpr int NDBL = NAGG + 2;
+  double rec[NDBL];
 #pragma unroll
-  for (int f = 0; f < RECD; ++f) rec[f] = 0.0;
+  for (int f = 0; f < NDBL; ++f) rec[f] = 0.0;
+  int ist[5] = {0, 0, 0, 0, 0};  // pivots, fail, ray, iter_limit, neg_ye
   const int gs = it.chunk * P.CHG + tid;  // slot in the group's execution order
   int tl = -1;                            // this lane's timestep within the group
   // pair state shared by the two halves of the pair's work (around the warp's
@@ -1208,13 +1213,12 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       v[c] = acc;
     }
     if (solved) rec[NAGG + S_RDUAL] = rd;
-    else rec[NAGG + S_FAIL] = 1.0;
     // failure kinds: RAY, ITER_LIMIT, y_e < -1e-6
-    rec[NAGG + S_RAY] = (st == ST_RAY) ? 1.0 : 0.0;
-    rec[NAGG + S_ITER] = (st == ST_ITER) ? 1.0 : 0.0;
-    rec[NAGG + S_NEGYE] = (st == ST_NEGYE) ? 1.0 : 0.0;
-    rec[NAGG + S_PIV] = (double)pivots;
-    rec[NAGG + S_PMAX] = (double)pivots;
+    ist[0] = pivots;
+    ist[1] = solved ? 0 : 1;
+    ist[2] = (st == ST_RAY) ? 1 : 0;
+    ist[3] = (st == ST_ITER) ? 1 : 0;
+    ist[4] = (st == ST_NEGYE) ? 1 : 0;
     P.pst[p] = (uint32_t)min(pivots, 65535) | ((uint32_t)st << 16) | (fallback ? (1u << 20) : 0u);
     if (P.zmask) P.zmask[p] = zb | (z0b ? 0x80000000u : 0u);
 #pragma unroll
@@ -1244,7 +1248,9 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   {  // @region cta_reduce
     // deterministic grouped reduction: one record per timestep of the group, lanes
     // summed in lane order, staged through the (now free) per-thread columns
-    group_reduce<RECD>(wcol, tid, tl, P.TG, P.agg + (long long)item * P.TG * RECD, RECD, rec, 0, NAGG + S_PMAX);
+    double* out = P.agg + (long long)item * P.TG * RECD;
+    group_reduce<NDBL>(wcol, tid, tl, P.TG, out, RECD, rec, 0, -1);
+    group_reduce_int(tid, tl, P.TG, out + NAGG, RECD, ist);
   }
   }  // work item
 }

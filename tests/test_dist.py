@@ -138,3 +138,82 @@ def test_obstacle_sharding_world2_gloo():
         u = K.T @ y + bvec
         ref[t - 1] += 0.5 * float(u @ u)
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)
+
+
+def _worker_grid(rank, world, port, n_scenes, eps, kmax, out):
+    """Scene grid (include/ca.h ca_dist_desc, scene_shards = world): rank keeps its scene
+    block; per ADMM iteration its scenes' Eq. 18 statistics go into a global table (zero
+    elsewhere) that ONE all_reduce makes identical on every rank; every rank then takes
+    the same per-scene stop decisions and the same global 'scenes still running' count,
+    so all ranks run the same number of collectives (no rank can hang)."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import scenes
+    from paper_2406_07048_b200._ca import grid_position
+
+    full = scenes.make_c5(scene_ids=range(n_scenes))
+    b0, b1 = grid_position(n_scenes, world, rank, world, 1)["scenes"]
+    mine = {b: oracle.Oracle(full.subset([b])) for b in range(b0, b1)}
+    active = np.ones(n_scenes, bool)
+    iters = np.zeros(n_scenes, np.int64)
+    loops = 0
+    for k in range(kmax):
+        table = torch.zeros(n_scenes, 2, dtype=torch.float64)
+        for b, o in mine.items():
+            if not active[b]:
+                continue
+            rd, _ = o.dual_sweep()
+            o.primal_step()
+            rp = o.multiplier_update()
+            table[b, 0], table[b, 1] = float(rp[0]), float(rd[0])
+        dist.all_reduce(table)  # the per-iteration exchange
+        loops += 1
+        for b in range(n_scenes):
+            if active[b]:
+                iters[b] = k + 1
+                if table[b, 0] <= eps and table[b, 1] <= eps:
+                    active[b] = False
+        if not active.any():
+            break
+    s = torch.zeros(n_scenes, full.horizon + 1, full.n_state, dtype=torch.float64)
+    for b, o in mine.items():
+        s[b] = torch.from_numpy(o.s[0])
+    dist.all_reduce(s)
+    cnt = torch.tensor([loops])
+    allc = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(allc, cnt)
+    if rank == 0:
+        out.put((s.numpy(), iters, [int(c) for c in allc]))
+    dist.destroy_process_group()
+
+
+def test_scene_grid_world2_gloo():
+    """The library's scene-sharded protocol on two gloo ranks: the union of the shards
+    equals the single-process ca_admm_solve semantics (orc_admm_solve per scene, Eq. 18)
+    bitwise, and both ranks ran the same number of collective rounds."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    import scenes
+
+    world, n, eps, kmax = 2, 3, 3.0, 25
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_grid, args=(r, world, port, n, eps, kmax, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    s, iters, loops = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert loops[0] == loops[1] == iters.max()
+    ref = oracle.Oracle(scenes.make_c5(scene_ids=range(n)))
+    it, cv, _, _, _ = ref.admm_solve(eps, eps, kmax)
+    assert np.array_equal(it, iters)
+    assert np.array_equal(s, ref.s)
