@@ -213,13 +213,36 @@ __device__ __forceinline__ Item item_of(const Dev& P, int item) {
 // pair's timestep slot tl (-1: no pair), staged in its smem column red[f*32];
 // out[tt*stride + f0 + f] = sum over lanes l = 0..31 with tl(l) == tt, in lane order
 // (field fmx, if any: the max, for S_PMAX).
+#ifndef CA_EXP_GRED
+#define CA_EXP_GRED 0  // 1: per-slot lane masks (fewer instructions, a serial load chain: measured slower)
+#endif
 template <int NFIELD>
 __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int TG, double* out, int stride,
                                              const double* rec, int f0, int fmx) {
-  __syncwarp();  // every lane is done with its columns (stl below crosses columns)
+  __syncwarp();  // every lane is done with its columns (the staging below crosses columns)
   double* red = col0 + lane;
 #pragma unroll
   for (int f = 0; f < NFIELD; ++f) red[f * 32] = rec[f];
+#if CA_EXP_GRED
+  // the lanes of each timestep slot (TG <= 8), visited in increasing lane order below
+  uint32_t* smask = reinterpret_cast<uint32_t*>(col0 + NFIELD * 32);
+  for (int tt = 0; tt < TG; ++tt) {
+    const uint32_t m = __ballot_sync(0xffffffffu, tl == tt);
+    if (lane == 0) smask[tt] = m;
+  }
+  __syncwarp();
+  for (int o = lane; o < TG * NFIELD; o += 32) {
+    const int tt = o / NFIELD, f = o % NFIELD;
+    const double* src = col0 + f * 32;
+    double acc = 0.0;
+    if (f == fmx) {
+      for (uint32_t bb = smask[tt]; bb; bb &= bb - 1) acc = fmax(acc, src[__ffs(bb) - 1]);
+    } else {
+      for (uint32_t bb = smask[tt]; bb; bb &= bb - 1) acc += src[__ffs(bb) - 1];
+    }
+    out[tt * stride + f0 + f] = acc;
+  }
+#else
   int* stl = reinterpret_cast<int*>(col0 + NFIELD * 32);
   stl[lane] = tl;
   __syncwarp();
@@ -235,6 +258,7 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
     }
     out[tt * stride + f0 + f] = acc;
   }
+#endif
   __syncwarp();
 }
 

@@ -298,4 +298,110 @@ __device__ __forceinline__ bool solve_small(const PairRows<D>& W, uint32_t wb, u
   return true;
 }
 
+// Exact replicas of solve_small for m = 1 and m = 2 structural columns (the first
+// pivots of almost every pair: z0 alone, then z0 and one z_j): the identity-padded 3 x 3
+// Gauss-Jordan of solve_small reduces on the real rows to the operations below (padding
+// rows and columns only ever contribute exact zeros and unit pivots), so the results
+// are bitwise those of solve_small, for a fraction of the work.
+template <int D>
+__device__ __forceinline__ void solve_m1(const PairRows<D>& W, uint32_t Rm, uint32_t zb, bool z0b, Var e,
+                                         SmallSol<D>& out) {
+  const int l = W.l, mz = __popc(zb);
+  const int i = __ffs(Rm) - 1;
+  double fi[D + 1], ki;
+  W.row(i, fi, ki);
+  double fe[D + 1], ke;
+  W.row(e.kind == 1 ? e.j : 0, fe, ke);
+  const int j = __ffs(zb) - 1;  // the column is z_j (mz = 1) or z0
+  double fc[D + 1], kc;
+  W.row(j < 0 ? 0 : j, fc, kc);
+  const double g = (mz == 1) ? -m_entry<D>(fi, ki, i, fc, kc, j, l) : -1.0;
+  const double me = -m_entry<D>(fi, ki, i, fe, ke, e.j, l);
+  const double a = (e.kind == 0) ? ((i == e.j) ? 1.0 : 0.0) : ((e.kind == 2) ? -1.0 : me);
+  const double x = a * (1.0 / g);
+  out.x[0] = x;
+  out.x[1] = out.x[2] = 0.0;
+  const bool col = mz == 1;
+  double uh[D + 1];
+#pragma unroll
+  for (int c = 0; c <= D; ++c) uh[c] = col ? __fma_rn(x, fc[c], 0.0) : 0.0;
+  const double sk = col ? __fma_rn(x, kc, 0.0) : 0.0;
+  const double sl = (col && j == l) ? 0.0 + x : 0.0;
+  double s0 = (!col && z0b) ? 0.0 + x : 0.0;
+  if (e.kind == 2) s0 -= 1.0;
+  const bool ez = e.kind == 1;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) out.uh[c] = ez ? uh[c] - fe[c] : uh[c];
+  out.sk = ez ? sk - ke : sk;
+  out.sl = (ez && e.j == l) ? sl - 1.0 : sl;
+  out.s0 = s0;
+}
+
+template <int D>
+__device__ __forceinline__ void solve_m2(const PairRows<D>& W, uint32_t Rm, uint32_t zb, bool z0b, Var e,
+                                         SmallSol<D>& out) {
+  const int l = W.l, mz = __popc(zb);
+  const int i0 = __ffs(Rm) - 1;
+  const int i1 = __ffs(Rm & (Rm - 1)) - 1;
+  const int j0 = __ffs(zb) - 1;              // column 0: z_j0 (mz >= 1) or z0
+  const int j1 = __ffs(zb & (zb - 1)) - 1;   // column 1: z_j1 (mz = 2) or z0
+  double f0[D + 1], k0, f1[D + 1], k1, fe[D + 1], ke, fa[D + 1], ka, fb[D + 1], kb;
+  W.row(i0, f0, k0);
+  W.row(i1, f1, k1);
+  W.row(e.kind == 1 ? e.j : 0, fe, ke);
+  W.row(j0 < 0 ? 0 : j0, fa, ka);
+  W.row(j1 < 0 ? 0 : j1, fb, kb);
+  // G = [[g00 g01 | a0], [g10 g11 | a1]] as solve_small builds it
+  auto gcol = [&](const double* fi, double ki, int i, int s) -> double {
+    const double me = (s == 0) ? -m_entry<D>(fi, ki, i, fa, ka, j0, l) : -m_entry<D>(fi, ki, i, fb, kb, j1, l);
+    return (s < mz) ? me : ((s == mz && z0b) ? -1.0 : 0.0);
+  };
+  auto rhs = [&](const double* fi, double ki, int i) -> double {
+    const double me = -m_entry<D>(fi, ki, i, fe, ke, e.j, l);
+    return (e.kind == 0) ? ((i == e.j) ? 1.0 : 0.0) : ((e.kind == 2) ? -1.0 : me);
+  };
+  double g00 = gcol(f0, k0, i0, 0), g01 = gcol(f0, k0, i0, 1), a0 = rhs(f0, k0, i0);
+  double g10 = gcol(f1, k1, i1, 0), g11 = gcol(f1, k1, i1, 1), a1 = rhs(f1, k1, i1);
+  // column 0: partial pivoting between the two real rows, one reciprocal
+  const bool sw = fabs(g10) > fabs(g00);
+  {
+    const double t0 = g00, t1 = g01, t3 = a0;
+    g00 = sw ? g10 : g00; g01 = sw ? g11 : g01; a0 = sw ? a1 : a0;
+    g10 = sw ? t0 : g10; g11 = sw ? t1 : g11; a1 = sw ? t3 : a1;
+  }
+  const double inv0 = 1.0 / g00;
+  g01 = g01 * inv0;
+  a0 = a0 * inv0;
+  g11 = __fma_rn(-g10, g01, g11);
+  a1 = __fma_rn(-g10, a0, a1);
+  // column 1
+  const double inv1 = 1.0 / g11;
+  a1 = a1 * inv1;
+  a0 = __fma_rn(-g01, a1, a0);
+  out.x[0] = a0;
+  out.x[1] = a1;
+  out.x[2] = 0.0;
+  double uh[D + 1], sl = 0.0, sk = 0.0, s0 = 0.0;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) uh[c] = 0.0;
+  const bool c0 = 0 < mz, c1 = 1 < mz;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) uh[c] = c0 ? __fma_rn(a0, fa[c], uh[c]) : uh[c];
+  sk = c0 ? __fma_rn(a0, ka, sk) : sk;
+  sl = (c0 && j0 == l) ? sl + a0 : sl;
+  s0 = (mz == 0 && z0b) ? s0 + a0 : s0;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) uh[c] = c1 ? __fma_rn(a1, fb[c], uh[c]) : uh[c];
+  sk = c1 ? __fma_rn(a1, kb, sk) : sk;
+  sl = (c1 && j1 == l) ? sl + a1 : sl;
+  s0 = (mz == 1 && z0b) ? s0 + a1 : s0;
+  if (e.kind == 2) s0 -= 1.0;
+  const bool ez = e.kind == 1;
+#pragma unroll
+  for (int c = 0; c <= D; ++c) out.uh[c] = ez ? uh[c] - fe[c] : uh[c];
+  out.sk = ez ? sk - ke : sk;
+  out.sl = (ez && e.j == l) ? sl - 1.0 : sl;
+  out.s0 = s0;
+}
+
 }  // namespace ca

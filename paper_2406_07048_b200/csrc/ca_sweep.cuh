@@ -29,6 +29,19 @@
 #define CA_MAX_DEVICES 64
 #endif
 
+#ifndef CA_EXP_M12
+#define CA_EXP_M12 0  // 1: exact m = 1, 2 specialisations of the structural solve (-5 % instructions,
+                      // +7 % time: the larger pivot loop misses the instruction cache, profiles/r02)
+#endif
+#ifndef CA_EXP_MU_PIPE
+#define CA_EXP_MU_PIPE 0
+#endif
+#ifndef CA_EXP_P1MERGE
+#define CA_EXP_P1MERGE 0
+#endif
+#ifndef CA_EXP_RESET
+#define CA_EXP_RESET 0  // 1: drop tie candidates on a clearly lower new minimum (measured slower)
+#endif
 #ifndef CA_EXP_MU_UNROLL
 #define CA_EXP_MU_UNROLL 1
 #endif
@@ -907,7 +920,18 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         if (n - __popc(wb) > D + 4) { status = ST_ITER; break; }  // rank bound (cannot happen exactly)
         // structural m x m system: registers for m <= 3, generic solver otherwise
         SmallSol<D> ss;  // @region solve_call
-        const bool small = solve_small<D>(W, wb, zb, z0b, ent, ss);
+        bool small = true;
+#if CA_EXP_M12
+        {
+          const uint32_t Rm = ~wb & nmask;
+          const int mr = __popc(Rm);
+          if (mr == 1) solve_m1<D>(W, Rm, zb, z0b, ent, ss);
+          else if (mr == 2) solve_m2<D>(W, Rm, zb, z0b, ent, ss);
+          else small = solve_small<D>(W, wb, zb, z0b, ent, ss);
+        }
+#else
+        small = solve_small<D>(W, wb, zb, z0b, ent, ss);
+#endif
         double* Gp = Gslow;
         if (!small) {
           // the first GSLOTS lanes of the warp needing it use shared memory
@@ -935,22 +959,29 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         // the running minimum, which only shrinks).
         double cmax = 0.0, bn = kInf, bd = 1.0, tn = kInf;
         uint32_t cand = 0;
-        auto ratio = [&](bool el, double c, double v) -> bool {  // branch-free
+        auto ratio = [&](bool el, double c, double v, uint32_t bit) {  // branch-free
           const double nu = (v > 0.0) ? v : 0.0;
           const double nbd = nu * bd;
           const bool lt = el && (nbd < bn * c);
           // a new minimum is its own candidate; otherwise compare with the band of the
           // running minimum: nu/c <= theta + tau' max(1, theta), tau' = tau + 1e-12 (superset)
-          const bool cnd = lt || (el && nbd <= tn * c);
+          const bool cnd = el && nbd <= tn * c;
           const double tnn = __fma_rn(tauS, (c > nu) ? c : nu, nu);  // (theta + tau' max(1,theta)) c
+#if CA_EXP_RESET
+          // a new minimum whose band lies below the old minimum drops the old candidates
+          // (they are all >= the old minimum): cand stays (nearly) exact, so the tie
+          // filter below only runs on real near-ties
+          const bool reset = lt && (tnn * bd < bn * c);
+#else
+          const bool reset = false;
+#endif
+          cand = reset ? bit : ((lt || cnd) ? (cand | bit) : cand);
           bn = lt ? nu : bn;
           bd = lt ? c : bd;
           tn = lt ? tnn : tn;
-          return cnd;
         };
-        auto rowc = [&](int i, double c) {
+        auto rowcv = [&](int i, double c, double vo, double co) {
           const uint32_t bit = 1u << i;
-          const double vo = VAL(i), co = CBV(i);
           const double vu = __fma_rn(-co, ve2p, vo);
           const double v = (pend & bit) ? vu : vo;
           VAL(i) = v;
@@ -958,8 +989,24 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
           const bool wbas = (wb & bit) != 0u;
           const double ac = fabs(c);
           cmax = (wbas && ac > cmax) ? ac : cmax;
-          cand |= ratio(wbas && c > ptol, c, v) ? bit : 0u;
+          ratio(wbas && c > ptol, c, v, bit);
         };
+        auto rowc = [&](int i, double c) { rowcv(i, c, VAL(i), CBV(i)); };
+#if CA_EXP_P1MERGE
+        // every row in one loop (one inlined copy of the row step: a smaller hot loop),
+        // rows fetched through the branch-free table select; bitwise the segmented form
+        // (the extra terms are exact zeros: f = 0 or k = 0)
+#pragma unroll 1
+        for (int i = 0; i < n; ++i) {
+          double f[D + 1], k;
+          W.row(i, f, k);
+          double c = ss.s0;
+#pragma unroll
+          for (int cc = 0; cc <= D; ++cc) c = __fma_rn(f[cc], ss.uh[cc], c);
+          c = __fma_rn(k, ss.sl, c);
+          rowc(i, (i == n - 1) ? c - ss.sk : c);
+        }
+#else
         // lambda rows (0, at_u, kt_u): CTA-shared table of part ip
 #pragma unroll 1
         for (int i = 0; i < nr1; ++i) {
@@ -969,6 +1016,32 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
           for (int cc = 0; cc <= D; ++cc) c = __fma_rn(r[cc], ss.uh[cc], c);
           rowc(i, __fma_rn(r[D + 1], ss.sl, c));
         }
+#if CA_EXP_MU_PIPE
+        // mu rows (d_l - c_l.rho, R^T c_l): kt = 0; software-pipelined -- the next row's
+        // data and its value / coefficient are loaded while this row is processed
+        {
+          double mr[D + 1], vo = VAL(nr1), co = CBV(nr1);
+#pragma unroll
+          for (int cc = 0; cc <= D; ++cc) mr[cc] = mu[cc * CTA];
+#pragma unroll 1
+          for (int l = 0; l < no; ++l) {
+            const int ln = (l + 1 < no) ? l + 1 : l;
+            const double* mn = mu + ln * L1 * CTA;
+            double nx[D + 1];
+#pragma unroll
+            for (int cc = 0; cc <= D; ++cc) nx[cc] = mn[cc * CTA];
+            const double vn = VAL(nr1 + ln), cn = CBV(nr1 + ln);
+            double c = ss.s0;
+#pragma unroll
+            for (int cc = 0; cc <= D; ++cc) c = __fma_rn(mr[cc], ss.uh[cc], c);
+            rowcv(nr1 + l, c, vo, co);
+#pragma unroll
+            for (int cc = 0; cc <= D; ++cc) mr[cc] = nx[cc];
+            vo = vn;
+            co = cn;
+          }
+        }
+#else
         // mu rows (d_l - c_l.rho, R^T c_l): kt = 0
 #if CA_EXP_MU_UNROLL == 2
 #pragma unroll 2
@@ -982,8 +1055,10 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
           for (int cc = 0; cc <= D; ++cc) c = __fma_rn(m[cc * CTA], ss.uh[cc], c);
           rowc(nr1 + l, c);
         }
+#endif
         rowc(n - 2, __fma_rn(1.0, ss.uh[0], ss.s0));  // gamma row (1, 0)
         rowc(n - 1, ss.s0 - ss.sk);                    // phi row (0, 0)
+#endif
         pend = 0;
         // basic z rows: cbar is the structural solution itself
         {
@@ -995,14 +1070,14 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
             CBV(i) = c;
             const double ac = fabs(c);
             cmax = (ac > cmax) ? ac : cmax;
-            cand |= ratio(c > ptol, c, VAL(i)) ? (1u << i) : 0u;
+            ratio(c > ptol, c, VAL(i), 1u << i);
           }
         }
         double cb0 = 0.0;
         if (z0b) {
           cb0 = xcol(__popc(zb));
           cmax = fmax(cmax, fabs(cb0));
-          ratio(cb0 > ptol, cb0, val0);
+          ratio(cb0 > ptol, cb0, val0, 0u);  // z0 has no row bit (a new minimum at z0 resets the rows)
         }
         const double thr = ptol * fmax(1.0, cmax);
         // rare: the provisional minimiser is not eligible (pivot_tol < cbar <= thr):
