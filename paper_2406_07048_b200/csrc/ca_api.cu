@@ -22,6 +22,7 @@
 #define CA_SWEEP_POOL_MIN_ITEMS 10000  // ~4 waves of resident warps on 148 SMs
 #endif
 #include "ca_kernels.cuh"
+#include "ca_riccati_scan.cuh"
 #include "ca_sweep.cuh"
 
 // the pair-sweep instantiations live in ca_sweep_d2.cu / ca_sweep_d3.cu
@@ -521,6 +522,36 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
     h->launches[1]++;
     return CA_OK;
   }
+  // parallel-in-time LQ (ca_riccati_scan.cuh): log2(N+1) combination levels instead of N
+  // dependent Riccati steps on one warp; n_s <= 4 (the element combination keeps its
+  // matrices in registers), CA_RICCATI_SCAN=0 selects the serial recursion
+  if constexpr (NS <= 4) {
+    size_t sms = sizeof(double) * (size_t)ca::riccati_scan_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
+    // the scene's records staged in shared memory as one block when they fit (and come
+    // from the sweep's own layout, not the allreduced per-(scene, t) buffer)
+    const size_t srec = sizeof(double) * (size_t)ca::riccati_scan_rec_doubles(
+                                             (long long)h->dev.NG * h->dev.nchunkG * h->dev.TG, h->dev.rec);
+    const int stage_recs = (nchunk && recs == h->dev.agg && sms + srec <= 200 * 1024) ? 1 : 0;
+    if (stage_recs) sms += srec;
+    static const bool scan_on = !(std::getenv("CA_RICCATI_SCAN") && std::getenv("CA_RICCATI_SCAN")[0] == '0');
+    if (scan_on && sms <= 200 * 1024 && ca::SCAN_GS * (h->N + 1) <= 1024 && h->N >= 16) {
+      {
+        static std::mutex mu;
+        static size_t configured[CA_MAX_DEVICES] = {};
+        if (h->device >= CA_MAX_DEVICES) return fail(CA_E_CUDA, "device ordinal too large");
+        std::lock_guard<std::mutex> lk(mu);
+        if (sms > 48 * 1024 && sms > configured[h->device]) {
+          CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati_scan<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms));
+          configured[h->device] = sms;
+        }
+      }
+      const int threads = 32 * ((ca::SCAN_GS * (h->N + 1) + 31) / 32);
+      ca::k_riccati_scan<NS, NU><<<(unsigned)h->B, threads, sms, h->stream>>>(h->dev, recs, nchunk, cur, prev,
+                                                                             stage_recs);
+      CUDA_TRY(cudaGetLastError());
+      return CA_OK;
+    }
+  }
   const size_t sm = sizeof(double) * (size_t)ca::riccati_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
   if (sm > 48 * 1024) {  // the attribute is per device: cached per device ordinal under a lock
     static std::mutex mu;
@@ -605,7 +636,7 @@ ca_status launch_collect(ca_problem* h, double* dst, int mask) {
   }
   // the box residual joins r_pri once (rank 0 of an obstacle-sharded run)
   const int add_box = ((mask & 2) && (!h->comm || h->rank == 0)) ? 1 : 0;
-  ca::k_collect<<<(h->B + 127) / 128, 128, 0, h->stream>>>(h->dev, dst, mask, add_box);
+  ca::k_collect<<<(h->B + 3) / 4, 128, 0, h->stream>>>(h->dev, dst, mask, add_box);
   CUDA_TRY(cudaGetLastError());
   h->launches[4]++;
   return CA_OK;

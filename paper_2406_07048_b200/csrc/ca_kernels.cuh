@@ -355,20 +355,28 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
 
 #ifdef CA_COMMON_KERNELS
 // per-scene statistics of the records -> dst[b*NSTAT + S_*] (fields with mask bit f
-// clear are left untouched; stopped scenes of ca_admm_solve keep theirs)
-__global__ void k_collect(Dev P, double* dst, int mask, int add_box) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+// clear are left untouched; stopped scenes of ca_admm_solve keep theirs).  One warp per
+// scene: lane l sums records l, l+32, ... in order, then a fixed shuffle tree (the
+// summation order is fixed, so results are bitwise reproducible).
+__global__ void __launch_bounds__(128) k_collect(Dev P, double* dst, int mask, int add_box) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= P.B || !scene_on(P, b)) return;
   double acc[NSTAT];
 #pragma unroll
   for (int f = 0; f < NSTAT; ++f) acc[f] = 0.0;
   const long long per = (long long)P.NG * P.nchunkG * P.TG;  // records of one scene (contiguous)
   const long long base = (long long)b * per;
-  for (long long r = 0; r < per; ++r) {
+  for (long long r = lane; r < per; r += 32) {
     const double* rec = P.agg + (base + r) * P.rec + P.nagg;
 #pragma unroll
     for (int f = 0; f < NSTAT; ++f) acc[f] = stat_comb(f, acc[f], rec[f]);
   }
+#pragma unroll
+  for (int f = 0; f < NSTAT; ++f)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[f] = stat_comb(f, acc[f], __shfl_xor_sync(0xffffffffu, acc[f], o));
+  if (lane != 0) return;
   if (P.box && add_box) acc[S_RPRI] += P.box_res[b];  // box block's ||x - w||^2 (reading #7)
 #pragma unroll
   for (int f = 0; f < NSTAT; ++f)
@@ -442,10 +450,15 @@ __global__ void k_pmax_back(Dev P, double* out, const double* pmax) {
 // Stage assembly of one (scene, t), t = 1..N: sums the (scene, t) chunk records in
 // fixed order and writes H_t (ns x ns), h_t (ns) and the (scene, t) statistics.
 // H_t, h_t and the statistics of (scene, t) = q from its summed record
-static __device__ void stage_assemble(const Dev& P, long long q, const double* rec, double* out, double* so) {
+// (Qs_, sref_, s_: optional shared-memory copies of Qs and of this scene's s_ref / s
+// rows [N+1][ns]; NULL = global memory)
+static __device__ void stage_assemble(const Dev& P, long long q, const double* rec, double* out, double* so,
+                                      const double* Qs_ = nullptr, const double* sref_ = nullptr,
+                                      const double* s_ = nullptr) {
   const int b = (int)(q / P.N), t = (int)(q % P.N) + 1;
   const int N = P.N, NS = P.ns, npc = P.npc, L1 = P.d + 1;
   const double sig = P.sigma;
+  const double* Qs = Qs_ ? Qs_ : P.Qs;
   double S[4][4], gv[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
@@ -454,13 +467,13 @@ static __device__ void stage_assemble(const Dev& P, long long q, const double* r
     for (int c = 0; c < 4; ++c) S[a][c] = (a < L1 && c >= a && c < L1) ? rec[sym_idx(a, c, L1)] : 0.0;
   }
   double* ho = out + NS * NS;
-  const double* sref = P.sref + ((long long)b * (N + 1) + t) * NS;
-  const double* sk = P.s + ((long long)b * (N + 1) + t) * NS;
+  const double* sref = sref_ ? sref_ + (long long)t * NS : P.sref + ((long long)b * (N + 1) + t) * NS;
+  const double* sk = s_ ? s_ + (long long)t * NS : P.s + ((long long)b * (N + 1) + t) * NS;
   for (int a = 0; a < NS; ++a) {
     double acc = 0.0;
     for (int c = 0; c < NS; ++c) {
-      out[a * NS + c] = 2.0 * P.Qs[a * NS + c];
-      acc += P.Qs[a * NS + c] * sref[c];
+      out[a * NS + c] = 2.0 * Qs[a * NS + c];
+      acc += Qs[a * NS + c] * sref[c];
     }
     ho[a] = -2.0 * acc;
   }

@@ -1,0 +1,639 @@
+// ca_riccati_scan.cuh -- ADMM step 2 (Eq. 16; one SQP QP per iteration,
+// P:349-351) for small batches by a PARALLEL-IN-TIME LQ solve: the backward Riccati
+// recursion of k_riccati (O(N) dependent steps on one warp) is replaced by an
+// associative scan over the N+1 stages (log2(N+1) levels), one thread per stage.
+//
+// Stage t of the LQ (the same data as k_riccati: stage blocks H_t, h_t from the sweep's
+// Gauss-Newton aggregates, dynamics s_{t+1} = A_t s_t + B_t u_t + c_t, control cost
+// 1/2 u^T R_t u + r_t^T u with R_t = 2 Qu (+ rho_b on bounded controls), r_t the box
+// block's linear term) is the element
+//     e_t = (A, b, C, eta, J) = (A_t, c_t + B_t u0_t, B_t R_t^-1 B_t^T, -h_t, H_t),
+//     u0_t = -R_t^-1 r_t   (t = 0: J = 0, eta = 0 -- s_0 is fixed; t = N: A = b = C = 0)
+// of the conditional value function V_{t->t+1}(s_t | s_{t+1}) (Sarkka & Garcia-Fernandez,
+// temporal parallelization of LQ control); the associative combination
+//     T = (I + C_ij J_jk)^-1
+//     A_ik = A_jk T A_ij          b_ik = A_jk T (b_ij + C_ij eta_jk) + b_jk
+//     C_ik = A_jk T C_ij A_jk^T + C_jk
+//     eta_ik = A_ij^T T^T (eta_jk - J_jk b_ij) + eta_ij
+//     J_ik = A_ij^T T^T J_jk A_ij + J_ij
+// composed over [t, N] (a suffix scan, Hillis-Steele, double-buffered in shared memory)
+// gives the value function V_t(s) = 1/2 s^T J s - eta^T s, i.e. the Riccati P_t = J,
+// p_t = -eta.  The gains then follow per stage in parallel with k_riccati's own formula
+// (QuuSolve), and one thread rolls the dynamics forward exactly (riccati_forward).
+// Different association order from the serial recursion: agreement to rounding of the
+// LQ's conditioning (the T1 / T2 tests against the oracle's condensed Cholesky hold).
+#pragma once
+#include "ca_kernels.cuh"
+
+namespace ca {
+
+// A scan element / scratch record stored field-major across the stages ([field][stage],
+// stage stride S): the threads of a warp (consecutive stages, rows a of a group) then hit
+// distinct shared-memory banks (S chosen by scan_stride).
+struct ElRef {
+  double* p;
+  int S;
+  __device__ __forceinline__ double& operator[](int k) const { return p[(long long)k * S]; }
+};
+// stage stride of the field-major arrays: >= n with S NS = 4 (mod 16) doubles, so that the
+// 16 (stage, row) accesses of a half-warp fall on distinct 64-bit bank pairs
+__host__ __device__ inline int scan_stride(int n, int NS) {
+  for (int S = n;; ++S)
+    if ((S * NS) % 16 == 4 % 16 || NS == 1) return S;
+}
+
+template <int NS>
+struct ScanEl {
+  static constexpr int A = 0, B = NS * NS, C = B + NS, ETA = C + NS * NS, J = ETA + NS, SIZE = J + NS * NS;
+};
+
+// eo = ei (x) ej (ei covers stages [i, j), ej covers [j, k)), operands in shared memory:
+// computed by a group of GS = 4 threads (row a of every output on thread a;
+// rows a >= NS idle), the intermediates exchanged through the group's scratch `sh`
+// (SCR doubles) -- the per-level latency of the scan is then a few short dependent
+// chains instead of one thread's ~700 FP64 operations.  Every thread of the warp calls
+// it (`on`: this group has a combination at this level) so the warp barriers match.
+template <int NS>
+struct ScanScr {
+  static constexpr int M = 0, G = NS * NS, H = G + NS, V = H + NS, X = V + NS * NS, Z = X + NS * NS, Y = Z + NS * NS,
+                       W = Y + NS, SIZE = W + NS * NS;
+};
+template <int NS>
+__device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a, bool on, ElRef sh,
+                                            long long* ts = nullptr) {
+#ifdef CA_RIC_PROFILE
+#define CG_TS(k) if (ts) ts[k] = clock64()
+#else
+#define CG_TS(k)
+#endif
+  CG_TS(0);
+  using L = ScanEl<NS>;
+  using S = ScanScr<NS>;
+#define Ai(k) ei[L::A + (k)]
+#define bi(k) ei[L::B + (k)]
+#define Ci(k) ei[L::C + (k)]
+#define ni(k) ei[L::ETA + (k)]
+#define Ji(k) ei[L::J + (k)]
+#define Aj(k) ej[L::A + (k)]
+#define bj(k) ej[L::B + (k)]
+#define Cj(k) ej[L::C + (k)]
+#define nj(k) ej[L::ETA + (k)]
+#define Jj(k) ej[L::J + (k)]
+  const bool row = on && a < NS;
+  // P1: row a of M = I + Ci Jj, g = bi + Ci nj, h = nj - Jj bi, V = Jj Ai
+  if (row) {
+    double gs = bi(a), hs = nj(a);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      gs = __fma_rn(Ci(a * NS + q), nj(q), gs);
+      hs = __fma_rn(-Jj(a * NS + q), bi(q), hs);
+    }
+    sh[S::G + a] = gs;
+    sh[S::H + a] = hs;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      double m = (a == c) ? 1.0 : 0.0, v = 0.0;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        m = __fma_rn(Ci(a * NS + q), Jj(q * NS + c), m);
+        v = __fma_rn(Jj(a * NS + q), Ai(q * NS + c), v);
+      }
+      sh[S::M + a * NS + c] = m;
+      sh[S::V + a * NS + c] = v;
+    }
+  }
+  CG_TS(1);
+  __syncwarp();
+  CG_TS(2);
+  // P2: T = M^-1 (Gauss-Jordan with partial pivoting, redundantly per thread); row a of
+  // X = T Ai, Z = T Ci, y = T g
+  if (row) {
+    double M[NS][NS], T[NS][NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r)
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        M[r][c] = sh[S::M + r * NS + c];
+        T[r][c] = (r == c) ? 1.0 : 0.0;
+      }
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+#pragma unroll
+      for (int r = c + 1; r < NS; ++r) {
+        const bool sw = fabs(M[r][c]) > fabs(M[c][c]);
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const double t0 = M[c][q], t1 = T[c][q];
+          M[c][q] = sw ? M[r][q] : t0;
+          M[r][q] = sw ? t0 : M[r][q];
+          T[c][q] = sw ? T[r][q] : t1;
+          T[r][q] = sw ? t1 : T[r][q];
+        }
+      }
+      const double inv = 1.0 / M[c][c];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        M[c][q] = M[c][q] * inv;
+        T[c][q] = T[c][q] * inv;
+      }
+#pragma unroll
+      for (int r = 0; r < NS; ++r) {
+        if (r == c) continue;
+        const double f = M[r][c];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          M[r][q] = __fma_rn(-f, M[c][q], M[r][q]);
+          T[r][q] = __fma_rn(-f, T[c][q], T[r][q]);
+        }
+      }
+    }
+    double Ta[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {  // row a of T (a run-time index: select, no local array)
+      double v = 0.0;
+#pragma unroll
+      for (int r = 0; r < NS; ++r) v = (r == a) ? T[r][q] : v;
+      Ta[q] = v;
+    }
+    double sy = 0.0;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) sy = __fma_rn(Ta[q], sh[S::G + q], sy);
+    sh[S::Y + a] = sy;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      double sx = 0.0, sz = 0.0;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        sx = __fma_rn(Ta[q], Ai(q * NS + c), sx);
+        sz = __fma_rn(Ta[q], Ci(q * NS + c), sz);
+      }
+      sh[S::X + a * NS + c] = sx;
+      sh[S::Z + a * NS + c] = sz;
+    }
+  }
+  CG_TS(3);
+  __syncwarp();
+  // P3: rows a of A_ik = Aj X, b_ik = Aj y + bj, W = Aj Z, eta_ik = X^T h + ni,
+  // J_ik = sym(X^T V) + Ji
+  if (row) {
+    double sb = bj(a);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) sb = __fma_rn(Aj(a * NS + q), sh[S::Y + q], sb);
+    eo[L::B + a] = sb;
+    double se = ni(a);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) se = __fma_rn(sh[S::X + q * NS + a], sh[S::H + q], se);
+    eo[L::ETA + a] = se;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      double sa = 0.0, sw = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        sa = __fma_rn(Aj(a * NS + q), sh[S::X + q * NS + c], sa);
+        sw = __fma_rn(Aj(a * NS + q), sh[S::Z + q * NS + c], sw);
+        s1 = __fma_rn(sh[S::X + q * NS + a], sh[S::V + q * NS + c], s1);
+        s2 = __fma_rn(sh[S::X + q * NS + c], sh[S::V + q * NS + a], s2);
+      }
+      eo[L::A + a * NS + c] = sa;
+      sh[S::W + a * NS + c] = sw;
+      eo[L::J + a * NS + c] = 0.5 * (s1 + s2) + Ji(a * NS + c);
+    }
+  }
+  CG_TS(4);
+  __syncwarp();
+  // P4: row a of C_ik = sym(W Aj^T) + Cj
+  if (row) {
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        s1 = __fma_rn(sh[S::W + a * NS + q], Aj(c * NS + q), s1);
+        s2 = __fma_rn(sh[S::W + c * NS + q], Aj(a * NS + q), s2);
+      }
+      eo[L::C + a * NS + c] = 0.5 * (s1 + s2) + Cj(a * NS + c);
+    }
+  }
+  CG_TS(5);
+#undef Ai
+#undef bi
+#undef Ci
+#undef ni
+#undef Ji
+#undef Aj
+#undef bj
+#undef Cj
+#undef nj
+#undef Jj
+#undef CG_TS
+}
+
+// threads per scan element (rows of the combination)
+constexpr int SCAN_GS = 4;
+__host__ __device__ inline long long riccati_scan_smem_doubles(int N, int NS, int NU, bool dyn_pt) {
+  const int EL = 3 * NS * NS + 2 * NS;
+  const int SCR = NS * NS * 5 + 3 * NS;        // ScanScr<NS>::SIZE
+  const int PHI = NS * NS + NS;                // closed-loop map of a stage
+  const long long S = scan_stride(N + 1, NS);  // field-major stage stride
+  return riccati_smem_doubles(N, NS, NU, dyn_pt) + 2LL * EL * S + (long long)SCR * S + (long long)N * PHI +
+         (long long)(N + 1) * NS + 2LL * N + NS * NS + 2LL * (N + 1) * NS;
+}
+// the scene's records staged as one block when they fit (see k_riccati_scan)
+__host__ __device__ inline long long riccati_scan_rec_doubles(long long nrec, int rec) { return nrec * rec; }
+
+// One CTA per scene, blockDim = SCAN_GS * (N + 1) rounded up to a multiple of 32.
+// Shared memory: k_riccati's layout (stage blocks, statistics, dynamics, gains), then two
+// element buffers, the combination scratch, the closed-loop maps, the states, and the
+// per-stage box residuals.
+template <int NS, int NU>
+__global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* dst_cur, double* dst_prev,
+                               int stage_recs) {
+  extern __shared__ double rsm[];
+  const int b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+  if (!scene_on(P, b)) return;  // stopped scene (ca_admm_solve)
+  const int N = P.N;
+  constexpr int SB = NS * NS + NS, DB = NS * NS + NS * NU + NS, EL = ScanEl<NS>::SIZE, SCR = ScanScr<NS>::SIZE,
+                PHI = NS * NS + NS;
+  using L = ScanEl<NS>;
+  double* sstg = rsm;                         // [N][SB]
+  double* sst = sstg + (long long)N * SB;     // [N][NSTAT]
+  double* sdyn = sst + (long long)NSTAT * N;  // [nd][DB]
+  const int nd = P.dyn_pt ? N : 1;
+  double* ric = sdyn + (long long)nd * DB;    // [N][NU][NS+1]
+  const int SS = scan_stride(N + 1, NS);         // field-major: element field k of stage t at [k * SS + t]
+  double* E0 = ric + (long long)N * NU * (NS + 1);
+  double* E1 = E0 + (long long)EL * SS;
+  double* scr = E1 + (long long)EL * SS;         // [SCR][SS]
+  double* phi = scr + (long long)SCR * SS;       // [N][PHI]: x_{t+1} = Phi_t x_t + phi_t
+  double* xs = phi + (long long)N * PHI;         // [N+1][NS]
+  double* rbx = xs + (long long)(N + 1) * NS;    // [N] box residual of stage t
+  double* sQs = rbx + 2LL * N;                   // Qs, this scene's s_ref and s rows
+  double* ssref = sQs + NS * NS;
+  double* ss_ = ssref + (long long)(N + 1) * NS;
+  double* srec = ss_ + (long long)(N + 1) * NS;  // stage_recs: this scene's records
+#ifdef CA_RIC_PROFILE
+  long long tp[8];
+  int np_ = 0;
+#define RIC_TS() (tp[np_++] = clock64())
+#else
+#define RIC_TS() ((void)0)
+#endif
+  RIC_TS();
+  // (1) bulk copies into shared memory (8 loads in flight per thread, all threads):
+  // this scene's records (one contiguous block in the sweep's layout, when stage_recs),
+  // Qs, s_ref and s rows, and the dynamics -- then the stage blocks from shared memory
+  auto bulk = [&](double* dst, const double* __restrict__ src, long long tot) {
+    constexpr int U = 8;
+    for (long long k0 = tid; k0 < tot; k0 += (long long)nth * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long k = k0 + (long long)nth * u;
+        v[u] = (k < tot) ? __ldg(src + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long k = k0 + (long long)nth * u;
+        if (k < tot) dst[k] = v[u];
+      }
+    }
+  };
+  const long long per_scene = (long long)P.NG * P.nchunkG * P.TG;  // records of one scene
+  if (stage_recs) bulk(srec, recs + (long long)b * per_scene * P.rec, per_scene * P.rec);
+  bulk(sQs, P.Qs, NS * NS);
+  bulk(ssref, P.sref + (long long)b * (N + 1) * NS, (long long)(N + 1) * NS);
+  bulk(ss_, P.s + (long long)b * (N + 1) * NS, (long long)(N + 1) * NS);
+  {
+    const long long idx0 = P.dyn_ps ? (long long)b * nd : 0;
+    auto stage_dyn = [&](const double* __restrict__ src, int blk, int off) {
+      constexpr int U = 8;  // loads in flight per thread before their stores
+      const int tot = nd * blk;
+      for (int k0 = tid; k0 < tot; k0 += nth * U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + nth * u;
+          v[u] = (k < tot) ? __ldg(src + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + nth * u;
+          if (k < tot) sdyn[(k / blk) * DB + off + k % blk] = v[u];
+        }
+      }
+    };
+    stage_dyn(P.dynA + idx0 * NS * NS, NS * NS, 0);
+    stage_dyn(P.dynB + idx0 * NS * NU, NS * NU, NS * NS);
+    stage_dyn(P.dync + idx0 * NS, NS, NS * NS + NS * NU);
+  }
+  __syncthreads();
+  // stage blocks: thread t sums the records of timestep t+1 in chunk order
+  for (int t = tid; t < N; t += nth) {
+    double ra[RECMAX];
+#pragma unroll
+    for (int f = 0; f < RECMAX; ++f) ra[f] = 0.0;
+    const long long q = (long long)b * N + t;
+    const int RC = P.rec, fm = P.nagg + S_PMAX;
+    const long long rb0 = (long long)b * per_scene;
+    for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
+      const double* r0 = stage_recs ? srec + (rec_index(P, b, t + 1, c) - rb0) * RC
+                                    : recs + (nchunk ? rec_index(P, b, t + 1, c) : q) * RC;
+#pragma unroll
+      for (int f = 0; f < RECMAX; ++f) {
+        if (f >= RC) continue;
+        const double v0 = r0[f];
+        ra[f] = (f == fm) ? fmax(ra[f], v0) : ra[f] + v0;
+      }
+    }
+    stage_assemble(P, q, ra, sstg + (long long)t * SB, sst + (long long)NSTAT * t, sQs, ssref, ss_);
+  }
+  __syncthreads();
+  RIC_TS();
+  // control weights R = 2 Qu + rho_b (bounded controls), shared by all stages
+  double Rm[NU][NU], urho[NU];
+#pragma unroll
+  for (int a = 0; a < NU; ++a) {
+    const double lo = P.box ? P.box_lim[2 * NS + a] : -INFINITY, hi = P.box ? P.box_lim[2 * NS + NU + a] : INFINITY;
+    urho[a] = (P.box && box_on(lo, hi)) ? P.box_rho : 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < NU; ++a)
+#pragma unroll
+    for (int c = 0; c < NU; ++c) Rm[a][c] = 2.0 * P.Qu[a * NU + c] + ((a == c) ? urho[a] : 0.0);
+  QuuSolve<NU> rs;
+  rs.factor(Rm);
+  // (2) elements
+  for (int t = tid; t <= N; t += nth) {
+    const ElRef e{E0 + t, SS};
+    if (t < N) {
+      const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
+      const double* Bm = A + NS * NS;
+      const double* cv = Bm + NS * NU;
+      // u0 = -R^-1 r_t (box block's linear control term), C = B R^-1 B^T
+      double u0[NU];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) {
+        const long long ku = ((long long)b * N + t) * NU + a;
+        u0[a] = (urho[a] != 0.0) ? urho[a] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;  // -r_t
+      }
+      rs.apply(u0);
+      double RB[NU][NS];  // R^-1 B^T
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double col[NU];
+#pragma unroll
+        for (int a = 0; a < NU; ++a) col[a] = Bm[c * NU + a];
+        rs.apply(col);
+#pragma unroll
+        for (int a = 0; a < NU; ++a) RB[a][c] = col[a];
+      }
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        double s = cv[a];
+#pragma unroll
+        for (int q = 0; q < NU; ++q) s = __fma_rn(Bm[a * NU + q], u0[q], s);
+        e[L::B + a] = s;
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+          e[L::A + a * NS + c] = A[a * NS + c];
+          double v = 0.0;
+#pragma unroll
+          for (int q = 0; q < NU; ++q) v = __fma_rn(Bm[a * NU + q], RB[q][c], v);
+          e[L::C + a * NS + c] = v;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NS * NS; ++k) e[L::A + k] = e[L::C + k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e[L::B + k] = 0.0;
+    }
+    if (t >= 1) {  // stage cost 1/2 s^T H_t s + h_t^T s  ->  J = H_t, eta = -h_t
+      const double* in = sstg + (long long)(t - 1) * SB;
+#pragma unroll
+      for (int k = 0; k < NS * NS; ++k) e[L::J + k] = in[k];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e[L::ETA + k] = -in[NS * NS + k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < NS * NS; ++k) e[L::J + k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) e[L::ETA + k] = 0.0;
+    }
+  }
+  __syncthreads();
+  RIC_TS();
+  // (3) suffix scan: e_t <- e_t (x) e_{t+1} (x) ... (x) e_N, SCAN_GS threads per element
+  double* cur = E0;
+  double* nxt = E1;
+  const int per = nth / SCAN_GS;
+  const int gi = tid / SCAN_GS, ga = tid % SCAN_GS;
+  for (int d = 1; d <= N; d <<= 1) {
+    for (int e0 = 0; e0 <= N; e0 += per) {
+      const int t = e0 + gi;
+      const bool have = t <= N, on = have && t + d <= N;
+      if (have && !on) {  // no partner: carried over
+        const ElRef ei{cur + t, SS}, eo{nxt + t, SS};
+        for (int k = ga; k < EL; k += SCAN_GS) eo[k] = ei[k];
+      }
+      const int tc = have ? t : 0;
+      const int tj = on ? t + d : tc;
+#ifdef CA_RIC_PROFILE
+      long long cg[6] = {0, 0, 0, 0, 0, 0};
+      scan_comb_g<NS>(ElRef{cur + tc, SS}, ElRef{cur + tj, SS}, ElRef{nxt + tc, SS}, ga, on, ElRef{scr + tc, SS}, cg);
+      if (tid == 0 && b == 0 && d == 1)
+        printf("comb cycles: P1 %lld sync %lld P2 %lld P3 %lld P4 %lld\n", cg[1] - cg[0], cg[2] - cg[1], cg[3] - cg[2],
+               cg[4] - cg[3], cg[5] - cg[4]);
+#else
+      scan_comb_g<NS>(ElRef{cur + tc, SS}, ElRef{cur + tj, SS}, ElRef{nxt + tc, SS}, ga, on, ElRef{scr + tc, SS});
+#endif
+    }
+    __syncthreads();
+    double* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  RIC_TS();
+  // (4) gains of every stage from P_{t+1} = J, p_{t+1} = -eta (k_riccati's formula), and
+  // the stage's closed-loop map x_{t+1} = (A + B K) x_t + (B k + c)
+  for (int t = tid; t < N; t += nth) {
+    const ElRef e{cur + t + 1, SS};
+    const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
+    const double* Bm = A + NS * NS;
+    const double* cv = Bm + NS * NU;
+    double PA[NS][NS], PB[NS][NU], w[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double acc = -e[L::ETA + a];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) acc = __fma_rn(e[L::J + a * NS + c], cv[c], acc);
+      w[a] = acc;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(e[L::J + a * NS + k], A[k * NS + c], s);
+        PA[a][c] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < NU; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(e[L::J + a * NS + k], Bm[k * NU + c], s);
+        PB[a][c] = s;
+      }
+    }
+    double Quu[NU][NU], Qux[NU][NS], qu[NU];
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+#pragma unroll
+      for (int c = 0; c < NU; ++c) {
+        double s = 2.0 * P.Qu[a * NU + c] + ((a == c) ? urho[a] : 0.0);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PB[k][c], s);
+        Quu[a][c] = s;
+      }
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PA[k][c], s);
+        Qux[a][c] = s;
+      }
+      const long long ku = ((long long)b * N + t) * NU + a;
+      double s = (urho[a] != 0.0) ? -urho[a] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
+      qu[a] = s;
+    }
+    QuuSolve<NU> qs;
+    qs.factor(Quu);
+    double Kg[NU][NS + 1];
+#pragma unroll
+    for (int c = 0; c <= NS; ++c) {
+      double rhs[NU];
+#pragma unroll
+      for (int a = 0; a < NU; ++a) rhs[a] = (c < NS) ? Qux[a][c] : qu[a];
+      qs.apply(rhs);
+#pragma unroll
+      for (int a = 0; a < NU; ++a) {
+        Kg[a][c] = -rhs[a];
+        ric[((long long)t * NU + a) * (NS + 1) + c] = -rhs[a];
+      }
+    }
+    double* ph = phi + (long long)t * PHI;
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      double s = cv[a];
+#pragma unroll
+      for (int q = 0; q < NU; ++q) s = __fma_rn(Bm[a * NU + q], Kg[q][NS], s);
+      ph[NS * NS + a] = s;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double v = A[a * NS + c];
+#pragma unroll
+        for (int q = 0; q < NU; ++q) v = __fma_rn(Bm[a * NU + q], Kg[q][c], v);
+        ph[a * NS + c] = v;
+      }
+    }
+  }
+  __syncthreads();
+  RIC_TS();
+  // (5) forward: x_{t+1} = Phi_t x_t + phi_t from s_0 (one thread: NS independent dot
+  // products per stage, the next stage's map loaded ahead)
+  if (tid == 0) {
+    double x[NS];
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      x[a] = P.s0[b * NS + a];
+      xs[a] = x[a];
+    }
+    double pc[PHI];  // Phi_t, phi_t of the current stage (the next one is loaded meanwhile)
+#pragma unroll
+    for (int k = 0; k < PHI; ++k) pc[k] = phi[k];
+    for (int t = 0; t < N; ++t) {
+      const double* pn = phi + (long long)((t + 1 < N) ? t + 1 : t) * PHI;
+      double nx[PHI];
+#pragma unroll
+      for (int k = 0; k < PHI; ++k) nx[k] = pn[k];
+      double xn[NS];
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        double s = pc[NS * NS + a];
+#pragma unroll
+        for (int c = 0; c < NS; ++c) s = __fma_rn(pc[a * NS + c], x[c], s);
+        xn[a] = s;
+      }
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        x[a] = xn[a];
+        xs[(long long)(t + 1) * NS + a] = xn[a];
+      }
+#pragma unroll
+      for (int k = 0; k < PHI; ++k) pc[k] = nx[k];
+    }
+  }
+  __syncthreads();
+  RIC_TS();
+  // (6) every stage in parallel: u_t = K_t x_t + k_t, the trajectory, the box block's
+  // w, l update (reading #7) and its residual terms
+  const double box_res_prev = (P.box && tid == 0) ? P.box_res[b] : 0.0;
+  for (int t = tid; t <= N; t += nth) {
+    double* sb = P.s + ((long long)b * (N + 1) + t) * NS;
+#pragma unroll
+    for (int a = 0; a < NS; ++a) sb[a] = xs[(long long)t * NS + a];
+    if (t == N) continue;
+    double r = 0.0;
+#pragma unroll
+    for (int a = 0; a < NU; ++a) {
+      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], xs[(long long)t * NS + c], s);
+      const long long ku = ((long long)b * N + t) * NU + a;
+      P.u[ku] = s;
+      if (P.box && urho[a] != 0.0) {
+        const double lo = P.box_lim[2 * NS + a], hi = P.box_lim[2 * NS + NU + a];
+        r += box_update(s, lo, hi, &P.box_wu[ku], &P.box_lu[ku]);
+      }
+    }
+    if (P.box) {  // states of t + 1
+      const long long k0 = ((long long)b * (N + 1) + t + 1) * NS;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        const double lo = P.box_lim[a], hi = P.box_lim[NS + a];
+        if (box_on(lo, hi)) r += box_update(xs[(long long)(t + 1) * NS + a], lo, hi, &P.box_ws[k0 + a], &P.box_ls[k0 + a]);
+      }
+    }
+    rbx[t] = r;
+  }
+  __syncthreads();
+  // (7) per-scene statistics: thread f sums field f over the stages in order, thread
+  // NSTAT the box residuals; thread 0 writes
+  double* sred = xs;  // (states no longer needed: reuse)
+  if (tid < NSTAT) {
+    double a = 0.0;
+    for (int t = 0; t < N; ++t) a = stat_comb(tid, a, sst[(long long)NSTAT * t + tid]);
+    sred[tid] = a;
+  } else if (tid == NSTAT && P.box) {
+    double br = 0.0;
+    for (int t = 0; t < N; ++t) br += rbx[t];
+    P.box_res[b] = br;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (dst_cur)
+#pragma unroll
+      for (int f = 0; f < NSTAT; ++f)
+        if (f != S_RPRI) dst_cur[b * NSTAT + f] = sred[f];
+    if (dst_prev) dst_prev[b * NSTAT + S_RPRI] = sred[S_RPRI] + box_res_prev;
+  }
+  RIC_TS();
+#ifdef CA_RIC_PROFILE
+  if (tid == 0 && b == 0)
+    printf("ric_scan cycles: stage %lld elements %lld scan %lld gains %lld forward %lld stages+stats %lld\n",
+           tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5]);
+#endif
+#undef RIC_TS
+}
+
+}  // namespace ca
