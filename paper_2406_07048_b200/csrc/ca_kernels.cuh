@@ -25,6 +25,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Checked build (-DCA_CHECKED, profiles/checked_build.sh): device-side bounds and
+// invariant checks on the indices the per-pair kernels derive (the substitute for
+// compute-sanitizer, which this pool does not run); a failed check prints and traps,
+// so the host call returns CA_E_CUDA.  Compiled out of the product library.
+#ifdef CA_CHECKED
+#include <cstdio>
+static __device__ __noinline__ void ca_check_fail(const char* what, const char* file, int line) {
+  printf("CA_CHECK failed %s:%d: %s (block %d thread %d)\n", file, line, what, (int)blockIdx.x, (int)threadIdx.x);
+  __trap();
+}
+#define CA_CHECK(c) ((c) ? (void)0 : ca_check_fail(#c, __FILE__, __LINE__))
+#else
+#define CA_CHECK(c) ((void)0)
+#endif
 
 namespace ca {
 
@@ -256,6 +270,7 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
 #pragma unroll 8
       for (int l = 0; l < 32; ++l) acc += (stl[l] == tt) ? col0[f * 32 + l] : 0.0;
     }
+    CA_CHECK(tt < TG && f0 + f < stride);
     out[tt * stride + f0 + f] = acc;
   }
 #endif
@@ -304,6 +319,7 @@ __global__ void __launch_bounds__(CTA) k_mult(Dev P) {
   if (!(pk & PAIR_UNSENSED)) {
     int i, j;
     unpack_pair(pk, tl, i, j);
+    CA_CHECK(i < P.np && j < P.M && tl < it.nt);
     const int g = i * P.M + j, t = it.grp * P.TG + tl + 1;
     const long long bt = (long long)it.b * P.N + t - 1;
     const long long p = bt * P.G + g, PP = P.P;

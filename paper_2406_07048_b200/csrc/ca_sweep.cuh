@@ -20,6 +20,7 @@
 // pressure stay small; the pivot trace and the scaling-centre terms are a separate
 // kernel variant (TRACE).
 #pragma once
+#include <cstdlib>
 #include <mutex>
 
 #include "ca_kernels.cuh"
@@ -715,9 +716,15 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   for (int k = threadIdx.x; k < P.np * LT; k += CTA * WPC) lamtab[k] = P.lam[k];
   if (threadIdx.x < 2 * (D + 2)) cst[threadIdx.x] = (threadIdx.x == 0) ? 1.0 : 0.0;
   __syncthreads();
+#ifdef CA_CHECKED
+#define VAL(i) sval[(CA_CHECK((i) >= 0 && (i) < NMAX), (i)) * CTA]
+#define CBV(i) scb[(CA_CHECK((i) >= 0 && (i) < NMAX), (i)) * CTA]
+#define YK(i) P.y[(long long)(CA_CHECK((i) >= 0 && (i) < P.ny && p >= 0 && p < PP), (i)) * PP + p]
+#else
 #define VAL(i) sval[(i) * CTA]
 #define CBV(i) scb[(i) * CTA]
 #define YK(i) P.y[(long long)(i) * PP + p]  // y^k from HBM (L1-resident re-reads)
+#endif
 #if CA_SWEEP_PERSIST
   // persistent warps: every warp pulls (b, group, chunk) work items from a
   // counter (reset by k_sortpairs); results depend only on the item, not on which
@@ -764,6 +771,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   if (act) {
     int j;
     unpack_pair(pk, tl, ip, j);
+    CA_CHECK(ip < P.np && j < P.M && tl < it.nt && item < P.nitems);
     const int g = ip * P.M + j;
     const long long bt = (long long)b * P.N + it.grp * P.TG + tl;  // b*N + (t-1)
     po = P.pose + bt * 12;                                        // pose(s_t^k) (k_sortpairs)
@@ -772,6 +780,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
     nr = P.part_off[ip + 1] - r0;
     const int o = b * P.M + j, l0 = P.obs_off[o];
     no = P.obs_off[o + 1] - l0;
+    CA_CHECK(p < PP && no >= 1 && no <= P.nomax && nr <= P.nrmax && nr + no + 1 <= NMAX && nr + no + 1 <= P.ny);
     n = nr + no + 1;
     prow = P.part_rows + 4 * r0;
     const double* orow = P.obs_rows + 4 * (long long)l0;
@@ -1375,6 +1384,10 @@ cudaError_t sweep_launch_v(const Dev& P, unsigned grid, cudaStream_t stream) {
   }
 #if CA_SWEEP_PERSIST
   unsigned warps = (unsigned)res_dev < grid ? (unsigned)res_dev : grid;
+  // diagnostics: CA_SWEEP_WARPS caps the persistent grid (a different item-to-warp
+  // interleaving; results must not change -- tests/test_gpu_checked.py)
+  static const int cap = std::getenv("CA_SWEEP_WARPS") ? std::atoi(std::getenv("CA_SWEEP_WARPS")) : 0;
+  if (cap > 0 && (unsigned)cap < warps) warps = (unsigned)cap;
 #else
   unsigned warps = grid;
 #endif
