@@ -192,19 +192,21 @@ def algorithmic_bytes_per_sweep(sc):
 
 
 def algorithmic_flops_per_sweep(sc, pivots_per_sweep):
-    """FP64 flops of the revised Lemke sweep, FMA = 2:
-    setup per pair 2[n_o(d + d^2) + (n_r-1) d + (n-1)(d+1)]; per pivot 2(d+2)n + 2n
-    (entering column of every basic variable + right-hand-side update)."""
+    """FP64 flops of one pair sweep by SURVEY §8(d)'s model (the contract's algorithmic
+    count, FMA = 2, division = 1), per pair with n = n_r + n_o + 1 and p its pivots:
+      F0   = 2 [(n-1) n / 2 (d+1) + 2 (n-1)(d+1) + n_o d (d+1)] + 70 + 50
+             (M = Kt Kt^T and q, elimination, obstacle rows at the pose; multiplier update;
+              recovery and aggregates)
+      Fpiv = 2 n (n + 2) + n        (one pivot of the compact tableau)
+    summed over pairs with the measured mean pivots per pair."""
     d = sc.dim
     n = sc.lcp_sizes().astype(np.float64)
-    nr = np.diff(sc.part_off)
     no = np.diff(sc.obs_off).reshape(sc.n_scenes, sc.n_obs)
     no_p = np.broadcast_to(no[:, None, None, :], (sc.n_scenes, sc.horizon, sc.n_parts, sc.n_obs)).reshape(-1)
-    nr_p = np.broadcast_to(nr[None, None, :, None], (sc.n_scenes, sc.horizon, sc.n_parts, sc.n_obs)).reshape(-1)
-    setup = 2.0 * (no_p * (d + d * d) + (nr_p - 1) * d + (n - 1) * (d + 1)).sum()
-    nbar = n.mean()
-    per_pivot = 2.0 * (d + 2) * nbar + 2.0 * nbar
-    return setup + pivots_per_sweep * per_pivot
+    f0 = (2.0 * ((n - 1) * n / 2 * (d + 1) + 2 * (n - 1) * (d + 1) + no_p * d * (d + 1)) + 120.0).sum()
+    p = pivots_per_sweep / max(1, sc.n_pairs)
+    fpiv = (2.0 * n * (n + 2) + n).sum() * p
+    return f0 + fpiv
 
 
 def pinned_scene(sc):
@@ -482,12 +484,16 @@ def run_ours(args, rank, world, local):
     if frac_hbm >= frac_fp:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": frac_hbm,
                 "traffic": traffic, "peak_source": hbm_src}
-    else:
+    else:  # the FP64 vector pipe (no tensor cores: not a dense contraction)
         roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64, "unit": "TFLOP/s", "frac": frac_fp,
-                "traffic": traffic, "peak_source": "measured FP64 DFMA loop (ca_fp64_peak)"}
+                "traffic": traffic,
+                "peak_source": "measured FP64 DFMA loop on all SMs (ca_fp64_peak); unit count: 148 SMs x 64 DFMA/clk "
+                               "x 2 x 1.965 GHz = 37.2 TFLOP/s"}
     roof.update({"kernel": "k_sweep (ADMM step 1 + fused step 3)", "launch_ms": avg_sweep_ms,
+                 "flop_model": "SURVEY 8(d): 2[(n-1)n/2 (d+1) + 2(n-1)(d+1) + n_o d(d+1)] + 120 per pair + "
+                               "(2n(n+2) + n) per pivot, measured pivots",
                  "pair_solver": ("dual semismooth Newton (NEXT f4; 'pivots' = Newton iterations, the flop "
-                                 "model is the revised Lemke's, indicative only)") if args.prox_eps > 0
+                                 "model is Lemke's, indicative only)") if args.prox_eps > 0
                                 else "revised Lemke (paper-exact Eq. 19)",
                  "algorithmic_bytes_per_launch": nbytes, "algorithmic_flops_per_launch": flops,
                  "hbm_frac": frac_hbm, "fp64_frac": frac_fp, "fp64_peak_tflops": fp64,

@@ -282,14 +282,18 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
 // ist[0..4] over the lanes with tl == tt, out[.. + S_PMAX] = max of ist[0].
 __device__ __forceinline__ void group_reduce_int(int lane, int tl, int TG, double* out, int stride, const int ist[5]) {
   constexpr unsigned FULL = 0xffffffffu;
+  const bool anyfail = __any_sync(FULL, ist[1] != 0);  // failures are rare: their kinds only then
   for (int tt = 0; tt < TG; ++tt) {
     const bool mine = tl == tt;
     const int piv = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[0] : 0u);
-    const int fl = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[1] : 0u);
-    const int ry = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[2] : 0u);
-    const int it = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[3] : 0u);
-    const int ng = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[4] : 0u);
     const int pm = (int)__reduce_max_sync(FULL, mine ? (unsigned)ist[0] : 0u);
+    int fl = 0, ry = 0, it = 0, ng = 0;
+    if (anyfail) {
+      fl = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[1] : 0u);
+      ry = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[2] : 0u);
+      it = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[3] : 0u);
+      ng = (int)__reduce_add_sync(FULL, mine ? (unsigned)ist[4] : 0u);
+    }
     if (lane == tt) {
       double* o = out + (long long)tt * stride;
       o[S_PIV] = piv;
