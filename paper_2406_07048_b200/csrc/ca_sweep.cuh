@@ -34,6 +34,14 @@
 #define CA_EXP_M12 0  // 1: exact m = 1, 2 specialisations of the structural solve (-5 % instructions,
                       // +7 % time: the larger pivot loop misses the instruction cache, profiles/r02)
 #endif
+#ifndef CA_EXP_COLD
+#define CA_EXP_COLD 1  // rare branches of the pivot loop marked unlikely (cold-code placement: -0.3..1 %)
+#endif
+#if CA_EXP_COLD
+#define CA_RARE(c) __builtin_expect(!!(c), 0)
+#else
+#define CA_RARE(c) (c)
+#endif
 #ifndef CA_EXP_MU_PIPE
 #define CA_EXP_MU_PIPE 0
 #endif
@@ -925,8 +933,8 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       uint32_t pend = 0;  // rows still owing the previous pivot's value update
       double ve2p = 0.0;
       for (;;) {
-        if (pivots >= maxpiv) { status = ST_ITER; break; }
-        if (n - __popc(wb) > D + 4) { status = ST_ITER; break; }  // rank bound (cannot happen exactly)
+        if (CA_RARE(pivots >= maxpiv)) { status = ST_ITER; break; }
+        if (CA_RARE(n - __popc(wb) > D + 4)) { status = ST_ITER; break; }  // rank bound (cannot happen exactly)
         // structural m x m system: registers for m <= 3, generic solver otherwise
         SmallSol<D> ss;  // @region solve_call
         bool small = true;
@@ -942,7 +950,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         small = solve_small<D>(W, wb, zb, z0b, ent, ss);
 #endif
         double* Gp = Gslow;
-        if (!small) {
+        if (CA_RARE(!small)) {
           // the first GSLOTS lanes of the warp needing it use shared memory
           const unsigned am = __activemask();
           const int slot = __popc(am & ((1u << tid) - 1u));
@@ -1091,15 +1099,15 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
         const double thr = ptol * fmax(1.0, cmax);
         // rare: the provisional minimiser is not eligible (pivot_tol < cbar <= thr):
         // the dense-tableau solve takes the exact L5 decision
-        if (bn < kInf && !(bd > thr)) { status = ST_TIE; break; }
-        if (!(bn < kInf)) { status = ST_RAY; break; }
+        if (CA_RARE(bn < kInf && !(bd > thr))) { status = ST_TIE; break; }
+        if (CA_RARE(!(bn < kInf))) { status = ST_RAY; break; }
         const double thmin = bn / bd;
         const double tt = thmin + tau * fmax(1.0, thmin);
         // tie set (L5.2): filter the candidates against the final minimum.  A lone
         // candidate is the minimising row itself (eligible: checked above), so the
         // filter only runs on real near-ties.
         uint32_t tiem = cand;
-        if (__popc(cand) > 1) {
+        if (CA_RARE(__popc(cand) > 1)) {
           tiem = 0;
 #pragma unroll 1
           for (uint32_t bb = cand; bb; bb &= bb - 1) {
@@ -1122,7 +1130,7 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
           // solve, which applies the oracle's rules verbatim; ties are rare (none in
           // 3000 sampled C5 pairs) and keeping the rule out of the pivot loop keeps
           // its register footprint small
-          if (__popc(tiem) > 1) { status = ST_TIE; break; }
+          if (CA_RARE(__popc(tiem) > 1)) { status = ST_TIE; break; }
           lm = __ffs(tiem) - 1;
           cr = CBV(lm);
           vr = VAL(lm);
