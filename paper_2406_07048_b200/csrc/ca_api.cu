@@ -1447,7 +1447,9 @@ ca_status iterate_impl(ca_problem* h, int32_t iters, ca_residuals* hist) {
   if (iters > h->slots_cap) h->drop_graph();  // slot buffers are reallocated
   if ((st = ensure_slots(h, iters))) return st;
   if ((st = flush_timing(h))) return st;
-  const bool graph = h->use_graphs && !h->timing && !h->comm && !h->comm_all && h->dev.dbg_p < 0 && !h->dev.active;
+  // the per-iteration NCCL collectives are captured too (NCCL supports stream capture):
+  // the sharded iteration replays as one graph like the single-GPU one
+  const bool graph = h->use_graphs && !h->timing && h->dev.dbg_p < 0 && !h->dev.active;
   if ((st = graph ? launch_iterations_graph(h, iters) : enqueue_iterations(h, iters))) return st;
   if (!hist) {
     CUDA_TRY(cudaStreamSynchronize(h->stream));
