@@ -177,17 +177,24 @@ def hbm_peak():
 
 
 def algorithmic_bytes_per_sweep(sc):
-    """HBM bytes one pair-sweep launch must move: per pair read
-    y^k (n_p doubles), zeta, xi (1+d) and write y^{k+1}, zeta, xi (fused multiplier
-    update) + a 4-byte pivot/status word; per scene the obstacle faces once
-    ((d+1) doubles per face); per (scene, t, chunk) one 20-double record."""
+    """HBM bytes one pair-sweep launch must move: per pair read y^k (n_p
+    doubles), zeta, xi (1+d) and write y^{k+1}, zeta, xi (fused multiplier update) + a
+    4-byte pivot/status word; per scene the obstacle faces once ((d+1) doubles per face);
+    one record of (d+1)(d+2)/2 + (d+1) + 8 doubles per (work item, timestep slot) -- the
+    library's layout: sort pools of TG timesteps (TG = min(8, 800 // (parts x obstacles))
+    when the sweep spans >= 10000 items of 32 pairs, else 1), chunks of 32 pairs."""
     n = sc.lcp_sizes().astype(np.float64)
     d = sc.dim
     per_pair = 16.0 * n.sum() + sc.n_pairs * (16.0 * (1 + d) + 4.0)
     faces = float(sc.obs_off[-1]) * 8.0 * (d + 1)
     G = sc.n_parts * sc.n_obs
-    nchunk = max(1, -(-G // 32))  # one-warp CTAs
-    recs = sc.n_scenes * sc.horizon * nchunk * 20 * 8.0
+    nchunk = max(1, -(-G // 32))
+    items1 = sc.n_scenes * sc.horizon * nchunk
+    TG = min(8, max(1, min(sc.horizon, 800 // max(1, G)))) if items1 >= 10000 else 1
+    NG = -(-sc.horizon // TG)
+    nchunkG = -(-(TG * max(1, G)) // 32)
+    rec = (d + 1) * (d + 2) // 2 + (d + 1) + 8
+    recs = sc.n_scenes * NG * nchunkG * TG * rec * 8.0
     return per_pair + faces + recs
 
 
