@@ -74,6 +74,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--prox-eps", type=float, default=0.0,
                     help="reading #2 proximal term (0 = paper-exact Eq. 19); > 0 runs the NEXT f4 dual Newton")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="at one GPU, run the --shard mode's multi-GPU code path anyway (NCCL communicator of one "
+                         "rank; scenes mode sets CA_FORCE_SCENE_GRID=1 so the per-iteration scene exchange runs)")
     return ap.parse_args()
 
 
@@ -364,7 +367,7 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     cfg = args.config
-    mode = args.shard if world > 1 else "single"
+    mode = args.shard if world > 1 or args.force_dist else "single"
     if cfg != 5 and mode == "scenes":
         mode = "obstacles"  # one scene: its obstacles are what can be split
     if mode in ("scenes", "obstacles"):
@@ -373,9 +376,12 @@ def run_ours(args, rank, world, local):
         # per ADMM iteration over NCCL
         sc = make_scene(cfg, 0, args.scenes)
         nid = ca.nccl_unique_id() if rank == 0 else None
-        box = [nid]
-        dist.broadcast_object_list(box, src=0)
-        nid = box[0]
+        if world > 1:
+            box = [nid]
+            dist.broadcast_object_list(box, src=0)
+            nid = box[0]
+        elif mode == "scenes":
+            os.environ["CA_FORCE_SCENE_GRID"] = "1"
         grid = (world, 1) if mode == "scenes" else (1, world)
         g = ca.Problem(sc, device=local, stream=stream.cuda_stream, dist=(world, rank, nid, *grid),
                        workspace="torch", prox_eps=args.prox_eps)
@@ -522,7 +528,8 @@ def run_ours(args, rank, world, local):
         "config": {"workload": workload_name(cfg, sc.n_scenes, iters, args.prox_eps, per_gpu=mode == "weak"),
                    "scenes_total": sc.n_scenes * units, "scenes_per_gpu": sc_local.n_scenes,
                    "admm_iters": iters, "pair_qps_per_iter_per_gpu": sc_local.n_pairs, "parallelism": par,
-                   "l2": "inputs larger than L2 (resident iterate %.1f GB per GPU)" % (g.device_bytes / 1e9)},
+                   "l2": "inputs larger than L2 (resident iterate %.1f GB per GPU)" % (g.device_bytes / 1e9),
+                   **({"force_dist": True} if args.force_dist and world == 1 else {})},
         "admm_solves_per_sec": solves,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,

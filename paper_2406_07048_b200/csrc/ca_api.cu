@@ -100,6 +100,9 @@ struct ca_problem {
   ncclComm_t comm = nullptr, comm_all = nullptr;
   int world = 1, rank = 0, j0 = 0, j1 = 0, n_obs_full = 0;
   int Ws = 1, Wo = 1, rs = 0, ro = 0, b0 = 0, B_total = 0;
+  // the per-iteration scene-statistics exchange is on (scene_shards > 1; at world 1 only with
+  // CA_FORCE_SCENE_GRID=1, which runs the scene-sharded code path on one rank for testing)
+  bool scene_xchg = false;
   double* glob = nullptr;  // scene-sharded: [slots_cap][B_total][NST] allreduced statistics
   double* pmx = nullptr;   // [max(B*N, B)] S_PMAX column for the max-allreduce
   // ca_admm_solve (Eq. 18 per scene)
@@ -785,7 +788,7 @@ ca_status ensure_slots(ca_problem* h, int n) {
   ca_status st;
   if ((st = h->alloc(&h->slots, (size_t)n * h->B * NST))) return st;
   if ((st = h->alloc(&h->hist_dev, (size_t)n * NST))) return st;
-  if (h->Ws > 1 && (st = h->alloc(&h->glob, (size_t)n * h->B_total * NST))) return st;
+  if (h->scene_xchg && (st = h->alloc(&h->glob, (size_t)n * h->B_total * NST))) return st;
   h->slots_cap = n;
   return CA_OK;
 }
@@ -862,6 +865,8 @@ void set_grid(ca_problem* h, const GridPos* g) {
   h->j1 = g->j1;
   h->n_obs_full = g->M_full;
   h->M_full = g->M_full;
+  const char* fg = std::getenv("CA_FORCE_SCENE_GRID");
+  h->scene_xchg = g->Ws > 1 || (g->world == 1 && fg && fg[0] == '1');
 }
 
 // Host-side setup of a handle: shapes, work decomposition and every device buffer
@@ -1211,7 +1216,7 @@ ca_status ca_problem_create_dist(const ca_problem_desc* D, const ca_dist_desc* d
     delete h;
     return fail(CA_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
-  if (g.Ws == 1) {
+  if (!h->scene_xchg) {
     h->comm = world;  // one scene shard: the world is the obstacle group
   } else {
     h->comm_all = world;
@@ -1535,6 +1540,24 @@ ca_status solve_impl(ca_problem* h, ca_solve_report* out) {
   }
   rep.iterations = h->comm_all ? done_iters : mx;
   rep.converged = conv;
+  if (h->comm_all) {  // statistics of every scene of every rank (each scene counted once)
+    double c[NST] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (h->ro == 0) {
+      c[ca::S_RDUAL] = rep.last.r_dual;
+      c[ca::S_RPRI] = rep.last.r_pri;
+      c[ca::S_PIV] = (double)rep.last.pivots;
+      c[ca::S_FAIL] = (double)rep.last.n_fail;
+      c[ca::S_RAY] = (double)rep.last.n_ray;
+      c[ca::S_ITER] = (double)rep.last.n_iterlimit;
+      c[ca::S_NEGYE] = (double)rep.last.n_neg_ye;
+      c[ca::S_PMAX] = (double)rep.last.max_pivots;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->tmpB, c, sizeof(c), cudaMemcpyHostToDevice, h->stream));
+    if ((st = allreduce_stats(h, h->tmpB, 1, h->comm_all))) return st;
+    CUDA_TRY(cudaMemcpyAsync(c, h->tmpB, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    fill_res(c, h->P, &rep.last);
+  }
   if (h->comm_all) {  // global: every scene of every rank
     int c = conv;
     int* dc = h->d_remaining;

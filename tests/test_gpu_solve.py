@@ -461,3 +461,39 @@ def test_c5_failures_reconciled_with_oracle(ca):
     print("C5 K=100 failed pair solves (iteration, pair, gpu status, oracle status):", seen)
     for k, p, sg, so in seen:
         assert sg == so, (k, p, sg, so)
+
+
+# ---------------------------------------------------------------------------
+# the scene-sharded code path (scene_shards > 1) run on one rank
+# ---------------------------------------------------------------------------
+
+def test_forced_scene_grid_matches_plain(ca, monkeypatch):
+    """CA_FORCE_SCENE_GRID=1 at world 1 runs the scene-shard machinery (the [B][8]
+    per-scene table allreduced every iteration, the global stop count, the global
+    final statistics) with one rank: results must equal the plain handle's -- the
+    trajectory bit for bit (the exchange only moves statistics), the summed
+    statistics to rounding order, the per-scene stop identical."""
+    sc = case("c5x16")
+    plain = ca.Problem(sc)
+    monkeypatch.setenv("CA_FORCE_SCENE_GRID", "1")
+    forced = ca.Problem(sc, dist=(1, 0, ca.nccl_unique_id(), 1, 1))
+    monkeypatch.delenv("CA_FORCE_SCENE_GRID")
+    _, ha = plain.admm_iterate(12)
+    _, hb = forced.admm_iterate(12)
+    for f in ha:
+        if not f.startswith("ms_"):
+            close(hb[f], ha[f], 1e-12, f"hist {f}")
+    for a, b in zip(plain.trajectory(), forced.trajectory()):
+        assert np.array_equal(a, b)
+    for a, b in zip(plain.scene_residuals(), forced.scene_residuals()):
+        assert np.array_equal(a, b)
+    plain.reset_iterate()
+    forced.reset_iterate()
+    _, ra, ia, ca_ = plain.admm_solve()
+    _, rb, ib, cb = forced.admm_solve()
+    assert np.array_equal(ia, ib) and np.array_equal(ca_, cb)
+    assert ra["iterations"] == rb["iterations"] and ra["converged"] == rb["converged"]
+    for f in ("r_pri", "r_dual", "pivots", "n_fail", "max_pivots", "n_pairs"):
+        close(rb[f], ra[f], 1e-12, f"solve {f}")
+    for a, b in zip(plain.trajectory(), forced.trajectory()):
+        assert np.array_equal(a, b)
