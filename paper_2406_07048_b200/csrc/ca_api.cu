@@ -538,17 +538,27 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
     if (stage_recs) sms += srec;
     static const bool scan_on = !(std::getenv("CA_RICCATI_SCAN") && std::getenv("CA_RICCATI_SCAN")[0] == '0');
     if (scan_on && sms <= 200 * 1024 && ca::SCAN_GS * (h->N + 1) <= 1024 && h->N >= 16) {
+      int tmax = 0;
       {
         static std::mutex mu;
         static size_t configured[CA_MAX_DEVICES] = {};
+        // one group of SCAN_GS threads per stage, capped by what the kernel's register
+        // count allows in one CTA (the kernel strides over the stages when fewer)
+        static int max_threads[CA_MAX_DEVICES] = {};
         if (h->device >= CA_MAX_DEVICES) return fail(CA_E_CUDA, "device ordinal too large");
         std::lock_guard<std::mutex> lk(mu);
         if (sms > 48 * 1024 && sms > configured[h->device]) {
           CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati_scan<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms));
           configured[h->device] = sms;
         }
+        if (!max_threads[h->device]) {
+          cudaFuncAttributes fa;
+          CUDA_TRY(cudaFuncGetAttributes(&fa, ca::k_riccati_scan<NS, NU>));
+          max_threads[h->device] = fa.maxThreadsPerBlock & ~31;
+        }
+        tmax = max_threads[h->device];
       }
-      const int threads = 32 * ((ca::SCAN_GS * (h->N + 1) + 31) / 32);
+      const int threads = std::min(tmax, 32 * ((ca::SCAN_GS * (h->N + 1) + 31) / 32));
       ca::k_riccati_scan<NS, NU><<<(unsigned)h->B, threads, sms, h->stream>>>(h->dev, recs, nchunk, cur, prev,
                                                                              stage_recs);
       CUDA_TRY(cudaGetLastError());

@@ -47,12 +47,130 @@ struct ScanEl {
   static constexpr int A = 0, B = NS * NS, C = B + NS, ETA = C + NS * NS, J = ETA + NS, SIZE = J + NS * NS;
 };
 
+// T = M^-1 of a small matrix (NS <= 4) in closed form: the adjugate over one reciprocal
+// of the determinant (2 x 2 minors for NS = 4) -- no pivoting, no data-dependent control,
+// every entry independent.  M = I + C_ij J_jk has real eigenvalues >= 1 (C, J symmetric
+// positive semidefinite), so det M >= 1.  CA_SCAN_INV_GE=1 selects Gauss-Jordan with
+// partial pivoting instead (C4 primal step 42.8 vs 39.9 us with the adjugate; kept for A/B).
+template <int NS>
+__device__ __forceinline__ void scan_inverse(const double (&m)[NS][NS], double (&t)[NS][NS]) {
+#if defined(CA_SCAN_INV_GE) && CA_SCAN_INV_GE
+  double M[NS][NS];
+#pragma unroll
+  for (int r = 0; r < NS; ++r)
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      M[r][c] = m[r][c];
+      t[r][c] = (r == c) ? 1.0 : 0.0;
+    }
+#pragma unroll
+  for (int c = 0; c < NS; ++c) {
+#pragma unroll
+    for (int r = c + 1; r < NS; ++r) {
+      const bool sw = fabs(M[r][c]) > fabs(M[c][c]);
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        const double t0 = M[c][q], t1 = t[c][q];
+        M[c][q] = sw ? M[r][q] : t0;
+        M[r][q] = sw ? t0 : M[r][q];
+        t[c][q] = sw ? t[r][q] : t1;
+        t[r][q] = sw ? t1 : t[r][q];
+      }
+    }
+    const double inv = 1.0 / M[c][c];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      M[c][q] = M[c][q] * inv;
+      t[c][q] = t[c][q] * inv;
+    }
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      if (r == c) continue;
+      const double f = M[r][c];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        M[r][q] = __fma_rn(-f, M[c][q], M[r][q]);
+        t[r][q] = __fma_rn(-f, t[c][q], t[r][q]);
+      }
+    }
+  }
+#else
+  if constexpr (NS == 1) {
+    t[0][0] = 1.0 / m[0][0];
+  } else if constexpr (NS == 2) {
+    const double inv = 1.0 / __fma_rn(m[0][0], m[1][1], -m[0][1] * m[1][0]);
+    t[0][0] = m[1][1] * inv;
+    t[0][1] = -m[0][1] * inv;
+    t[1][0] = -m[1][0] * inv;
+    t[1][1] = m[0][0] * inv;
+  } else if constexpr (NS == 3) {
+    double a[3][3];  // adjugate
+    a[0][0] = __fma_rn(m[1][1], m[2][2], -m[1][2] * m[2][1]);
+    a[0][1] = __fma_rn(m[0][2], m[2][1], -m[0][1] * m[2][2]);
+    a[0][2] = __fma_rn(m[0][1], m[1][2], -m[0][2] * m[1][1]);
+    a[1][0] = __fma_rn(m[1][2], m[2][0], -m[1][0] * m[2][2]);
+    a[1][1] = __fma_rn(m[0][0], m[2][2], -m[0][2] * m[2][0]);
+    a[1][2] = __fma_rn(m[0][2], m[1][0], -m[0][0] * m[1][2]);
+    a[2][0] = __fma_rn(m[1][0], m[2][1], -m[1][1] * m[2][0]);
+    a[2][1] = __fma_rn(m[0][1], m[2][0], -m[0][0] * m[2][1]);
+    a[2][2] = __fma_rn(m[0][0], m[1][1], -m[0][1] * m[1][0]);
+    const double det = __fma_rn(m[0][0], a[0][0], __fma_rn(m[0][1], a[1][0], m[0][2] * a[2][0]));
+    const double inv = 1.0 / det;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) t[r][c] = a[r][c] * inv;
+  } else {
+    static_assert(NS == 4, "scan_inverse: NS <= 4");
+    const double s0 = __fma_rn(m[0][0], m[1][1], -m[1][0] * m[0][1]);
+    const double s1 = __fma_rn(m[0][0], m[1][2], -m[1][0] * m[0][2]);
+    const double s2 = __fma_rn(m[0][0], m[1][3], -m[1][0] * m[0][3]);
+    const double s3 = __fma_rn(m[0][1], m[1][2], -m[1][1] * m[0][2]);
+    const double s4 = __fma_rn(m[0][1], m[1][3], -m[1][1] * m[0][3]);
+    const double s5 = __fma_rn(m[0][2], m[1][3], -m[1][2] * m[0][3]);
+    const double c5 = __fma_rn(m[2][2], m[3][3], -m[3][2] * m[2][3]);
+    const double c4 = __fma_rn(m[2][1], m[3][3], -m[3][1] * m[2][3]);
+    const double c3 = __fma_rn(m[2][1], m[3][2], -m[3][1] * m[2][2]);
+    const double c2 = __fma_rn(m[2][0], m[3][3], -m[3][0] * m[2][3]);
+    const double c1 = __fma_rn(m[2][0], m[3][2], -m[3][0] * m[2][2]);
+    const double c0 = __fma_rn(m[2][0], m[3][1], -m[3][0] * m[2][1]);
+    const double det = (s0 * c5 - s1 * c4) + (s2 * c3 + s3 * c2) + (s5 * c0 - s4 * c1);
+    const double inv = 1.0 / det;
+    auto e3 = [](double x0, double y0, double x1, double y1, double x2, double y2) {
+      return __fma_rn(x2, y2, __fma_rn(x1, y1, x0 * y0));
+    };
+    t[0][0] = e3(m[1][1], c5, -m[1][2], c4, m[1][3], c3) * inv;
+    t[0][1] = e3(-m[0][1], c5, m[0][2], c4, -m[0][3], c3) * inv;
+    t[0][2] = e3(m[3][1], s5, -m[3][2], s4, m[3][3], s3) * inv;
+    t[0][3] = e3(-m[2][1], s5, m[2][2], s4, -m[2][3], s3) * inv;
+    t[1][0] = e3(-m[1][0], c5, m[1][2], c2, -m[1][3], c1) * inv;
+    t[1][1] = e3(m[0][0], c5, -m[0][2], c2, m[0][3], c1) * inv;
+    t[1][2] = e3(-m[3][0], s5, m[3][2], s2, -m[3][3], s1) * inv;
+    t[1][3] = e3(m[2][0], s5, -m[2][2], s2, m[2][3], s1) * inv;
+    t[2][0] = e3(m[1][0], c4, -m[1][1], c2, m[1][3], c0) * inv;
+    t[2][1] = e3(-m[0][0], c4, m[0][1], c2, -m[0][3], c0) * inv;
+    t[2][2] = e3(m[3][0], s4, -m[3][1], s2, m[3][3], s0) * inv;
+    t[2][3] = e3(-m[2][0], s4, m[2][1], s2, -m[2][3], s0) * inv;
+    t[3][0] = e3(-m[1][0], c3, m[1][1], c1, -m[1][2], c0) * inv;
+    t[3][1] = e3(m[0][0], c3, -m[0][1], c1, m[0][2], c0) * inv;
+    t[3][2] = e3(-m[3][0], s3, m[3][1], s1, -m[3][2], s0) * inv;
+    t[3][3] = e3(m[2][0], s3, -m[2][1], s1, m[2][2], s0) * inv;
+  }
+#endif
+}
+
 // eo = ei (x) ej (ei covers stages [i, j), ej covers [j, k)), operands in shared memory:
 // computed by a group of GS = 4 threads (row a of every output on thread a;
 // rows a >= NS idle), the intermediates exchanged through the group's scratch `sh`
 // (SCR doubles) -- the per-level latency of the scan is then a few short dependent
-// chains instead of one thread's ~700 FP64 operations.  Every thread of the warp calls
-// it (`on`: this group has a combination at this level) so the warp barriers match.
+// chains instead of one thread's ~700 FP64 operations.  Each phase first loads all of
+// its shared-memory operands into registers, then computes, then stores: operands and
+// results live in one shared array, so interleaved loads and stores would be serialised
+// by possible aliasing.  Every thread of the warp calls it (`on`: this group has a
+// combination at this level) so the warp barriers match.  (One thread per matrix entry,
+// 16 per element, measured slower: on the one SM of a single scene the 16-fold
+// redundant inverse and operand loads saturate the FP64 pipe and shared-memory
+// bandwidth -- profiles/README.md.)
 template <int NS>
 struct ScanScr {
   static constexpr int M = 0, G = NS * NS, H = G + NS, V = H + NS, X = V + NS * NS, Z = X + NS * NS, Y = Z + NS * NS,
@@ -69,106 +187,92 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
   CG_TS(0);
   using L = ScanEl<NS>;
   using S = ScanScr<NS>;
-#define Ai(k) ei[L::A + (k)]
-#define bi(k) ei[L::B + (k)]
-#define Ci(k) ei[L::C + (k)]
-#define ni(k) ei[L::ETA + (k)]
-#define Ji(k) ei[L::J + (k)]
-#define Aj(k) ej[L::A + (k)]
-#define bj(k) ej[L::B + (k)]
-#define Cj(k) ej[L::C + (k)]
-#define nj(k) ej[L::ETA + (k)]
-#define Jj(k) ej[L::J + (k)]
   const bool row = on && a < NS;
   // P1: row a of M = I + Ci Jj, g = bi + Ci nj, h = nj - Jj bi, V = Jj Ai
   if (row) {
-    double gs = bi(a), hs = nj(a);
+    double ca_[NS], ja[NS], bi_[NS], nj_[NS], Jj_[NS][NS], Ai_[NS][NS];
+    double gs = ei[L::B + a], hs = ej[L::ETA + a];
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
-      gs = __fma_rn(Ci(a * NS + q), nj(q), gs);
-      hs = __fma_rn(-Jj(a * NS + q), bi(q), hs);
+      ca_[q] = ei[L::C + a * NS + q];
+      ja[q] = ej[L::J + a * NS + q];
+      bi_[q] = ei[L::B + q];
+      nj_[q] = ej[L::ETA + q];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        Jj_[q][c] = ej[L::J + q * NS + c];
+        Ai_[q][c] = ei[L::A + q * NS + c];
+      }
     }
-    sh[S::G + a] = gs;
-    sh[S::H + a] = hs;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      gs = __fma_rn(ca_[q], nj_[q], gs);
+      hs = __fma_rn(-ja[q], bi_[q], hs);
+    }
+    double m_[NS], v_[NS];
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
       double m = (a == c) ? 1.0 : 0.0, v = 0.0;
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
-        m = __fma_rn(Ci(a * NS + q), Jj(q * NS + c), m);
-        v = __fma_rn(Jj(a * NS + q), Ai(q * NS + c), v);
+        m = __fma_rn(ca_[q], Jj_[q][c], m);
+        v = __fma_rn(ja[q], Ai_[q][c], v);
       }
-      sh[S::M + a * NS + c] = m;
-      sh[S::V + a * NS + c] = v;
+      m_[c] = m;
+      v_[c] = v;
+    }
+    sh[S::G + a] = gs;
+    sh[S::H + a] = hs;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      sh[S::M + a * NS + c] = m_[c];
+      sh[S::V + a * NS + c] = v_[c];
     }
   }
   CG_TS(1);
   __syncwarp();
   CG_TS(2);
-  // P2: T = M^-1 (Gauss-Jordan with partial pivoting, redundantly per thread); row a of
-  // X = T Ai, Z = T Ci, y = T g
+  // P2: T = M^-1 (redundantly per thread, scan_inverse); row a of X = T Ai, Z = T Ci, y = T g
   if (row) {
-    double M[NS][NS], T[NS][NS];
+    double M[NS][NS], T[NS][NS], Ai_[NS][NS], Ci_[NS][NS], g_[NS];
 #pragma unroll
-    for (int r = 0; r < NS; ++r)
+    for (int r = 0; r < NS; ++r) {
+      g_[r] = sh[S::G + r];
 #pragma unroll
       for (int c = 0; c < NS; ++c) {
         M[r][c] = sh[S::M + r * NS + c];
-        T[r][c] = (r == c) ? 1.0 : 0.0;
-      }
-#pragma unroll
-    for (int c = 0; c < NS; ++c) {
-#pragma unroll
-      for (int r = c + 1; r < NS; ++r) {
-        const bool sw = fabs(M[r][c]) > fabs(M[c][c]);
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          const double t0 = M[c][q], t1 = T[c][q];
-          M[c][q] = sw ? M[r][q] : t0;
-          M[r][q] = sw ? t0 : M[r][q];
-          T[c][q] = sw ? T[r][q] : t1;
-          T[r][q] = sw ? t1 : T[r][q];
-        }
-      }
-      const double inv = 1.0 / M[c][c];
-#pragma unroll
-      for (int q = 0; q < NS; ++q) {
-        M[c][q] = M[c][q] * inv;
-        T[c][q] = T[c][q] * inv;
-      }
-#pragma unroll
-      for (int r = 0; r < NS; ++r) {
-        if (r == c) continue;
-        const double f = M[r][c];
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          M[r][q] = __fma_rn(-f, M[c][q], M[r][q]);
-          T[r][q] = __fma_rn(-f, T[c][q], T[r][q]);
-        }
+        Ai_[r][c] = ei[L::A + r * NS + c];
+        Ci_[r][c] = ei[L::C + r * NS + c];
       }
     }
+    scan_inverse<NS>(M, T);
     double Ta[NS];
 #pragma unroll
     for (int q = 0; q < NS; ++q) {  // row a of T (a run-time index: select, no local array)
-      double v = 0.0;
+      double v = T[0][q];
 #pragma unroll
-      for (int r = 0; r < NS; ++r) v = (r == a) ? T[r][q] : v;
+      for (int r = 1; r < NS; ++r) v = (r == a) ? T[r][q] : v;
       Ta[q] = v;
     }
-    double sy = 0.0;
+    double sy = 0.0, sx_[NS], sz_[NS];
 #pragma unroll
-    for (int q = 0; q < NS; ++q) sy = __fma_rn(Ta[q], sh[S::G + q], sy);
-    sh[S::Y + a] = sy;
+    for (int q = 0; q < NS; ++q) sy = __fma_rn(Ta[q], g_[q], sy);
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
       double sx = 0.0, sz = 0.0;
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
-        sx = __fma_rn(Ta[q], Ai(q * NS + c), sx);
-        sz = __fma_rn(Ta[q], Ci(q * NS + c), sz);
+        sx = __fma_rn(Ta[q], Ai_[q][c], sx);
+        sz = __fma_rn(Ta[q], Ci_[q][c], sz);
       }
-      sh[S::X + a * NS + c] = sx;
-      sh[S::Z + a * NS + c] = sz;
+      sx_[c] = sx;
+      sz_[c] = sz;
+    }
+    sh[S::Y + a] = sy;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      sh[S::X + a * NS + c] = sx_[c];
+      sh[S::Z + a * NS + c] = sz_[c];
     }
   }
   CG_TS(3);
@@ -176,57 +280,91 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
   // P3: rows a of A_ik = Aj X, b_ik = Aj y + bj, W = Aj Z, eta_ik = X^T h + ni,
   // J_ik = sym(X^T V) + Ji
   if (row) {
-    double sb = bj(a);
+    double aj[NS], y_[NS], h_[NS], X_[NS][NS], Z_[NS][NS], V_[NS][NS], xa[NS], va[NS], ji[NS];
+    double sb = ej[L::B + a], se = ei[L::ETA + a];
 #pragma unroll
-    for (int q = 0; q < NS; ++q) sb = __fma_rn(Aj(a * NS + q), sh[S::Y + q], sb);
-    eo[L::B + a] = sb;
-    double se = ni(a);
+    for (int q = 0; q < NS; ++q) {
+      aj[q] = ej[L::A + a * NS + q];
+      y_[q] = sh[S::Y + q];
+      h_[q] = sh[S::H + q];
+      xa[q] = sh[S::X + q * NS + a];
+      va[q] = sh[S::V + q * NS + a];
+      ji[q] = ei[L::J + a * NS + q];
 #pragma unroll
-    for (int q = 0; q < NS; ++q) se = __fma_rn(sh[S::X + q * NS + a], sh[S::H + q], se);
-    eo[L::ETA + a] = se;
+      for (int c = 0; c < NS; ++c) {
+        X_[q][c] = sh[S::X + q * NS + c];
+        Z_[q][c] = sh[S::Z + q * NS + c];
+        V_[q][c] = sh[S::V + q * NS + c];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NS; ++q) sb = __fma_rn(aj[q], y_[q], sb);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) se = __fma_rn(xa[q], h_[q], se);
+    double oa[NS], ow[NS], oj[NS];
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
       double sa = 0.0, sw = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
-        sa = __fma_rn(Aj(a * NS + q), sh[S::X + q * NS + c], sa);
-        sw = __fma_rn(Aj(a * NS + q), sh[S::Z + q * NS + c], sw);
-        s1 = __fma_rn(sh[S::X + q * NS + a], sh[S::V + q * NS + c], s1);
-        s2 = __fma_rn(sh[S::X + q * NS + c], sh[S::V + q * NS + a], s2);
+        sa = __fma_rn(aj[q], X_[q][c], sa);
+        sw = __fma_rn(aj[q], Z_[q][c], sw);
+        s1 = __fma_rn(xa[q], V_[q][c], s1);
+        s2 = __fma_rn(X_[q][c], va[q], s2);
       }
-      eo[L::A + a * NS + c] = sa;
-      sh[S::W + a * NS + c] = sw;
-      eo[L::J + a * NS + c] = 0.5 * (s1 + s2) + Ji(a * NS + c);
+      oa[c] = sa;
+      ow[c] = sw;
+      oj[c] = 0.5 * (s1 + s2) + ji[c];
+    }
+    eo[L::B + a] = sb;
+    eo[L::ETA + a] = se;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      eo[L::A + a * NS + c] = oa[c];
+      sh[S::W + a * NS + c] = ow[c];
+      eo[L::J + a * NS + c] = oj[c];
     }
   }
   CG_TS(4);
   __syncwarp();
   // P4: row a of C_ik = sym(W Aj^T) + Cj
   if (row) {
+    double W_[NS][NS], Aj_[NS][NS], wa[NS], aa[NS], cj[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      wa[r] = sh[S::W + a * NS + r];
+      aa[r] = ej[L::A + a * NS + r];
+      cj[r] = ej[L::C + a * NS + r];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        W_[r][q] = sh[S::W + r * NS + q];
+        Aj_[r][q] = ej[L::A + r * NS + q];
+      }
+    }
+    double oc[NS];
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
       double s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int q = 0; q < NS; ++q) {
-        s1 = __fma_rn(sh[S::W + a * NS + q], Aj(c * NS + q), s1);
-        s2 = __fma_rn(sh[S::W + c * NS + q], Aj(a * NS + q), s2);
+        s1 = __fma_rn(wa[q], Aj_[c][q], s1);
+        s2 = __fma_rn(W_[c][q], aa[q], s2);
       }
-      eo[L::C + a * NS + c] = 0.5 * (s1 + s2) + Cj(a * NS + c);
+      oc[c] = 0.5 * (s1 + s2) + cj[c];
     }
+#pragma unroll
+    for (int c = 0; c < NS; ++c) eo[L::C + a * NS + c] = oc[c];
   }
   CG_TS(5);
-#undef Ai
-#undef bi
-#undef Ci
-#undef ni
-#undef Ji
-#undef Aj
-#undef bj
-#undef Cj
-#undef nj
-#undef Jj
 #undef CG_TS
 }
+
+// asynchronous 8-byte global -> shared copy (cp.async, L1-allocating) and its wait
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // threads per scan element (rows of the combination)
 constexpr int SCAN_GS = 4;
@@ -272,31 +410,19 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   double* ss_ = ssref + (long long)(N + 1) * NS;
   double* srec = ss_ + (long long)(N + 1) * NS;  // stage_recs: this scene's records
 #ifdef CA_RIC_PROFILE
-  long long tp[8];
+  long long tp[10];
   int np_ = 0;
 #define RIC_TS() (tp[np_++] = clock64())
 #else
 #define RIC_TS() ((void)0)
 #endif
   RIC_TS();
-  // (1) bulk copies into shared memory (8 loads in flight per thread, all threads):
-  // this scene's records (one contiguous block in the sweep's layout, when stage_recs),
-  // Qs, s_ref and s rows, and the dynamics -- then the stage blocks from shared memory
+  // (1) bulk copies into shared memory by asynchronous 8-byte copies (cp.async: every
+  // element in flight at once, no register staging): this scene's records (one
+  // contiguous block in the sweep's layout, when stage_recs), Qs, s_ref and s rows, and
+  // the dynamics
   auto bulk = [&](double* dst, const double* __restrict__ src, long long tot) {
-    constexpr int U = 8;
-    for (long long k0 = tid; k0 < tot; k0 += (long long)nth * U) {
-      double v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long k = k0 + (long long)nth * u;
-        v[u] = (k < tot) ? __ldg(src + k) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long k = k0 + (long long)nth * u;
-        if (k < tot) dst[k] = v[u];
-      }
-    }
+    for (long long k = tid; k < tot; k += nth) cp_async8(dst + k, src + k);
   };
   const long long per_scene = (long long)P.NG * P.nchunkG * P.TG;  // records of one scene
   if (stage_recs) bulk(srec, recs + (long long)b * per_scene * P.rec, per_scene * P.rec);
@@ -306,46 +432,43 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   {
     const long long idx0 = P.dyn_ps ? (long long)b * nd : 0;
     auto stage_dyn = [&](const double* __restrict__ src, int blk, int off) {
-      constexpr int U = 8;  // loads in flight per thread before their stores
       const int tot = nd * blk;
-      for (int k0 = tid; k0 < tot; k0 += nth * U) {
-        double v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int k = k0 + nth * u;
-          v[u] = (k < tot) ? __ldg(src + k) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int k = k0 + nth * u;
-          if (k < tot) sdyn[(k / blk) * DB + off + k % blk] = v[u];
-        }
-      }
+      for (int k = tid; k < tot; k += nth) cp_async8(sdyn + (k / blk) * DB + off + k % blk, src + k);
     };
     stage_dyn(P.dynA + idx0 * NS * NS, NS * NS, 0);
     stage_dyn(P.dynB + idx0 * NS * NU, NS * NU, NS * NS);
     stage_dyn(P.dync + idx0 * NS, NS, NS * NS + NS * NU);
   }
+  cp_async_wait_all();
   __syncthreads();
-  // stage blocks: thread t sums the records of timestep t+1 in chunk order
-  for (int t = tid; t < N; t += nth) {
-    double ra[RECMAX];
-#pragma unroll
-    for (int f = 0; f < RECMAX; ++f) ra[f] = 0.0;
-    const long long q = (long long)b * N + t;
-    const int RC = P.rec, fm = P.nagg + S_PMAX;
+  RIC_TS();
+  // stage blocks: the (timestep, field) sums in parallel -- entry k = (t, f) sums field f
+  // of timestep t+1 over the chunk records in chunk order (max for S_PMAX) into rsum
+  // [N][rec] (the second element buffer and the scratch, free until the scan: (EL + SCR)
+  // (N + 1) >= 22 N doubles) -- then thread t assembles stage t+1 from its row
+  {
+    double* rsum = E1;
+    const int RC = P.rec, fm = P.nagg + S_PMAX, nc = nchunk ? nchunk : 1;
+    CA_CHECK((long long)N * RC <= (long long)(EL + SCR) * SS);
     const long long rb0 = (long long)b * per_scene;
-    for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
-      const double* r0 = stage_recs ? srec + (rec_index(P, b, t + 1, c) - rb0) * RC
-                                    : recs + (nchunk ? rec_index(P, b, t + 1, c) : q) * RC;
-#pragma unroll
-      for (int f = 0; f < RECMAX; ++f) {
-        if (f >= RC) continue;
-        const double v0 = r0[f];
-        ra[f] = (f == fm) ? fmax(ra[f], v0) : ra[f] + v0;
+    for (int k = tid; k < N * RC; k += nth) {
+      const int t = k / RC, f = k - t * RC;
+      // rec_index(P, b, t + 1, c) = base + c TG
+      const long long base = (((long long)b * P.NG + t / P.TG) * P.nchunkG) * P.TG + t % P.TG;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < nc; ++c) {
+        const double v0 = stage_recs ? srec[(base + (long long)c * P.TG - rb0) * RC + f]
+                                     : recs[(nchunk ? base + (long long)c * P.TG : (long long)b * N + t) * RC + f];
+        acc = (f == fm) ? fmax(acc, v0) : acc + v0;
       }
+      rsum[k] = acc;
     }
-    stage_assemble(P, q, ra, sstg + (long long)t * SB, sst + (long long)NSTAT * t, sQs, ssref, ss_);
+    __syncthreads();
+    RIC_TS();
+    for (int t = tid; t < N; t += nth)
+      stage_assemble(P, (long long)b * N + t, rsum + (long long)t * RC, sstg + (long long)t * SB,
+                     sst + (long long)NSTAT * t, sQs, ssref, ss_);
   }
   __syncthreads();
   RIC_TS();
@@ -630,8 +753,9 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   RIC_TS();
 #ifdef CA_RIC_PROFILE
   if (tid == 0 && b == 0)
-    printf("ric_scan cycles: stage %lld elements %lld scan %lld gains %lld forward %lld stages+stats %lld\n",
-           tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5]);
+    printf("ric_scan cycles: loads %lld sums %lld assemble %lld elements %lld scan %lld gains %lld forward %lld "
+           "stages+stats %lld\n", tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5],
+           tp[7] - tp[6], tp[8] - tp[7]);
 #endif
 #undef RIC_TS
 }
