@@ -534,8 +534,13 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
     // from the sweep's own layout, not the allreduced per-(scene, t) buffer)
     const size_t srec = sizeof(double) * (size_t)ca::riccati_scan_rec_doubles(
                                              (long long)h->dev.NG * h->dev.nchunkG * h->dev.TG, h->dev.rec);
-    const int stage_recs = (nchunk && recs == h->dev.agg && sms + srec <= 200 * 1024) ? 1 : 0;
-    if (stage_recs) sms += srec;
+    // overlaid on buffers the scan needs only later, extended by ovx doubles where the
+    // records and their sums need more
+    const long long ovd = (long long)(srec / sizeof(double)) + (long long)h->N * h->dev.rec -
+                          ca::riccati_scan_overlay_doubles(h->N, NS);
+    const int ovx = (int)std::max(0LL, ovd);
+    const int stage_recs = (nchunk && recs == h->dev.agg && sms + sizeof(double) * ovx <= 200 * 1024) ? 1 : 0;
+    if (stage_recs) sms += sizeof(double) * ovx;
     static const bool scan_on = !(std::getenv("CA_RICCATI_SCAN") && std::getenv("CA_RICCATI_SCAN")[0] == '0');
     if (scan_on && sms <= 200 * 1024 && ca::SCAN_GS * (h->N + 1) <= 1024 && h->N >= 16) {
       int tmax = 0;
@@ -560,7 +565,7 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
       }
       const int threads = std::min(tmax, 32 * ((ca::SCAN_GS * (h->N + 1) + 31) / 32));
       ca::k_riccati_scan<NS, NU><<<(unsigned)h->B, threads, sms, h->stream>>>(h->dev, recs, nchunk, cur, prev,
-                                                                             stage_recs);
+                                                                             stage_recs, stage_recs ? ovx : 0);
       CUDA_TRY(cudaGetLastError());
       return CA_OK;
     }

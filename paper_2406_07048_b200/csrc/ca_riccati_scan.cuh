@@ -27,20 +27,15 @@
 
 namespace ca {
 
-// A scan element / scratch record stored field-major across the stages ([field][stage],
-// stage stride S): the threads of a warp (consecutive stages, rows a of a group) then hit
-// distinct shared-memory banks (S chosen by scan_stride).
+// A scan element / scratch record: one stage's fields contiguous, consecutive stages an
+// odd number of doubles apart (scan_pad) -- every field offset is then an immediate
+// (no per-access stride arithmetic) and the threads of a warp, on consecutive stages,
+// hit distinct shared-memory banks.
 struct ElRef {
   double* p;
-  int S;
-  __device__ __forceinline__ double& operator[](int k) const { return p[(long long)k * S]; }
+  __device__ __forceinline__ double& operator[](int k) const { return p[k]; }
 };
-// stage stride of the field-major arrays: >= n with S NS = 4 (mod 16) doubles, so that the
-// 16 (stage, row) accesses of a half-warp fall on distinct 64-bit bank pairs
-__host__ __device__ inline int scan_stride(int n, int NS) {
-  for (int S = n;; ++S)
-    if ((S * NS) % 16 == 4 % 16 || NS == 1) return S;
-}
+__host__ __device__ constexpr int scan_pad(int n) { return n | 1; }
 
 template <int NS>
 struct ScanEl {
@@ -369,15 +364,24 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // threads per scan element (rows of the combination)
 constexpr int SCAN_GS = 4;
 __host__ __device__ inline long long riccati_scan_smem_doubles(int N, int NS, int NU, bool dyn_pt) {
+  // the kernel's layout (k_riccati_scan below); per-stage rows padded to an odd number of
+  // doubles so that consecutive stages fall on distinct shared-memory banks
   const int EL = 3 * NS * NS + 2 * NS;
   const int SCR = NS * NS * 5 + 3 * NS;        // ScanScr<NS>::SIZE
-  const int PHI = NS * NS + NS;                // closed-loop map of a stage
-  const long long S = scan_stride(N + 1, NS);  // field-major stage stride
-  return riccati_smem_doubles(N, NS, NU, dyn_pt) + 2LL * EL * S + (long long)SCR * S + (long long)N * PHI +
-         (long long)(N + 1) * NS + 2LL * N + NS * NS + 2LL * (N + 1) * NS;
+  const int SBS = (NS * NS + NS) | 1, DBS = (NS * NS + NS * NU + NS) | 1, PHIS = (NS * NS + NS) | 1, XSS = NS | 1;
+  return (long long)N * SBS + (long long)NSTAT * N + (long long)(dyn_pt ? N : 1) * DBS + (long long)N * NU * (NS + 1) +
+         (N + 1LL) * (2 * scan_pad(EL) + scan_pad(SCR)) + (long long)N * PHIS + (long long)(N + 1) * XSS + 2LL * N +
+         NS * NS + 2LL * (N + 1) * NS;
 }
 // the scene's records staged as one block when they fit (see k_riccati_scan)
 __host__ __device__ inline long long riccati_scan_rec_doubles(long long nrec, int rec) { return nrec * rec; }
+// the overlay region the staged records (and their per-(t, field) sums) borrow before the
+// scan needs it: the element buffers, the scratch, the closed-loop maps, the states and
+// the box residuals (contiguous in k_riccati_scan's layout)
+__host__ __device__ inline long long riccati_scan_overlay_doubles(int N, int NS) {
+  const int EL = 3 * NS * NS + 2 * NS, SCR = NS * NS * 5 + 3 * NS, PHIS = (NS * NS + NS) | 1, XSS = NS | 1;
+  return (N + 1LL) * (2 * scan_pad(EL) + scan_pad(SCR)) + (long long)N * PHIS + (long long)(N + 1) * XSS + 2LL * N;
+}
 
 // One CTA per scene, blockDim = SCAN_GS * (N + 1) rounded up to a multiple of 32.
 // Shared memory: k_riccati's layout (stage blocks, statistics, dynamics, gains), then two
@@ -385,30 +389,34 @@ __host__ __device__ inline long long riccati_scan_rec_doubles(long long nrec, in
 // per-stage box residuals.
 template <int NS, int NU>
 __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* dst_cur, double* dst_prev,
-                               int stage_recs) {
+                               int stage_recs, int ovx) {
   extern __shared__ double rsm[];
   const int b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
   if (!scene_on(P, b)) return;  // stopped scene (ca_admm_solve)
   const int N = P.N;
   constexpr int SB = NS * NS + NS, DB = NS * NS + NS * NU + NS, EL = ScanEl<NS>::SIZE, SCR = ScanScr<NS>::SIZE,
                 PHI = NS * NS + NS;
+  // per-stage row strides, odd: consecutive stages on distinct banks (riccati_scan_smem_doubles)
+  constexpr int SBS = SB | 1, DBS = DB | 1, PHIS = PHI | 1, XSS = NS | 1;
   using L = ScanEl<NS>;
   double* sstg = rsm;                         // [N][SB]
-  double* sst = sstg + (long long)N * SB;     // [N][NSTAT]
+  double* sst = sstg + (long long)N * SBS;    // [N][NSTAT]
   double* sdyn = sst + (long long)NSTAT * N;  // [nd][DB]
   const int nd = P.dyn_pt ? N : 1;
-  double* ric = sdyn + (long long)nd * DB;    // [N][NU][NS+1]
-  const int SS = scan_stride(N + 1, NS);         // field-major: element field k of stage t at [k * SS + t]
-  double* E0 = ric + (long long)N * NU * (NS + 1);
-  double* E1 = E0 + (long long)EL * SS;
-  double* scr = E1 + (long long)EL * SS;         // [SCR][SS]
-  double* phi = scr + (long long)SCR * SS;       // [N][PHI]: x_{t+1} = Phi_t x_t + phi_t
-  double* xs = phi + (long long)N * PHI;         // [N+1][NS]
-  double* rbx = xs + (long long)(N + 1) * NS;    // [N] box residual of stage t
-  double* sQs = rbx + 2LL * N;                   // Qs, this scene's s_ref and s rows
+  double* ric = sdyn + (long long)nd * DBS;   // [N][NU][NS+1]
+  constexpr int ELP = scan_pad(EL), SCRP = scan_pad(SCR);  // element / scratch record strides
+  double* E0 = ric + (long long)N * NU * (NS + 1);  // [N+1][ELP]
+  double* E1 = E0 + (N + 1LL) * ELP;
+  double* scr = E1 + (N + 1LL) * ELP;            // [N+1][SCRP]
+  double* phi = scr + (N + 1LL) * SCRP;          // [N][PHIS]: x_{t+1} = Phi_t x_t + phi_t
+  double* xs = phi + (long long)N * PHIS;        // [N+1][XSS]
+  double* rbx = xs + (long long)(N + 1) * XSS;   // [N] box residual of stage t
+  double* sQs = rbx + 2LL * N + ovx;             // Qs, this scene's s_ref and s rows (ovx: overlay extension)
   double* ssref = sQs + NS * NS;
   double* ss_ = ssref + (long long)(N + 1) * NS;
-  double* srec = ss_ + (long long)(N + 1) * NS;  // stage_recs: this scene's records
+  // stage_recs: this scene's records, then their (t, field) sums, overlaid on E0 .. rbx
+  // (riccati_scan_overlay_doubles: free until the elements are built)
+  double* srec = E0;
 #ifdef CA_RIC_PROFILE
   long long tp[10];
   int np_ = 0;
@@ -433,7 +441,7 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
     const long long idx0 = P.dyn_ps ? (long long)b * nd : 0;
     auto stage_dyn = [&](const double* __restrict__ src, int blk, int off) {
       const int tot = nd * blk;
-      for (int k = tid; k < tot; k += nth) cp_async8(sdyn + (k / blk) * DB + off + k % blk, src + k);
+      for (int k = tid; k < tot; k += nth) cp_async8(sdyn + (k / blk) * DBS + off + k % blk, src + k);
     };
     stage_dyn(P.dynA + idx0 * NS * NS, NS * NS, 0);
     stage_dyn(P.dynB + idx0 * NS * NU, NS * NU, NS * NS);
@@ -447,9 +455,9 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   // [N][rec] (the second element buffer and the scratch, free until the scan: (EL + SCR)
   // (N + 1) >= 22 N doubles) -- then thread t assembles stage t+1 from its row
   {
-    double* rsum = E1;
+    double* rsum = E0 + (stage_recs ? per_scene * P.rec : 0);
     const int RC = P.rec, fm = P.nagg + S_PMAX, nc = nchunk ? nchunk : 1;
-    CA_CHECK((long long)N * RC <= (long long)(EL + SCR) * SS);
+    CA_CHECK(rsum + (long long)N * RC <= rbx + 2LL * N + ovx);
     const long long rb0 = (long long)b * per_scene;
     for (int k = tid; k < N * RC; k += nth) {
       const int t = k / RC, f = k - t * RC;
@@ -467,7 +475,7 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
     __syncthreads();
     RIC_TS();
     for (int t = tid; t < N; t += nth)
-      stage_assemble(P, (long long)b * N + t, rsum + (long long)t * RC, sstg + (long long)t * SB,
+      stage_assemble(P, (long long)b * N + t, rsum + (long long)t * RC, sstg + (long long)t * SBS,
                      sst + (long long)NSTAT * t, sQs, ssref, ss_);
   }
   __syncthreads();
@@ -485,64 +493,70 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
     for (int c = 0; c < NU; ++c) Rm[a][c] = 2.0 * P.Qu[a * NU + c] + ((a == c) ? urho[a] : 0.0);
   QuuSolve<NU> rs;
   rs.factor(Rm);
-  // (2) elements
-  for (int t = tid; t <= N; t += nth) {
-    const ElRef e{E0 + t, SS};
-    if (t < N) {
-      const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
-      const double* Bm = A + NS * NS;
-      const double* cv = Bm + NS * NU;
-      // u0 = -R^-1 r_t (box block's linear control term), C = B R^-1 B^T
-      double u0[NU];
+  // (2) elements, SCAN_GS threads per stage (row a each): u0 = -R^-1 r_t (the box block's
+  // linear control term, redundantly), column a of R^-1 B^T through the scratch, then
+  // row a of A, b = c + B u0, C = B R^-1 B^T, J = H_t, eta = -h_t
+  constexpr int RBF = 0;  // scratch field of (R^-1 B^T)[q][c]: RBF + q NS + c of the stage's record
+  for (int t0 = 0; t0 <= N; t0 += nth / SCAN_GS) {
+    const int t = t0 + tid / SCAN_GS, a = tid % SCAN_GS;
+    const bool live = t < N && a < NS;
+    const double* A = sdyn + (P.dyn_pt ? (long long)(t < N ? t : 0) * DBS : 0);
+    const double* Bm = A + NS * NS;
+    const double* cv = Bm + NS * NU;
+    const ElRef sc{scr + (long long)t * SCRP};
+    if (live) {
+      double col[NU];
 #pragma unroll
-      for (int a = 0; a < NU; ++a) {
-        const long long ku = ((long long)b * N + t) * NU + a;
-        u0[a] = (urho[a] != 0.0) ? urho[a] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;  // -r_t
-      }
-      rs.apply(u0);
-      double RB[NU][NS];  // R^-1 B^T
+      for (int q = 0; q < NU; ++q) col[q] = Bm[a * NU + q];
+      rs.apply(col);
 #pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double col[NU];
+      for (int q = 0; q < NU; ++q) sc[RBF + q * NS + a] = col[q];
+    }
+    __syncwarp();
+    if (t <= N && a < NS) {
+      const ElRef e{E0 + (long long)t * ELP};
+      if (t < N) {
+        double u0[NU];
 #pragma unroll
-        for (int a = 0; a < NU; ++a) col[a] = Bm[c * NU + a];
-        rs.apply(col);
-#pragma unroll
-        for (int a = 0; a < NU; ++a) RB[a][c] = col[a];
-      }
-#pragma unroll
-      for (int a = 0; a < NS; ++a) {
+        for (int q = 0; q < NU; ++q) {
+          const long long ku = ((long long)b * N + t) * NU + q;
+          u0[q] = (urho[q] != 0.0) ? urho[q] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;  // -r_t
+        }
+        rs.apply(u0);
         double s = cv[a];
 #pragma unroll
         for (int q = 0; q < NU; ++q) s = __fma_rn(Bm[a * NU + q], u0[q], s);
         e[L::B + a] = s;
+        double rb[NU][NS];
+#pragma unroll
+        for (int q = 0; q < NU; ++q)
+#pragma unroll
+          for (int c = 0; c < NS; ++c) rb[q][c] = sc[RBF + q * NS + c];
 #pragma unroll
         for (int c = 0; c < NS; ++c) {
           e[L::A + a * NS + c] = A[a * NS + c];
           double v = 0.0;
 #pragma unroll
-          for (int q = 0; q < NU; ++q) v = __fma_rn(Bm[a * NU + q], RB[q][c], v);
+          for (int q = 0; q < NU; ++q) v = __fma_rn(Bm[a * NU + q], rb[q][c], v);
           e[L::C + a * NS + c] = v;
         }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NS; ++c) e[L::A + a * NS + c] = e[L::C + a * NS + c] = 0.0;
+        e[L::B + a] = 0.0;
       }
-    } else {
+      if (t >= 1) {  // stage cost 1/2 s^T H_t s + h_t^T s  ->  J = H_t, eta = -h_t
+        const double* in = sstg + (long long)(t - 1) * SBS;
 #pragma unroll
-      for (int k = 0; k < NS * NS; ++k) e[L::A + k] = e[L::C + k] = 0.0;
+        for (int c = 0; c < NS; ++c) e[L::J + a * NS + c] = in[a * NS + c];
+        e[L::ETA + a] = -in[NS * NS + a];
+      } else {
 #pragma unroll
-      for (int k = 0; k < NS; ++k) e[L::B + k] = 0.0;
+        for (int c = 0; c < NS; ++c) e[L::J + a * NS + c] = 0.0;
+        e[L::ETA + a] = 0.0;
+      }
     }
-    if (t >= 1) {  // stage cost 1/2 s^T H_t s + h_t^T s  ->  J = H_t, eta = -h_t
-      const double* in = sstg + (long long)(t - 1) * SB;
-#pragma unroll
-      for (int k = 0; k < NS * NS; ++k) e[L::J + k] = in[k];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) e[L::ETA + k] = -in[NS * NS + k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < NS * NS; ++k) e[L::J + k] = 0.0;
-#pragma unroll
-      for (int k = 0; k < NS; ++k) e[L::ETA + k] = 0.0;
-    }
+    __syncwarp();
   }
   __syncthreads();
   RIC_TS();
@@ -556,19 +570,19 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
       const int t = e0 + gi;
       const bool have = t <= N, on = have && t + d <= N;
       if (have && !on) {  // no partner: carried over
-        const ElRef ei{cur + t, SS}, eo{nxt + t, SS};
+        const ElRef ei{cur + (long long)t * ELP}, eo{nxt + (long long)t * ELP};
         for (int k = ga; k < EL; k += SCAN_GS) eo[k] = ei[k];
       }
       const int tc = have ? t : 0;
       const int tj = on ? t + d : tc;
 #ifdef CA_RIC_PROFILE
       long long cg[6] = {0, 0, 0, 0, 0, 0};
-      scan_comb_g<NS>(ElRef{cur + tc, SS}, ElRef{cur + tj, SS}, ElRef{nxt + tc, SS}, ga, on, ElRef{scr + tc, SS}, cg);
+      scan_comb_g<NS>(ElRef{cur + tc * ELP}, ElRef{cur + tj * ELP}, ElRef{nxt + tc * ELP}, ga, on, ElRef{scr + tc * SCRP}, cg);
       if (tid == 0 && b == 0 && d == 1)
         printf("comb cycles: P1 %lld sync %lld P2 %lld P3 %lld P4 %lld\n", cg[1] - cg[0], cg[2] - cg[1], cg[3] - cg[2],
                cg[4] - cg[3], cg[5] - cg[4]);
 #else
-      scan_comb_g<NS>(ElRef{cur + tc, SS}, ElRef{cur + tj, SS}, ElRef{nxt + tc, SS}, ga, on, ElRef{scr + tc, SS});
+      scan_comb_g<NS>(ElRef{cur + tc * ELP}, ElRef{cur + tj * ELP}, ElRef{nxt + tc * ELP}, ga, on, ElRef{scr + tc * SCRP});
 #endif
     }
     __syncthreads();
@@ -577,123 +591,195 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
     nxt = tmp;
   }
   RIC_TS();
-  // (4) gains of every stage from P_{t+1} = J, p_{t+1} = -eta (k_riccati's formula), and
-  // the stage's closed-loop map x_{t+1} = (A + B K) x_t + (B k + c)
-  for (int t = tid; t < N; t += nth) {
-    const ElRef e{cur + t + 1, SS};
-    const double* A = sdyn + (P.dyn_pt ? (long long)t * DB : 0);
-    const double* Bm = A + NS * NS;
-    const double* cv = Bm + NS * NU;
-    double PA[NS][NS], PB[NS][NU], w[NS];
+  // (4) gains of every stage from P_{t+1} = J, p_{t+1} = -eta (k_riccati's formula, the
+  // same sums in the same order), SCAN_GS threads per stage through the scratch:
+  //   G1 row a < NS of PA = P A, PB = P B, w = P c - eta_{t+1}
+  //   G2 row a < NU of Quu = R + B^T PB, Qux = B^T PA, qu = -r + B^T w
+  //   G3 Quu factored (redundantly), columns a, a + GS, .. of K = -Quu^-1 [Qux | qu]
+  //   G4 row a < NS of the closed-loop map x_{t+1} = (A + B K) x_t + (B k + c)
+  {
+    constexpr int FPA = 0, FPB = FPA + NS * NS, FW = FPB + NS * NU, FQUU = FW + NS, FQUX = FQUU + NU * NU,
+                  FQU = FQUX + NU * NS;
+    static_assert(FQU + NU <= ScanScr<NS>::SIZE, "gains scratch");
+    for (int t0 = 0; t0 < N; t0 += nth / SCAN_GS) {
+      const int t = t0 + tid / SCAN_GS, a = tid % SCAN_GS;
+      const bool st = t < N;
+      const int tt = st ? t : 0;
+      const ElRef e{cur + (tt + 1LL) * ELP}, sc{scr + (long long)tt * SCRP};
+      const double* A = sdyn + (P.dyn_pt ? (long long)tt * DBS : 0);
+      const double* Bm = A + NS * NS;
+      const double* cv = Bm + NS * NU;
+      if (st && a < NS) {  // G1
+        double jr[NS];
 #pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      double acc = -e[L::ETA + a];
+        for (int k = 0; k < NS; ++k) jr[k] = e[L::J + a * NS + k];
+        double acc = -e[L::ETA + a];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) acc = __fma_rn(e[L::J + a * NS + c], cv[c], acc);
-      w[a] = acc;
+        for (int c = 0; c < NS; ++c) acc = __fma_rn(jr[c], cv[c], acc);
+        sc[FW + a] = acc;
 #pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double s = 0.0;
+        for (int c = 0; c < NS; ++c) {
+          double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(e[L::J + a * NS + k], A[k * NS + c], s);
-        PA[a][c] = s;
+          for (int k = 0; k < NS; ++k) s = __fma_rn(jr[k], A[k * NS + c], s);
+          sc[FPA + a * NS + c] = s;
+        }
+#pragma unroll
+        for (int c = 0; c < NU; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < NS; ++k) s = __fma_rn(jr[k], Bm[k * NU + c], s);
+          sc[FPB + a * NU + c] = s;
+        }
       }
+      __syncwarp();
+      if (st && a < NU) {  // G2
+        double bc[NS];
 #pragma unroll
-      for (int c = 0; c < NU; ++c) {
-        double s = 0.0;
+        for (int k = 0; k < NS; ++k) bc[k] = Bm[k * NU + a];
 #pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(e[L::J + a * NS + k], Bm[k * NU + c], s);
-        PB[a][c] = s;
+        for (int c = 0; c < NU; ++c) {
+          double s = 2.0 * P.Qu[a * NU + c] + ((a == c) ? urho[a] : 0.0);
+#pragma unroll
+          for (int k = 0; k < NS; ++k) s = __fma_rn(bc[k], sc[FPB + k * NU + c], s);
+          sc[FQUU + a * NU + c] = s;
+        }
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < NS; ++k) s = __fma_rn(bc[k], sc[FPA + k * NS + c], s);
+          sc[FQUX + a * NS + c] = s;
+        }
+        const long long ku = ((long long)b * N + t) * NU + a;
+        double s = (urho[a] != 0.0) ? -urho[a] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s = __fma_rn(bc[k], sc[FW + k], s);
+        sc[FQU + a] = s;
       }
-    }
-    double Quu[NU][NU], Qux[NU][NS], qu[NU];
+      __syncwarp();
+      if (st) {  // G3
+        double Quu[NU][NU];
 #pragma unroll
-    for (int a = 0; a < NU; ++a) {
+        for (int q = 0; q < NU; ++q)
 #pragma unroll
-      for (int c = 0; c < NU; ++c) {
-        double s = 2.0 * P.Qu[a * NU + c] + ((a == c) ? urho[a] : 0.0);
+          for (int c = 0; c < NU; ++c) Quu[q][c] = sc[FQUU + q * NU + c];
+        QuuSolve<NU> qs;
+        qs.factor(Quu);
+        for (int c = a; c <= NS; c += SCAN_GS) {
+          double rhs[NU];
 #pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PB[k][c], s);
-        Quu[a][c] = s;
+          for (int q = 0; q < NU; ++q) rhs[q] = (c < NS) ? sc[FQUX + q * NS + c] : sc[FQU + q];
+          qs.apply(rhs);
+#pragma unroll
+          for (int q = 0; q < NU; ++q) ric[((long long)t * NU + q) * (NS + 1) + c] = -rhs[q];
+        }
       }
+      __syncwarp();
+      if (st && a < NS) {  // G4
+        double kg[NU][NS + 1];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double s = 0.0;
+        for (int q = 0; q < NU; ++q)
 #pragma unroll
-        for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], PA[k][c], s);
-        Qux[a][c] = s;
+          for (int c = 0; c <= NS; ++c) kg[q][c] = ric[((long long)t * NU + q) * (NS + 1) + c];
+        double* ph = phi + (long long)t * PHIS;
+        double s = cv[a];
+#pragma unroll
+        for (int q = 0; q < NU; ++q) s = __fma_rn(Bm[a * NU + q], kg[q][NS], s);
+        ph[NS * NS + a] = s;
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+          double v = A[a * NS + c];
+#pragma unroll
+          for (int q = 0; q < NU; ++q) v = __fma_rn(Bm[a * NU + q], kg[q][c], v);
+          ph[a * NS + c] = v;
+        }
       }
-      const long long ku = ((long long)b * N + t) * NU + a;
-      double s = (urho[a] != 0.0) ? -urho[a] * (P.box_wu[ku] - P.box_lu[ku]) : 0.0;
-#pragma unroll
-      for (int k = 0; k < NS; ++k) s = __fma_rn(Bm[k * NU + a], w[k], s);
-      qu[a] = s;
-    }
-    QuuSolve<NU> qs;
-    qs.factor(Quu);
-    double Kg[NU][NS + 1];
-#pragma unroll
-    for (int c = 0; c <= NS; ++c) {
-      double rhs[NU];
-#pragma unroll
-      for (int a = 0; a < NU; ++a) rhs[a] = (c < NS) ? Qux[a][c] : qu[a];
-      qs.apply(rhs);
-#pragma unroll
-      for (int a = 0; a < NU; ++a) {
-        Kg[a][c] = -rhs[a];
-        ric[((long long)t * NU + a) * (NS + 1) + c] = -rhs[a];
-      }
-    }
-    double* ph = phi + (long long)t * PHI;
-#pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      double s = cv[a];
-#pragma unroll
-      for (int q = 0; q < NU; ++q) s = __fma_rn(Bm[a * NU + q], Kg[q][NS], s);
-      ph[NS * NS + a] = s;
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double v = A[a * NS + c];
-#pragma unroll
-        for (int q = 0; q < NU; ++q) v = __fma_rn(Bm[a * NU + q], Kg[q][c], v);
-        ph[a * NS + c] = v;
-      }
+      __syncwarp();
     }
   }
   __syncthreads();
   RIC_TS();
-  // (5) forward: x_{t+1} = Phi_t x_t + phi_t from s_0 (one thread: NS independent dot
-  // products per stage, the next stage's map loaded ahead)
-  if (tid == 0) {
-    double x[NS];
+  // (5) forward x_{t+1} = Phi_t x_t + phi_t from s_0, in chunks of FC stages:
+  //   F1 each chunk's composed map (Psi, psi), column c of it on thread (chunk, c)
+  //      (column NS = the affine part), so no exchange is needed;
+  //   F2 one thread: the chunk start states x_{jFC} = Psi x + psi, chunk after chunk;
+  //   F3 each chunk rolls its own stages from its start state, one rounding per step
+  //      (Eq. 13b holds to one rounding per step inside a chunk, and to the chunk map's
+  //      rounding at a chunk's last step).
+  {
+    constexpr int FC = 7, CW = NS * NS + NS;  // stages per chunk (odd: chunk rows on distinct banks); map size
+    const int nch = (N + FC - 1) / FC;
+    double* cmap = scr;  // [nch][CW]: Psi (row-major), psi
+    for (int k = tid; k < nch * (NS + 1); k += nth) {  // F1
+      const int j = k / (NS + 1), c = k % (NS + 1);
+      double v[NS];
 #pragma unroll
-    for (int a = 0; a < NS; ++a) {
-      x[a] = P.s0[b * NS + a];
-      xs[a] = x[a];
+      for (int a = 0; a < NS; ++a) v[a] = (c < NS && a == c) ? 1.0 : 0.0;
+      const int t1 = min(N, (j + 1) * FC);
+      for (int t = j * FC; t < t1; ++t) {
+        const double* ph = phi + (long long)t * PHIS;
+        double w[NS];
+#pragma unroll
+        for (int a = 0; a < NS; ++a) {
+          double s = (c == NS) ? ph[NS * NS + a] : 0.0;
+#pragma unroll
+          for (int q = 0; q < NS; ++q) s = __fma_rn(ph[a * NS + q], v[q], s);
+          w[a] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < NS; ++a) v[a] = w[a];
+      }
+#pragma unroll
+      for (int a = 0; a < NS; ++a) cmap[(long long)j * CW + ((c < NS) ? a * NS + c : NS * NS + a)] = v[a];
     }
-    double pc[PHI];  // Phi_t, phi_t of the current stage (the next one is loaded meanwhile)
-#pragma unroll
-    for (int k = 0; k < PHI; ++k) pc[k] = phi[k];
-    for (int t = 0; t < N; ++t) {
-      const double* pn = phi + (long long)((t + 1 < N) ? t + 1 : t) * PHI;
-      double nx[PHI];
-#pragma unroll
-      for (int k = 0; k < PHI; ++k) nx[k] = pn[k];
-      double xn[NS];
+    __syncthreads();
+    if (tid == 0) {  // F2
+      double x[NS];
 #pragma unroll
       for (int a = 0; a < NS; ++a) {
-        double s = pc[NS * NS + a];
-#pragma unroll
-        for (int c = 0; c < NS; ++c) s = __fma_rn(pc[a * NS + c], x[c], s);
-        xn[a] = s;
+        x[a] = P.s0[b * NS + a];
+        xs[a] = x[a];
       }
+      for (int j = 0; j + 1 < nch; ++j) {
+        const double* m = cmap + (long long)j * CW;
+        double xn[NS];
 #pragma unroll
-      for (int a = 0; a < NS; ++a) {
-        x[a] = xn[a];
-        xs[(long long)(t + 1) * NS + a] = xn[a];
+        for (int a = 0; a < NS; ++a) {
+          double s = m[NS * NS + a];
+#pragma unroll
+          for (int c = 0; c < NS; ++c) s = __fma_rn(m[a * NS + c], x[c], s);
+          xn[a] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < NS; ++a) {
+          x[a] = xn[a];
+          xs[(long long)(j + 1) * FC * XSS + a] = xn[a];
+        }
       }
+    }
+    __syncthreads();
+    for (int j = tid; j < nch; j += nth) {  // F3
+      double x[NS];
 #pragma unroll
-      for (int k = 0; k < PHI; ++k) pc[k] = nx[k];
+      for (int a = 0; a < NS; ++a) x[a] = xs[(long long)j * FC * XSS + a];
+      const int t1 = min(N, (j + 1) * FC);
+      for (int t = j * FC; t < t1; ++t) {
+        const double* ph = phi + (long long)t * PHIS;
+        double xn[NS];
+#pragma unroll
+        for (int a = 0; a < NS; ++a) {
+          double s = ph[NS * NS + a];
+#pragma unroll
+          for (int c = 0; c < NS; ++c) s = __fma_rn(ph[a * NS + c], x[c], s);
+          xn[a] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < NS; ++a) x[a] = xn[a];
+        if (t + 1 < t1 || t + 1 == N)
+#pragma unroll
+          for (int a = 0; a < NS; ++a) xs[(long long)(t + 1) * XSS + a] = xn[a];
+      }
     }
   }
   __syncthreads();
@@ -704,14 +790,14 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   for (int t = tid; t <= N; t += nth) {
     double* sb = P.s + ((long long)b * (N + 1) + t) * NS;
 #pragma unroll
-    for (int a = 0; a < NS; ++a) sb[a] = xs[(long long)t * NS + a];
+    for (int a = 0; a < NS; ++a) sb[a] = xs[(long long)t * XSS + a];
     if (t == N) continue;
     double r = 0.0;
 #pragma unroll
     for (int a = 0; a < NU; ++a) {
       double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], xs[(long long)t * NS + c], s);
+      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], xs[(long long)t * XSS + c], s);
       const long long ku = ((long long)b * N + t) * NU + a;
       P.u[ku] = s;
       if (P.box && urho[a] != 0.0) {
@@ -724,7 +810,7 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
 #pragma unroll
       for (int a = 0; a < NS; ++a) {
         const double lo = P.box_lim[a], hi = P.box_lim[NS + a];
-        if (box_on(lo, hi)) r += box_update(xs[(long long)(t + 1) * NS + a], lo, hi, &P.box_ws[k0 + a], &P.box_ls[k0 + a]);
+        if (box_on(lo, hi)) r += box_update(xs[(long long)(t + 1) * XSS + a], lo, hi, &P.box_ws[k0 + a], &P.box_ls[k0 + a]);
       }
     }
     rbx[t] = r;
@@ -735,10 +821,12 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   double* sred = xs;  // (states no longer needed: reuse)
   if (tid < NSTAT) {
     double a = 0.0;
+#pragma unroll 8
     for (int t = 0; t < N; ++t) a = stat_comb(tid, a, sst[(long long)NSTAT * t + tid]);
     sred[tid] = a;
   } else if (tid == NSTAT && P.box) {
     double br = 0.0;
+#pragma unroll 8
     for (int t = 0; t < N; ++t) br += rbx[t];
     P.box_res[b] = br;
   }
@@ -753,6 +841,7 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   RIC_TS();
 #ifdef CA_RIC_PROFILE
   if (tid == 0 && b == 0)
+    printf("stage_recs %d ovx %d nchunk %d per_scene %lld\n", stage_recs, ovx, nchunk, (long long)P.NG * P.nchunkG * P.TG);
     printf("ric_scan cycles: loads %lld sums %lld assemble %lld elements %lld scan %lld gains %lld forward %lld "
            "stages+stats %lld\n", tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5],
            tp[7] - tp[6], tp[8] - tp[7]);
