@@ -529,18 +529,7 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
   // dependent Riccati steps on one warp; n_s <= 4 (the element combination keeps its
   // matrices in registers), CA_RICCATI_SCAN=0 selects the serial recursion
   if constexpr (NS <= 4) {
-    size_t sms = sizeof(double) * (size_t)ca::riccati_scan_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
-    // the scene's records staged in shared memory as one block when they fit (and come
-    // from the sweep's own layout, not the allreduced per-(scene, t) buffer)
-    const size_t srec = sizeof(double) * (size_t)ca::riccati_scan_rec_doubles(
-                                             (long long)h->dev.NG * h->dev.nchunkG * h->dev.TG, h->dev.rec);
-    // overlaid on buffers the scan needs only later, extended by ovx doubles where the
-    // records and their sums need more
-    const long long ovd = (long long)(srec / sizeof(double)) + (long long)h->N * h->dev.rec -
-                          ca::riccati_scan_overlay_doubles(h->N, NS);
-    const int ovx = (int)std::max(0LL, ovd);
-    const int stage_recs = (nchunk && recs == h->dev.agg && sms + sizeof(double) * ovx <= 200 * 1024) ? 1 : 0;
-    if (stage_recs) sms += sizeof(double) * ovx;
+    const size_t sms = sizeof(double) * (size_t)ca::riccati_scan_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
     static const bool scan_on = !(std::getenv("CA_RICCATI_SCAN") && std::getenv("CA_RICCATI_SCAN")[0] == '0');
     if (scan_on && sms <= 200 * 1024 && ca::SCAN_GS * (h->N + 1) <= 1024 && h->N >= 16) {
       int tmax = 0;
@@ -552,8 +541,12 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
         static int max_threads[CA_MAX_DEVICES] = {};
         if (h->device >= CA_MAX_DEVICES) return fail(CA_E_CUDA, "device ordinal too large");
         std::lock_guard<std::mutex> lk(mu);
-        if (sms > 48 * 1024 && sms > configured[h->device]) {
-          CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati_scan<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms));
+        if (sms > configured[h->device]) {
+          if (sms > 48 * 1024)
+            CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati_scan<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms));
+          // the same L1 / shared split as the sweep: no SM reconfiguration between the two
+          // kernels of an iteration (C4 primal step 25.9 -> 24.2 us)
+          CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati_scan<NS, NU>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
           configured[h->device] = sms;
         }
         if (!max_threads[h->device]) {
@@ -564,8 +557,7 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
         tmax = max_threads[h->device];
       }
       const int threads = std::min(tmax, 32 * ((ca::SCAN_GS * (h->N + 1) + 31) / 32));
-      ca::k_riccati_scan<NS, NU><<<(unsigned)h->B, threads, sms, h->stream>>>(h->dev, recs, nchunk, cur, prev,
-                                                                             stage_recs, stage_recs ? ovx : 0);
+      ca::k_riccati_scan<NS, NU><<<(unsigned)h->B, threads, sms, h->stream>>>(h->dev, recs, nchunk, cur, prev);
       CUDA_TRY(cudaGetLastError());
       return CA_OK;
     }
@@ -578,6 +570,7 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
     std::lock_guard<std::mutex> lk(mu);
     if (sm > configured[h->device]) {
       CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati<NS, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CUDA_TRY(cudaFuncSetAttribute(ca::k_riccati<NS, NU>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       configured[h->device] = sm;
     }
   }
@@ -1055,6 +1048,23 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
 }
 
 // create a handle for the (rank-local) problem D; g = its grid position (NULL: one GPU)
+// Every kernel of an ADMM iteration prefers the same L1 / shared-memory split as the
+// sweep (all shared): the SMs are not reconfigured between consecutive kernels, which
+// costs microseconds per switch on the single-scene configurations.  Once per device.
+static ca_status prefer_shared_carveout(int device) {
+  static std::mutex mu;
+  static bool done[CA_MAX_DEVICES] = {};
+  if (device >= CA_MAX_DEVICES) return fail(CA_E_CUDA, "device ordinal too large");
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[device]) return CA_OK;
+  const void* ks[] = {(const void*)ca::k_sortpairs, (const void*)ca::k_stage_grouped, (const void*)ca::k_stage,
+                      (const void*)ca::k_mult<2>, (const void*)ca::k_mult<3>, (const void*)ca::k_collect,
+                      (const void*)ca::k_hist};
+  for (const void* k : ks) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  done[device] = true;
+  return CA_OK;
+}
+
 ca_status create_impl(const ca_problem_desc* D, int device, void* stream, const GridPos* g, ca_problem** out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
@@ -1063,6 +1073,7 @@ ca_status create_impl(const ca_problem_desc* D, int device, void* stream, const 
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) return fail(CA_E_CUDA, "built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
   CUDA_TRY(cudaSetDevice(device));
+  if (ca_status st0 = prefer_shared_carveout(device)) return st0;
   ca_problem* h = new ca_problem();
   h->device = device;
   h->stream = static_cast<cudaStream_t>(stream);

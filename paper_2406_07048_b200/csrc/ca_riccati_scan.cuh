@@ -27,15 +27,48 @@
 
 namespace ca {
 
-// A scan element / scratch record: one stage's fields contiguous, consecutive stages an
-// odd number of doubles apart (scan_pad) -- every field offset is then an immediate
-// (no per-access stride arithmetic) and the threads of a warp, on consecutive stages,
-// hit distinct shared-memory banks.
+// A scan element / scratch record: one stage's fields contiguous, consecutive stages
+// scan_pad doubles apart -- every field offset is then an immediate (no per-access
+// stride arithmetic) and the threads of a warp, on consecutive stages, hit distinct
+// shared-memory banks.
 struct ElRef {
   double* p;
   __device__ __forceinline__ double& operator[](int k) const { return p[k]; }
 };
-__host__ __device__ constexpr int scan_pad(int n) { return n | 1; }
+// record stride: >= n, = 2 (mod 4) doubles -- 16-byte aligned records (vector loads of
+// rows) whose 16-byte halves of consecutive stages fall on distinct bank groups
+__host__ __device__ constexpr int scan_pad(int n) { return (n + 1) / 4 * 4 + 2; }
+// rows of NS contiguous doubles to / from registers (16-byte vector accesses for even NS:
+// every row offset of the element and scratch records is then even)
+template <int NS>
+__device__ __forceinline__ void ldrow(const double* p, double (&d)[NS]) {
+  if constexpr (NS % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < NS / 2; ++i) {
+      const double2 v = reinterpret_cast<const double2*>(p)[i];
+      d[2 * i] = v.x;
+      d[2 * i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) d[i] = p[i];
+  }
+}
+template <int NS>
+__device__ __forceinline__ void strow(double* p, const double (&d)[NS]) {
+  if constexpr (NS % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < NS / 2; ++i) reinterpret_cast<double2*>(p)[i] = make_double2(d[2 * i], d[2 * i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) p[i] = d[i];
+  }
+}
+template <int NS>
+__device__ __forceinline__ void ldmat(const double* p, double (&d)[NS][NS]) {
+#pragma unroll
+  for (int r = 0; r < NS; ++r) ldrow<NS>(p + r * NS, d[r]);
+}
 
 template <int NS>
 struct ScanEl {
@@ -187,18 +220,12 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
   if (row) {
     double ca_[NS], ja[NS], bi_[NS], nj_[NS], Jj_[NS][NS], Ai_[NS][NS];
     double gs = ei[L::B + a], hs = ej[L::ETA + a];
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-      ca_[q] = ei[L::C + a * NS + q];
-      ja[q] = ej[L::J + a * NS + q];
-      bi_[q] = ei[L::B + q];
-      nj_[q] = ej[L::ETA + q];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        Jj_[q][c] = ej[L::J + q * NS + c];
-        Ai_[q][c] = ei[L::A + q * NS + c];
-      }
-    }
+    ldrow<NS>(&ei[L::C + a * NS], ca_);
+    ldrow<NS>(&ej[L::J + a * NS], ja);
+    ldrow<NS>(&ei[L::B], bi_);
+    ldrow<NS>(&ej[L::ETA], nj_);
+    ldmat<NS>(&ej[L::J], Jj_);
+    ldmat<NS>(&ei[L::A], Ai_);
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
       gs = __fma_rn(ca_[q], nj_[q], gs);
@@ -218,11 +245,8 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
     }
     sh[S::G + a] = gs;
     sh[S::H + a] = hs;
-#pragma unroll
-    for (int c = 0; c < NS; ++c) {
-      sh[S::M + a * NS + c] = m_[c];
-      sh[S::V + a * NS + c] = v_[c];
-    }
+    strow<NS>(&sh[S::M + a * NS], m_);
+    strow<NS>(&sh[S::V + a * NS], v_);
   }
   CG_TS(1);
   __syncwarp();
@@ -230,16 +254,10 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
   // P2: T = M^-1 (redundantly per thread, scan_inverse); row a of X = T Ai, Z = T Ci, y = T g
   if (row) {
     double M[NS][NS], T[NS][NS], Ai_[NS][NS], Ci_[NS][NS], g_[NS];
-#pragma unroll
-    for (int r = 0; r < NS; ++r) {
-      g_[r] = sh[S::G + r];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        M[r][c] = sh[S::M + r * NS + c];
-        Ai_[r][c] = ei[L::A + r * NS + c];
-        Ci_[r][c] = ei[L::C + r * NS + c];
-      }
-    }
+    ldrow<NS>(&sh[S::G], g_);
+    ldmat<NS>(&sh[S::M], M);
+    ldmat<NS>(&ei[L::A], Ai_);
+    ldmat<NS>(&ei[L::C], Ci_);
     scan_inverse<NS>(M, T);
     double Ta[NS];
 #pragma unroll
@@ -264,11 +282,8 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
       sz_[c] = sz;
     }
     sh[S::Y + a] = sy;
-#pragma unroll
-    for (int c = 0; c < NS; ++c) {
-      sh[S::X + a * NS + c] = sx_[c];
-      sh[S::Z + a * NS + c] = sz_[c];
-    }
+    strow<NS>(&sh[S::X + a * NS], sx_);
+    strow<NS>(&sh[S::Z + a * NS], sz_);
   }
   CG_TS(3);
   __syncwarp();
@@ -277,21 +292,18 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
   if (row) {
     double aj[NS], y_[NS], h_[NS], X_[NS][NS], Z_[NS][NS], V_[NS][NS], xa[NS], va[NS], ji[NS];
     double sb = ej[L::B + a], se = ei[L::ETA + a];
+    ldrow<NS>(&ej[L::A + a * NS], aj);
+    ldrow<NS>(&sh[S::Y], y_);
+    ldrow<NS>(&sh[S::H], h_);
+    ldrow<NS>(&ei[L::J + a * NS], ji);
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
-      aj[q] = ej[L::A + a * NS + q];
-      y_[q] = sh[S::Y + q];
-      h_[q] = sh[S::H + q];
       xa[q] = sh[S::X + q * NS + a];
       va[q] = sh[S::V + q * NS + a];
-      ji[q] = ei[L::J + a * NS + q];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        X_[q][c] = sh[S::X + q * NS + c];
-        Z_[q][c] = sh[S::Z + q * NS + c];
-        V_[q][c] = sh[S::V + q * NS + c];
-      }
     }
+    ldmat<NS>(&sh[S::X], X_);
+    ldmat<NS>(&sh[S::Z], Z_);
+    ldmat<NS>(&sh[S::V], V_);
 #pragma unroll
     for (int q = 0; q < NS; ++q) sb = __fma_rn(aj[q], y_[q], sb);
 #pragma unroll
@@ -313,29 +325,20 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
     }
     eo[L::B + a] = sb;
     eo[L::ETA + a] = se;
-#pragma unroll
-    for (int c = 0; c < NS; ++c) {
-      eo[L::A + a * NS + c] = oa[c];
-      sh[S::W + a * NS + c] = ow[c];
-      eo[L::J + a * NS + c] = oj[c];
-    }
+    strow<NS>(&eo[L::A + a * NS], oa);
+    strow<NS>(&sh[S::W + a * NS], ow);
+    strow<NS>(&eo[L::J + a * NS], oj);
   }
   CG_TS(4);
   __syncwarp();
   // P4: row a of C_ik = sym(W Aj^T) + Cj
   if (row) {
     double W_[NS][NS], Aj_[NS][NS], wa[NS], aa[NS], cj[NS];
-#pragma unroll
-    for (int r = 0; r < NS; ++r) {
-      wa[r] = sh[S::W + a * NS + r];
-      aa[r] = ej[L::A + a * NS + r];
-      cj[r] = ej[L::C + a * NS + r];
-#pragma unroll
-      for (int q = 0; q < NS; ++q) {
-        W_[r][q] = sh[S::W + r * NS + q];
-        Aj_[r][q] = ej[L::A + r * NS + q];
-      }
-    }
+    ldrow<NS>(&sh[S::W + a * NS], wa);
+    ldrow<NS>(&ej[L::A + a * NS], aa);
+    ldrow<NS>(&ej[L::C + a * NS], cj);
+    ldmat<NS>(&sh[S::W], W_);
+    ldmat<NS>(&ej[L::A], Aj_);
     double oc[NS];
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
@@ -347,11 +350,52 @@ __device__ __forceinline__ void scan_comb_g(ElRef ei, ElRef ej, ElRef eo, int a,
       }
       oc[c] = 0.5 * (s1 + s2) + cj[c];
     }
-#pragma unroll
-    for (int c = 0; c < NS; ++c) eo[L::C + a * NS + c] = oc[c];
+    strow<NS>(&eo[L::C + a * NS], oc);
   }
   CG_TS(5);
 #undef CG_TS
+}
+
+// Row r of stage_assemble (ca_kernels.cuh) for stage t of scene b: the same arithmetic in
+// the same order per entry (H_t row r, h_t entry r; the statistics on row 0), so the stage
+// blocks equal the serial path's bit for bit.  sref / sk: this stage's s_ref and s rows.
+template <int NS>
+__device__ __forceinline__ void stage_assemble_row(const Dev& P, int b, int t, int r, const double* rec, double* out,
+                                                   double* so, const double* Qs, const double* sref,
+                                                   const double* sk) {
+  const int N = P.N, npc = P.npc, L1 = P.d + 1;
+  const double sig = P.sigma;
+  double* ho = out + NS * NS;
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < NS; ++c) {
+    out[r * NS + c] = 2.0 * Qs[r * NS + c];
+    acc += Qs[r * NS + c] * sref[c];
+  }
+  ho[r] = -2.0 * acc;
+  // the pose component a with pidx[a] = r (if any): S (Gauss-Newton block) and g terms
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (a >= npc || P.pidx[a] != r) continue;
+    double spv = (a < L1) ? rec[L1 * (L1 + 1) / 2 + a] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= npc) continue;
+      const int lo = (a <= c) ? a : c, hi = (a <= c) ? c : a;
+      const double Sac = (hi < L1) ? rec[sym_idx(lo, hi, L1)] : 0.0;
+      spv -= Sac * sk[P.pidx[c]];
+      out[r * NS + P.pidx[c]] += sig * Sac;
+    }
+    ho[r] += sig * spv;
+  }
+  if (P.box && box_on(P.box_lim[r], P.box_lim[NS + r])) {  // (rho_b/2) ||s_t - w_t + l_t||^2 (reading #7)
+    const long long k0 = ((long long)b * (N + 1) + t) * NS;
+    out[r * NS + r] += P.box_rho;
+    ho[r] += -P.box_rho * (P.box_ws[k0 + r] - P.box_ls[k0 + r]);
+  }
+  if (r == 0)
+#pragma unroll
+    for (int f = 0; f < NSTAT; ++f) so[f] = rec[P.nagg + f];
 }
 
 // asynchronous 8-byte global -> shared copy (cp.async, L1-allocating) and its wait
@@ -370,17 +414,8 @@ __host__ __device__ inline long long riccati_scan_smem_doubles(int N, int NS, in
   const int SCR = NS * NS * 5 + 3 * NS;        // ScanScr<NS>::SIZE
   const int SBS = (NS * NS + NS) | 1, DBS = (NS * NS + NS * NU + NS) | 1, PHIS = (NS * NS + NS) | 1, XSS = NS | 1;
   return (long long)N * SBS + (long long)NSTAT * N + (long long)(dyn_pt ? N : 1) * DBS + (long long)N * NU * (NS + 1) +
-         (N + 1LL) * (2 * scan_pad(EL) + scan_pad(SCR)) + (long long)N * PHIS + (long long)(N + 1) * XSS + 2LL * N +
+         1 + (N + 1LL) * (2 * scan_pad(EL) + scan_pad(SCR)) + (long long)N * PHIS + (long long)(N + 1) * XSS + 2LL * N +
          NS * NS + 2LL * (N + 1) * NS;
-}
-// the scene's records staged as one block when they fit (see k_riccati_scan)
-__host__ __device__ inline long long riccati_scan_rec_doubles(long long nrec, int rec) { return nrec * rec; }
-// the overlay region the staged records (and their per-(t, field) sums) borrow before the
-// scan needs it: the element buffers, the scratch, the closed-loop maps, the states and
-// the box residuals (contiguous in k_riccati_scan's layout)
-__host__ __device__ inline long long riccati_scan_overlay_doubles(int N, int NS) {
-  const int EL = 3 * NS * NS + 2 * NS, SCR = NS * NS * 5 + 3 * NS, PHIS = (NS * NS + NS) | 1, XSS = NS | 1;
-  return (N + 1LL) * (2 * scan_pad(EL) + scan_pad(SCR)) + (long long)N * PHIS + (long long)(N + 1) * XSS + 2LL * N;
 }
 
 // One CTA per scene, blockDim = SCAN_GS * (N + 1) rounded up to a multiple of 32.
@@ -388,8 +423,7 @@ __host__ __device__ inline long long riccati_scan_overlay_doubles(int N, int NS)
 // element buffers, the combination scratch, the closed-loop maps, the states, and the
 // per-stage box residuals.
 template <int NS, int NU>
-__global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* dst_cur, double* dst_prev,
-                               int stage_recs, int ovx) {
+__global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* dst_cur, double* dst_prev) {
   extern __shared__ double rsm[];
   const int b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
   if (!scene_on(P, b)) return;  // stopped scene (ca_admm_solve)
@@ -405,18 +439,17 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   const int nd = P.dyn_pt ? N : 1;
   double* ric = sdyn + (long long)nd * DBS;   // [N][NU][NS+1]
   constexpr int ELP = scan_pad(EL), SCRP = scan_pad(SCR);  // element / scratch record strides
-  double* E0 = ric + (long long)N * NU * (NS + 1);  // [N+1][ELP]
+  // [N+1][ELP], 16-byte aligned (vector row accesses)
+  double* E0 = ric + (((long long)N * NU * (NS + 1) + (ric - rsm) + 1) & ~1LL) - (ric - rsm);
   double* E1 = E0 + (N + 1LL) * ELP;
   double* scr = E1 + (N + 1LL) * ELP;            // [N+1][SCRP]
   double* phi = scr + (N + 1LL) * SCRP;          // [N][PHIS]: x_{t+1} = Phi_t x_t + phi_t
   double* xs = phi + (long long)N * PHIS;        // [N+1][XSS]
   double* rbx = xs + (long long)(N + 1) * XSS;   // [N] box residual of stage t
-  double* sQs = rbx + 2LL * N + ovx;             // Qs, this scene's s_ref and s rows (ovx: overlay extension)
+  double* sQs = rbx + 2LL * N;                   // Qs, this scene's s_ref and s rows
   double* ssref = sQs + NS * NS;
   double* ss_ = ssref + (long long)(N + 1) * NS;
-  // stage_recs: this scene's records, then their (t, field) sums, overlaid on E0 .. rbx
-  // (riccati_scan_overlay_doubles: free until the elements are built)
-  double* srec = E0;
+  double* rsum = E0;  // [N][rec] per-(t, field) record sums (E0 is free until the elements are built)
 #ifdef CA_RIC_PROFILE
   long long tp[10];
   int np_ = 0;
@@ -425,15 +458,14 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
 #define RIC_TS() ((void)0)
 #endif
   RIC_TS();
-  // (1) bulk copies into shared memory by asynchronous 8-byte copies (cp.async: every
-  // element in flight at once, no register staging): this scene's records (one
-  // contiguous block in the sweep's layout, when stage_recs), Qs, s_ref and s rows, and
-  // the dynamics
+  // (1) asynchronous 8-byte copies into shared memory (cp.async: every element in flight
+  // at once, no register staging) of Qs, this scene's s_ref and s rows and the dynamics;
+  // meanwhile the per-(t, field) sums of the chunk records straight from global memory
+  // (entry k = (t, f): field f of timestep t+1 summed over the chunk records in chunk
+  // order, the max for S_PMAX; the loads of up to RU entries per thread in flight together)
   auto bulk = [&](double* dst, const double* __restrict__ src, long long tot) {
     for (long long k = tid; k < tot; k += nth) cp_async8(dst + k, src + k);
   };
-  const long long per_scene = (long long)P.NG * P.nchunkG * P.TG;  // records of one scene
-  if (stage_recs) bulk(srec, recs + (long long)b * per_scene * P.rec, per_scene * P.rec);
   bulk(sQs, P.Qs, NS * NS);
   bulk(ssref, P.sref + (long long)b * (N + 1) * NS, (long long)(N + 1) * NS);
   bulk(ss_, P.s + (long long)b * (N + 1) * NS, (long long)(N + 1) * NS);
@@ -447,36 +479,59 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
     stage_dyn(P.dynB + idx0 * NS * NU, NS * NU, NS * NS);
     stage_dyn(P.dync + idx0 * NS, NS, NS * NS + NS * NU);
   }
+  {
+    const int RC = P.rec, fm = P.nagg + S_PMAX, nc = nchunk ? nchunk : 1, tot = N * RC;
+    CA_CHECK(rsum + (long long)tot <= E0 + (N + 1LL) * ELP);
+    constexpr int RU = 4, CU = 4;  // entries per thread in flight together; chunks per batch
+    for (int k0 = tid; k0 < tot; k0 += RU * nth) {
+      const double* src[RU];
+      long long step = 0;
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const int k = k0 + u * nth, kk = (k < tot) ? k : 0;
+        const int t = kk / RC, f = kk - t * RC;
+        // rec_index(P, b, t + 1, c) = base + c TG (the sweep's layout), else (scene, t)
+        const long long base =
+            nchunk ? (((long long)b * P.NG + t / P.TG) * P.nchunkG) * P.TG + t % P.TG : (long long)b * N + t;
+        src[u] = recs + base * RC + f;
+        step = (long long)P.TG * RC;
+      }
+      double acc[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) acc[u] = 0.0;
+      for (int c0 = 0; c0 < nc; c0 += CU) {
+        double v[RU][CU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+#pragma unroll
+          for (int cc = 0; cc < CU; ++cc)
+            v[u][cc] = (k0 + u * nth < tot && c0 + cc < nc) ? __ldg(src[u] + (c0 + cc) * step) : 0.0;
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const bool mx = (k0 + u * nth) % RC == fm;
+#pragma unroll
+          for (int cc = 0; cc < CU; ++cc)
+            if (c0 + cc < nc) acc[u] = mx ? fmax(acc[u], v[u][cc]) : acc[u] + v[u][cc];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u)
+        if (k0 + u * nth < tot) rsum[k0 + u * nth] = acc[u];
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
   RIC_TS();
-  // stage blocks: the (timestep, field) sums in parallel -- entry k = (t, f) sums field f
-  // of timestep t+1 over the chunk records in chunk order (max for S_PMAX) into rsum
-  // [N][rec] (the second element buffer and the scratch, free until the scan: (EL + SCR)
-  // (N + 1) >= 22 N doubles) -- then thread t assembles stage t+1 from its row
   {
-    double* rsum = E0 + (stage_recs ? per_scene * P.rec : 0);
-    const int RC = P.rec, fm = P.nagg + S_PMAX, nc = nchunk ? nchunk : 1;
-    CA_CHECK(rsum + (long long)N * RC <= rbx + 2LL * N + ovx);
-    const long long rb0 = (long long)b * per_scene;
-    for (int k = tid; k < N * RC; k += nth) {
-      const int t = k / RC, f = k - t * RC;
-      // rec_index(P, b, t + 1, c) = base + c TG
-      const long long base = (((long long)b * P.NG + t / P.TG) * P.nchunkG) * P.TG + t % P.TG;
-      double acc = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < nc; ++c) {
-        const double v0 = stage_recs ? srec[(base + (long long)c * P.TG - rb0) * RC + f]
-                                     : recs[(nchunk ? base + (long long)c * P.TG : (long long)b * N + t) * RC + f];
-        acc = (f == fm) ? fmax(acc, v0) : acc + v0;
-      }
-      rsum[k] = acc;
+    const int RC = P.rec;
+    // stage_assemble's H_t, h_t and statistics, row r of stage t+1 on thread (t, r)
+    for (int t0 = 0; t0 < N; t0 += nth / SCAN_GS) {
+      const int t = t0 + tid / SCAN_GS, r = tid % SCAN_GS;
+      if (t < N && r < NS)
+        stage_assemble_row<NS>(P, b, t + 1, r, rsum + (long long)t * RC, sstg + (long long)t * SBS,
+                               sst + (long long)NSTAT * t, sQs, ssref + (long long)(t + 1) * NS,
+                               ss_ + (long long)(t + 1) * NS);
     }
-    __syncthreads();
-    RIC_TS();
-    for (int t = tid; t < N; t += nth)
-      stage_assemble(P, (long long)b * N + t, rsum + (long long)t * RC, sstg + (long long)t * SBS,
-                     sst + (long long)NSTAT * t, sQs, ssref, ss_);
   }
   __syncthreads();
   RIC_TS();
@@ -717,7 +772,10 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
 #pragma unroll
       for (int a = 0; a < NS; ++a) v[a] = (c < NS && a == c) ? 1.0 : 0.0;
       const int t1 = min(N, (j + 1) * FC);
-      for (int t = j * FC; t < t1; ++t) {
+#pragma unroll
+      for (int u = 0; u < FC; ++u) {
+        const int t = j * FC + u;
+        if (t >= t1) break;
         const double* ph = phi + (long long)t * PHIS;
         double w[NS];
 #pragma unroll
@@ -764,7 +822,10 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
 #pragma unroll
       for (int a = 0; a < NS; ++a) x[a] = xs[(long long)j * FC * XSS + a];
       const int t1 = min(N, (j + 1) * FC);
-      for (int t = j * FC; t < t1; ++t) {
+#pragma unroll
+      for (int u = 0; u < FC; ++u) {
+        const int t = j * FC + u;
+        if (t >= t1) break;
         const double* ph = phi + (long long)t * PHIS;
         double xn[NS];
 #pragma unroll
@@ -841,10 +902,9 @@ __global__ void k_riccati_scan(Dev P, const double* recs, int nchunk, double* ds
   RIC_TS();
 #ifdef CA_RIC_PROFILE
   if (tid == 0 && b == 0)
-    printf("stage_recs %d ovx %d nchunk %d per_scene %lld\n", stage_recs, ovx, nchunk, (long long)P.NG * P.nchunkG * P.TG);
-    printf("ric_scan cycles: loads %lld sums %lld assemble %lld elements %lld scan %lld gains %lld forward %lld "
+    printf("ric_scan cycles: loads+sums %lld assemble %lld elements %lld scan %lld gains %lld forward %lld "
            "stages+stats %lld\n", tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5],
-           tp[7] - tp[6], tp[8] - tp[7]);
+           tp[7] - tp[6]);
 #endif
 #undef RIC_TS
 }
