@@ -237,7 +237,7 @@ ca_status validate(const ca_problem_desc* D) {
     if (D->pose_idx[a] < 0 || D->pose_idx[a] >= D->n_state) return fail(CA_E_DIM, "pose index out of range");
   if (!riccati_supported(D->n_state, D->n_ctrl))
     return fail(CA_E_UNSUPPORTED, "(n_state, n_ctrl) combination not instantiated");
-  if (ca::riccati_smem_doubles(D->horizon, D->n_state, D->n_ctrl, D->dyn_per_time != 0) * 8 > 227 * 1024)
+  if (ca::riccati_k_smem_doubles(D->horizon, D->n_state, D->n_ctrl, D->dyn_per_time != 0) * 8 > 227 * 1024)
     return fail(CA_E_UNSUPPORTED, "horizon too long for the shared-memory Riccati step");
   if (D->n_parts > ca::NPMAX) return fail(CA_E_UNSUPPORTED, "more than 8 robot parts");
   if ((long long)D->n_parts * D->n_obs > 65535) return fail(CA_E_UNSUPPORTED, "more than 65535 pairs per (scene, t)");
@@ -562,7 +562,7 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
       return CA_OK;
     }
   }
-  const size_t sm = sizeof(double) * (size_t)ca::riccati_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
+  const size_t sm = sizeof(double) * (size_t)ca::riccati_k_smem_doubles(h->N, NS, NU, h->dev.dyn_pt != 0);
   if (sm > 48 * 1024) {  // the attribute is per device: cached per device ordinal under a lock
     static std::mutex mu;
     static size_t configured[CA_MAX_DEVICES] = {};
@@ -574,7 +574,7 @@ ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double
       configured[h->device] = sm;
     }
   }
-  ca::k_riccati<NS, NU><<<(unsigned)h->B, 32, sm, h->stream>>>(h->dev, recs, nchunk, cur, prev);
+  ca::k_riccati<NS, NU><<<(unsigned)h->B, 32 * ca::RIC_WARPS, sm, h->stream>>>(h->dev, recs, nchunk, cur, prev);
   CUDA_TRY(cudaGetLastError());
   return CA_OK;
 }

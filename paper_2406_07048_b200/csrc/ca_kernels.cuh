@@ -1028,16 +1028,23 @@ __host__ __device__ inline long long riccati_smem_doubles(int N, int NS, int NU,
   return (long long)N * (NS * NS + NS) + (long long)NSTAT * N + (dyn_pt ? N : 1) * (NS * NS + NS * NU + NS) +
          (long long)N * NU * (NS + 1);
 }
+// ... and with its per-(t, field) record sums
+__host__ __device__ inline long long riccati_k_smem_doubles(int N, int NS, int NU, bool dyn_pt) {
+  return riccati_smem_doubles(N, NS, NU, dyn_pt) + (long long)N * RECMAX;
+}
 
-// One CTA (one warp) per scene: the lanes assemble the N stage blocks from the
-// sweep records (fixed order per (scene, t)) and stage this scene's dynamics in
-// shared memory with coalesced loads; lane 0 then runs the O(N) recursion out of
-// shared memory (no global-memory latency on the dependent chain).
+// One CTA per scene, RIC_WARPS warps: all of them sum the chunk records per (t, field)
+// (loads of several entries in flight together; chunk order fixed per (scene, t)),
+// assemble the N stage blocks and stage this scene's dynamics in shared memory; warp 0
+// then runs the O(N) recursion out of shared memory (no global-memory latency on the
+// dependent chain).  (One warp alone spent ~100 us of C3's latency-mode iteration --
+// 24 records per (scene, t) -- summing them.)
+constexpr int RIC_WARPS = 8;
 template <int NS, int NU>
-__global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int nchunk, double* dst_cur,
-                                               double* dst_prev) {
+__global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double* recs, int nchunk, double* dst_cur,
+                                                           double* dst_prev) {
   extern __shared__ double rsm[];
-  const int b = blockIdx.x, lane = threadIdx.x;
+  const int b = blockIdx.x, lane = threadIdx.x & 31, tid = threadIdx.x, nth = blockDim.x;
   if (!scene_on(P, b)) return;  // stopped scene (ca_admm_solve)
   const int N = P.N;
   constexpr int SB = NS * NS + NS, DB = NS * NS + NS * NU + NS;
@@ -1048,30 +1055,50 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
   double* ric = sdyn + (long long)nd * DB;  // [N][NU][NS+1]: feedback K_t | k_t
   // recursion work area (static): value function, products, gains
   __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Qux[NU][NS + 1], xs[NS], xs2[NS];
-  // stage blocks: each lane sums the records of two timesteps (all loads in flight
-  // before either block is assembled), same chunk order as stage_block
-  for (int t0 = lane; t0 < N; t0 += 64) {
-    const int t1 = t0 + 32;
-    double ra[RECMAX], rb[RECMAX];
+  double* rsum = ric + (long long)N * NU * (NS + 1);  // [N][rec] record sums (riccati_smem_doubles)
+  // stage blocks: entry k = (t, f) sums field f of timestep t+1 over the chunk records in
+  // chunk order (max for S_PMAX) -- the order of stage_block -- with the loads of RU
+  // entries x CU chunks per thread in flight together; then thread t assembles stage t+1
+  {
+    const int RC = P.rec, fm = P.nagg + S_PMAX, nc = nchunk ? nchunk : 1, tot = N * RC;
+    constexpr int RU = 4, CU = 4;
+    for (int k0 = tid; k0 < tot; k0 += RU * nth) {
+      const double* src[RU];
+      long long step = 0;
 #pragma unroll
-    for (int f = 0; f < RECMAX; ++f) ra[f] = rb[f] = 0.0;
-    const long long q0 = (long long)b * N + t0, q1 = q0 + 32;
-    const int RC = P.rec, fm = P.nagg + S_PMAX;
-#pragma unroll 4
-    for (int c = 0; c < (nchunk ? nchunk : 1); ++c) {
-      const double* r0 = recs + (nchunk ? rec_index(P, b, t0 + 1, c) : q0) * RC;
-      const double* r1 = recs + (nchunk ? rec_index(P, b, min(t1, N - 1) + 1, c) : min(q1, q0 - t0 + N - 1)) * RC;
-#pragma unroll
-      for (int f = 0; f < RECMAX; ++f) {
-        if (f >= RC) continue;
-        const double v0 = __ldg(r0 + f), v1 = __ldg(r1 + f);
-        ra[f] = (f == fm) ? fmax(ra[f], v0) : ra[f] + v0;
-        rb[f] = (f == fm) ? fmax(rb[f], v1) : rb[f] + v1;
+      for (int u = 0; u < RU; ++u) {
+        const int k = k0 + u * nth, kk = (k < tot) ? k : 0;
+        const int t = kk / RC, f = kk - t * RC;
+        src[u] = recs + (nchunk ? rec_index(P, b, t + 1, 0) : (long long)b * N + t) * RC + f;
+        step = (long long)P.TG * RC;  // rec_index(.., c + 1) - rec_index(.., c) = TG
       }
+      double acc[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) acc[u] = 0.0;
+      for (int c0 = 0; c0 < nc; c0 += CU) {
+        double v[RU][CU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+#pragma unroll
+          for (int cc = 0; cc < CU; ++cc)
+            v[u][cc] = (k0 + u * nth < tot && c0 + cc < nc) ? __ldg(src[u] + (c0 + cc) * step) : 0.0;
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const bool mx = (k0 + u * nth) % RC == fm;
+#pragma unroll
+          for (int cc = 0; cc < CU; ++cc)
+            if (c0 + cc < nc) acc[u] = mx ? fmax(acc[u], v[u][cc]) : acc[u] + v[u][cc];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u)
+        if (k0 + u * nth < tot) rsum[k0 + u * nth] = acc[u];
     }
-    stage_assemble(P, q0, ra, sstg + (long long)t0 * SB, sst + (long long)NSTAT * t0);
-    if (t1 < N) stage_assemble(P, q1, rb, sstg + (long long)t1 * SB, sst + (long long)NSTAT * t1);
   }
+  __syncthreads();
+  for (int t = tid; t < N; t += nth)
+    stage_assemble(P, (long long)b * N + t, rsum + (long long)t * P.rec, sstg + (long long)t * SB,
+                   sst + (long long)NSTAT * t);
   {
     // dynamics blocks, 8 coalesced loads in flight per lane before their stores (a
     // load-store loop would serialise one global round trip per element)
@@ -1079,16 +1106,16 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
     auto stage_dyn = [&](const double* __restrict__ src, int blk, int off) {
       constexpr int U = 8;
       const int tot = nd * blk;
-      for (int k0 = lane; k0 < tot; k0 += 32 * U) {
+      for (int k0 = tid; k0 < tot; k0 += nth * U) {
         double v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int k = k0 + 32 * u;
+          const int k = k0 + nth * u;
           v[u] = (k < tot) ? __ldg(src + k) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int k = k0 + 32 * u;
+          const int k = k0 + nth * u;
           if (k < tot) sdyn[(k / blk) * DB + off + k % blk] = v[u];
         }
       }
@@ -1097,7 +1124,8 @@ __global__ void __launch_bounds__(32) k_riccati(Dev P, const double* recs, int n
     stage_dyn(P.dynB + idx0 * NS * NU, NS * NU, NS * NS);
     stage_dyn(P.dync + idx0 * NS, NS, NS * NS + NS * NU);
   }
-  __syncwarp();
+  __syncthreads();
+  if (tid >= 32) return;  // the recursion: warp 0
   // The recursion is a chain of small dependent products.  For n_s <= 4 one thread
   // with every matrix in registers and its operands in shared memory is fastest
   // (C4: 126 vs 135 us per ADMM iteration); larger states would spill, so they split
