@@ -1050,23 +1050,6 @@ ca_status setup_handle(ca_problem* h, const ca_problem_desc* D) {
 }
 
 // create a handle for the (rank-local) problem D; g = its grid position (NULL: one GPU)
-// Every kernel of an ADMM iteration prefers the same L1 / shared-memory split as the
-// sweep (all shared): the SMs are not reconfigured between consecutive kernels, which
-// costs microseconds per switch on the single-scene configurations.  Once per device.
-static ca_status prefer_shared_carveout(int device) {
-  static std::mutex mu;
-  static bool done[CA_MAX_DEVICES] = {};
-  if (device >= CA_MAX_DEVICES) return fail(CA_E_CUDA, "device ordinal too large");
-  std::lock_guard<std::mutex> lk(mu);
-  if (done[device]) return CA_OK;
-  const void* ks[] = {(const void*)ca::k_sortpairs, (const void*)ca::k_stage_grouped, (const void*)ca::k_stage,
-                      (const void*)ca::k_mult<2>, (const void*)ca::k_mult<3>, (const void*)ca::k_collect,
-                      (const void*)ca::k_hist};
-  for (const void* k : ks) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  done[device] = true;
-  return CA_OK;
-}
-
 ca_status create_impl(const ca_problem_desc* D, int device, void* stream, const GridPos* g, ca_problem** out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
@@ -1075,7 +1058,6 @@ ca_status create_impl(const ca_problem_desc* D, int device, void* stream, const 
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) return fail(CA_E_CUDA, "built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
   CUDA_TRY(cudaSetDevice(device));
-  if (ca_status st0 = prefer_shared_carveout(device)) return st0;
   ca_problem* h = new ca_problem();
   h->device = device;
   h->stream = static_cast<cudaStream_t>(stream);

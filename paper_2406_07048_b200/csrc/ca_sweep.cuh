@@ -314,15 +314,33 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
     for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
     return v;
   };
-  auto col = [&](int c) {  // T[c] for a run-time column c (select, no indexed access)
-    double v = 0.0;
-#pragma unroll
-    for (int j = 0; j < WC; ++j) v = (j == c) ? T[j] : v;
-    return v;
+  // min / max over the warp of NON-NEGATIVE doubles, exactly, by two integer reductions
+  // on the bit patterns (for x, y >= 0 the IEEE order is the unsigned (hi, lo) order)
+  auto wmin_nn = [&](double v) {
+    const unsigned long long u = __double_as_longlong(v == 0.0 ? 0.0 : v);  // -0 -> +0
+    const unsigned hi = (unsigned)(u >> 32), lo = (unsigned)u;
+    const unsigned mh = __reduce_min_sync(FULL, hi);
+    const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
   };
-  // L3 pivot on (row r, column c): row r / T[r][c]; other rows fma(-T_ic, T_rj, T_ij)
-  auto pivot = [&](int r, int c) {
-    const double tc = col(c);
+  auto wmax_nn = [&](double v) {
+    const unsigned long long u = __double_as_longlong(v == 0.0 ? 0.0 : v);  // -0 -> +0
+    const unsigned hi = (unsigned)(u >> 32), lo = (unsigned)u;
+    const unsigned mh = __reduce_max_sync(FULL, hi);
+    const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+  };
+  auto col = [&](int c) {  // T[c] for a run-time column c: four short select chains, then one
+    constexpr int GS = (WC + 3) / 4;  // of them (dependent depth GS + 3 instead of WC)
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < WC; ++j) v[j / GS] = (j == c) ? T[j] : v[j / GS];
+    return (c < GS) ? v[0] : (c < 2 * GS) ? v[1] : (c < 3 * GS) ? v[2] : v[3];
+  };
+  // L3 pivot on (row r, column c), tc = this lane's T[c]: row r / T[r][c]; other rows
+  // fma(-T_ic, T_rj / T[r][c], T_ij).  The unscaled pivot row is broadcast while the
+  // reciprocal is formed; every lane scales it (the same product lane r forms).
+  auto pivot = [&](int r, int c, double tc) {
     const double inv = 1.0 / __shfl_sync(FULL, own ? tc : 0.0, r);
     if (lane == r) {
 #pragma unroll
@@ -347,7 +365,7 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
     const double tl = qmin + tau * fmax(1.0, fabs(qmin));
     const int r = 31 - __clz(__ballot_sync(FULL, own && T[RHS] <= tl));  // ties -> largest index
     const int leaving = r;                                               // basis[r] = w_r
-    pivot(r, Z0);
+    pivot(r, Z0, T[Z0]);
     if (lane == r) basis = Z0;
     ++pivots;
     int entering = NMAX + leaving;  // z_r
@@ -355,11 +373,11 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
     for (;;) {
       if (pivots >= maxpiv) { status = ST_ITER; break; }
       const double ci = own ? col(entering) : 0.0;
-      const double cmax = -wmin(own ? -fabs(ci) : 0.0);
+      const double cmax = wmax_nn(fabs(ci));
       const double thr = LP.pivot_tol * fmax(1.0, cmax);
       const bool el = own && ci > thr;
       const double th = el ? fmax(T[RHS], 0.0) / ci : 1e308;
-      const double thmin = wmin(th);
+      const double thmin = wmin_nn(th);
       if (!(thmin < 1e308)) { status = ST_RAY; break; }
       const double ttol = thmin + tau * fmax(1.0, thmin);
       uint32_t tie = __ballot_sync(FULL, el && th <= ttol);
@@ -380,7 +398,7 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
         r2 = __ffs(tie) - 1;  // L5.5: smallest row
       }
       const int leaving2 = __shfl_sync(FULL, basis, r2);
-      pivot(r2, entering);
+      pivot(r2, entering, ci);
       if (lane == r2) basis = entering;
       ++pivots;
       if (leaving2 == Z0) break;
