@@ -337,11 +337,11 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
     for (int j = 0; j < WC; ++j) v[j / GS] = (j == c) ? T[j] : v[j / GS];
     return (c < GS) ? v[0] : (c < 2 * GS) ? v[1] : (c < 3 * GS) ? v[2] : v[3];
   };
-  // L3 pivot on (row r, column c), tc = this lane's T[c]: row r / T[r][c]; other rows
-  // fma(-T_ic, T_rj / T[r][c], T_ij).  The unscaled pivot row is broadcast while the
-  // reciprocal is formed; every lane scales it (the same product lane r forms).
-  auto pivot = [&](int r, int c, double tc) {
-    const double inv = 1.0 / __shfl_sync(FULL, own ? tc : 0.0, r);
+  // L3 pivot on (row r, column c), tc = this lane's T[c] and rc = 1 / tc (formed by every
+  // lane beforehand, off the chain; lane r's is the one division of the rule): row r
+  // scaled by it, other rows fma(-T_ic, T_rj, T_ij)
+  auto pivot = [&](int r, int c, double tc, double rc) {
+    const double inv = __shfl_sync(FULL, own ? rc : 0.0, r);
     if (lane == r) {
 #pragma unroll
       for (int j = 0; j < WC; ++j)
@@ -365,7 +365,7 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
     const double tl = qmin + tau * fmax(1.0, fabs(qmin));
     const int r = 31 - __clz(__ballot_sync(FULL, own && T[RHS] <= tl));  // ties -> largest index
     const int leaving = r;                                               // basis[r] = w_r
-    pivot(r, Z0, T[Z0]);
+    pivot(r, Z0, T[Z0], 1.0 / T[Z0]);
     if (lane == r) basis = Z0;
     ++pivots;
     int entering = NMAX + leaving;  // z_r
@@ -377,6 +377,7 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
       const double thr = LP.pivot_tol * fmax(1.0, cmax);
       const bool el = own && ci > thr;
       const double th = el ? fmax(T[RHS], 0.0) / ci : 1e308;
+      const double rci = 1.0 / ci;  // the pivot's reciprocal if this row leaves
       const double thmin = wmin_nn(th);
       if (!(thmin < 1e308)) { status = ST_RAY; break; }
       const double ttol = thmin + tau * fmax(1.0, thmin);
@@ -398,7 +399,7 @@ __device__ __noinline__ int lemke_warp_reg(const PairRows<D> W, const double bti
         r2 = __ffs(tie) - 1;  // L5.5: smallest row
       }
       const int leaving2 = __shfl_sync(FULL, basis, r2);
-      pivot(r2, entering, ci);
+      pivot(r2, entering, ci, rci);
       if (lane == r2) basis = entering;
       ++pivots;
       if (leaving2 == Z0) break;
