@@ -257,19 +257,6 @@ __device__ __forceinline__ void group_reduce(double* col0, int lane, int tl, int
     out[tt * stride + f0 + f] = acc;
   }
 #else
-  // one pair in the warp (the latency mode's one pair per warp, on lane 0): its record
-  // alone -- the lane-ordered sum it equals (0 + x, the other terms absent)
-  if (__ballot_sync(0xffffffffu, tl >= 0) == 1u) {
-    const int tt0 = __shfl_sync(0xffffffffu, tl, 0);
-    __syncwarp();
-    for (int o = lane; o < TG * NFIELD; o += 32) {
-      const int tt = o / NFIELD, f = o % NFIELD;
-      const double v = (tt == tt0) ? col0[f * 32] : 0.0;
-      out[tt * stride + f0 + f] = (f == fmx) ? fmax(0.0, v) : 0.0 + v;
-    }
-    __syncwarp();
-    return;
-  }
   int* stl = reinterpret_cast<int*>(col0 + NFIELD * 32);
   stl[lane] = tl;
   __syncwarp();
