@@ -57,6 +57,9 @@
 #ifndef CA_SWEEP_PERSIST
 #define CA_SWEEP_PERSIST 1  // persistent warps pulling work items (no per-CTA launch / retire gaps)
 #endif
+#ifndef CA_SWEEP_PREFETCH
+#define CA_SWEEP_PREFETCH 0  // 1: claim the next work item one ahead, prefetch its pair data into L2 (C5: 23.16 -> 24.15 ms, dropped)
+#endif
 #ifndef CA_SWEEP_MINB
 #define CA_SWEEP_MINB 16  // resident warps per SM the register budget targets
 #endif
@@ -76,6 +79,8 @@ constexpr int MFAST = 3;   // m x m systems up to this size live in shared memor
 
 // Tableau-row labels (L5.5 final tie-break): 4-bit fields of one register when
 // they fit (NMAX <= 15: labels <= 14, slot NMAX holds z0's row), else bytes in smem.
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 template <int NMAX, bool REG = (NMAX <= 15)>
 struct RowLab {
   uint64_t v;
@@ -755,12 +760,27 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
 #if CA_SWEEP_PERSIST
   // persistent warps: every warp pulls (b, group, chunk) work items from a
   // counter (reset by k_sortpairs); results depend only on the item, not on which
-  // warp ran it, so the order of the pulls does not change any output bit
+  // warp ran it, so the order of the pulls does not change any output bit.  With
+  // CA_SWEEP_PREFETCH the next item is claimed one ahead and its pairs' y^k, zeta, xi
+  // and pose lines are prefetched into L2 while this item is solved.
+  int nxt = 0;
+  if (CA_SWEEP_PREFETCH) {
+    if (tid == 0) nxt = atomicAdd(P.work, 1);
+    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  }
   for (;;) {
   int item = 0;
-  if (tid == 0) item = atomicAdd(P.work, 1);
-  item = __shfl_sync(0xffffffffu, item, 0);
-  if (item >= P.nitems) break;
+  if (CA_SWEEP_PREFETCH) {
+    item = nxt;
+    if (item >= P.nitems) break;
+    int n2 = 0;
+    if (tid == 0) n2 = atomicAdd(P.work, 1);
+    nxt = __shfl_sync(0xffffffffu, n2, 0);
+  } else {
+    if (tid == 0) item = atomicAdd(P.work, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= P.nitems) break;
+  }
 #else
   for (int item = blockIdx.x * WPC + warp, once = 1; once && item < P.nitems; once = 0) {
 #endif
@@ -790,6 +810,18 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
   bool z0b = false, fallback = false;
   const uint32_t pk = (tid < P.CHG && gs < it.size) ? P.gperm2[((long long)b * P.NG + it.grp) * P.GG + gs]
                                                     : PAIR_UNSENSED;
+  // the next item's pair of this lane (prefetch, CA_SWEEP_PREFETCH): its slot, loaded now
+  uint32_t pk2 = PAIR_UNSENSED;
+  int b2 = 0, grp2 = 0;
+#if CA_SWEEP_PERSIST
+  if (CA_SWEEP_PREFETCH && nxt < P.nitems) {
+    const Item i2 = item_of(P, nxt);
+    const int gs2 = i2.chunk * P.CHG + tid;
+    b2 = i2.b;
+    grp2 = i2.grp;
+    if (tid < P.CHG && gs2 < i2.size) pk2 = P.gperm2[((long long)b2 * P.NG + grp2) * P.GG + gs2];
+  }
+#endif
 #ifndef CA_EXP_NO_SENSE
   const bool act = !(pk & PAIR_UNSENSED);  // padding lane or unsensed obstacle (NEXT f3): idle
 #else
@@ -892,6 +924,18 @@ __global__ void __launch_bounds__(CTA * WPC, CA_SWEEP_MINB / WPC) k_sweep(Dev P)
       for (int c = 0; c <= D; ++c) acc = __fma_rn(f[c], bt_[c], acc);
       VAL(i) = acc;
       qmin = fmin(qmin, acc);
+    }
+    if (CA_SWEEP_PREFETCH && !(pk2 & PAIR_UNSENSED)) {  // the next item's pair data into L2
+      int tl2, ip2, j2;
+      unpack_pair(pk2, tl2, ip2, j2);
+      const long long bt2 = (long long)b2 * P.N + grp2 * P.TG + tl2;
+      const long long p2 = bt2 * P.G + ip2 * P.M + j2;
+      prefetch_l2(P.zeta + p2);
+#pragma unroll
+      for (int a = 0; a < D; ++a) prefetch_l2(P.xi + (long long)a * PP + p2);
+#pragma unroll 1
+      for (int k = 0; k < P.ny; ++k) prefetch_l2(P.y + (long long)k * PP + p2);
+      prefetch_l2(P.pose + bt2 * 12);
     }
     // ------------------------------------------------------------------ Lemke  // @region lemke_init
     const LemkeParams& LP = P.lp;
