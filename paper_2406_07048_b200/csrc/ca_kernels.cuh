@@ -584,8 +584,8 @@ __global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
 // dominated by this solve); n_u = 4: Cholesky with reciprocal diagonal.
 template <int NU>
 struct QuuSolve {
-  double m[NU][NU];  // adjugate (n_u <= 3) or Cholesky factor (n_u = 4)
-  double inv[NU];    // 1/det in inv[0] (n_u <= 3) or 1/L_jj
+  double m[NU][NU];  // adjugate (n_u <= 4) or Cholesky factor (n_u > 4)
+  double inv[NU];    // 1/det in inv[0] (n_u <= 4) or 1/L_jj
   __device__ __forceinline__ void factor(const double Q[NU][NU]) {
     if constexpr (NU == 1) {
       m[0][0] = 1.0;
@@ -607,6 +607,34 @@ struct QuuSolve {
       m[2][1] = Q[0][1] * Q[2][0] - Q[0][0] * Q[2][1];
       m[2][2] = Q[0][0] * Q[1][1] - Q[0][1] * Q[1][0];
       inv[0] = 1.0 / (Q[0][0] * m[0][0] + Q[0][1] * m[1][0] + Q[0][2] * m[2][0]);
+    } else if constexpr (NU == 4) {
+      // adjugate from the 2 x 2 minors of rows (0, 1) and (2, 3), one reciprocal of the
+      // determinant (Quu is SPD: det > 0); a short dependent chain where the Cholesky
+      // factor needs four square roots and four divisions in sequence (C3: ~1/3 of the
+      // per-step latency of the warp recursion)
+      const double s0 = Q[0][0] * Q[1][1] - Q[1][0] * Q[0][1], s1 = Q[0][0] * Q[1][2] - Q[1][0] * Q[0][2];
+      const double s2 = Q[0][0] * Q[1][3] - Q[1][0] * Q[0][3], s3 = Q[0][1] * Q[1][2] - Q[1][1] * Q[0][2];
+      const double s4 = Q[0][1] * Q[1][3] - Q[1][1] * Q[0][3], s5 = Q[0][2] * Q[1][3] - Q[1][2] * Q[0][3];
+      const double c5 = Q[2][2] * Q[3][3] - Q[3][2] * Q[2][3], c4 = Q[2][1] * Q[3][3] - Q[3][1] * Q[2][3];
+      const double c3 = Q[2][1] * Q[3][2] - Q[3][1] * Q[2][2], c2 = Q[2][0] * Q[3][3] - Q[3][0] * Q[2][3];
+      const double c1 = Q[2][0] * Q[3][2] - Q[3][0] * Q[2][2], c0 = Q[2][0] * Q[3][1] - Q[3][0] * Q[2][1];
+      m[0][0] = Q[1][1] * c5 - Q[1][2] * c4 + Q[1][3] * c3;
+      m[0][1] = -Q[0][1] * c5 + Q[0][2] * c4 - Q[0][3] * c3;
+      m[0][2] = Q[3][1] * s5 - Q[3][2] * s4 + Q[3][3] * s3;
+      m[0][3] = -Q[2][1] * s5 + Q[2][2] * s4 - Q[2][3] * s3;
+      m[1][0] = -Q[1][0] * c5 + Q[1][2] * c2 - Q[1][3] * c1;
+      m[1][1] = Q[0][0] * c5 - Q[0][2] * c2 + Q[0][3] * c1;
+      m[1][2] = -Q[3][0] * s5 + Q[3][2] * s2 - Q[3][3] * s1;
+      m[1][3] = Q[2][0] * s5 - Q[2][2] * s2 + Q[2][3] * s1;
+      m[2][0] = Q[1][0] * c4 - Q[1][1] * c2 + Q[1][3] * c0;
+      m[2][1] = -Q[0][0] * c4 + Q[0][1] * c2 - Q[0][3] * c0;
+      m[2][2] = Q[3][0] * s4 - Q[3][1] * s2 + Q[3][3] * s0;
+      m[2][3] = -Q[2][0] * s4 + Q[2][1] * s2 - Q[2][3] * s0;
+      m[3][0] = -Q[1][0] * c3 + Q[1][1] * c1 - Q[1][2] * c0;
+      m[3][1] = Q[0][0] * c3 - Q[0][1] * c1 + Q[0][2] * c0;
+      m[3][2] = -Q[3][0] * s3 + Q[3][1] * s1 - Q[3][2] * s0;
+      m[3][3] = Q[2][0] * s3 - Q[2][1] * s1 + Q[2][2] * s0;
+      inv[0] = 1.0 / ((s0 * c5 - s1 * c4) + (s2 * c3 + s3 * c2) + (s5 * c0 - s4 * c1));
     } else {
 #pragma unroll
       for (int a = 0; a < NU; ++a)
@@ -632,7 +660,7 @@ struct QuuSolve {
   }
   // r <- Quu^{-1} r
   __device__ __forceinline__ void apply(double r[NU]) const {
-    if constexpr (NU <= 3) {
+    if constexpr (NU <= 4) {
       double x[NU];
 #pragma unroll
       for (int a = 0; a < NU; ++a) {
