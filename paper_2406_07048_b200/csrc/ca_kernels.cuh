@@ -1082,7 +1082,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
   const int nd = P.dyn_pt ? N : 1;
   double* ric = sdyn + (long long)nd * DB;  // [N][NU][NS+1]: feedback K_t | k_t
   // recursion work area (static): value function, products, gains
-  __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Qux[NU][NS + 1], xs[NS], xs2[NS];
+  __shared__ double Pm[NS][NS], pv[NS], PA[NS][NS], PB[NS][NU], w[NS], Qux[NU][NS + 1], QuuS[NU][NU], xs[NS], xs2[NS];
   double* rsum = ric + (long long)N * NU * (NS + 1);  // [N][rec] record sums (riccati_smem_doubles)
   // stage blocks: entry k = (t, f) sums field f of timestep t+1 over the chunk records in
   // chunk order (max for S_PMAX) -- the order of stage_block -- with the loads of RU
@@ -1186,11 +1186,12 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     urho[a_] = (P.box && box_on(ulo[a_], uhi[a_])) ? P.box_rho : 0.0;
   }
   const double box_res_prev = (P.box && lane == 0) ? P.box_res[b] : 0.0;
-  double qu2[NU][NU];  // 2 Qu (+ rho_b on bounded controls), kept in registers
+  auto urho_at = [&](int i) {  // urho[i] for a run-time i (select: no local-memory array)
+    double v = 0.0;
 #pragma unroll
-  for (int a_ = 0; a_ < NU; ++a_)
-#pragma unroll
-    for (int c = 0; c < NU; ++c) qu2[a_][c] = 2.0 * P.Qu[a_ * NU + c] + ((a_ == c) ? urho[a_] : 0.0);
+    for (int j = 0; j < NU; ++j) v = (j == i) ? urho[j] : v;
+    return v;
+  };
   // P_N = H_N, p_N = h_N
   for (int k = lane; k < SB; k += 32) {
     const double v = sstg[(long long)(N - 1) * SB + k];
@@ -1227,30 +1228,39 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
       }
     }
     __syncwarp();
-    // phase 2: lane c <= NS forms Quu = 2Qu + B^T P B (every lane the same, no
-    // exchange), its column c of [Qux | qu] = B^T [P A | w], factors Quu = L L^T and
-    // solves column c of the gains -Quu^{-1} [Qux | qu]
+    // phase 2a: the entries of Quu = 2Qu + B^T P B and of [Qux | qu] = B^T [P A | w], one
+    // per lane (same sums, same order as k_riccati_thread)
+    for (int k = lane; k < NU * NU + NU * (NS + 1); k += 32) {
+      if (k < NU * NU) {
+        const int a_ = k / NU, cc = k % NU;
+        double s_ = 2.0 * P.Qu[a_ * NU + cc] + ((a_ == cc) ? urho_at(a_) : 0.0);
+#pragma unroll
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], PB[q][cc], s_);
+        QuuS[a_][cc] = s_;
+      } else {
+        const int kk = k - NU * NU, a_ = kk / (NS + 1), c = kk % (NS + 1);
+        double s_ = 0.0;
+        const double ur = urho_at(a_);
+        if (c == NS && ur != 0.0) {  // control part of the box term: -rho_b (w_t - l_t)
+          const long long ku = ((long long)b * N + t) * NU + a_;
+          s_ = -ur * (P.box_wu[ku] - P.box_lu[ku]);
+        }
+#pragma unroll
+        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], (c < NS) ? PA[q][c] : w[q], s_);
+        Qux[a_][c] = s_;
+      }
+    }
+    __syncwarp();
+    // phase 2b: lane c <= NS factors Quu (redundantly) and solves column c of the gains
+    // -Quu^{-1} [Qux | qu]
     if (lane <= NS) {
       const int c = lane;
       double Qm[NU][NU], qx[NU];
 #pragma unroll
       for (int a_ = 0; a_ < NU; ++a_) {
 #pragma unroll
-        for (int cc = 0; cc < NU; ++cc) {
-          double s_ = qu2[a_][cc];
-#pragma unroll
-          for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], PB[q][cc], s_);
-          Qm[a_][cc] = s_;
-        }
-        double s_ = 0.0;
-        if (c == NS && urho[a_] != 0.0) {  // control part of the box term: -rho_b (w_t - l_t)
-          const long long ku = ((long long)b * N + t) * NU + a_;
-          s_ = -urho[a_] * (P.box_wu[ku] - P.box_lu[ku]);
-        }
-#pragma unroll
-        for (int q = 0; q < NS; ++q) s_ = __fma_rn(Bm[q * NU + a_], (c < NS) ? PA[q][c] : w[q], s_);
-        qx[a_] = s_;
-        Qux[a_][c] = s_;
+        for (int cc = 0; cc < NU; ++cc) Qm[a_][cc] = QuuS[a_][cc];
+        qx[a_] = Qux[a_][c];
       }
       QuuSolve<NU> qs;
       qs.factor(Qm);
