@@ -43,3 +43,21 @@ def test_scan_long_horizon_t1(ca, N):
     s, u = g.trajectory()
     close(s, o.s, 1e-9, "s after primal step")
     close(u, o.u, 1e-9, "u after primal step")
+
+
+def test_serial_recursion_path_still_matches_oracle():
+    """The warp recursion (`k_riccati`) is what n_s > 4 and CA_RICCATI_SCAN=0 run; with the
+    scan taking every small n_s <= 4 batch, run the T1 / T2 parity tests of those configs
+    once more with the scan off (the switch is read once per process: a subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CA_RICCATI_SCAN="0")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+           os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+           "t1_primal and (1 or 2 or 4 or 8) or t2_full and (2 or 4)"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert " passed" in out.stdout
