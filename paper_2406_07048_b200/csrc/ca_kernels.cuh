@@ -10,9 +10,12 @@
 //                          (item, timestep).
 //   k_sortpairs            per sweep: poses of s^k and the execution order of every
 //                          sort pool (stable counting sort by last pivot count).
-//   k_stage_grouped / k_stage + k_riccati_thread (large batches), k_riccati (small:
-//                          warp per scene)  ADMM step 2 (Eq. 16, one SQP QP,
-//                          P:349-351) as a Riccati recursion per scene.
+//   k_stage_grouped / k_stage + k_riccati_thread (large batches), k_riccati (small
+//                          batches: one CTA per scene, warp 0 recurses)  ADMM step 2
+//                          (Eq. 16, one SQP QP) as a Riccati
+//                          recursion per scene; k_riccati_scan (ca_riccati_scan.cuh,
+//                          small batches, n_s <= 4) the same LQ by a parallel-in-time
+//                          associative scan.
 //   k_mult<D>              ADMM step 3 (Eq. 17) standalone + r_pri.
 //   k_scale2 (d = 2, separating axes) / k_scale<3> (vertex enumeration)  Eq. 3
 //                           per pair; k_vertices2d polygon vertices.
