@@ -1,5 +1,6 @@
-"""The parallel-in-time primal step (k_riccati_scan) beyond one thread group per stage:
-a horizon long enough that 4 (N + 1) threads exceed what the kernel's register count
+"""The parallel-in-time primal step (k_riccati_scan) over horizons from the scan's
+threshold (N = 8: 9 elements, 4 levels; partial last chunks of the forward rollout) to
+horizons long enough that 4 (N + 1) threads exceed what the kernel's register count
 allows in one CTA, so the kernel strides over the stages (ca_api.cu caps the CTA at
 cudaFuncAttributes.maxThreadsPerBlock).  T1 primal step against the oracle at 1e-9."""
 import numpy as np
@@ -27,7 +28,7 @@ def close(a, b, rtol, what):
     assert err.max() <= rtol, f"{what}: max rel err {err.max():.3e}"
 
 
-@pytest.mark.parametrize("N", [64, 90])
+@pytest.mark.parametrize("N", [8, 9, 15, 16, 17, 33, 64, 90])
 def test_scan_long_horizon_t1(ca, N):
     polys = [scenes.box_hrep([6.0, 0.5], [1.0, 1.0]), scenes.box_hrep([14.0, -0.6], [1.2, 0.8])]
     sc = scenes._car_common("C2L", 2, 7, N=N, iters=20, speed=8.0, polys_per_scene=[polys])
