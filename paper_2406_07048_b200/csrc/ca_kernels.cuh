@@ -1209,6 +1209,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     const double* Bm = A + NS * NS;
     const double* cv = Bm + NS * NU;
     // phase 1: PA = P A, PB = P B, w = P c + p
+#pragma unroll  // the rounds are independent: their chains interleave
     for (int k = lane; k < NS * NS + NS * NU + NS; k += 32) {
       if (k < NS * NS) {
         const int a_ = k / NS, c = k % NS;
@@ -1233,6 +1234,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     __syncwarp();
     // phase 2a: the entries of Quu = 2Qu + B^T P B and of [Qux | qu] = B^T [P A | w], one
     // per lane (same sums, same order as k_riccati_thread)
+#pragma unroll  // the rounds are independent: their chains interleave
     for (int k = lane; k < NU * NU + NU * (NS + 1); k += 32) {
       if (k < NU * NU) {
         const int a_ = k / NU, cc = k % NU;
@@ -1285,6 +1287,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
       return v;
     };
     // (phase 3 reads PA, w, Qux, K only, so P and p are written in place)
+#pragma unroll  // the rounds are independent: their chains interleave
     for (int k = lane; k < NS * (NS + 1) / 2 + NS; k += 32) {
       if (k < NS * (NS + 1) / 2) {
         const int a_ = tri_row[k >> 5], c = tri_col[k >> 5];  // this lane's upper-triangle entry
