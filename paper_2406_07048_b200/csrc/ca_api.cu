@@ -492,7 +492,13 @@ ca_status launch_sweep_d(ca_problem* h) {
 
 ca_status launch_sweep(ca_problem* h, bool fused) {
   if (h->P == 0) return CA_OK;
-  ca::k_sortpairs<<<(unsigned)((long long)h->B * h->dev.NG), 32, 0, h->stream>>>(h->dev);
+  // each warp stages its group's status words and the n-order when they fit (48 KB per CTA)
+  // -- on large batches, where the scattered 4-byte reads bound the kernel (C5: 338 -> 274
+  // us per launch); a one-wave batch keeps the shorter unstaged chain (same output bits)
+  const size_t sort_sm = sizeof(uint32_t) * ca::SORT_WPC * ((size_t)h->dev.GG + h->dev.G);
+  const int sort_staged = (sort_sm <= 48 * 1024 && (long long)h->B * h->dev.NG >= 1024) ? 1 : 0;
+  ca::k_sortpairs<<<(unsigned)(((long long)h->B * h->dev.NG + ca::SORT_WPC - 1) / ca::SORT_WPC), 32 * ca::SORT_WPC,
+                     sort_staged ? sort_sm : 0, h->stream>>>(h->dev, sort_staged);
   CUDA_TRY(cudaGetLastError());
   h->launches[4]++;
   cudaEvent_t e0 = nullptr;

@@ -1683,10 +1683,14 @@ __global__ void k_lamtab(Dev P) {
   }
 }
 
-__global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
+constexpr int SORT_WPC = 4;  // independent warps (sort pools) per CTA: more resident warps per SM
+__global__ void __launch_bounds__(32 * SORT_WPC) k_sortpairs(Dev P, int staged) {
   constexpr int NB = 32;
-  __shared__ int cnt[NB][33];
-  const int bg = blockIdx.x, b = bg / P.NG, grp = bg % P.NG, tid = threadIdx.x;
+  __shared__ int cnt_all[SORT_WPC][NB][33];
+  const int bg = blockIdx.x * SORT_WPC + (threadIdx.x >> 5), tid = threadIdx.x & 31;
+  if (bg >= P.B * P.NG) return;  // whole warps only: the warps of a CTA are independent
+  auto& cnt = cnt_all[threadIdx.x >> 5];
+  const int b = bg / P.NG, grp = bg % P.NG;
   const int t0 = grp * P.TG + 1, nt = min(P.TG, P.N - grp * P.TG);
   if (bg == 0 && tid == 0 && P.work) *P.work = 0;  // persistent-sweep work counter
   if (!scene_on(P, b)) return;  // stopped scene: its items are skipped by the sweep
@@ -1701,6 +1705,18 @@ __global__ void __launch_bounds__(32) k_sortpairs(Dev P) {
   const int per = (S + 31) / 32, lo = tid * per, hi = min(S, lo + per);
   const int* base = P.gperm + (long long)b * G;
   const uint32_t* pst = P.pst + ((long long)b * P.N + t0 - 1) * G;
+  if (staged) {
+    // the group's status words and the scene's n-order, read coalesced into this warp's
+    // shared memory (the keyed reads below are then shared-memory gathers, not scattered
+    // 4-byte global reads that each fetch a sector)
+    extern __shared__ uint32_t sort_sm[];
+    uint32_t* sp = sort_sm + (threadIdx.x >> 5) * (P.GG + G);
+    for (int k = tid; k < S; k += 32) sp[k] = pst[k];
+    for (int k = tid; k < G; k += 32) sp[P.GG + k] = (uint32_t)base[k];
+    __syncwarp();
+    pst = sp;
+    base = reinterpret_cast<const int*>(sp + P.GG);
+  }
   auto key_of = [&](int s_, uint32_t& u) {
     const int tl = s_ / G, g = base[s_ % G];
     u = pack_pair(tl, g / P.M, g % P.M);
