@@ -517,7 +517,9 @@ constexpr int RIC_THREAD_MIN_B = 1024;
 
 template <int NS, int NU>
 ca_status launch_riccati_t(ca_problem* h, const double* recs, int nchunk, double* cur, double* prev) {
-  if (h->B > RIC_THREAD_MIN_B) {
+  static const int thread_min_b =
+      std::getenv("CA_RIC_THREAD_MIN_B") ? std::atoi(std::getenv("CA_RIC_THREAD_MIN_B")) : RIC_THREAD_MIN_B;
+  if (h->B > thread_min_b) {
     const long long nq = (long long)h->B * h->N;
     if (nchunk) {
       const long long nbg = (long long)h->B * h->dev.NG;

@@ -726,16 +726,33 @@ __device__ __forceinline__ void riccati_forward(const Dev& P, int b, const doubl
     x[a] = P.s0[b * NS + a];
     sb[a] = x[a];
   }
+  // the gains of the next step are loaded one step ahead (their latency overlaps this
+  // step's dependent arithmetic)
+  double Kn[NU][NS + 1];
+#pragma unroll
+  for (int a = 0; a < NU; ++a)
+#pragma unroll
+    for (int c = 0; c <= NS; ++c) Kn[a][c] = ric[(long long)a * (NS + 1) + c];
   for (int t = 0; t < N; ++t) {
     const double* A = A0 + t * sA;
     const double* Bm = B0 + t * sB;
     const double* cv = c0 + t * sC;
+    double Kt[NU][NS + 1];
+#pragma unroll
+    for (int a = 0; a < NU; ++a)
+#pragma unroll
+      for (int c = 0; c <= NS; ++c) Kt[a][c] = Kn[a][c];
+    if (t + 1 < N)
+#pragma unroll
+      for (int a = 0; a < NU; ++a)
+#pragma unroll
+        for (int c = 0; c <= NS; ++c) Kn[a][c] = ric[((long long)(t + 1) * NU + a) * (NS + 1) + c];
     double uu[NU];
 #pragma unroll
     for (int a = 0; a < NU; ++a) {
-      double s = ric[((long long)t * NU + a) * (NS + 1) + NS];
+      double s = Kt[a][NS];
 #pragma unroll
-      for (int c = 0; c < NS; ++c) s = __fma_rn(ric[((long long)t * NU + a) * (NS + 1) + c], x[c], s);
+      for (int c = 0; c < NS; ++c) s = __fma_rn(Kt[a][c], x[c], s);
       uu[a] = s;
       P.u[((long long)b * N + t) * NU + a] = s;
     }
@@ -820,13 +837,23 @@ __device__ __forceinline__ void riccati_serial(const Dev& P, int b, const double
       for (int c = 0; c < NS; ++c) Pm[a][c] = H[a][c];
     }
   }
+  // the next (earlier) stage's cost block is loaded one step ahead: its global-memory
+  // latency overlaps this step's dependent arithmetic
+  double Hn[NS][NS], hn[NS];
+  if (N - 1 >= 1) stage(N - 1, Hn, hn);
   for (int t = N - 1; t >= 0; --t) {
     const double* A = A0 + t * sA;
     const double* Bm = B0 + t * sB;
     const double* cv = c0 + t * sC;
     double H[NS][NS], h[NS];
     if (t >= 1) {
-      stage(t, H, h);
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        h[a] = hn[a];
+#pragma unroll
+        for (int c = 0; c < NS; ++c) H[a][c] = Hn[a][c];
+      }
+      if (t - 1 >= 1) stage(t - 1, Hn, hn);
     } else {
 #pragma unroll
       for (int a = 0; a < NS; ++a) {
