@@ -564,9 +564,11 @@ __global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
   if (!scene_on(P, b)) return;
   const int RC = P.rec, fm = P.nagg + S_PMAX;
   const double* base = P.agg + bg * P.nchunkG * P.TG * RC;
+  // loads batched (8 chunks in flight); each entry summed in chunk order
   for (int o = lane; o < nt * RC; o += 32) {
     double acc = 0.0;
     const bool mx = (o % RC) == fm;
+#pragma unroll 8
     for (int c = 0; c < P.nchunkG; ++c) {
       const double v = base[(long long)c * P.TG * RC + o];
       acc = mx ? fmax(acc, v) : acc + v;
@@ -582,9 +584,9 @@ __global__ void __launch_bounds__(128) k_stage_grouped(Dev P) {
 #endif  // CA_COMMON_KERNELS
 
 // Quu^{-1} applied to a column, shared by every Riccati path so their gains agree
-// bitwise.  n_u <= 3: adjugate and one reciprocal of the determinant (Quu is SPD; a
+// bitwise.  n_u <= 4: adjugate and one reciprocal of the determinant (Quu is SPD; a
 // short dependency chain: the per-step latency of the small-batch recursion is
-// dominated by this solve); n_u = 4: Cholesky with reciprocal diagonal.
+// dominated by this solve); larger n_u: Cholesky with reciprocal diagonal.
 template <int NU>
 struct QuuSolve {
   double m[NU][NU];  // adjugate (n_u <= 4) or Cholesky factor (n_u > 4)
