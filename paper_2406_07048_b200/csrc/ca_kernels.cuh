@@ -1100,6 +1100,10 @@ __host__ __device__ inline long long riccati_k_smem_doubles(int N, int NS, int N
 // dependent chain).  (One warp alone spent ~100 us of C3's latency-mode iteration --
 // 24 records per (scene, t) -- summing them.)
 constexpr int RIC_WARPS = 8;
+#ifndef CA_RIC_REC_WARPS
+#define CA_RIC_REC_WARPS 4
+#endif
+constexpr int RIC_REC_WARPS = CA_RIC_REC_WARPS;  // warps of the three-phase recursion (n_s^2 + n_s n_u + n_s > 32)
 template <int NS, int NU>
 __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double* recs, int nchunk, double* dst_cur,
                                                            double* dst_prev) {
@@ -1185,7 +1189,18 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     stage_dyn(P.dync + idx0 * NS, NS, NS * NS + NS * NU);
   }
   __syncthreads();
-  if (tid >= 32) return;  // the recursion: warp 0
+  // the recursion: warp 0 (n_s <= 4: lane-level riccati_lanes), or RIC_REC_WARPS warps
+  // for the three-phase split of larger states (each phase's entries spread over
+  // 32 RW threads: the issue of one warp was the bound), named barrier 1 among them
+  constexpr bool kLanes = NS * NS + NS * NU + NS <= 32;
+  constexpr int RW = kLanes ? 1 : RIC_REC_WARPS, RT = 32 * RW;
+  static_assert(RW <= RIC_WARPS, "recursion warps within the CTA");
+  if (tid >= RT) return;
+  auto rsync = [&]() {
+    if constexpr (RW == 1) __syncwarp();
+    else asm volatile("bar.sync 1, %0;" ::"n"(RT) : "memory");
+  };
+  const int rt = tid;  // thread index among the recursion threads
   // The recursion is a chain of small dependent products.  For n_s <= 4 one thread
   // with every matrix in registers and its operands in shared memory is fastest
   // (C4: 126 vs 135 us per ADMM iteration); larger states would spill, so they split
@@ -1199,16 +1214,16 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
                               dst_prev);
     return;
   }
-  // 2 Qu of this lane's phase-2 entry (kept in a register)
-  // this lane's upper-triangle entries (row-major order), decoded once
-  int tri_row[2] = {0, 0}, tri_col[2] = {0, 0};
-  for (int k = lane, u = 0; k < NS * (NS + 1) / 2 && u < 2; k += 32, ++u) {
-    int a_ = 0, r = k;
-    while (r >= NS - a_) { r -= NS - a_; ++a_; }
+  // this thread's upper-triangle entries (row-major order), decoded once
+  constexpr int T3 = NS * (NS + 1) / 2 + NS, R3 = (T3 + RT - 1) / RT;
+  int tri_row[R3], tri_col[R3];
+#pragma unroll
+  for (int u = 0; u < R3; ++u) {
+    int a_ = 0, r = rt + u * RT;
+    while (a_ < NS && r >= NS - a_) { r -= NS - a_; ++a_; }
     tri_row[u] = a_;
     tri_col[u] = a_ + r;
   }
-  static_assert(NS * (NS + 1) / 2 <= 64, "two upper-triangle entries per lane at most");
   // box block (reading #7): control bounds and their penalty on the Quu diagonal
   double ulo[NU], uhi[NU], urho[NU];
 #pragma unroll
@@ -1217,7 +1232,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     uhi[a_] = P.box ? P.box_lim[2 * NS + NU + a_] : INFINITY;
     urho[a_] = (P.box && box_on(ulo[a_], uhi[a_])) ? P.box_rho : 0.0;
   }
-  const double box_res_prev = (P.box && lane == 0) ? P.box_res[b] : 0.0;
+  const double box_res_prev = (P.box && rt == 0) ? P.box_res[b] : 0.0;
   auto urho_at = [&](int i) {  // urho[i] for a run-time i (select: no local-memory array)
     double v = 0.0;
 #pragma unroll
@@ -1225,12 +1240,12 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     return v;
   };
   // P_N = H_N, p_N = h_N
-  for (int k = lane; k < SB; k += 32) {
+  for (int k = rt; k < SB; k += RT) {
     const double v = sstg[(long long)(N - 1) * SB + k];
     if (k < NS * NS) Pm[k / NS][k % NS] = v;
     else pv[k - NS * NS] = v;
   }
-  __syncwarp();
+  rsync();
   // Backward Riccati recursion, warp-cooperative, three phases per step; every
   // matrix entry keeps the serial summation order (bitwise equal to k_riccati_thread).
   for (int t = N - 1; t >= 0; --t) {
@@ -1239,7 +1254,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     const double* cv = Bm + NS * NU;
     // phase 1: PA = P A, PB = P B, w = P c + p
 #pragma unroll  // the rounds are independent: their chains interleave
-    for (int k = lane; k < NS * NS + NS * NU + NS; k += 32) {
+    for (int k = rt; k < NS * NS + NS * NU + NS; k += RT) {
       if (k < NS * NS) {
         const int a_ = k / NS, c = k % NS;
         double s_ = 0.0;
@@ -1260,11 +1275,11 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
         w[a_] = acc;
       }
     }
-    __syncwarp();
+    rsync();
     // phase 2a: the entries of Quu = 2Qu + B^T P B and of [Qux | qu] = B^T [P A | w], one
     // per lane (same sums, same order as k_riccati_thread)
 #pragma unroll  // the rounds are independent: their chains interleave
-    for (int k = lane; k < NU * NU + NU * (NS + 1); k += 32) {
+    for (int k = rt; k < NU * NU + NU * (NS + 1); k += RT) {
       if (k < NU * NU) {
         const int a_ = k / NU, cc = k % NU;
         double s_ = 2.0 * P.Qu[a_ * NU + cc] + ((a_ == cc) ? urho_at(a_) : 0.0);
@@ -1284,11 +1299,11 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
         Qux[a_][c] = s_;
       }
     }
-    __syncwarp();
-    // phase 2b: lane c <= NS factors Quu (redundantly) and solves column c of the gains
+    rsync();
+    // phase 2b: thread c <= NS factors Quu (redundantly) and solves column c of the gains
     // -Quu^{-1} [Qux | qu]
-    if (lane <= NS) {
-      const int c = lane;
+    if (rt <= NS) {
+      const int c = rt;
       double Qm[NU][NU], qx[NU];
 #pragma unroll
       for (int a_ = 0; a_ < NU; ++a_) {
@@ -1302,7 +1317,7 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
 #pragma unroll
       for (int a_ = 0; a_ < NU; ++a_) ric[((long long)t * NU + a_) * (NS + 1) + c] = -qx[a_];
     }
-    __syncwarp();
+    rsync();
     // phase 3: P <- sym(H + A^T P A + Qux^T K) (both triangle entries by one lane),
     // p <- h + A^T w + Qux^T k
     const double* H = sstg + (long long)(t - 1) * SB;  // stage t (zero at t = 0)
@@ -1317,9 +1332,11 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
     };
     // (phase 3 reads PA, w, Qux, K only, so P and p are written in place)
 #pragma unroll  // the rounds are independent: their chains interleave
-    for (int k = lane; k < NS * (NS + 1) / 2 + NS; k += 32) {
+    for (int u = 0; u < R3; ++u) {
+      const int k = rt + u * RT;
+      if (k >= T3) break;
       if (k < NS * (NS + 1) / 2) {
-        const int a_ = tri_row[k >> 5], c = tri_col[k >> 5];  // this lane's upper-triangle entry
+        const int a_ = tri_row[u], c = tri_col[u];  // this thread's upper-triangle entry
         const double v = 0.5 * (pn_entry(a_, c) + pn_entry(c, a_));
         Pm[a_][c] = v;
         Pm[c][a_] = v;
@@ -1333,8 +1350,9 @@ __global__ void __launch_bounds__(32 * RIC_WARPS) k_riccati(Dev P, const double*
         pv[a_] = s_;
       }
     }
-    __syncwarp();
+    rsync();
   }
+  if (tid >= 32) return;  // the forward rollout: warp 0
   // forward rollout from s_0 (Eq. 13b holds exactly): every lane forms u_t = K_t x_t
   // + k_t (same arithmetic), lane a < NS then x_{t+1}[a] = A x + B u + c: one
   // exchange per step (double-buffered state)
